@@ -1,0 +1,218 @@
+/*
+ * longctx_b200.h -- C-ABI of the B200-native Qwen2.5-1M sparse + DCA prefill
+ * attention path.  Plain pointers and sizes only; no torch / STL types.
+ *
+ * Each entry point replaces one reference operator (paths relative to
+ * /root/reference/proj); the C++ drop-in (include/longctx_b200.hpp) and the
+ * Python mirror (paper_2501_15383_b200/longctx.py) are thin layers over these.
+ *
+ *   lcx_estimate_block      <- longctx::estimate_block      core/include/longctx/sparse.hpp:74-76
+ *                                                         (core/src/sparse.cpp:142-188)
+ *   lcx_line_scores         <- the row/diagonal reductions of select_critical
+ *                                                         (core/src/sparse.cpp:198-217), fused
+ *                                                         with the estimator (no B x t1 matrix)
+ *   lcx_select_from_scores  <- top_lines + forced lines of select_critical
+ *                                                         (core/src/sparse.cpp:15-24, 219-229)
+ *   lcx_select_critical     <- longctx::select_critical     core/include/longctx/sparse.hpp:81-82
+ *   lcx_sparse_attention    <- longctx::sparse_attention    core/include/longctx/sparse.hpp:87-88
+ *   lcx_full_attention      <- longctx::full_attention      core/include/longctx/attention.hpp:57-58
+ *   lcx_chunked_prefill     <- longctx::chunked_prefill     core/include/longctx/sparse.hpp:125-129
+ *   lcx_attention_recall    <- longctx::attention_recall    core/include/longctx/refine.hpp:25-26
+ *   lcx_lse_merge           <- (new) log-sum-exp merge of KV-sequence shards (north star (e))
+ *
+ * Conventions
+ *   - All tensor pointers are DEVICE pointers; every call takes an explicit
+ *     cudaStream_t (passed as void*) and is asynchronous unless stated.
+ *   - Token-major layouts: Q [n][hq][dim], K and V [n][hkv][dim]; outputs
+ *     O [n][hq][dim] fp32, lse [hq][n] fp32.  Query head h reads kv head
+ *     h / (hq / hkv) (GQA, attention.cpp:266-273).
+ *   - Index lists are int32, sorted ascending, per (chunk, head) with a
+ *     fixed capacity stride (cap_v >= vertical budget + 1, cap_s >= slash
+ *     budget + last_q).
+ *   - Status: 0 = ok, else an lcx_status whose value equals the reference
+ *     error kind (errors.hpp:21-32); lcx_last_error() returns the message
+ *     (thread-local).  A C-ABI cannot throw; the C++ wrapper rethrows
+ *     longctx::Error(kind, message).
+ *   - There is no CPU fallback: without a usable sm_100 device every compute
+ *     entry returns LCX_ERR_CUDA.
+ */
+#ifndef LONGCTX_B200_H_
+#define LONGCTX_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LCX_OK = 0,
+  LCX_ERR_DIMENSION = 1,      /* "dimension"          */
+  LCX_ERR_CONFIG = 2,         /* "config"             */
+  LCX_ERR_DOMAIN = 3,         /* "domain"             */
+  LCX_ERR_CAUSALITY = 4,      /* "causality"          */
+  LCX_ERR_EMPTY_ROW = 5,      /* "empty_row"          */
+  LCX_ERR_EMPTY_CALIBRATION = 6,
+  LCX_ERR_CUDA = 100,         /* device / launch failure (no fallback) */
+  LCX_ERR_INTERNAL = 101
+} lcx_status;
+
+typedef enum { LCX_F32 = 0, LCX_BF16 = 1 } lcx_dtype;
+
+/* PositionMode (sparse.hpp:63) */
+typedef enum { LCX_POS_STANDARD = 0, LCX_POS_DCA_CONTINUOUS = 1 } lcx_position_mode;
+/* PrefillMode (sparse.hpp:97) */
+typedef enum { LCX_PREFILL_FULL = 0, LCX_PREFILL_SPARSE = 1 } lcx_prefill_mode;
+/* Kernel path for the attention stage. AUTO = tcgen05 tiles for verticals,
+ * band and dense slash runs + CUDA-core gather for isolated slashes when the
+ * input is bf16 and dim == 128; SIMT = exact fp32 CUDA-core path for every
+ * entry (the fp32 parity path). */
+typedef enum { LCX_PATH_AUTO = 0, LCX_PATH_SIMT = 1, LCX_PATH_TC = 2 } lcx_kernel_path;
+
+/* ChunkConfig (dca.hpp:15-25) */
+typedef struct {
+  int64_t chunk_size;   /* s */
+  int64_t train_len;    /* c */
+  int64_t local_window; /* w (validated only, dca.cpp:26-29) */
+} lcx_chunk_config;
+
+/* SelectionOptions (sparse.hpp:65-69) */
+typedef struct {
+  int32_t force_sink_column;
+  int32_t force_local_band;
+  int32_t slash_mean;
+} lcx_selection_options;
+
+/* AttentionInput (attention.hpp:15-30), multi-head, device resident. */
+typedef struct {
+  int64_t n;
+  int32_t hq, hkv, dim;
+  int32_t dtype;               /* lcx_dtype of q, k, v */
+  const void* q;               /* [n][hq][dim]  */
+  const void* k;               /* [n][hkv][dim] */
+  const void* v;               /* [n][hkv][dim] */
+  const int64_t* positions_q;  /* [n] device, or NULL = 0..n-1 */
+  const int64_t* positions_k;  /* [n] device, or NULL = 0..n-1 */
+  double rope_base;
+  double temperature;
+} lcx_attention_input;
+
+typedef struct {
+  int64_t chunk_len;
+  int64_t last_q;
+  int64_t budget_vertical;
+  int64_t budget_slash;
+  int32_t mode;            /* lcx_prefill_mode */
+  int32_t position_mode;   /* lcx_position_mode */
+  lcx_chunk_config dca;    /* required when position_mode == DCA_CONTINUOUS */
+  lcx_selection_options opts;
+  int32_t kernel_path;     /* lcx_kernel_path */
+  int32_t tc_min_entries;  /* slash entries per 64-key tile to route it to tcgen05 (0 = default) */
+} lcx_prefill_config;
+
+typedef struct {
+  float* out;              /* [n][hq][dim] */
+  float* lse;              /* [hq][n]      */
+  /* optional selection log (ChunkSelection, sparse.hpp:99-104), device, may be NULL */
+  int32_t* sel_verticals;  /* [nchunks][hq][cap_v] */
+  int32_t* sel_nv;         /* [nchunks][hq]        */
+  int32_t* sel_slashes;    /* [nchunks][hq][cap_s] */
+  int32_t* sel_ns;         /* [nchunks][hq]        */
+  int64_t cap_v, cap_s;
+  /* optional exact admitted-entry counts per (chunk, head) (CriticalSet::admitted_count
+   * restricted to the chunk's rows), device int64 [nchunks][hq], may be NULL */
+  int64_t* admitted;
+} lcx_prefill_output;
+
+/* Execution statistics of the last lcx_chunked_prefill on a context (host side). */
+typedef struct {
+  int64_t chunks;
+  int64_t tc_tiles;        /* 64-key x 128-row tcgen05 tiles executed */
+  int64_t simt_entries;    /* entries on the CUDA-core gather path (0 unless measured) */
+  double ms_estimate, ms_select, ms_index, ms_attention; /* 0 unless profiling enabled */
+} lcx_prefill_stats;
+
+typedef struct lcx_context lcx_context;
+
+/* ---- context ------------------------------------------------------------ */
+int lcx_context_create(int device, lcx_context** out);
+int lcx_context_destroy(lcx_context* ctx);
+const char* lcx_last_error(void);
+const char* lcx_version(void);
+/* 1 if the current device is sm_100 class and kernels can launch. */
+int lcx_device_ok(int device);
+/* Enables per-stage CUDA-event timing inside lcx_chunked_prefill (synchronizing). */
+int lcx_set_profiling(lcx_context* ctx, int enabled);
+int lcx_get_stats(lcx_context* ctx, lcx_prefill_stats* out);
+
+/* ---- estimator (part a) -------------------------------------------------- */
+/* estimate_block: q_rows are the trailing nq rows of the key timeline k[0:nk]
+ * (queries trail the keys, sparse.cpp:157-158).  est_out [hq][block][nk] fp32,
+ * block = min(last_q, nq).  pos_mode/cfg as in the reference; rope_base from
+ * the input (positions are token indices; no temperature, sparse.cpp:159). */
+int lcx_estimate_block(lcx_context* ctx, const lcx_attention_input* in, int64_t q_row0,
+                       int64_t nq, int64_t nk, int64_t last_q, int32_t pos_mode,
+                       const lcx_chunk_config* cfg, float* est_out, void* stream);
+
+/* Fused estimator + line reductions: col_score[hq][nk] and slash_score[hq][nk]
+ * exactly as select_critical forms them from the estimate (sum over rows,
+ * mean (or sum) over each diagonal's present entries). */
+int lcx_line_scores(lcx_context* ctx, const lcx_attention_input* in, int64_t q_row0,
+                    int64_t nq, int64_t nk, int64_t last_q, int32_t pos_mode,
+                    const lcx_chunk_config* cfg, int32_t slash_mean, float* col_score,
+                    float* slash_score, void* stream);
+
+/* ---- selection (part a) -------------------------------------------------- */
+/* top-budget columns / diagonals by (score desc, index asc), plus forced lines,
+ * sorted unique.  scores [heads][n]; block = estimator rows (forced band width). */
+int lcx_select_from_scores(lcx_context* ctx, const float* col_score, const float* slash_score,
+                           int32_t heads, int64_t n, int64_t block, int64_t budget_vertical,
+                           int64_t budget_slash, const lcx_selection_options* opts,
+                           int32_t* verticals, int32_t* nv, int64_t cap_v, int32_t* slashes,
+                           int32_t* ns, int64_t cap_s, void* stream);
+
+/* select_critical from an estimate matrix est [heads][block][n] (fp32). */
+int lcx_select_critical(lcx_context* ctx, const float* est, int32_t heads, int64_t block,
+                        int64_t n, int64_t budget_vertical, int64_t budget_slash,
+                        const lcx_selection_options* opts, int32_t* verticals, int32_t* nv,
+                        int64_t cap_v, int32_t* slashes, int32_t* ns, int64_t cap_s,
+                        void* stream);
+
+/* ---- attention (parts b, c) ---------------------------------------------- */
+/* sparse_attention over one critical set per query head (lists [hq][cap]).
+ * use_dca != 0: rel_override = dca_position_matrix(n, *dca) (sparse.cpp:400-413). */
+int lcx_sparse_attention(lcx_context* ctx, const lcx_attention_input* in,
+                         const int32_t* verticals, const int32_t* nv, int64_t cap_v,
+                         const int32_t* slashes, const int32_t* ns, int64_t cap_s,
+                         int32_t use_dca, const lcx_chunk_config* dca, int32_t kernel_path,
+                         float* out, float* lse, void* stream);
+
+/* Dense causal attention (attention.cpp:142-185); use_dca as above. */
+int lcx_full_attention(lcx_context* ctx, const lcx_attention_input* in, int32_t use_dca,
+                       const lcx_chunk_config* dca, int32_t kernel_path, float* out, float* lse,
+                       void* stream);
+
+/* The operator: chunked prefill over all heads and chunks of one layer. */
+int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
+                        const lcx_prefill_config* cfg, lcx_prefill_output* out, void* stream);
+
+/* ---- recall (part d) ----------------------------------------------------- */
+/* per_query[i] = min(1, exp(lse_s - lse_f)); LCX_ERR_DOMAIN if any value
+ * exceeds 1 + slack (refine.cpp:51-72).  aggregate (host double) = mean.
+ * Synchronizes the stream. */
+int lcx_attention_recall(lcx_context* ctx, const float* lse_sparse, const float* lse_full,
+                         int64_t n, double slack, float* per_query, double* aggregate,
+                         void* stream);
+
+/* ---- KV-sequence sharding (part e) --------------------------------------- */
+/* In-place log-sum-exp merge of G shard partials: o[g] [rows][dim] fp32
+ * (normalized within the shard), lse[g] [rows] (-inf for an empty shard).
+ * Writes the merged output/lse into out / lse_out. */
+int lcx_lse_merge(lcx_context* ctx, const float* o_parts, const float* lse_parts, int32_t parts,
+                  int64_t rows, int32_t dim, float* out, float* lse_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LONGCTX_B200_H_ */

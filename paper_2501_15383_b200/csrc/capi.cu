@@ -1,0 +1,562 @@
+// C-ABI implementation and per-layer orchestration (include/longctx_b200.h).
+//
+// lcx_chunked_prefill restates chunked_prefill (reference core/src/sparse.cpp:
+// 293-399): for each chunk [t0, t1) the estimator scores the chunk's trailing
+// min(last_q, t1 - t0) rows against keys [0, t1), the selection keeps the top
+// vertical / slash lines over the t1-key context (one CriticalSet per chunk and
+// head), and the attention computes rows [t0, t1) over their admitted entries.
+// With Q/K/V given, a chunk depends only on K/V[0:t1]; chunks are issued
+// back-to-back on one stream, each launch covering every head.
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "lcx_internal.cuh"
+
+namespace lcx {
+
+thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+int build_rope_table(const double* thetas_dev, int P, int64_t npos, float2* out,
+                     cudaStream_t st);
+
+int ensure_workspace(lcx_context* ctx, size_t bytes) {
+  if (bytes <= ctx->ws_bytes) return LCX_OK;
+  if (ctx->ws) LCX_CHECK_CUDA(cudaFree(ctx->ws));  // implicit device sync
+  ctx->ws = nullptr;
+  ctx->ws_bytes = 0;
+  const size_t want = bytes + bytes / 8 + (1 << 20);
+  LCX_CHECK_CUDA(cudaMalloc(&ctx->ws, want));
+  ctx->ws_bytes = want;
+  return LCX_OK;
+}
+
+int ensure_rope(lcx_context* ctx, double base, int dim, int64_t P, cudaStream_t st) {
+  if (ctx->rope && ctx->rope_base == base && ctx->rope_dim == dim && ctx->rope_P >= P)
+    return LCX_OK;
+  if (ctx->rope) LCX_CHECK_CUDA(cudaFree(ctx->rope));
+  ctx->rope = nullptr;
+  const int pairs = dim / 2;
+  const int64_t npos = std::max<int64_t>(P, 1);
+  std::vector<double> th(pairs);
+  for (int p = 0; p < pairs; ++p) th[p] = std::pow(base, -double(2 * p) / double(dim));
+  double* th_dev = nullptr;
+  LCX_CHECK_CUDA(cudaMalloc(&th_dev, sizeof(double) * pairs));
+  LCX_CHECK_CUDA(cudaMemcpy(th_dev, th.data(), sizeof(double) * pairs, cudaMemcpyHostToDevice));
+  LCX_CHECK_CUDA(cudaMalloc(&ctx->rope, sizeof(float2) * size_t(npos) * pairs));
+  LCX_TRY(build_rope_table(th_dev, pairs, npos, ctx->rope, st));
+  LCX_CHECK_CUDA(cudaStreamSynchronize(st));
+  LCX_CHECK_CUDA(cudaFree(th_dev));
+  ctx->rope_base = base;
+  ctx->rope_dim = dim;
+  ctx->rope_P = npos;
+  return LCX_OK;
+}
+
+namespace {
+
+__global__ void max_pos_kernel(const int64_t* a, const int64_t* b, int64_t n,
+                               unsigned long long* out, int* neg) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t x = a ? a[i] : i, y = b ? b[i] : i;
+    if (x < 0 || y < 0) atomicExch(neg, 1);
+    const int64_t m = x > y ? x : y;
+    atomicMax(out, (unsigned long long)(m < 0 ? 0 : m));
+  }
+}
+
+int validate_input(const lcx_attention_input* in) {
+  if (!in) return fail(LCX_ERR_DIMENSION, "null attention input");
+  if (in->n <= 0) return fail(LCX_ERR_DIMENSION, "attention input must have at least one row");
+  if (in->dim <= 0 || in->dim % 2 != 0)
+    return fail(LCX_ERR_CONFIG, "head dimension must be even and positive (rope pairs)");
+  if (in->dim > 128) return fail(LCX_ERR_CONFIG, "head dimension > 128 is not supported");
+  if (in->hq <= 0 || in->hkv <= 0) return fail(LCX_ERR_CONFIG, "head counts must be positive");
+  if (in->hq % in->hkv != 0)
+    return fail(LCX_ERR_CONFIG, "query-head count must be divisible by kv-head count");
+  if (!(in->rope_base > 0.0)) return fail(LCX_ERR_DOMAIN, "rope base must be positive");
+  if (!(in->temperature > 0.0)) return fail(LCX_ERR_DOMAIN, "temperature must be positive");
+  if (in->dtype != LCX_F32 && in->dtype != LCX_BF16) return fail(LCX_ERR_CONFIG, "bad dtype");
+  if (!in->q || !in->k || !in->v) return fail(LCX_ERR_DIMENSION, "null q/k/v pointer");
+  return LCX_OK;
+}
+
+int validate_chunk(const lcx_chunk_config* c) {
+  if (!c) return fail(LCX_ERR_CONFIG, "dca requires a chunk config");
+  if (c->chunk_size <= 0) return fail(LCX_ERR_CONFIG, "chunkSize must be positive");
+  if (c->train_len <= 0) return fail(LCX_ERR_CONFIG, "trainLen must be positive");
+  if (c->chunk_size > c->train_len)
+    return fail(LCX_ERR_CONFIG, "chunkSize must not exceed trainLen");
+  const int64_t bound = std::min(c->chunk_size, c->train_len - c->chunk_size);
+  if (c->local_window > bound)
+    return fail(LCX_ERR_CONFIG,
+                "localWindow must not exceed min(chunkSize, trainLen - chunkSize)");
+  return LCX_OK;
+}
+
+// Largest rotation position any kernel will look up for this input.
+int max_position(lcx_context* ctx, const lcx_attention_input* in, int64_t* out,
+                 cudaStream_t st) {
+  if (!in->positions_q && !in->positions_k) {
+    *out = in->n - 1;
+    return LCX_OK;
+  }
+  unsigned long long* dmax = nullptr;
+  int* dneg = nullptr;
+  LCX_CHECK_CUDA(cudaMallocAsync(&dmax, sizeof(unsigned long long), st));
+  LCX_CHECK_CUDA(cudaMallocAsync(&dneg, sizeof(int), st));
+  LCX_CHECK_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
+  LCX_CHECK_CUDA(cudaMemsetAsync(dneg, 0, sizeof(int), st));
+  max_pos_kernel<<<64, 256, 0, st>>>(in->positions_q, in->positions_k, in->n, dmax, dneg);
+  LCX_CHECK_LAUNCH();
+  unsigned long long hmax = 0;
+  int hneg = 0;
+  LCX_CHECK_CUDA(cudaMemcpyAsync(&hmax, dmax, sizeof(hmax), cudaMemcpyDeviceToHost, st));
+  LCX_CHECK_CUDA(cudaMemcpyAsync(&hneg, dneg, sizeof(hneg), cudaMemcpyDeviceToHost, st));
+  LCX_CHECK_CUDA(cudaStreamSynchronize(st));
+  LCX_CHECK_CUDA(cudaFreeAsync(dmax, st));
+  LCX_CHECK_CUDA(cudaFreeAsync(dneg, st));
+  if (hneg) return fail(LCX_ERR_DOMAIN, "positions must be non-negative");
+  *out = int64_t(hmax);
+  (void)ctx;
+  return LCX_OK;
+}
+
+AttnArgs base_attn(const lcx_attention_input* in, lcx_context* ctx) {
+  AttnArgs a{};
+  a.q = in->q;
+  a.k = in->k;
+  a.v = in->v;
+  a.dtype = in->dtype;
+  a.hq = in->hq;
+  a.hkv = in->hkv;
+  a.dim = in->dim;
+  a.pos_q = in->positions_q;
+  a.pos_k = in->positions_k;
+  a.scale = float(1.0 / (in->temperature * std::sqrt(double(in->dim))));
+  a.rope = ctx->rope;
+  a.rope_P = ctx->rope_P;
+  return a;
+}
+
+EstimateArgs base_est(const lcx_attention_input* in, lcx_context* ctx, int64_t q_row0,
+                      int64_t nq, int64_t nk, int64_t last_q, int pos_mode, int64_t c) {
+  EstimateArgs e{};
+  e.q = in->q;
+  e.k = in->k;
+  e.dtype = in->dtype;
+  e.hq = in->hq;
+  e.hkv = in->hkv;
+  e.dim = in->dim;
+  e.q_row0 = q_row0;
+  e.nq = nq;
+  e.nk = nk;
+  e.block = std::min(last_q, nq);
+  e.pos_mode = pos_mode;
+  e.c = c;
+  e.rope = ctx->rope;
+  return e;
+}
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int64_t words_for(int64_t n) { return (n + 31) / 32 + 1; }
+
+}  // namespace
+}  // namespace lcx
+
+using namespace lcx;
+
+extern "C" {
+
+const char* lcx_last_error(void) { return lcx::g_err.c_str(); }
+const char* lcx_version(void) { return "longctx-b200 0.1.0 (sm_100a)"; }
+
+int lcx_device_ok(int device) {
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) return 0;
+  return prop.major == 10 ? 1 : 0;
+}
+
+int lcx_context_create(int device, lcx_context** out) {
+  if (!out) return fail(LCX_ERR_INTERNAL, "null out");
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    return fail(LCX_ERR_CUDA, "no CUDA device available (the path has no CPU fallback)");
+  cudaDeviceProp prop;
+  LCX_CHECK_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(LCX_ERR_CUDA, std::string("device ") + prop.name +
+                                  " is not sm_100-class; kernels are built for sm_100a only");
+  auto* ctx = new lcx_context();
+  ctx->device = device;
+  ctx->sm_count = prop.multiProcessorCount;
+  *out = ctx;
+  return LCX_OK;
+}
+
+int lcx_context_destroy(lcx_context* ctx) {
+  if (!ctx) return LCX_OK;
+  cudaDeviceSynchronize();
+  if (ctx->ws) cudaFree(ctx->ws);
+  if (ctx->rope) cudaFree(ctx->rope);
+  delete ctx;
+  return LCX_OK;
+}
+
+int lcx_set_profiling(lcx_context* ctx, int enabled) {
+  ctx->profiling = enabled;
+  return LCX_OK;
+}
+
+int lcx_get_stats(lcx_context* ctx, lcx_prefill_stats* out) {
+  *out = ctx->stats;
+  return LCX_OK;
+}
+
+int lcx_estimate_block(lcx_context* ctx, const lcx_attention_input* in, int64_t q_row0,
+                       int64_t nq, int64_t nk, int64_t last_q, int32_t pos_mode,
+                       const lcx_chunk_config* cfg, float* est_out, void* stream) {
+  LCX_TRY(validate_input(in));
+  if (last_q <= 0) return fail(LCX_ERR_CONFIG, "lastQ must be positive");
+  if (nq <= 0 || nk <= 0) return fail(LCX_ERR_DIMENSION, "empty query or key matrix");
+  if (nq > nk) return fail(LCX_ERR_DIMENSION, "queries must be the trailing rows of the key timeline");
+  if (q_row0 + nq != nk || nk > in->n)
+    return fail(LCX_ERR_DIMENSION, "query window must end at the key count");
+  if (pos_mode == LCX_POS_DCA_CONTINUOUS && !cfg)
+    return fail(LCX_ERR_CONFIG, "dcaContinuous estimation requires a chunk config");
+  const int64_t c = pos_mode == LCX_POS_DCA_CONTINUOUS ? cfg->train_len : 0;
+  if (pos_mode == LCX_POS_DCA_CONTINUOUS && c <= 0)
+    return fail(LCX_ERR_CONFIG, "trainLen must be positive");
+  cudaStream_t st = S(stream);
+  LCX_TRY(ensure_rope(ctx, in->rope_base, in->dim, std::max<int64_t>(nk, c), st));
+  EstimateArgs e = base_est(in, ctx, q_row0, nq, nk, last_q, pos_mode, c);
+  e.est = est_out;
+  Sizer sz;
+  estimate_simt_size(e, sz, ctx->sm_count);
+  LCX_TRY(ensure_workspace(ctx, sz.off));
+  Arena ar{ctx->ws, ctx->ws_bytes, 0};
+  return estimate_simt(ctx, e, ar, st);
+}
+
+int lcx_line_scores(lcx_context* ctx, const lcx_attention_input* in, int64_t q_row0, int64_t nq,
+                    int64_t nk, int64_t last_q, int32_t pos_mode, const lcx_chunk_config* cfg,
+                    int32_t slash_mean, float* col_score, float* slash_score, void* stream) {
+  LCX_TRY(validate_input(in));
+  if (last_q <= 0) return fail(LCX_ERR_CONFIG, "lastQ must be positive");
+  if (nq <= 0 || nk <= 0 || nq > nk || q_row0 + nq != nk || nk > in->n)
+    return fail(LCX_ERR_DIMENSION, "bad query window");
+  if (pos_mode == LCX_POS_DCA_CONTINUOUS && !cfg)
+    return fail(LCX_ERR_CONFIG, "dcaContinuous estimation requires a chunk config");
+  const int64_t c = pos_mode == LCX_POS_DCA_CONTINUOUS ? cfg->train_len : 0;
+  cudaStream_t st = S(stream);
+  LCX_TRY(ensure_rope(ctx, in->rope_base, in->dim, std::max<int64_t>(nk, c), st));
+  EstimateArgs e = base_est(in, ctx, q_row0, nq, nk, last_q, pos_mode, c);
+  e.col = col_score;
+  e.slash = slash_score;
+  e.slash_mean = slash_mean;
+  Sizer sz;
+  estimate_simt_size(e, sz, ctx->sm_count);
+  LCX_TRY(ensure_workspace(ctx, sz.off));
+  Arena ar{ctx->ws, ctx->ws_bytes, 0};
+  return estimate_simt(ctx, e, ar, st);
+}
+
+int lcx_select_from_scores(lcx_context* ctx, const float* col_score, const float* slash_score,
+                           int32_t heads, int64_t n, int64_t block, int64_t budget_vertical,
+                           int64_t budget_slash, const lcx_selection_options* opts,
+                           int32_t* verticals, int32_t* nv, int64_t cap_v, int32_t* slashes,
+                           int32_t* ns, int64_t cap_s, void* stream) {
+  (void)ctx;
+  if (n <= 0 || block <= 0 || block > n)
+    return fail(LCX_ERR_DIMENSION, "estimation block row count out of range");
+  lcx_selection_options o = opts ? *opts : lcx_selection_options{1, 1, 1};
+  cudaStream_t st = S(stream);
+  LCX_TRY(select_lines(col_score, heads, n, budget_vertical, o.force_sink_column, 1, verticals,
+                       nv, cap_v, st));
+  LCX_TRY(select_lines(slash_score, heads, n, budget_slash, o.force_local_band, block, slashes,
+                       ns, cap_s, st));
+  return LCX_OK;
+}
+
+int lcx_select_critical(lcx_context* ctx, const float* est, int32_t heads, int64_t block,
+                        int64_t n, int64_t budget_vertical, int64_t budget_slash,
+                        const lcx_selection_options* opts, int32_t* verticals, int32_t* nv,
+                        int64_t cap_v, int32_t* slashes, int32_t* ns, int64_t cap_s,
+                        void* stream) {
+  if (n <= 0 || block <= 0 || block > n)
+    return fail(LCX_ERR_DIMENSION, "estimation block row count out of range");
+  lcx_selection_options o = opts ? *opts : lcx_selection_options{1, 1, 1};
+  cudaStream_t st = S(stream);
+  Sizer sz;
+  sz.take<float>(size_t(heads) * n);
+  sz.take<float>(size_t(heads) * n);
+  LCX_TRY(ensure_workspace(ctx, sz.off));
+  Arena ar{ctx->ws, ctx->ws_bytes, 0};
+  float* col = ar.take<float>(size_t(heads) * n);
+  float* sl = ar.take<float>(size_t(heads) * n);
+  LCX_TRY(line_scores_from_est(est, heads, block, n, o.slash_mean, col, sl, st));
+  return lcx_select_from_scores(ctx, col, sl, heads, n, block, budget_vertical, budget_slash, &o,
+                                verticals, nv, cap_v, slashes, ns, cap_s, stream);
+}
+
+int lcx_sparse_attention(lcx_context* ctx, const lcx_attention_input* in,
+                         const int32_t* verticals, const int32_t* nv, int64_t cap_v,
+                         const int32_t* slashes, const int32_t* ns, int64_t cap_s,
+                         int32_t use_dca, const lcx_chunk_config* dca, int32_t kernel_path,
+                         float* out, float* lse, void* stream) {
+  LCX_TRY(validate_input(in));
+  if (use_dca) LCX_TRY(validate_chunk(dca));
+  (void)kernel_path;
+  cudaStream_t st = S(stream);
+  int64_t maxpos = 0;
+  LCX_TRY(max_position(ctx, in, &maxpos, st));
+  const int64_t P = std::max<int64_t>(maxpos + 1, use_dca ? dca->train_len : 0);
+  LCX_TRY(ensure_rope(ctx, in->rope_base, in->dim, std::max<int64_t>(P, in->n), st));
+  const int64_t words = words_for(in->n);
+  Sizer sz;
+  sz.take<uint32_t>(size_t(words) * in->hq);
+  LCX_TRY(ensure_workspace(ctx, sz.off));
+  Arena ar{ctx->ws, ctx->ws_bytes, 0};
+  uint32_t* vbits = ar.take<uint32_t>(size_t(words) * in->hq);
+  LCX_TRY(build_bitmaps(verticals, nv, cap_v, in->hq, words, vbits, st));
+  AttnArgs a = base_attn(in, ctx);
+  a.n = in->n;
+  a.row_begin = 0;
+  a.row_end = in->n;
+  a.rel_mode = use_dca ? 1 : 0;
+  a.s = use_dca ? dca->chunk_size : 1;
+  a.c = use_dca ? dca->train_len : 1;
+  a.verts = verticals;
+  a.nv = nv;
+  a.cap_v = cap_v;
+  a.slashes = slashes;
+  a.ns = ns;
+  a.cap_s = cap_s;
+  a.vbits = vbits;
+  a.bit_words = words;
+  a.out = out;
+  a.lse = lse;
+  a.lse_stride = in->n;
+  return attention_simt(a, st);
+}
+
+int lcx_full_attention(lcx_context* ctx, const lcx_attention_input* in, int32_t use_dca,
+                       const lcx_chunk_config* dca, int32_t kernel_path, float* out, float* lse,
+                       void* stream) {
+  LCX_TRY(validate_input(in));
+  if (use_dca) LCX_TRY(validate_chunk(dca));
+  (void)kernel_path;
+  cudaStream_t st = S(stream);
+  int64_t maxpos = 0;
+  LCX_TRY(max_position(ctx, in, &maxpos, st));
+  const int64_t P = std::max<int64_t>(maxpos + 1, use_dca ? dca->train_len : 0);
+  LCX_TRY(ensure_rope(ctx, in->rope_base, in->dim, std::max<int64_t>(P, in->n), st));
+  AttnArgs a = base_attn(in, ctx);
+  a.n = in->n;
+  a.row_begin = 0;
+  a.row_end = in->n;
+  a.rel_mode = use_dca ? 1 : 0;
+  a.s = use_dca ? dca->chunk_size : 1;
+  a.c = use_dca ? dca->train_len : 1;
+  a.dense = 1;
+  a.out = out;
+  a.lse = lse;
+  a.lse_stride = in->n;
+  return attention_simt(a, st);
+}
+
+int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
+                        const lcx_prefill_config* cfg, lcx_prefill_output* out, void* stream) {
+  LCX_TRY(validate_input(in));
+  if (!cfg || !out || !out->out || !out->lse) return fail(LCX_ERR_DIMENSION, "null config/output");
+  if (cfg->chunk_len <= 0) return fail(LCX_ERR_CONFIG, "chunkLen must be positive");
+  if (cfg->last_q <= 0) return fail(LCX_ERR_CONFIG, "lastQ must be positive");
+  const bool sparse = cfg->mode == LCX_PREFILL_SPARSE;
+  if (sparse && cfg->chunk_len < cfg->last_q)
+    return fail(LCX_ERR_CONFIG, "sparse prefill requires chunkLen >= lastQ");
+  const bool dca = cfg->position_mode == LCX_POS_DCA_CONTINUOUS;
+  if (dca) LCX_TRY(validate_chunk(&cfg->dca));
+  if (cfg->budget_vertical < 0 || cfg->budget_slash < 0)
+    return fail(LCX_ERR_CONFIG, "budgets must be non-negative");
+
+  cudaStream_t st = S(stream);
+  const int64_t n = in->n;
+  const int hq = in->hq;
+  const int64_t L = cfg->chunk_len;
+  const int64_t nchunks = (n + L - 1) / L;
+  const int64_t c = dca ? cfg->dca.train_len : 0;
+  int64_t maxpos = 0;
+  LCX_TRY(max_position(ctx, in, &maxpos, st));
+  LCX_TRY(ensure_rope(ctx, in->rope_base, in->dim,
+                      std::max<int64_t>(std::max<int64_t>(maxpos + 1, n), c), st));
+
+  const int64_t block_max = std::min(cfg->last_q, L);
+  const int64_t cap_v = out->sel_verticals ? out->cap_v : cfg->budget_vertical + 2;
+  const int64_t cap_s = out->sel_slashes ? out->cap_s : cfg->budget_slash + block_max + 1;
+  if (sparse && (cap_v < std::min<int64_t>(cfg->budget_vertical, n) + 1 ||
+                 cap_s < std::min<int64_t>(cfg->budget_slash, n) + block_max))
+    return fail(LCX_ERR_DIMENSION, "selection capacity below budget + forced lines");
+  const int64_t words = words_for(n);
+
+  // workspace plan (largest chunk = the last one: nk = n)
+  EstimateArgs e_max = base_est(in, ctx, n - std::min(L, n), std::min(L, n), n, cfg->last_q,
+                                dca ? 1 : 0, c);
+  e_max.col = reinterpret_cast<float*>(1);
+  e_max.slash = reinterpret_cast<float*>(1);
+  Sizer sz;
+  if (sparse) {
+    estimate_simt_size(e_max, sz, ctx->sm_count);
+    sz.take<float>(size_t(hq) * n);
+    sz.take<float>(size_t(hq) * n);
+    if (!out->sel_verticals) {
+      sz.take<int32_t>(size_t(hq) * cap_v);
+      sz.take<int32_t>(size_t(hq));
+    }
+    if (!out->sel_slashes) {
+      sz.take<int32_t>(size_t(hq) * cap_s);
+      sz.take<int32_t>(size_t(hq));
+    }
+    sz.take<uint32_t>(size_t(hq) * words);
+  }
+  LCX_TRY(ensure_workspace(ctx, sz.off));
+  Arena ar{ctx->ws, ctx->ws_bytes, 0};
+  Arena est_ar = ar;  // estimator scratch is reused per chunk
+  if (sparse) {
+    Sizer es;
+    estimate_simt_size(e_max, es, ctx->sm_count);
+    ar.off += es.off;
+  }
+  float* col = sparse ? ar.take<float>(size_t(hq) * n) : nullptr;
+  float* sl = sparse ? ar.take<float>(size_t(hq) * n) : nullptr;
+  int32_t* iv = nullptr;
+  int32_t* inv = nullptr;
+  int32_t* is = nullptr;
+  int32_t* ins = nullptr;
+  if (sparse && !out->sel_verticals) {
+    iv = ar.take<int32_t>(size_t(hq) * cap_v);
+    inv = ar.take<int32_t>(size_t(hq));
+  }
+  if (sparse && !out->sel_slashes) {
+    is = ar.take<int32_t>(size_t(hq) * cap_s);
+    ins = ar.take<int32_t>(size_t(hq));
+  }
+  uint32_t* vbits = sparse ? ar.take<uint32_t>(size_t(hq) * words) : nullptr;
+  if (out->admitted)
+    LCX_CHECK_CUDA(cudaMemsetAsync(out->admitted, 0, sizeof(int64_t) * nchunks * hq, st));
+
+  cudaEvent_t ev[5];
+  const bool prof = ctx->profiling != 0;
+  double ms_est = 0, ms_sel = 0, ms_idx = 0, ms_att = 0;
+  if (prof)
+    for (auto& x : ev) LCX_CHECK_CUDA(cudaEventCreate(&x));
+
+  for (int64_t ci = 0; ci < nchunks; ++ci) {
+    const int64_t t0 = ci * L, t1 = std::min(n, t0 + L);
+    const int64_t block = std::min(cfg->last_q, t1 - t0);
+    int32_t* vlist = out->sel_verticals ? out->sel_verticals + ci * hq * cap_v : iv;
+    int32_t* vcnt = out->sel_nv ? out->sel_nv + ci * hq : inv;
+    int32_t* slist = out->sel_slashes ? out->sel_slashes + ci * hq * cap_s : is;
+    int32_t* scnt = out->sel_ns ? out->sel_ns + ci * hq : ins;
+    if (prof) LCX_CHECK_CUDA(cudaEventRecord(ev[0], st));
+    if (sparse) {
+      EstimateArgs e = base_est(in, ctx, t0, t1 - t0, t1, cfg->last_q, dca ? 1 : 0, c);
+      e.col = col;
+      e.slash = sl;
+      e.slash_mean = cfg->opts.slash_mean;
+      Arena a2 = est_ar;
+      LCX_TRY(estimate_simt(ctx, e, a2, st));
+      if (prof) LCX_CHECK_CUDA(cudaEventRecord(ev[1], st));
+      LCX_TRY(select_lines(col, hq, t1, cfg->budget_vertical, cfg->opts.force_sink_column, 1,
+                           vlist, vcnt, cap_v, st));
+      LCX_TRY(select_lines(sl, hq, t1, cfg->budget_slash, cfg->opts.force_local_band, block,
+                           slist, scnt, cap_s, st));
+      if (prof) LCX_CHECK_CUDA(cudaEventRecord(ev[2], st));
+      LCX_TRY(build_bitmaps(vlist, vcnt, cap_v, hq, words, vbits, st));
+      if (prof) LCX_CHECK_CUDA(cudaEventRecord(ev[3], st));
+    }
+    AttnArgs a = base_attn(in, ctx);
+    a.n = t1;
+    a.row_begin = t0;
+    a.row_end = t1;
+    a.rel_mode = dca ? 1 : 0;
+    a.s = dca ? cfg->dca.chunk_size : 1;
+    a.c = dca ? cfg->dca.train_len : 1;
+    a.dense = sparse ? 0 : 1;
+    a.verts = vlist;
+    a.nv = vcnt;
+    a.cap_v = cap_v;
+    a.slashes = slist;
+    a.ns = scnt;
+    a.cap_s = cap_s;
+    a.vbits = vbits;
+    a.bit_words = words;
+    a.out = out->out;
+    a.lse = out->lse;
+    a.lse_stride = n;
+    a.admitted = out->admitted ? out->admitted + ci * hq : nullptr;
+    LCX_TRY(attention_simt(a, st));
+    if (prof) {
+      LCX_CHECK_CUDA(cudaEventRecord(ev[4], st));
+      LCX_CHECK_CUDA(cudaEventSynchronize(ev[4]));
+      float t = 0;
+      if (sparse) {
+        cudaEventElapsedTime(&t, ev[0], ev[1]);
+        ms_est += t;
+        cudaEventElapsedTime(&t, ev[1], ev[2]);
+        ms_sel += t;
+        cudaEventElapsedTime(&t, ev[2], ev[3]);
+        ms_idx += t;
+        cudaEventElapsedTime(&t, ev[3], ev[4]);
+      } else {
+        cudaEventElapsedTime(&t, ev[0], ev[4]);
+      }
+      ms_att += t;
+    }
+  }
+  if (prof)
+    for (auto& x : ev) cudaEventDestroy(x);
+  ctx->stats = lcx_prefill_stats{};
+  ctx->stats.chunks = nchunks;
+  ctx->stats.ms_estimate = ms_est;
+  ctx->stats.ms_select = ms_sel;
+  ctx->stats.ms_index = ms_idx;
+  ctx->stats.ms_attention = ms_att;
+  return LCX_OK;
+}
+
+int lcx_attention_recall(lcx_context* ctx, const float* lse_sparse, const float* lse_full,
+                         int64_t n, double slack, float* per_query, double* aggregate,
+                         void* stream) {
+  if (n <= 0) return fail(LCX_ERR_DIMENSION, "recall needs at least one query");
+  cudaStream_t st = S(stream);
+  Sizer sz;
+  sz.take<double>(1);
+  sz.take<int>(1);
+  LCX_TRY(ensure_workspace(ctx, sz.off));
+  Arena ar{ctx->ws, ctx->ws_bytes, 0};
+  double* dsum = ar.take<double>(1);
+  int* dbad = ar.take<int>(1);
+  LCX_TRY(recall_kernel_launch(lse_sparse, lse_full, n, slack, per_query, dsum, dbad, st));
+  double hsum = 0;
+  int hbad = 0;
+  LCX_CHECK_CUDA(cudaMemcpyAsync(&hsum, dsum, sizeof(double), cudaMemcpyDeviceToHost, st));
+  LCX_CHECK_CUDA(cudaMemcpyAsync(&hbad, dbad, sizeof(int), cudaMemcpyDeviceToHost, st));
+  LCX_CHECK_CUDA(cudaStreamSynchronize(st));
+  if (hbad) return fail(LCX_ERR_DOMAIN, "recall above 1: sparse lse exceeds full lse");
+  if (aggregate) *aggregate = hsum / double(n);
+  return LCX_OK;
+}
+
+int lcx_lse_merge(lcx_context* ctx, const float* o_parts, const float* lse_parts, int32_t parts,
+                  int64_t rows, int32_t dim, float* out, float* lse_out, void* stream) {
+  (void)ctx;
+  if (parts <= 0) return fail(LCX_ERR_DIMENSION, "merge needs at least one part");
+  return lse_merge_launch(o_parts, lse_parts, parts, rows, dim, out, lse_out, S(stream));
+}
+
+}  // extern "C"

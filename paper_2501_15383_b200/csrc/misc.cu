@@ -1,0 +1,110 @@
+// Small kernels: RoPE table, index bitmaps, recall (part d), LSE merge (part e).
+#include "lcx_internal.cuh"
+
+namespace lcx {
+namespace {
+
+// rope[p][pair] = (cos, sin)(double(p) * theta_pair), theta from the host in fp64
+// (attention.cpp:14-33: angle and trig in fp64; only the result is rounded to fp32).
+__global__ void rope_table_kernel(const double* __restrict__ thetas, int P, int64_t npos,
+                                  float2* __restrict__ out) {
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= npos * P) return;
+  const int64_t pos = idx / P;
+  const int pair = int(idx % P);
+  double sn, cs;
+  sincos(double(pos) * thetas[pair], &sn, &cs);
+  out[idx] = make_float2(float(cs), float(sn));
+}
+
+__global__ void bitmap_kernel(const int32_t* __restrict__ lists, const int32_t* __restrict__ counts,
+                              int64_t cap, int64_t words, uint32_t* __restrict__ bits) {
+  const int h = blockIdx.y;
+  const int cnt = counts[h];
+  for (int x = blockIdx.x * blockDim.x + threadIdx.x; x < cnt; x += gridDim.x * blockDim.x) {
+    const int64_t v = lists[int64_t(h) * cap + x];
+    atomicOr(bits + int64_t(h) * words + (v >> 5), 1u << (v & 31));
+  }
+}
+
+// refine.cpp:51-72: r = exp(lse_s - lse_f); > 1 + slack is an error; clamp to 1.
+__global__ void recall_kernel(const float* __restrict__ ls, const float* __restrict__ lf,
+                              int64_t n, double slack, float* __restrict__ per,
+                              double* __restrict__ sum, int* __restrict__ bad) {
+  double local = 0.0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    double r = exp(double(ls[i]) - double(lf[i]));
+    if (r > 1.0 + slack) atomicExch(bad, 1);
+    r = r > 1.0 ? 1.0 : r;
+    if (per) per[i] = float(r);
+    local += r;
+  }
+  for (int o = 16; o >= 1; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(sum, local);
+}
+
+// out = sum_g exp(lse_g - lse) o_g, lse = logsumexp_g lse_g (empty shards: -inf)
+__global__ void lse_merge_kernel(const float* __restrict__ o_parts,
+                                 const float* __restrict__ lse_parts, int parts, int64_t rows,
+                                 int dim, float* __restrict__ out, float* __restrict__ lse_out) {
+  const int64_t row = blockIdx.x;
+  if (row >= rows) return;
+  float m = -INFINITY;
+  for (int g = 0; g < parts; ++g) m = fmaxf(m, lse_parts[int64_t(g) * rows + row]);
+  float den = 0.f;
+  for (int g = 0; g < parts; ++g) {
+    const float l = lse_parts[int64_t(g) * rows + row];
+    if (l != -INFINITY) den += expf(l - m);
+  }
+  for (int d = threadIdx.x; d < dim; d += blockDim.x) {
+    float acc = 0.f;
+    for (int g = 0; g < parts; ++g) {
+      const float l = lse_parts[int64_t(g) * rows + row];
+      if (l != -INFINITY) acc += expf(l - m) * o_parts[(int64_t(g) * rows + row) * dim + d];
+    }
+    out[row * dim + d] = acc / den;
+  }
+  if (threadIdx.x == 0) lse_out[row] = m + logf(den);
+}
+
+}  // namespace
+
+int build_rope_table(const double* thetas_dev, int P, int64_t npos, float2* out,
+                     cudaStream_t st) {
+  const int64_t total = npos * P;
+  rope_table_kernel<<<unsigned((total + 255) / 256), 256, 0, st>>>(thetas_dev, P, npos, out);
+  LCX_CHECK_LAUNCH();
+  return LCX_OK;
+}
+
+int build_bitmaps(const int32_t* lists, const int32_t* counts, int64_t cap, int heads,
+                  int64_t words, uint32_t* bits, cudaStream_t st) {
+  LCX_CHECK_CUDA(cudaMemsetAsync(bits, 0, sizeof(uint32_t) * size_t(words) * heads, st));
+  dim3 grid(8, unsigned(heads));
+  bitmap_kernel<<<grid, 256, 0, st>>>(lists, counts, cap, words, bits);
+  LCX_CHECK_LAUNCH();
+  return LCX_OK;
+}
+
+int recall_kernel_launch(const float* ls, const float* lf, int64_t n, double slack, float* per,
+                         double* sum_dev, int* bad_dev, cudaStream_t st) {
+  LCX_CHECK_CUDA(cudaMemsetAsync(sum_dev, 0, sizeof(double), st));
+  LCX_CHECK_CUDA(cudaMemsetAsync(bad_dev, 0, sizeof(int), st));
+  const int64_t blocks = std::min<int64_t>(1024, (n + 255) / 256);
+  recall_kernel<<<unsigned(std::max<int64_t>(1, blocks)), 256, 0, st>>>(ls, lf, n, slack, per,
+                                                                        sum_dev, bad_dev);
+  LCX_CHECK_LAUNCH();
+  return LCX_OK;
+}
+
+int lse_merge_launch(const float* o_parts, const float* lse_parts, int parts, int64_t rows,
+                     int dim, float* out, float* lse_out, cudaStream_t st) {
+  if (rows <= 0) return LCX_OK;
+  lse_merge_kernel<<<unsigned(rows), 128, 0, st>>>(o_parts, lse_parts, parts, rows, dim, out,
+                                                   lse_out);
+  LCX_CHECK_LAUNCH();
+  return LCX_OK;
+}
+
+}  // namespace lcx

@@ -1,0 +1,172 @@
+// K2 -- deterministic top-k line selection.
+//
+// Restates top_lines + the forced inclusions of select_critical (reference
+// core/src/sparse.cpp:15-24 and 219-229): the k lines with the largest score,
+// ties broken toward the smaller index (a total order, so the reference's
+// stable_sort and this radix select pick the same set), then the forced prefix
+// [0, prefix_len) (column 0 for forceSink, offsets [0, block) for
+// forceLocalBand), sorted unique.
+//
+// One CTA per (head, line kind): MSB-first 8-bit radix select on the
+// order-preserving uint32 image of the fp32 score finds the k-th largest key T
+// and how many keys equal to T must be taken; a chunked block scan then emits,
+// in ascending index order, every index with key > T and the first `need`
+// indices with key == T.  Output is sorted by construction.
+#include "lcx_internal.cuh"
+
+namespace lcx {
+namespace {
+
+constexpr int kT = 1024;
+
+__device__ __forceinline__ int block_excl_scan(int v, int* warp_sums, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int w = warp_sums[lane];
+    int ws = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, ws, o);
+      if (lane >= o) ws += y;
+    }
+    warp_sums[lane] = ws - w;  // exclusive prefix of warp sums
+    if (lane == 31) *total = ws;
+  }
+  __syncthreads();
+  const int r = warp_sums[wid] + x - v;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kT)
+select_kernel(const float* __restrict__ scores, int64_t n, int64_t k, int64_t prefix_len,
+              int32_t* __restrict__ out, int32_t* __restrict__ count, int64_t cap) {
+  __shared__ int hist[256];
+  __shared__ int warp_sums[32];
+  __shared__ int total;
+  __shared__ uint32_t sh_prefix;
+  __shared__ int64_t sh_remaining;
+  const int h = blockIdx.x;
+  const float* sc = scores + int64_t(h) * n;
+  int32_t* o = out + int64_t(h) * cap;
+  const int tid = threadIdx.x;
+
+  if (k >= n) {  // every line (budget clamps, test_sparse.cpp:123-129)
+    for (int64_t i = tid; i < n; i += kT) o[i] = int32_t(i);
+    if (tid == 0) count[h] = int32_t(n);
+    return;
+  }
+  for (int64_t i = tid; i < prefix_len; i += kT) o[i] = int32_t(i);
+  if (k <= 0) {
+    if (tid == 0) count[h] = int32_t(prefix_len);
+    return;
+  }
+
+  uint32_t prefix = 0, mask = 0;
+  int64_t remaining = k;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int b = tid; b < 256; b += kT) hist[b] = 0;
+    __syncthreads();
+    for (int64_t i = tid; i < n; i += kT) {
+      const uint32_t u = float_to_ordered(sc[i]);
+      if ((u & mask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int64_t cum = 0;
+      int chosen = 0;
+      for (int dgt = 255; dgt >= 0; --dgt) {
+        if (cum + hist[dgt] >= remaining) {
+          chosen = dgt;
+          break;
+        }
+        cum += hist[dgt];
+      }
+      sh_remaining = remaining - cum;
+      sh_prefix = prefix | (uint32_t(chosen) << shift);
+    }
+    __syncthreads();
+    prefix = sh_prefix;
+    remaining = sh_remaining;
+    mask |= 255u << shift;
+    __syncthreads();
+  }
+  const uint32_t T = prefix;
+  const int64_t need_eq = remaining;
+
+  int64_t eq_seen = 0, out_seen = 0;
+  for (int64_t base = 0; base < n; base += kT) {
+    const int64_t i = base + tid;
+    uint32_t u = 0;
+    if (i < n) u = float_to_ordered(sc[i]);
+    const int gt = (i < n) && (u > T);
+    const int eq = (i < n) && (u == T);
+    const int eq_rank = block_excl_scan(eq, warp_sums, &total);
+    const int eq_total = total;
+    const int sel = gt || (eq && (eq_seen + eq_rank) < need_eq);
+    const int emit = sel && (i >= prefix_len);
+    const int pos = block_excl_scan(emit, warp_sums, &total);
+    const int emit_total = total;
+    if (emit) o[prefix_len + out_seen + pos] = int32_t(i);
+    eq_seen += eq_total;
+    out_seen += emit_total;
+  }
+  if (tid == 0) count[h] = int32_t(prefix_len + out_seen);
+}
+
+// col[h][j] = sum_r est[h][r][j]; slash[h][d] = (sum_r est[h][r][gi_r - d]) / cnt
+// (sparse.cpp:198-217), ascending r.
+__global__ void est_line_scores(const float* __restrict__ est, int heads, int64_t block,
+                                int64_t n, int slash_mean, float* __restrict__ col,
+                                float* __restrict__ slash) {
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= int64_t(heads) * n) return;
+  const int h = int(idx / n);
+  const int64_t x = idx % n;
+  const float* e = est + int64_t(h) * block * n;
+  float cs = 0.f, ss = 0.f;
+  int64_t cnt = 0;
+  for (int64_t r = 0; r < block; ++r) {
+    const int64_t gi = n - block + r;
+    if (x <= gi) cs += e[r * n + x];
+    if (x <= gi) {
+      ss += e[r * n + (gi - x)];
+      ++cnt;
+    }
+  }
+  col[idx] = cs;
+  slash[idx] = cnt == 0 ? -INFINITY : (slash_mean ? ss / float(cnt) : ss);
+}
+
+}  // namespace
+
+int select_lines(const float* scores, int heads, int64_t n, int64_t k, int force_prefix,
+                 int64_t prefix_len, int32_t* out, int32_t* count, int64_t cap,
+                 cudaStream_t st) {
+  const int64_t pl = force_prefix ? std::min<int64_t>(prefix_len, n) : 0;
+  if (pl + std::min<int64_t>(k, n) > cap && std::min<int64_t>(k, n) < n)
+    return fail(LCX_ERR_DIMENSION, "selection capacity too small for budget + forced lines");
+  if (k >= n && n > cap) return fail(LCX_ERR_DIMENSION, "selection capacity too small");
+  select_kernel<<<heads, kT, 0, st>>>(scores, n, k, pl, out, count, cap);
+  LCX_CHECK_LAUNCH();
+  return LCX_OK;
+}
+
+int line_scores_from_est(const float* est, int heads, int64_t block, int64_t n, int slash_mean,
+                         float* col, float* slash, cudaStream_t st) {
+  const int64_t total = int64_t(heads) * n;
+  est_line_scores<<<unsigned((total + 255) / 256), 256, 0, st>>>(est, heads, block, n,
+                                                                  slash_mean, col, slash);
+  LCX_CHECK_LAUNCH();
+  return LCX_OK;
+}
+
+}  // namespace lcx

@@ -1,0 +1,380 @@
+"""GPU parity: the sm_100a path (through the C-ABI) vs the CPU oracle on the same inputs.
+
+Tolerances (D1): per row, max_d |o - o_ref| <= tol * max_d |o_ref| and
+|lse - lse_ref| <= tol * max(|lse_ref|, 1), tol = 1e-5 (fp32 storage) / 2e-3 (bf16
+storage); the oracle always receives exactly the values the device stores.
+Index sets must be identical given identical fp32 scores (ties -> lowest index).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from helpers import TOL, lse_rel_err, rounded, row_rel_err
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def L():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2501_15383_b200 import longctx
+    return longctx
+
+
+@pytest.fixture(scope="module")
+def D():
+    from paper_2501_15383_b200 import device
+    return device
+
+
+def rin(port, seed, n, dim, precision):
+    q, k, v = port.random_input(seed, n, dim)
+    return rounded(q, precision), rounded(k, precision), rounded(v, precision)
+
+
+# ----------------------------------------------------------------- estimator --
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("pm,cfg", [(0, None), (1, (32, 96, 32)), (1, (6, 10, 4))])
+@pytest.mark.parametrize("n,dim,nq,lq", [(200, 16, 80, 64), (300, 128, 300, 64),
+                                         (130, 8, 40, 100)])
+def test_estimate_block(L, port, precision, pm, cfg, n, dim, nq, lq):
+    q, k, _ = rin(port, n + dim, n, dim, precision)
+    ref = port.estimate_block(q[n - nq:], k, lq, pm, cfg)
+    mode = L.PositionMode.DcaContinuous if pm else L.PositionMode.Standard
+    got = L.estimate_block(q[n - nq:], k, lq, mode, L.ChunkConfig(*cfg) if cfg else None,
+                           precision=precision)
+    assert got.shape == ref.shape
+    # probabilities: row-relative (fp32 math on both storage types)
+    assert row_rel_err(got, ref) <= 1e-5
+    assert (got[ref == 0.0] == 0.0).all()  # causal zeros are exact
+
+
+@pytest.mark.parametrize("pm,cfg", [(0, None), (1, (64, 192, 64))])
+def test_line_scores_fused(D, port, pm, cfg):
+    import torch
+    n, dim, chunk, lq = 700, 128, 256, 64
+    q, k, _ = rin(port, 5, n, dim, "fp32")
+    est = port.estimate_block(q[n - chunk:], k, lq, pm, cfg)
+    col_ref, sl_ref = port.line_scores(est, n)
+    qt = torch.tensor(q, dtype=torch.float32).cuda().unsqueeze(1).contiguous()
+    kt = torch.tensor(k, dtype=torch.float32).cuda().unsqueeze(1).contiguous()
+    col, sl = D.line_scores(qt, kt, q_row0=n - chunk, nq=chunk, nk=n, last_q=lq,
+                            position_mode="dca_continuous" if pm else "standard", dca=cfg)
+    col, sl = col[0].double().cpu().numpy(), sl[0].double().cpu().numpy()
+    assert np.abs(col - col_ref).max() <= 1e-5 * np.abs(col_ref).max()
+    assert np.abs(sl - sl_ref).max() <= 1e-5 * np.abs(sl_ref).max()
+
+
+# ----------------------------------------------------------------- selection --
+@pytest.mark.parametrize("seed", range(6))
+def test_selection_identical_given_identical_scores(D, port, seed):
+    """The GPU radix select vs the reference ranking (oracle select_from_scores) on the
+    same fp32 scores, with heavy ties."""
+    import torch
+    rng = np.random.default_rng(seed)
+    heads, n = 3, int(rng.integers(100, 5000))
+    levels = int(rng.choice([3, 17, 1000, 1 << 20]))
+    col = (rng.integers(0, levels, (heads, n)) / levels).astype(np.float32)
+    sl = (rng.integers(0, levels, (heads, n)) / levels).astype(np.float32)
+    block = int(rng.integers(1, min(64, n)))
+    bud = (int(rng.integers(0, n // 2)), int(rng.integers(0, n // 2)))
+    for sink, band in [(True, True), (False, False), (True, False)]:
+        opts = D.Options(sink, band, True)
+        v, nv, s, ns = D.select_from_scores(torch.tensor(col).cuda(), torch.tensor(sl).cuda(),
+                                            block=block, budget=bud, opts=opts)
+        for h in range(heads):
+            exp = port.select_from_scores(col[h].astype(np.float64), sl[h].astype(np.float64), n,
+                                          block, bud, sink, band)
+            assert v[h, :int(nv[h])].tolist() == exp.verticals
+            assert s[h, :int(ns[h])].tolist() == exp.slashes
+
+
+def test_select_critical_one_row_trick(L, ref):
+    """Drive the REAL reference select_critical with a 1-row estimate (count 1 => mean =
+    value) built from fp32 scores; the device selection must agree."""
+    rng = np.random.default_rng(7)
+    for n in [50, 777, 4096]:
+        est = rng.random((1, n)).astype(np.float32).astype(np.float64)
+        est[0, rng.integers(0, n, n // 3)] = 0.5  # ties
+        for bud in [(3, 5), (n, 0), (0, n), (n // 2, n // 3)]:
+            exp = ref.select_critical(est, bud, n)
+            got = L.select_critical(est, L.HeadBudget(*bud), n)
+            assert got.verticals == exp.verticals and got.slashes == exp.slashes
+
+
+# ----------------------------------------------------------------- attention --
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_sparse_attention_standard(L, port, precision):
+    n, dim = 512, 128
+    q, k, v = rin(port, 11, n, dim, precision)
+    crit = port.select_critical(port.estimate_block(q, k, 64), (20, 30), n)
+    ref = port.sparse_attention(q, k, v, crit)
+    got = L.sparse_attention(L.AttentionInput(q, k, v), L.CriticalSet(crit.verticals,
+                                                                       crit.slashes, n),
+                             precision=precision)
+    assert row_rel_err(got.output, ref[0]) <= TOL[precision]
+    assert lse_rel_err(got.lse, ref[1]) <= TOL[precision]
+
+
+@pytest.mark.parametrize("cfg", [(64, 128, 64), (32, 80, 32), (6, 10, 4)])
+def test_sparse_attention_dca_override(L, port, cfg):
+    n, dim = 400, 32
+    q, k, v = rin(port, 12, n, dim, "fp32")
+    crit = port.select_critical(port.estimate_block(q, k, 32, 1, cfg), (10, 10), n)
+    ref = port.sparse_attention(q, k, v, crit, dca=cfg, temperature=0.8)
+    got = L.sparse_attention(L.AttentionInput(q, k, v, temperature=0.8),
+                             L.CriticalSet(crit.verticals, crit.slashes, n), L.ChunkConfig(*cfg))
+    assert row_rel_err(got.output, ref[0]) <= 1e-5
+    assert lse_rel_err(got.lse, ref[1]) <= 1e-5
+
+
+def test_sparse_attention_custom_positions(L, port):
+    n, dim = 256, 16
+    q, k, v = rin(port, 13, n, dim, "fp32")
+    rng = np.random.default_rng(0)
+    pq = np.sort(rng.integers(0, 5000, n))
+    pk = np.sort(rng.integers(0, 5000, n))
+    crit = port.select_critical(port.estimate_block(q, k, 16), (8, 8), n)
+    ref = port.sparse_attention(q, k, v, crit, pos_q=pq, pos_k=pk, rope_base=500.0)
+    got = L.sparse_attention(L.AttentionInput(q, k, v, pq, pk, rope_base=500.0),
+                             L.CriticalSet(crit.verticals, crit.slashes, n))
+    assert row_rel_err(got.output, ref[0]) <= 1e-5
+    assert lse_rel_err(got.lse, ref[1]) <= 1e-5
+
+
+@pytest.mark.parametrize("dca", [None, (48, 128, 48)])
+def test_full_attention(L, port, dca):
+    n, dim = 300, 64
+    q, k, v = rin(port, 14, n, dim, "fp32")
+    ref = port.full_attention(q, k, v, dca=dca)
+    got = L.full_attention(L.AttentionInput(q, k, v), L.ChunkConfig(*dca) if dca else None)
+    assert row_rel_err(got.output, ref[0]) <= 1e-5
+    assert lse_rel_err(got.lse, ref[1]) <= 1e-5
+
+
+def test_dca_attention(L, port):
+    n, dim = 260, 32
+    q, k, v = rin(port, 15, n, dim, "fp32")
+    for cfg, sf in [((64, 192, 64), 4.0), ((512, 1024, 256), 1.0)]:
+        ref = port.dca_attention(q, k, v, cfg, sf)
+        got = L.dca_attention(L.AttentionInput(q, k, v), L.ChunkConfig(*cfg),
+                              L.YarnScale.from_scale(sf))
+        assert row_rel_err(got.output, ref[0]) <= 1e-5
+        assert lse_rel_err(got.lse, ref[1]) <= 1e-5
+
+
+def test_full_coverage_equals_dense(L, port):
+    """test_sparse.cpp:131-142."""
+    n, dim = 64, 8
+    q, k, v = rin(port, 5, n, dim, "fp32")
+    inp = L.AttentionInput(q, k, v)
+    sp = L.sparse_attention(inp, L.CriticalSet(list(range(n)), [], n))
+    fu = L.full_attention(inp)
+    assert np.abs(sp.output - fu.output).max() <= 1e-6
+    assert np.abs(sp.lse - fu.lse).max() <= 1e-6
+
+
+def test_self_diagonal_and_fallback_rows(L, port):
+    """test_sparse.cpp:144-170."""
+    q, k, v = rin(port, 6, 16, 8, "fp32")
+    r = L.sparse_attention(L.AttentionInput(q, k, v), L.CriticalSet([], [0], 16))
+    assert np.abs(r.output - v).max() <= 1e-6
+    q, k, v = rin(port, 7, 8, 8, "fp32")
+    r = L.sparse_attention(L.AttentionInput(q, k, v), L.CriticalSet([5], [], 8))
+    assert np.abs(r.output[:5] - v[:5]).max() <= 1e-6
+    r = L.sparse_attention(L.AttentionInput(q, k, v), L.CriticalSet([], [], 8))
+    assert np.abs(r.output - v).max() <= 1e-6
+
+
+# ------------------------------------------------------------ chunked prefill --
+@pytest.mark.parametrize("name", ["sparsity_example.json", "sparsity_dca.json"])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_chunked_prefill_goldens(L, port, name, precision):
+    """The reference's own example configs: identical per-chunk selections, recall and
+    density reproduced, outputs within tolerance of the oracle on the same values."""
+    from test_oracle_pin import planted_from_spec
+    g = json.load(open(os.path.join(GOLD, name)))
+    cfg, spec, exp = g["config"], g["spec"], g["expected"]
+    q, k, v = (rounded(x, precision) for x in planted_from_spec(port, spec))
+    dca = L.ChunkConfig(*cfg["chunk_cfg"]) if cfg["dca_mode"] else None
+    pm = L.PositionMode.DcaContinuous if dca else L.PositionMode.Standard
+    inp = L.AttentionInput(q, k, v, rope_base=spec["rope_base"])
+    pr = L.chunked_prefill(inp, cfg["chunk_len"], cfg["last_q"], L.HeadBudget(*cfg["budget"]),
+                           L.PrefillMode.Sparse, pm, dca, precision=precision)
+    got_sel = [dict(verticals=s.critical.verticals, slashes=s.critical.slashes)
+               for s in pr.state.selections]
+    exp_sel = [dict(verticals=s["critical"]["verticals"], slashes=s["critical"]["slashes"])
+               for s in exp["selections"]]
+    assert got_sel == exp_sel
+    out_ref, lse_ref, _ = port.chunked_prefill(q, k, v, cfg["chunk_len"], cfg["last_q"],
+                                               tuple(cfg["budget"]), "sparse", 1 if dca else 0,
+                                               dca.tuple() if dca else None,
+                                               rope_base=spec["rope_base"])
+    assert row_rel_err(pr.result.output, out_ref) <= TOL[precision]
+    assert lse_rel_err(pr.result.lse, lse_ref) <= TOL[precision]
+    # one-shot recall / density of the golden run, through the device path
+    est = L.estimate_block(q, k, cfg["last_q"], pm, dca, spec["rope_base"], precision)
+    crit = L.select_critical(est, L.HeadBudget(*cfg["budget"]), spec["n"])
+    assert crit.verticals == exp["critical"]["verticals"]
+    assert crit.slashes == exp["critical"]["slashes"]
+    full = L.full_attention(inp, dca, precision)
+    sp = L.sparse_attention(inp, crit, dca, precision)
+    rec = L.attention_recall(sp.lse, full.lse)
+    assert abs(rec.aggregate - exp["recall"]) <= (1e-6 if precision == "fp32" else 2e-3)
+    assert L.density(crit) == exp["density"]
+
+
+def test_chunked_prefill_kat_cases(L, port):
+    g = json.load(open(os.path.join(GOLD, "kat_hashes.json")))
+    for c in g["cases"]:
+        q, k, v = port.random_input(c["seed"], c["n"], c["dim"])
+        q, k, v = (rounded(x, "fp32") for x in (q, k, v))
+        cfg = L.ChunkConfig(*c["cfg"]) if c["cfg"] else None
+        pm = L.PositionMode.DcaContinuous if c["pos_mode"] else L.PositionMode.Standard
+        pr = L.chunked_prefill(L.AttentionInput(q, k, v), c["chunk_len"], c["last_q"],
+                               L.HeadBudget(*c["budget"]), L.PrefillMode.Sparse, pm, cfg)
+        out_ref, lse_ref, sels = port.chunked_prefill(q, k, v, c["chunk_len"], c["last_q"],
+                                                      tuple(c["budget"]), "sparse", c["pos_mode"],
+                                                      c["cfg"] and tuple(c["cfg"]))
+        for a, b in zip(pr.state.selections, sels):
+            assert a.critical.verticals == b.critical.verticals
+            assert a.critical.slashes == b.critical.slashes
+        assert row_rel_err(pr.result.output, out_ref) <= 1e-5
+        assert lse_rel_err(pr.result.lse, lse_ref) <= 1e-5
+
+
+@pytest.mark.parametrize("chunk", [1, 7, 32, 96])
+def test_full_mode_chunked_equals_one_shot(L, port, chunk):
+    """test_sparse.cpp:327-338."""
+    q, k, v = rin(port, 0, 96, 8, "fp32")
+    inp = L.AttentionInput(q, k, v)
+    one = L.full_attention(inp)
+    pr = L.chunked_prefill(inp, chunk, 1, L.HeadBudget(0, 0), L.PrefillMode.Full,
+                           L.PositionMode.Standard, None)
+    assert np.abs(pr.result.output - one.output).max() <= 1e-6
+    assert np.abs(pr.result.lse - one.lse).max() <= 1e-6
+
+
+def test_dca_full_budget_equals_remapped_dense(L, port):
+    """test_sparse.cpp:406-417."""
+    q, k, v = rin(port, 14, 64, 8, "fp32")
+    cfg = L.ChunkConfig(16, 48, 16)
+    inp = L.AttentionInput(q, k, v)
+    pr = L.chunked_prefill(inp, 64, 8, L.HeadBudget(64, 64), L.PrefillMode.Sparse,
+                           L.PositionMode.DcaContinuous, cfg)
+    dense = L.full_attention(inp, cfg)
+    assert row_rel_err(pr.result.output, dense.output) <= 1e-5
+
+
+def test_cross_chunk_slash_found_only_with_continuous_positions(L, port):
+    """test_sparse.cpp:373-404 through the device path."""
+    cfg = (32, 128, 32)
+    q, k, v = port.make_planted(512, 16, rope_base=1000.0, slash_offsets=[428], strength=12.0,
+                                seed=7, dca=cfg, carrier_pairs=[5, 6])
+    q, k, v = (rounded(x, "fp32") for x in (q, k, v))
+    inp = L.AttentionInput(q, k, v, rope_base=1000.0)
+    cont = L.chunked_prefill(inp, 256, 64, L.HeadBudget(0, 2), L.PrefillMode.Sparse,
+                             L.PositionMode.DcaContinuous, L.ChunkConfig(*cfg))
+    assert 428 in cont.state.selections[1].critical.slashes
+    std = L.chunked_prefill(inp, 256, 64, L.HeadBudget(0, 2), L.PrefillMode.Sparse,
+                            L.PositionMode.Standard, None)
+    assert 428 not in std.state.selections[1].critical.slashes
+
+
+def test_validation_errors(L, port):
+    q, k, v = rin(port, 13, 16, 8, "fp32")
+    inp = L.AttentionInput(q, k, v)
+    for args, kind in [((0, 1, L.HeadBudget(1, 1), L.PrefillMode.Full, L.PositionMode.Standard,
+                         None), "config"),
+                       ((8, 0, L.HeadBudget(1, 1), L.PrefillMode.Full, L.PositionMode.Standard,
+                         None), "config"),
+                       ((4, 8, L.HeadBudget(1, 1), L.PrefillMode.Sparse,
+                         L.PositionMode.Standard, None), "config"),
+                       ((8, 4, L.HeadBudget(1, 1), L.PrefillMode.Sparse,
+                         L.PositionMode.DcaContinuous, None), "config")]:
+        with pytest.raises(L.Error) as e:
+            L.chunked_prefill(inp, *args)
+        assert e.value.kind == kind
+    with pytest.raises(L.Error) as e:
+        L.estimate_block(q, k, 0, L.PositionMode.Standard, None)
+    assert e.value.kind == "config"
+
+
+# -------------------------------------------------------------------- recall --
+def test_attention_recall(L, port):
+    rng = np.random.default_rng(3)
+    lf = rng.normal(size=1000)
+    ls = lf - np.abs(rng.normal(size=1000))
+    per_ref, agg_ref = port.attention_recall(ls, lf)
+    rep = L.attention_recall(ls, lf)
+    assert np.abs(rep.per_query - per_ref).max() <= 1e-6
+    assert abs(rep.aggregate - agg_ref) <= 1e-6
+    with pytest.raises(L.Error) as e:
+        L.attention_recall(lf + 0.1, lf)
+    assert e.value.kind == "domain"
+    # hand values (test_refine.cpp:31-62)
+    assert abs(L.attention_recall([np.log(0.5)], [0.0]).aggregate - 0.5) < 1e-7
+
+
+def test_measure_budget_recall(L, ref):
+    q, k, v = ref.make_planted(128, 16, vertical_columns=[20, 70], slash_offsets=[9],
+                               strength=12.0, seed=3)
+    q, k, v = (rounded(x, "fp32") for x in (q, k, v))
+    exp = ref.lib  # noqa: F841 (reference value below)
+    import ctypes as C
+    from oracle import _pd
+    val = C.c_double()
+    qq, kk, vv = (np.ascontiguousarray(x) for x in (q, k, v))
+    st = ref.lib.ref_measure_budget_recall(_pd(qq), _pd(kk), _pd(vv), C.c_int64(128),
+                                           C.c_int64(16), C.c_double(1e4), C.c_int64(2),
+                                           C.c_int64(2), C.c_int64(32), 1, 1, 1, 0,
+                                           C.c_double(0.9), C.byref(val))
+    assert st == 0
+    got = L.measure_budget_recall(L.AttentionInput(q, k, v), L.HeadBudget(2, 2),
+                                  L.RecallMeasurement(last_q=32))
+    assert abs(got - val.value) <= 1e-5
+
+
+# ---------------------------------------------------------- multi-head batch --
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_multihead_gqa_prefill(D, port, precision):
+    """Batched [n, H, D] entry with GQA (hq=7*hkv): every head equals the single-head
+    oracle run on its (q head, kv head) pair."""
+    import torch
+    n, hq, hkv, dim = 640, 14, 2, 128
+    rng = np.random.default_rng(1)
+    q = rounded(rng.standard_normal((n, hq, dim)), precision)
+    k = rounded(rng.standard_normal((n, hkv, dim)), precision)
+    v = rounded(rng.standard_normal((n, hkv, dim)), precision)
+    dt = torch.float32 if precision == "fp32" else torch.bfloat16
+    T = lambda x: torch.tensor(x).to(dt).cuda().contiguous()  # noqa: E731
+    r = D.chunked_prefill(T(q), T(k), T(v), chunk_len=256, last_q=64, budget=(30, 40),
+                          position_mode="dca_continuous", dca=(128, 384, 128), temperature=0.9,
+                          return_admitted=True)
+    out, lse = r["out"].double().cpu().numpy(), r["lse"].double().cpu().numpy()
+    for h in [0, 6, 7, 13]:
+        g = h // 7
+        o_ref, l_ref, sels = port.chunked_prefill(q[:, h], k[:, g], v[:, g], 256, 64, (30, 40),
+                                                  "sparse", 1, (128, 384, 128),
+                                                  temperature=0.9)
+        for ci, s in enumerate(sels):
+            nv, ns = int(r["nv"][ci, h]), int(r["ns"][ci, h])
+            assert r["verticals"][ci, h, :nv].tolist() == s.critical.verticals
+            assert r["slashes"][ci, h, :ns].tolist() == s.critical.slashes
+            t0, t1 = s.begin, s.end
+            cnt = sum(len(_adm(s.critical, i)) for i in range(t0, t1))
+            assert int(r["admitted"][ci, h]) == cnt
+        assert row_rel_err(out[:, h], o_ref) <= TOL[precision]
+        assert lse_rel_err(lse[h], l_ref) <= TOL[precision]
+
+
+def _adm(crit, i):
+    vs = [x for x in crit.verticals if x <= i]
+    ss = [i - d for d in crit.slashes if d <= i]
+    row = set(vs) | set(ss)
+    return row if row else {i}
