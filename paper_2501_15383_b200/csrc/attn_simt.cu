@@ -153,21 +153,22 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(AttnArgs a) {
         if (verts[mid] <= i) lo = mid + 1;
         else hi = mid;
       }
-      entries += lo;
+      (void)lo;
     }
     if (a.segs) {
       // tcgen05 mode: only the slash entries routed to the CUDA-core path
       const int4* sg = a.segs + int64_t(h) * a.cap_seg;
       const int nseg = a.nseg[h];
-      const int64_t r = i - (i / 128) * 128;  // row within its 128-row block
+      const int64_t r = i & 127;  // row within its 128-row block
       for (int x = 0; x < nseg; ++x) {
-        const int4 e = sg[x];                  // (d, r0, r1, -)
-        if (r < e.y || r >= e.z) continue;
+        const int4 e = sg[x];     // (d, r0, r1, -), ascending d
         const int64_t d = e.x;
-        if (d > i) continue;
+        if (d > i) break;
+        if (r < e.y || r >= e.z) continue;
         const int64_t j = i - d;
         if (is_vertical(vb, j)) continue;
         process_entry<T, PPL>(a, s, i, j, pq_i, g, lane4, qmask);
+        ++entries;
       }
     } else {
       for (int x = 0; x < ns; ++x) {
@@ -183,6 +184,8 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(AttnArgs a) {
       process_entry<T, PPL>(a, s, i, i, pq_i, g, lane4, qmask);
       entries = 1;
     }
+    // tcgen05 mode: nothing on this path for the row -> the tile result stands
+    if (a.segs && entries == 0) return;
   }
 
   const float inv_l = 1.f / s.l;
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(AttnArgs a) {
   }
   if (lane4 == 0) {
     a.lse[int64_t(h) * a.lse_stride + i] = s.m + logf(s.l);
-    if (a.admitted && !a.segs) atomicAdd(reinterpret_cast<unsigned long long*>(a.admitted + h),
+    if (a.admitted) atomicAdd(reinterpret_cast<unsigned long long*>(a.admitted + h),
                                          (unsigned long long)entries);
   }
 }

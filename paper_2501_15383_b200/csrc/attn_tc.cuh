@@ -1,0 +1,74 @@
+// Host-visible declarations of the tensor-core attention path (attn_tc.cu).
+#pragma once
+
+#include <cuda.h>
+
+#include "lcx_internal.cuh"
+
+namespace lcx {
+
+struct TcParams {
+  const __nv_bfloat16* q;
+  int hq, hkv, group;
+  int64_t n;           // keys visible
+  int64_t t1;          // chunk end (row bound)
+  int64_t block0;      // first 128-row block index
+  int nblocks;
+  int nitems;
+  int rel_mode;        // 0 standard, 1 dca
+  int64_t s, c;
+  const int64_t* pos_q;
+  const float2* rope;
+  float scale_log2;
+  int dense;
+  const int32_t* verts; const int32_t* nv; int64_t cap_v;
+  // compacted verticals: per DCA key chunk m a 64-aligned segment starting at vbase[h][m]
+  const int32_t* ckeys; const int32_t* vbase; const int32_t* vfirst; int64_t capp; int nseg_k;
+  int64_t seg_len;     // key-chunk length used for the segments (s, or >= n when standard)
+  const int32_t* tc_u; const int32_t* n_tc_u; int64_t cap_u;
+  const uint32_t* sbits; const uint32_t* vbits; int64_t words;
+  float* out; float* lse; int64_t lse_stride;
+  int64_t* tile_count;  // optional: executed tiles (atomicAdd)
+};
+
+struct TcBuffers {
+  __nv_bfloat16 *khi = nullptr, *klo = nullptr, *kchi = nullptr, *kclo = nullptr;
+  __half *vt = nullptr, *vct = nullptr;
+  int32_t *ckeys = nullptr, *vbase = nullptr, *vfirst = nullptr;
+  int64_t npad = 0, capp = 0, seg_len = 0;
+  int nseg_k = 0;
+  CUtensorMap m_khi, m_klo, m_vt, m_kchi, m_kclo, m_vct;
+};
+
+// layout of the tensor-core buffers (Arena or Sizer)
+template <class A>
+void tc_layout(A& ar, int64_t n, int hq, int hkv, int64_t cap_v, int64_t seg_len, TcBuffers& B) {
+  B.npad = (n + 63) / 64 * 64;
+  B.seg_len = seg_len;
+  B.nseg_k = int((n + seg_len - 1) / seg_len);
+  B.capp = (cap_v + 63) / 64 * 64 + 64 * (B.nseg_k + 1);
+  const int64_t capp = B.capp;
+  B.ckeys = ar.template take<int32_t>(size_t(hq) * capp);
+  B.vbase = ar.template take<int32_t>(size_t(hq) * (B.nseg_k + 1));
+  B.vfirst = ar.template take<int32_t>(size_t(hq) * (B.nseg_k + 1));
+  B.khi = ar.template take<__nv_bfloat16>(size_t(n) * hkv * 128);
+  B.klo = ar.template take<__nv_bfloat16>(size_t(n) * hkv * 128);
+  B.vt = ar.template take<__half>(size_t(hkv) * 128 * B.npad);
+  B.kchi = ar.template take<__nv_bfloat16>(size_t(hq) * capp * 128);
+  B.kclo = ar.template take<__nv_bfloat16>(size_t(hq) * capp * 128);
+  B.vct = ar.template take<__half>(size_t(hq) * 128 * capp);
+}
+
+int tc_prepare(const void* k, const void* v, int64_t n, int hq, int hkv, const int64_t* pos_k,
+               int rel_mode, int64_t s, const float2* rope, TcBuffers& B, cudaStream_t st);
+int tc_compact(const void* v, int hq, int hkv, const int32_t* verts, const int32_t* nv,
+               int64_t cap_v, TcBuffers& B, cudaStream_t st);
+int tc_classify(const int32_t* slashes, const int32_t* ns, int64_t cap_s, int hq, int64_t U,
+                int min_entries, int32_t* hist_ws, int32_t* tc_u, int32_t* n_tc_u, int64_t cap_u,
+                int4* segs, int32_t* nseg, int64_t cap_seg, cudaStream_t st);
+int tc_attention(const TcParams& p, const TcBuffers& B, int sm_count, cudaStream_t st);
+int admitted_counts(const int32_t* verts, const int32_t* nv, int64_t cap_v,
+                    const int32_t* slashes, const int32_t* ns, int64_t cap_s, int hq,
+                    int64_t t0, int64_t t1, int64_t* out, cudaStream_t st);
+
+}  // namespace lcx

@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "attn_tc.cuh"
 #include "lcx_internal.cuh"
 
 namespace lcx {
@@ -57,6 +58,19 @@ int ensure_rope(lcx_context* ctx, double base, int dim, int64_t P, cudaStream_t 
 }
 
 namespace {
+
+constexpr int kDefaultTcMin = 96;  // slash entries per 64-key tile to use tcgen05
+
+__global__ void dense_count_kernel(int hq, int64_t t0, int64_t t1, int64_t* out) {
+  const int h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h < hq) out[h] = (t1 * (t1 + 1) - t0 * (t0 + 1)) / 2;  // sum_{i=t0}^{t1-1} (i + 1)
+}
+
+int dense_counts(int hq, int64_t t0, int64_t t1, int64_t* out, cudaStream_t st) {
+  dense_count_kernel<<<(hq + 127) / 128, 128, 0, st>>>(hq, t0, t1, out);
+  LCX_CHECK_LAUNCH();
+  return LCX_OK;
+}
 
 __global__ void max_pos_kernel(const int64_t* a, const int64_t* b, int64_t n,
                                unsigned long long* out, int* neg) {
@@ -162,6 +176,177 @@ EstimateArgs base_est(const lcx_attention_input* in, lcx_context* ctx, int64_t q
   return e;
 }
 
+
+// ---------------------------------------------------------------------------
+// Attention stage shared by sparse_attention / full_attention / chunked_prefill.
+// Path: tcgen05 tiles (+ CUDA-core gather for isolated slashes) when the input is
+// bf16 with dim 128, the chunk boundaries are 128-aligned and DCA chunks are
+// multiples of 128; otherwise the exact CUDA-core path for every entry.
+struct AttnWS {
+  bool tc = false;
+  int64_t words = 0, U = 0, cap_u = 0, cap_seg = 0;
+  uint32_t* vbits = nullptr;
+  uint32_t* sbits = nullptr;
+  int32_t* hist = nullptr;
+  int32_t* tc_u = nullptr;
+  int32_t* n_tc_u = nullptr;
+  int4* segs = nullptr;
+  int32_t* nseg = nullptr;
+  TcBuffers B;
+};
+
+template <class A>
+void attn_layout(A& ar, const lcx_attention_input* in, bool tc, bool sparse, int64_t cap_v,
+                 int64_t cap_s, int64_t seg_len, AttnWS& w) {
+  w.tc = tc;
+  w.words = (in->n + 31) / 32 + 4;
+  if (sparse) {
+    w.vbits = ar.template take<uint32_t>(size_t(in->hq) * w.words);
+    if (tc) {
+      w.sbits = ar.template take<uint32_t>(size_t(in->hq) * w.words);
+      w.U = in->n / 64 + 4;
+      w.cap_u = w.U;
+      w.cap_seg = 2 * cap_s;
+      w.hist = ar.template take<int32_t>(size_t(in->hq) * w.U);
+      w.tc_u = ar.template take<int32_t>(size_t(in->hq) * w.cap_u);
+      w.n_tc_u = ar.template take<int32_t>(size_t(in->hq));
+      w.segs = ar.template take<int4>(size_t(in->hq) * w.cap_seg);
+      w.nseg = ar.template take<int32_t>(size_t(in->hq));
+    }
+  }
+  if (tc) tc_layout(ar, in->n, in->hq, in->hkv, sparse ? cap_v : 0, seg_len, w.B);
+}
+
+bool tc_eligible(const lcx_attention_input* in, int64_t chunk_len, bool dca, int64_t s) {
+  if (in->dtype != LCX_BF16 || in->dim != 128) return false;
+  if (chunk_len % 128 != 0) return false;
+  if (dca && s % 128 != 0) return false;
+  if (in->n >= (int64_t(1) << 31)) return false;
+  return true;
+}
+
+int resolve_path(int32_t kernel_path, const lcx_attention_input* in, int64_t chunk_len, bool dca,
+                 int64_t s, bool* tc) {
+  const bool ok = tc_eligible(in, chunk_len, dca, s);
+  if (kernel_path == LCX_PATH_TC && !ok)
+    return fail(LCX_ERR_CONFIG,
+                "tcgen05 path needs bf16 q/k/v, head dim 128, 128-aligned chunks and DCA "
+                "chunk size");
+  *tc = (kernel_path == LCX_PATH_AUTO || kernel_path == LCX_PATH_TC) && ok;
+  return LCX_OK;
+}
+
+// rows [t0, t1) over keys [0, t1) with the given per-head lists (sparse) or dense.
+int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, int64_t t0,
+                    int64_t t1, bool sparse, const int32_t* verts, const int32_t* nv,
+                    int64_t cap_v, const int32_t* slashes, const int32_t* ns, int64_t cap_s,
+                    bool dca, int64_t s, int64_t c, int tc_min_entries, float* out, float* lse,
+                    int64_t lse_stride, int64_t* admitted, cudaStream_t st) {
+  const int hq = in->hq;
+  if (sparse) LCX_TRY(build_bitmaps(verts, nv, cap_v, hq, w.words, w.vbits, st));
+  if (!w.tc) {
+    AttnArgs a = base_attn(in, ctx);
+    a.n = t1;
+    a.row_begin = t0;
+    a.row_end = t1;
+    a.rel_mode = dca ? 1 : 0;
+    a.s = dca ? s : 1;
+    a.c = dca ? c : 1;
+    a.dense = sparse ? 0 : 1;
+    a.verts = verts;
+    a.nv = nv;
+    a.cap_v = cap_v;
+    a.slashes = slashes;
+    a.ns = ns;
+    a.cap_s = cap_s;
+    a.vbits = w.vbits;
+    a.bit_words = w.words;
+    a.out = out;
+    a.lse = lse;
+    a.lse_stride = lse_stride;
+    a.admitted = admitted;
+    return attention_simt(a, st);
+  }
+  if (sparse) {
+    LCX_TRY(build_bitmaps(slashes, ns, cap_s, hq, w.words, w.sbits, st));
+    LCX_TRY(tc_compact(in->v, hq, in->hkv, verts, nv, cap_v, w.B, st));
+    const int64_t U = t1 / 64 + 4;
+    LCX_TRY(tc_classify(slashes, ns, cap_s, hq, std::min(U, w.U), tc_min_entries, w.hist,
+                        w.tc_u, w.n_tc_u, w.cap_u, w.segs, w.nseg, w.cap_seg, st));
+  }
+  TcParams p{};
+  p.q = reinterpret_cast<const __nv_bfloat16*>(in->q);
+  p.hq = hq;
+  p.hkv = in->hkv;
+  p.group = hq / in->hkv;
+  p.n = t1;
+  p.t1 = t1;
+  p.block0 = t0 / 128;
+  p.nblocks = int((t1 - t0 + 127) / 128);
+  p.nitems = p.nblocks * hq;
+  p.rel_mode = dca ? 1 : 0;
+  p.s = dca ? s : 1;
+  p.c = dca ? c : 1;
+  p.pos_q = in->positions_q;
+  p.rope = ctx->rope;
+  p.scale_log2 = float(1.4426950408889634 / (in->temperature * std::sqrt(double(in->dim))));
+  p.dense = sparse ? 0 : 1;
+  p.verts = sparse ? verts : nullptr;
+  p.nv = nv;
+  p.cap_v = cap_v;
+  p.ckeys = w.B.ckeys;
+  p.vbase = w.B.vbase;
+  p.vfirst = w.B.vfirst;
+  p.capp = w.B.capp;
+  p.nseg_k = w.B.nseg_k;
+  p.seg_len = w.B.seg_len;
+  p.tc_u = sparse ? w.tc_u : nullptr;
+  p.n_tc_u = w.n_tc_u;
+  p.cap_u = w.cap_u;
+  p.sbits = w.sbits;
+  p.vbits = w.vbits;
+  p.words = w.words;
+  p.out = out;
+  p.lse = lse;
+  p.lse_stride = lse_stride;
+  p.tile_count = ctx->tile_counter;
+  LCX_TRY(tc_attention(p, w.B, ctx->sm_count, st));
+  if (sparse) {
+    // isolated slashes + self-fallback rows on the CUDA-core path, merged in place
+    AttnArgs a = base_attn(in, ctx);
+    a.n = t1;
+    a.row_begin = t0;
+    a.row_end = t1;
+    a.rel_mode = dca ? 1 : 0;
+    a.s = dca ? s : 1;
+    a.c = dca ? c : 1;
+    a.verts = verts;
+    a.nv = nv;
+    a.cap_v = cap_v;
+    a.slashes = slashes;
+    a.ns = ns;
+    a.cap_s = cap_s;
+    a.vbits = w.vbits;
+    a.bit_words = w.words;
+    a.skip_verticals = 1;
+    a.segs = w.segs;
+    a.nseg = w.nseg;
+    a.cap_seg = w.cap_seg;
+    a.o_part = out;
+    a.lse_part = lse;
+    a.out = out;
+    a.lse = lse;
+    a.lse_stride = lse_stride;
+    LCX_TRY(attention_simt(a, st));
+    if (admitted)
+      LCX_TRY(admitted_counts(verts, nv, cap_v, slashes, ns, cap_s, hq, t0, t1, admitted, st));
+  } else if (admitted) {
+    // dense rows: entries = i + 1
+    LCX_TRY(dense_counts(hq, t0, t1, admitted, st));
+  }
+  return LCX_OK;
+}
+
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int64_t words_for(int64_t n) { return (n + 31) / 32 + 1; }
@@ -195,6 +380,8 @@ int lcx_context_create(int device, lcx_context** out) {
   auto* ctx = new lcx_context();
   ctx->device = device;
   ctx->sm_count = prop.multiProcessorCount;
+  LCX_CHECK_CUDA(cudaMalloc(&ctx->tile_counter, sizeof(int64_t)));
+  LCX_CHECK_CUDA(cudaMemset(ctx->tile_counter, 0, sizeof(int64_t)));
   *out = ctx;
   return LCX_OK;
 }
@@ -204,6 +391,7 @@ int lcx_context_destroy(lcx_context* ctx) {
   cudaDeviceSynchronize();
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->rope) cudaFree(ctx->rope);
+  if (ctx->tile_counter) cudaFree(ctx->tile_counter);
   delete ctx;
   return LCX_OK;
 }
@@ -311,38 +499,27 @@ int lcx_sparse_attention(lcx_context* ctx, const lcx_attention_input* in,
                          float* out, float* lse, void* stream) {
   LCX_TRY(validate_input(in));
   if (use_dca) LCX_TRY(validate_chunk(dca));
-  (void)kernel_path;
   cudaStream_t st = S(stream);
+  bool tc = false;
+  const int64_t n = in->n;
+  LCX_TRY(resolve_path(kernel_path, in, (n + 127) / 128 * 128, use_dca != 0,
+                       use_dca ? dca->chunk_size : 128, &tc));
   int64_t maxpos = 0;
   LCX_TRY(max_position(ctx, in, &maxpos, st));
   const int64_t P = std::max<int64_t>(maxpos + 1, use_dca ? dca->train_len : 0);
-  LCX_TRY(ensure_rope(ctx, in->rope_base, in->dim, std::max<int64_t>(P, in->n), st));
-  const int64_t words = words_for(in->n);
+  LCX_TRY(ensure_rope(ctx, in->rope_base, in->dim, std::max<int64_t>(P, n), st));
+  AttnWS w;
   Sizer sz;
-  sz.take<uint32_t>(size_t(words) * in->hq);
+  attn_layout(sz, in, tc, true, cap_v, cap_s, use_dca ? dca->chunk_size : n, w);
   LCX_TRY(ensure_workspace(ctx, sz.off));
   Arena ar{ctx->ws, ctx->ws_bytes, 0};
-  uint32_t* vbits = ar.take<uint32_t>(size_t(words) * in->hq);
-  LCX_TRY(build_bitmaps(verticals, nv, cap_v, in->hq, words, vbits, st));
-  AttnArgs a = base_attn(in, ctx);
-  a.n = in->n;
-  a.row_begin = 0;
-  a.row_end = in->n;
-  a.rel_mode = use_dca ? 1 : 0;
-  a.s = use_dca ? dca->chunk_size : 1;
-  a.c = use_dca ? dca->train_len : 1;
-  a.verts = verticals;
-  a.nv = nv;
-  a.cap_v = cap_v;
-  a.slashes = slashes;
-  a.ns = ns;
-  a.cap_s = cap_s;
-  a.vbits = vbits;
-  a.bit_words = words;
-  a.out = out;
-  a.lse = lse;
-  a.lse_stride = in->n;
-  return attention_simt(a, st);
+  attn_layout(ar, in, tc, true, cap_v, cap_s, use_dca ? dca->chunk_size : n, w);
+  if (tc)
+    LCX_TRY(tc_prepare(in->k, in->v, n, in->hq, in->hkv, in->positions_k, use_dca ? 1 : 0,
+                       use_dca ? dca->chunk_size : 1, ctx->rope, w.B, st));
+  return attention_chunk(ctx, in, w, 0, n, true, verticals, nv, cap_v, slashes, ns, cap_s,
+                         use_dca != 0, use_dca ? dca->chunk_size : 1,
+                         use_dca ? dca->train_len : 1, kDefaultTcMin, out, lse, n, nullptr, st);
 }
 
 int lcx_full_attention(lcx_context* ctx, const lcx_attention_input* in, int32_t use_dca,
@@ -350,24 +527,27 @@ int lcx_full_attention(lcx_context* ctx, const lcx_attention_input* in, int32_t 
                        void* stream) {
   LCX_TRY(validate_input(in));
   if (use_dca) LCX_TRY(validate_chunk(dca));
-  (void)kernel_path;
   cudaStream_t st = S(stream);
+  bool tc = false;
+  const int64_t n = in->n;
+  LCX_TRY(resolve_path(kernel_path, in, (n + 127) / 128 * 128, use_dca != 0,
+                       use_dca ? dca->chunk_size : 128, &tc));
   int64_t maxpos = 0;
   LCX_TRY(max_position(ctx, in, &maxpos, st));
   const int64_t P = std::max<int64_t>(maxpos + 1, use_dca ? dca->train_len : 0);
-  LCX_TRY(ensure_rope(ctx, in->rope_base, in->dim, std::max<int64_t>(P, in->n), st));
-  AttnArgs a = base_attn(in, ctx);
-  a.n = in->n;
-  a.row_begin = 0;
-  a.row_end = in->n;
-  a.rel_mode = use_dca ? 1 : 0;
-  a.s = use_dca ? dca->chunk_size : 1;
-  a.c = use_dca ? dca->train_len : 1;
-  a.dense = 1;
-  a.out = out;
-  a.lse = lse;
-  a.lse_stride = in->n;
-  return attention_simt(a, st);
+  LCX_TRY(ensure_rope(ctx, in->rope_base, in->dim, std::max<int64_t>(P, n), st));
+  AttnWS w;
+  Sizer sz;
+  attn_layout(sz, in, tc, false, 0, 0, use_dca ? dca->chunk_size : n, w);
+  LCX_TRY(ensure_workspace(ctx, sz.off));
+  Arena ar{ctx->ws, ctx->ws_bytes, 0};
+  attn_layout(ar, in, tc, false, 0, 0, use_dca ? dca->chunk_size : n, w);
+  if (tc)
+    LCX_TRY(tc_prepare(in->k, in->v, n, in->hq, in->hkv, in->positions_k, use_dca ? 1 : 0,
+                       use_dca ? dca->chunk_size : 1, ctx->rope, w.B, st));
+  return attention_chunk(ctx, in, w, 0, n, false, nullptr, nullptr, 0, nullptr, nullptr, 0,
+                         use_dca != 0, use_dca ? dca->chunk_size : 1,
+                         use_dca ? dca->train_len : 1, kDefaultTcMin, out, lse, n, nullptr, st);
 }
 
 int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
@@ -389,7 +569,10 @@ int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
   const int hq = in->hq;
   const int64_t L = cfg->chunk_len;
   const int64_t nchunks = (n + L - 1) / L;
+  const int64_t s = dca ? cfg->dca.chunk_size : 1;
   const int64_t c = dca ? cfg->dca.train_len : 0;
+  bool tc = false;
+  LCX_TRY(resolve_path(cfg->kernel_path, in, L, dca, s, &tc));
   int64_t maxpos = 0;
   LCX_TRY(max_position(ctx, in, &maxpos, st));
   LCX_TRY(ensure_rope(ctx, in->rope_base, in->dim,
@@ -401,57 +584,53 @@ int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
   if (sparse && (cap_v < std::min<int64_t>(cfg->budget_vertical, n) + 1 ||
                  cap_s < std::min<int64_t>(cfg->budget_slash, n) + block_max))
     return fail(LCX_ERR_DIMENSION, "selection capacity below budget + forced lines");
-  const int64_t words = words_for(n);
+  const int tc_min = cfg->tc_min_entries > 0 ? cfg->tc_min_entries : kDefaultTcMin;
 
   // workspace plan (largest chunk = the last one: nk = n)
   EstimateArgs e_max = base_est(in, ctx, n - std::min(L, n), std::min(L, n), n, cfg->last_q,
                                 dca ? 1 : 0, c);
   e_max.col = reinterpret_cast<float*>(1);
   e_max.slash = reinterpret_cast<float*>(1);
-  Sizer sz;
-  if (sparse) {
-    estimate_simt_size(e_max, sz, ctx->sm_count);
-    sz.take<float>(size_t(hq) * n);
-    sz.take<float>(size_t(hq) * n);
-    if (!out->sel_verticals) {
-      sz.take<int32_t>(size_t(hq) * cap_v);
-      sz.take<int32_t>(size_t(hq));
+  auto layout = [&](auto& A, AttnWS& w, float** col, float** sl, int32_t** iv, int32_t** inv,
+                    int32_t** is, int32_t** ins, size_t* est_off) {
+    *est_off = A.off;
+    if (sparse) {
+      Sizer es;
+      estimate_simt_size(e_max, es, ctx->sm_count);
+      A.off += es.off;
+      *col = A.template take<float>(size_t(hq) * n);
+      *sl = A.template take<float>(size_t(hq) * n);
+      if (!out->sel_verticals) {
+        *iv = A.template take<int32_t>(size_t(hq) * cap_v);
+        *inv = A.template take<int32_t>(size_t(hq));
+      }
+      if (!out->sel_slashes) {
+        *is = A.template take<int32_t>(size_t(hq) * cap_s);
+        *ins = A.template take<int32_t>(size_t(hq));
+      }
     }
-    if (!out->sel_slashes) {
-      sz.take<int32_t>(size_t(hq) * cap_s);
-      sz.take<int32_t>(size_t(hq));
-    }
-    sz.take<uint32_t>(size_t(hq) * words);
+    attn_layout(A, in, tc, sparse, cap_v, cap_s, dca ? s : n, w);
+  };
+  float *col = nullptr, *sl = nullptr;
+  int32_t *iv = nullptr, *inv = nullptr, *is = nullptr, *ins = nullptr;
+  size_t est_off = 0;
+  AttnWS w;
+  {
+    Sizer sz;
+    layout(sz, w, &col, &sl, &iv, &inv, &is, &ins, &est_off);
+    LCX_TRY(ensure_workspace(ctx, sz.off));
   }
-  LCX_TRY(ensure_workspace(ctx, sz.off));
   Arena ar{ctx->ws, ctx->ws_bytes, 0};
-  Arena est_ar = ar;  // estimator scratch is reused per chunk
-  if (sparse) {
-    Sizer es;
-    estimate_simt_size(e_max, es, ctx->sm_count);
-    ar.off += es.off;
-  }
-  float* col = sparse ? ar.take<float>(size_t(hq) * n) : nullptr;
-  float* sl = sparse ? ar.take<float>(size_t(hq) * n) : nullptr;
-  int32_t* iv = nullptr;
-  int32_t* inv = nullptr;
-  int32_t* is = nullptr;
-  int32_t* ins = nullptr;
-  if (sparse && !out->sel_verticals) {
-    iv = ar.take<int32_t>(size_t(hq) * cap_v);
-    inv = ar.take<int32_t>(size_t(hq));
-  }
-  if (sparse && !out->sel_slashes) {
-    is = ar.take<int32_t>(size_t(hq) * cap_s);
-    ins = ar.take<int32_t>(size_t(hq));
-  }
-  uint32_t* vbits = sparse ? ar.take<uint32_t>(size_t(hq) * words) : nullptr;
-  if (out->admitted)
-    LCX_CHECK_CUDA(cudaMemsetAsync(out->admitted, 0, sizeof(int64_t) * nchunks * hq, st));
+  layout(ar, w, &col, &sl, &iv, &inv, &is, &ins, &est_off);
+  Arena est_ar{ctx->ws, ctx->ws_bytes, est_off};
+  if (tc)
+    LCX_TRY(tc_prepare(in->k, in->v, n, hq, in->hkv, in->positions_k, dca ? 1 : 0, s, ctx->rope,
+                       w.B, st));
+  if (ctx->tile_counter) LCX_CHECK_CUDA(cudaMemsetAsync(ctx->tile_counter, 0, 8, st));
 
   cudaEvent_t ev[5];
   const bool prof = ctx->profiling != 0;
-  double ms_est = 0, ms_sel = 0, ms_idx = 0, ms_att = 0;
+  double ms_est = 0, ms_sel = 0, ms_att = 0;
   if (prof)
     for (auto& x : ev) LCX_CHECK_CUDA(cudaEventCreate(&x));
 
@@ -476,33 +655,13 @@ int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
       LCX_TRY(select_lines(sl, hq, t1, cfg->budget_slash, cfg->opts.force_local_band, block,
                            slist, scnt, cap_s, st));
       if (prof) LCX_CHECK_CUDA(cudaEventRecord(ev[2], st));
-      LCX_TRY(build_bitmaps(vlist, vcnt, cap_v, hq, words, vbits, st));
-      if (prof) LCX_CHECK_CUDA(cudaEventRecord(ev[3], st));
     }
-    AttnArgs a = base_attn(in, ctx);
-    a.n = t1;
-    a.row_begin = t0;
-    a.row_end = t1;
-    a.rel_mode = dca ? 1 : 0;
-    a.s = dca ? cfg->dca.chunk_size : 1;
-    a.c = dca ? cfg->dca.train_len : 1;
-    a.dense = sparse ? 0 : 1;
-    a.verts = vlist;
-    a.nv = vcnt;
-    a.cap_v = cap_v;
-    a.slashes = slist;
-    a.ns = scnt;
-    a.cap_s = cap_s;
-    a.vbits = vbits;
-    a.bit_words = words;
-    a.out = out->out;
-    a.lse = out->lse;
-    a.lse_stride = n;
-    a.admitted = out->admitted ? out->admitted + ci * hq : nullptr;
-    LCX_TRY(attention_simt(a, st));
+    LCX_TRY(attention_chunk(ctx, in, w, t0, t1, sparse, vlist, vcnt, cap_v, slist, scnt, cap_s,
+                            dca, s, dca ? c : 1, tc_min, out->out, out->lse, n,
+                            out->admitted ? out->admitted + ci * hq : nullptr, st));
     if (prof) {
-      LCX_CHECK_CUDA(cudaEventRecord(ev[4], st));
-      LCX_CHECK_CUDA(cudaEventSynchronize(ev[4]));
+      LCX_CHECK_CUDA(cudaEventRecord(ev[3], st));
+      LCX_CHECK_CUDA(cudaEventSynchronize(ev[3]));
       float t = 0;
       if (sparse) {
         cudaEventElapsedTime(&t, ev[0], ev[1]);
@@ -510,10 +669,8 @@ int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
         cudaEventElapsedTime(&t, ev[1], ev[2]);
         ms_sel += t;
         cudaEventElapsedTime(&t, ev[2], ev[3]);
-        ms_idx += t;
-        cudaEventElapsedTime(&t, ev[3], ev[4]);
       } else {
-        cudaEventElapsedTime(&t, ev[0], ev[4]);
+        cudaEventElapsedTime(&t, ev[0], ev[3]);
       }
       ms_att += t;
     }
@@ -524,8 +681,12 @@ int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
   ctx->stats.chunks = nchunks;
   ctx->stats.ms_estimate = ms_est;
   ctx->stats.ms_select = ms_sel;
-  ctx->stats.ms_index = ms_idx;
   ctx->stats.ms_attention = ms_att;
+  if (prof && ctx->tile_counter) {
+    long long tiles = 0;
+    LCX_CHECK_CUDA(cudaMemcpy(&tiles, ctx->tile_counter, 8, cudaMemcpyDeviceToHost));
+    ctx->stats.tc_tiles = tiles;
+  }
   return LCX_OK;
 }
 

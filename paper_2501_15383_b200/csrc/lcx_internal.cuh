@@ -94,8 +94,9 @@ struct Arena {
 struct Sizer {
   size_t off = 0;
   template <typename T>
-  void take(size_t count) {
+  T* take(size_t count) {
     off += (count * sizeof(T) + 255) & ~size_t(255);
+    return nullptr;
   }
 };
 
@@ -114,6 +115,7 @@ struct lcx_context {
   size_t ws_bytes = 0;
   // persistent device scratch (counters)
   int profiling = 0;
+  int64_t* tile_counter = nullptr;  // device: executed tcgen05 tiles of the last call
   lcx_prefill_stats stats{};
 };
 
@@ -185,7 +187,11 @@ struct AttnArgs {
 };
 int attention_simt(const AttnArgs& a, cudaStream_t st);
 
-// index.cu
+// attn_tc.cu
+struct TcBuffers;
+struct TcParams;
+
+// index / bitmaps (misc.cu)
 int build_bitmaps(const int32_t* lists, const int32_t* counts, int64_t cap, int heads,
                   int64_t words, uint32_t* bits, cudaStream_t st);
 

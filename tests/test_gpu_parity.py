@@ -224,7 +224,7 @@ def test_chunked_prefill_goldens(L, port, name, precision):
     assert crit.slashes == exp["critical"]["slashes"]
     full = L.full_attention(inp, dca, precision)
     sp = L.sparse_attention(inp, crit, dca, precision)
-    rec = L.attention_recall(sp.lse, full.lse)
+    rec = L.attention_recall(sp.lse, full.lse, slack=1e-5 if precision == "fp32" else 4e-3)
     assert abs(rec.aggregate - exp["recall"]) <= (1e-6 if precision == "fp32" else 2e-3)
     assert L.density(crit) == exp["density"]
 
@@ -378,3 +378,93 @@ def _adm(crit, i):
     ss = [i - d for d in crit.slashes if d <= i]
     row = set(vs) | set(ss)
     return row if row else {i}
+
+
+# ------------------------------------------------------------ tcgen05 path --
+def _mh_inputs(n, hq, hkv, dim, precision, seed, kind="normal"):
+    rng = np.random.default_rng(seed)
+    q = rng.standard_normal((n, hq, dim))
+    k = rng.standard_normal((n, hkv, dim))
+    v = rng.standard_normal((n, hkv, dim))
+    if kind == "peaked":  # large-logit rows: a few keys aligned with the queries
+        k[rng.integers(0, n, n // 16)] *= 6.0
+        q *= 1.5
+    return (rounded(q, precision), rounded(k, precision), rounded(v, precision))
+
+
+TC_CASES = [
+    # n, hq, hkv, chunk, lq, budget, dca, opts(sink, band), kind, temperature
+    (1024, 4, 2, 256, 64, (40, 300), None, (True, True), "normal", 1.0),
+    (1536, 6, 2, 512, 64, (100, 200), (256, 768, 256), (True, True), "normal", 0.8),
+    (1024, 2, 1, 512, 32, (10, 600), (512, 1024, 512), (False, False), "peaked", 1.0),
+    (768, 4, 4, 128, 128, (5, 40), (128, 300, 128), (True, True), "peaked", 1.0),
+    (1280, 7, 1, 640, 64, (64, 6), None, (True, False), "normal", 1.0),
+]
+
+
+@pytest.mark.parametrize("case", TC_CASES)
+def test_tc_prefill_matches_oracle(D, port, case):
+    """bf16 storage, the tcgen05 tiles + CUDA-core slash path: per head identical
+    selections and outputs within 2e-3 of the oracle on the same bf16 values; the TC
+    and pure CUDA-core paths agree; admitted-entry counts are exact."""
+    import torch
+    n, hq, hkv, chunk, lq, bud, dca, (sink, band), kind, temp = case
+    q, k, v = _mh_inputs(n, hq, hkv, 128, "bf16", n + hq, kind)
+    T = lambda x: torch.tensor(x).to(torch.bfloat16).cuda().contiguous()  # noqa: E731
+    opts = D.Options(sink, band, True)
+    kw = dict(chunk_len=chunk, last_q=lq, budget=bud, opts=opts, temperature=temp,
+              position_mode="dca_continuous" if dca else "standard", dca=dca,
+              return_admitted=True)
+    r = D.chunked_prefill(T(q), T(k), T(v), kernel_path="tc", **kw)
+    rs = D.chunked_prefill(T(q), T(k), T(v), kernel_path="simt", **kw)
+    out, lse = r["out"].double().cpu().numpy(), r["lse"].double().cpu().numpy()
+    out_s = rs["out"].double().cpu().numpy()
+    assert torch.equal(r["admitted"], rs["admitted"])
+    assert row_rel_err(out.reshape(n * hq, -1), out_s.reshape(n * hq, -1)) <= 2e-3
+    g = hq // hkv
+    for h in sorted({0, hq - 1, hq // 2}):
+        o_ref, l_ref, sels = port.chunked_prefill(q[:, h], k[:, h // g], v[:, h // g], chunk, lq,
+                                                  bud, "sparse", 1 if dca else 0, dca,
+                                                  force_sink=sink, force_band=band,
+                                                  temperature=temp)
+        for ci, s in enumerate(sels):
+            assert r["verticals"][ci, h, :int(r["nv"][ci, h])].tolist() == s.critical.verticals
+            assert r["slashes"][ci, h, :int(r["ns"][ci, h])].tolist() == s.critical.slashes
+            cnt = sum(len(_adm(s.critical, i)) for i in range(s.begin, s.end))
+            assert int(r["admitted"][ci, h]) == cnt
+        assert row_rel_err(out[:, h], o_ref) <= 2e-3, h
+        assert lse_rel_err(lse[h], l_ref) <= 2e-3, h
+
+
+@pytest.mark.parametrize("dca", [None, (256, 640, 256)])
+def test_tc_full_attention(D, port, dca):
+    import torch
+    n, hq, hkv = 1024, 2, 1
+    q, k, v = _mh_inputs(n, hq, hkv, 128, "bf16", 3, "peaked")
+    T = lambda x: torch.tensor(x).to(torch.bfloat16).cuda().contiguous()  # noqa: E731
+    out, lse = D.full_attention(T(q), T(k), T(v), dca=dca, kernel_path="tc", temperature=0.9)
+    out, lse = out.double().cpu().numpy(), lse.double().cpu().numpy()
+    for h in range(hq):
+        o_ref, l_ref = port.full_attention(q[:, h], k[:, 0], v[:, 0], dca=dca, temperature=0.9)
+        assert row_rel_err(out[:, h], o_ref) <= 2e-3
+        assert lse_rel_err(lse[h], l_ref) <= 2e-3
+
+
+def test_tc_sparse_attention_custom_positions(D, port):
+    import torch
+    n = 512
+    q, k, v = _mh_inputs(n, 1, 1, 128, "bf16", 9)
+    rng = np.random.default_rng(2)
+    pq = np.sort(rng.integers(0, 20000, n))
+    pk = np.sort(rng.integers(0, 20000, n))
+    crit = port.select_critical(port.estimate_block(q[:, 0], k[:, 0], 64), (30, 200), n)
+    ref = port.sparse_attention(q[:, 0], k[:, 0], v[:, 0], crit, pos_q=pq, pos_k=pk)
+    T = lambda x: torch.tensor(x).to(torch.bfloat16).cuda().contiguous()  # noqa: E731
+    Ti = lambda x: torch.tensor(np.asarray(x, np.int32)).cuda().reshape(1, -1)  # noqa: E731
+    out, lse = D.sparse_attention(T(q), T(k), T(v), Ti(crit.verticals),
+                                  Ti([len(crit.verticals)]).reshape(1),
+                                  Ti(crit.slashes), Ti([len(crit.slashes)]).reshape(1),
+                                  positions_q=torch.tensor(pq).cuda(),
+                                  positions_k=torch.tensor(pk).cuda(), kernel_path="tc")
+    assert row_rel_err(out[:, 0].double().cpu().numpy(), ref[0]) <= 2e-3
+    assert lse_rel_err(lse[0].double().cpu().numpy(), ref[1]) <= 2e-3
