@@ -124,12 +124,20 @@ typedef struct {
   int64_t* admitted;
 } lcx_prefill_output;
 
-/* Execution statistics of the last lcx_chunked_prefill on a context (host side). */
+/* Execution statistics of the last lcx_chunked_prefill on a context (host side).
+ * Counters and stage times are filled only when profiling is enabled
+ * (lcx_set_profiling), which records CUDA events around each stage of each chunk
+ * and synchronizes once at the end of the call. */
 typedef struct {
   int64_t chunks;
+  int64_t launches;        /* kernels launched by the call */
   int64_t tc_tiles;        /* 64-key x 128-row tcgen05 tiles executed */
-  int64_t simt_entries;    /* entries on the CUDA-core gather path (0 unless measured) */
-  double ms_estimate, ms_select, ms_index, ms_attention; /* 0 unless profiling enabled */
+  int64_t simt_entries;    /* admitted entries computed on the CUDA-core gather path */
+  double ms_estimate;      /* K1 estimator (all chunks) */
+  double ms_select;        /* K2 selection */
+  double ms_attention;     /* K3 index build + K4 attention (tcgen05 + CUDA-core) */
+  double ms_tc_kernel;     /* the tcgen05 attention kernel alone */
+  double ms_total;
 } lcx_prefill_stats;
 
 typedef struct lcx_context lcx_context;
@@ -144,6 +152,9 @@ int lcx_device_ok(int device);
 /* Enables per-stage CUDA-event timing inside lcx_chunked_prefill (synchronizing). */
 int lcx_set_profiling(lcx_context* ctx, int enabled);
 int lcx_get_stats(lcx_context* ctx, lcx_prefill_stats* out);
+/* Debug: record CTA-0 per-tile clock64 timestamps of the tcgen05 attention
+ * pipeline (512 tiles x 8 columns) and copy them to host_out (may be NULL). */
+int lcx_debug_trace(lcx_context* ctx, int enable, long long* host_out);
 
 /* ---- estimator (part a) -------------------------------------------------- */
 /* estimate_block: q_rows are the trailing nq rows of the key timeline k[0:nk]

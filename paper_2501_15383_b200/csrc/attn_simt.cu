@@ -202,6 +202,8 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(AttnArgs a) {
     a.lse[int64_t(h) * a.lse_stride + i] = s.m + logf(s.l);
     if (a.admitted) atomicAdd(reinterpret_cast<unsigned long long*>(a.admitted + h),
                                          (unsigned long long)entries);
+    if (a.simt_count) atomicAdd(reinterpret_cast<unsigned long long*>(a.simt_count),
+                                (unsigned long long)entries);
   }
 }
 

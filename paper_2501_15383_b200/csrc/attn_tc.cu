@@ -45,21 +45,29 @@ namespace lcx {
 namespace {
 
 constexpr int BM = 128, BN = 64, HD = 128;
-constexpr int kThreads = 256;
-constexpr uint32_t kQHalf = BM * 64 * 2;             // 16 KB
+// warps 0-7 softmax (TMEM lane quadrant = warp % 4, column half = warp / 4),
+// warp 8 producer (tile metadata + K TMA), warp 9 QK issuer + TMEM allocator,
+// warp 10 PV issuer, warp 11 V TMA
+constexpr int kThreads = 384;
+constexpr int kSoftmaxWarps = 8;
+constexpr int kWarpProducer = 8, kWarpMma = 9, kWarpPv = 10, kWarpV = 11;
+constexpr int NK = 4, NV = 4, NS = 4;                // K / V smem stages, S (+P) TMEM buffers
 constexpr uint32_t kKHalf = BN * 64 * 2;             // 8 KB
 constexpr uint32_t kKStage = 4 * kKHalf;             // hi0 hi1 lo0 lo1 = 32 KB
 constexpr uint32_t kVStage = HD * BN * 2;            // 16 KB
-constexpr uint32_t kPBuf = BM * BN * 2;              // 16 KB
-constexpr uint32_t OFF_QHI = 0;
-constexpr uint32_t OFF_QLO = 2 * kQHalf;
-constexpr uint32_t OFF_K = 4 * kQHalf;               // 64 KB
-constexpr uint32_t OFF_V = OFF_K + 2 * kKStage;      // 128 KB
-constexpr uint32_t OFF_P = OFF_V + 2 * kVStage;      // 160 KB
-constexpr uint32_t OFF_BAR = OFF_P + 2 * kPBuf;      // 192 KB
-constexpr uint32_t kSmemBytes = OFF_BAR + 256 + 1024;  // + alignment slack
-constexpr uint32_t kTmemCols = 256;
-constexpr uint32_t COL_O = 128;
+constexpr uint32_t OFF_K = 0;
+constexpr uint32_t OFF_V = OFF_K + NK * kKStage;     // 128 KB
+constexpr uint32_t OFF_BAR = OFF_V + NV * kVStage;   // 192 KB
+constexpr uint32_t OFF_META = OFF_BAR + 512;
+constexpr uint32_t OFF_RED = OFF_META + 8 * 448;  // [2 buf][2 part][128] max, then [2][128] sum
+constexpr uint32_t kSmemBytes = OFF_RED + 3 * 2 * 128 * 4 + 1024;  // + alignment slack
+// TMEM (512 columns x 128 lanes): S/P buffers [0, 256), O [256, 384), rotated
+// Q hi [384, 448) and lo [448, 512) as the A operand of every QK MMA (bf16 pairs
+// per 32-bit column), so all MMAs read only B from shared memory.
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t COL_O = NS * BN;
+constexpr uint32_t COL_QHI = COL_O + HD;
+constexpr uint32_t COL_QLO = COL_QHI + HD / 2;
 constexpr float kRescaleThresh = 8.f;
 
 constexpr uint32_t IDESC_QK = tc::idesc_f16(BM, BN, 1, 1);   // bf16 x bf16
@@ -210,19 +218,20 @@ __device__ __forceinline__ int64_t qpos_of(const TcParams& p, int pattern, int64
   return p.c - 1;
 }
 
-// Rotate this thread's query row by its pattern position and write the bf16
-// hi / lo split into the SW128 K-major Q tiles.
+// Rotate this thread's query row (its 64-dim half) by its pattern position and
+// store the bf16 hi / lo split into TMEM (row = lane, dim pair = column).
 __device__ __forceinline__ void rotate_q(const TcParams& p, const Item& it, int pattern, int r,
-                                         uint8_t* smem) {
+                                         int part, uint32_t tmem_row) {
   const int64_t i = it.i0 + r;
   const bool ok = i < it.rend;
   const uint4* src = reinterpret_cast<const uint4*>(p.q + (i * p.hq + it.h) * int64_t(HD));
   const float2* cs = p.rope + (ok ? qpos_of(p, pattern, i) : 0) * (HD / 2);
-#pragma unroll 4
-  for (int ch = 0; ch < HD / 8; ++ch) {  // 16 chunks of 8 dims (4 pairs)
+  uint32_t hi[32], lo[32];
+#pragma unroll
+  for (int c8 = 0; c8 < 8; ++c8) {  // 8 chunks of 8 dims in this half
+    const int ch = part * 8 + c8;
     uint4 raw = ok ? src[ch] : make_uint4(0, 0, 0, 0);
     const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-    uint32_t hi[4], lo[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const float2 xy = __bfloat1622float2(x2[k]);
@@ -232,14 +241,48 @@ __device__ __forceinline__ void rotate_q(const TcParams& p, const Item& it, int 
       const __nv_bfloat162 h2 = __floats2bfloat162_rn(rx, ry);
       const float2 hf = __bfloat1622float2(h2);
       const __nv_bfloat162 l2 = __floats2bfloat162_rn(rx - hf.x, ry - hf.y);
-      hi[k] = *reinterpret_cast<const uint32_t*>(&h2);
-      lo[k] = *reinterpret_cast<const uint32_t*>(&l2);
+      hi[c8 * 4 + k] = *reinterpret_cast<const uint32_t*>(&h2);
+      lo[c8 * 4 + k] = *reinterpret_cast<const uint32_t*>(&l2);
     }
-    const int half = ch >> 3, c16 = ch & 7;
-    const uint32_t off = half * kQHalf + tc::sw128_off(r, c16);
-    *reinterpret_cast<uint4*>(smem + OFF_QHI + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-    *reinterpret_cast<uint4*>(smem + OFF_QLO + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
   }
+  tc::tmem_st32(tmem_row + COL_QHI + part * 32, reinterpret_cast<const float*>(hi));
+  tc::tmem_st32(tmem_row + COL_QLO + part * 32, reinterpret_cast<const float*>(lo));
+  tc::tmem_wait_st();
+}
+
+// Per-tile control record, written by the producer warp into a 4-deep shared
+// ring so that the MMA and softmax warps never touch global memory for control.
+enum { T_EMPTY = 3, T_END = 4 };
+enum { F_FIRST = 1, F_LAST = 2, F_EPOCH = 4, F_EPOCH_AFTER = 8 };
+struct TileMeta {
+  int32_t kind, flags, pattern, next_pattern;
+  int32_t h, count, nfar, pad;
+  int64_t i0, rend, key0, sbase;
+  uint64_t vmask;
+  uint32_t sw[8];
+  int32_t keys[64];
+};
+constexpr int kMetaSlots = 8;
+constexpr int kTraceTiles = 512;
+// trace columns: 0 meta ready (producer), 1 K TMA issued, 2 V TMA issued,
+// 3 QK issued (MMA), 4 PV issued, 5 softmax got S, 6 softmax P written, 7 kind
+__device__ __forceinline__ void trace_mark(const TcParams& p, uint32_t T, int col) {
+  if (p.trace && blockIdx.x == 0 && T < kTraceTiles) p.trace[T * 8 + col] = clock64();
+}
+static_assert(sizeof(TileMeta) <= 448, "tile metadata slot overflow");
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint64_t window64(const uint32_t* sw, int off) {
+  // bits [off, off + 64) of the 256-bit array sw (off in [0, 192])
+  const int w = off >> 5, sh = off & 31;
+  const uint64_t a = uint64_t(sw[w]) | (uint64_t(sw[w + 1]) << 32);
+  const uint64_t b = (w + 2 < 8) ? sw[w + 2] : 0u;
+  return sh ? ((a >> sh) | (b << (64 - sh))) : a;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -249,39 +292,50 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
                const __grid_constant__ CUtensorMap map_kc_hi,
                const __grid_constant__ CUtensorMap map_kc_lo,
                const __grid_constant__ CUtensorMap map_vct) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // stay in the shared address space (LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* k_full = bars + 0;
-  uint64_t* k_empty = bars + 2;
-  uint64_t* v_full = bars + 4;
-  uint64_t* v_empty = bars + 6;
-  uint64_t* s_full = bars + 8;
-  uint64_t* s_free = bars + 10;
-  uint64_t* p_full = bars + 12;
-  uint64_t* p_free = bars + 14;
-  uint64_t* q_ready = bars + 16;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* k_full = bars;                 // [NK] TMA -> MMA
+  uint64_t* k_empty = k_full + NK;         // [NK] QK commit -> producer
+  uint64_t* v_full = k_empty + NK;         // [NV]
+  uint64_t* v_empty = v_full + NV;         // [NV] PV commit -> producer
+  uint64_t* s_full = v_empty + NV;         // [NS] QK commit -> softmax
+  uint64_t* s_free = s_full + NS;          // [NS] PV commit (S/P buffer, O updated)
+  uint64_t* p_full = s_free + NS;          // [NS] softmax wrote P -> PV issuer
+  uint64_t* q_ready = p_full + NS;         // softmax rotated Q -> QK issuer
+  uint64_t* m_full = q_ready + 1;          // [kMetaSlots]
+  uint64_t* m_empty = m_full + kMetaSlots; // [kMetaSlots]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(m_empty + kMetaSlots);
+  static_assert((2 * NK + 2 * NV + 3 * NS + 1 + 2 * kMetaSlots + 1) * 8 <= 512,
+                "barrier area overflow");
+  TileMeta* metas = reinterpret_cast<TileMeta*>(smem + OFF_META);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NK; ++b) {
       tc::mbar_init(k_full + b, 1);
       tc::mbar_init(k_empty + b, 1);
+    }
+    for (int b = 0; b < NV; ++b) {
       tc::mbar_init(v_full + b, 1);
       tc::mbar_init(v_empty + b, 1);
-      tc::mbar_init(s_full + b, 1);
-      tc::mbar_init(s_free + b, 4);
-      tc::mbar_init(p_full + b, 4);
-      tc::mbar_init(p_free + b, 1);
     }
-    tc::mbar_init(q_ready, 4);
+    for (int b = 0; b < NS; ++b) {
+      tc::mbar_init(s_full + b, 1);
+      tc::mbar_init(s_free + b, 1);
+      tc::mbar_init(p_full + b, kSoftmaxWarps);
+    }
+    tc::mbar_init(q_ready, kSoftmaxWarps);
+    for (int b = 0; b < kMetaSlots; ++b) {
+      tc::mbar_init(m_full + b, 1);
+      tc::mbar_init(m_empty + b, kSoftmaxWarps + 3);  // softmax + QK + PV + V warps
+    }
     tc::fence_barrier_init();
     tc::fence_proxy_async();
   }
-  if (warp == 2) tc::tmem_alloc(tmem_slot, kTmemCols);
-  if (warp == 0 && lane == 0) {
+  if (warp == kWarpMma) tc::tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == kWarpProducer && lane == 0) {
     tc::tma_prefetch(&map_k_hi);
     tc::tma_prefetch(&map_k_lo);
     tc::tma_prefetch(&map_vt);
@@ -294,245 +348,403 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
-    // ================================================= TMA producer ====
-    if (lane == 0) {
-      uint32_t T = 0;
-      for (int item = blockIdx.x; item < p.nitems; item += gridDim.x) {
-        Item it;
-        setup_item(p, item, it);
-        for (int t = 0; t < it.ntiles; ++t, ++T) {
-          const Tile tl = get_tile(p, it, t);
-          const int b = T & 1;
-          const uint32_t ph = (T >> 1) & 1;
-          tc::mbar_wait(k_empty + b, ph ^ 1);
-          tc::mbar_expect_tx(k_full + b, kKStage);
-          uint8_t* kdst = smem + OFF_K + b * kKStage;
-          if (tl.kind == T_VERT) {
-            const int r = int(tl.key0);
-            tc::tma_load_3d(kdst + 0 * kKHalf, &map_kc_hi, k_full + b, 0, r, it.h);
-            tc::tma_load_3d(kdst + 1 * kKHalf, &map_kc_hi, k_full + b, 64, r, it.h);
-            tc::tma_load_3d(kdst + 2 * kKHalf, &map_kc_lo, k_full + b, 0, r, it.h);
-            tc::tma_load_3d(kdst + 3 * kKHalf, &map_kc_lo, k_full + b, 64, r, it.h);
-          } else {
-            const int j = int(tl.key0);
-            tc::tma_load_3d(kdst + 0 * kKHalf, &map_k_hi, k_full + b, 0, it.g, j);
-            tc::tma_load_3d(kdst + 1 * kKHalf, &map_k_hi, k_full + b, 64, it.g, j);
-            tc::tma_load_3d(kdst + 2 * kKHalf, &map_k_lo, k_full + b, 0, it.g, j);
-            tc::tma_load_3d(kdst + 3 * kKHalf, &map_k_lo, k_full + b, 64, it.g, j);
+  if (warp == kWarpProducer) {
+    // ============================ producer: tile stream + metadata + TMA ====
+    // Tiles are processed in batches of 4 so that every global load of a batch
+    // (tile list entries, bitmap windows, compacted keys) is in flight at once.
+    uint32_t T = 0, M = 0;
+    auto next_slot = [&]() -> TileMeta& {
+      const int slot = M % kMetaSlots;
+      tc::mbar_wait(m_empty + slot, ((M / kMetaSlots) & 1) ^ 1);
+      return metas[slot];
+    };
+    auto publish = [&]() {
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(m_full + (M % kMetaSlots));
+      ++M;
+    };
+    for (int item = blockIdx.x; item < p.nitems; item += gridDim.x) {
+      const Item it = reinterpret_cast<const Item*>(p.plans)[item];
+      if (it.ntiles == 0) {
+        TileMeta& mt = next_slot();
+        if (lane == 0) {
+          mt.kind = T_EMPTY;
+          mt.flags = F_FIRST | F_LAST;
+          mt.h = it.h;
+          mt.i0 = it.i0;
+          mt.rend = it.rend;
+        }
+        publish();
+        continue;
+      }
+      int prev_grp = -1;
+      for (int tb = 0; tb < it.ntiles; tb += 4) {
+        const int nb = min(4, it.ntiles - tb);
+        // A: lane j (j <= nb) resolves tile tb + j (one tile-list load each, in parallel)
+        Tile my{};
+        my.grp = -1;
+        if (lane <= nb && tb + lane < it.ntiles) my = get_tile(p, it, tb + lane);
+        int kinds[5], grps[5], counts[4];
+        int64_t key0s[4];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+          kinds[j] = __shfl_sync(0xffffffffu, my.kind, j);
+          grps[j] = __shfl_sync(0xffffffffu, my.grp, j);
+          if (j < 4) {
+            counts[j] = __shfl_sync(0xffffffffu, my.count, j);
+            key0s[j] = __shfl_sync(0xffffffffu, (long long)my.key0, j);
           }
-          tc::mbar_wait(v_empty + b, ph ^ 1);
-          tc::mbar_expect_tx(v_full + b, kVStage);
-          uint8_t* vdst = smem + OFF_V + b * kVStage;
-          if (tl.kind == T_VERT)
-            tc::tma_load_3d(vdst, &map_vct, v_full + b, int(tl.key0), 0, it.h);
-          else
-            tc::tma_load_3d(vdst, &map_vt, v_full + b, int(tl.key0), 0, it.g);
+        }
+        // B: all loads of the batch
+        const int jj = lane >> 3, w = lane & 7;
+        uint32_t swv = 0, vbv = 0;
+        int64_t wbase = 0;
+        if (jj < nb && kinds[jj] == T_SLASH) {
+          const int64_t lo = it.i0 - key0s[jj] - 63;
+          wbase = lo >= 0 ? (lo >> 5) : -((-lo + 31) >> 5);
+          const int64_t wi = wbase + w;
+          const uint32_t* sb = p.sbits + int64_t(it.h) * p.words;
+          swv = (wi >= 0 && wi < p.words) ? sb[wi] : 0u;
+          if (w < 2) {
+            const int64_t kw = (key0s[jj] >> 5) + w;
+            vbv = kw < p.words ? p.vbits[int64_t(it.h) * p.words + kw] : 0u;
+          }
+        }
+        int32_t ck[4][2];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          ck[j][0] = ck[j][1] = -1;
+          if (j < nb && kinds[j] == T_VERT) {
+            const int32_t* c = p.ckeys + int64_t(it.h) * p.capp + key0s[j];
+            if (lane < counts[j]) ck[j][0] = c[lane];
+            if (lane + 32 < counts[j]) ck[j][1] = c[lane + 32];
+          }
+        }
+        // C: publish the metadata, then issue the TMA loads
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j >= nb) break;
+          const int t = tb + j;
+          int flags = 0;
+          if (t == 0) flags |= F_FIRST;
+          if (grps[j] != prev_grp) flags |= F_EPOCH;
+          if (t + 1 == it.ntiles) flags |= F_LAST;
+          else if (grps[j + 1] != grps[j]) flags |= F_EPOCH_AFTER;
+          prev_grp = grps[j];
+          TileMeta& mt = next_slot();
+          const uint32_t sw_j = __shfl_sync(0xffffffffu, swv, 8 * j + (lane & 7));
+          const uint32_t vb0 = __shfl_sync(0xffffffffu, vbv, 8 * j);
+          const uint32_t vb1 = __shfl_sync(0xffffffffu, vbv, 8 * j + 1);
+          const long long wb_j = __shfl_sync(0xffffffffu, (long long)wbase, 8 * j);
+          if (kinds[j] == T_SLASH && lane < 8) mt.sw[lane] = sw_j;
+          if (kinds[j] == T_VERT) {
+            mt.keys[lane] = ck[j][0];
+            mt.keys[lane + 32] = ck[j][1];
+            const unsigned f0 =
+                __ballot_sync(0xffffffffu, ck[j][0] >= 0 && int64_t(ck[j][0]) < it.i0);
+            const unsigned f1 =
+                __ballot_sync(0xffffffffu, ck[j][1] >= 0 && int64_t(ck[j][1]) < it.i0);
+            if (lane == 0) mt.nfar = __popc(f0) + __popc(f1);
+          }
+          if (lane == 0) {
+            mt.kind = kinds[j];
+            mt.flags = flags;
+            mt.pattern = it.grp[grps[j]].pattern;
+            mt.next_pattern = (flags & F_EPOCH_AFTER) ? it.grp[grps[j + 1]].pattern : 0;
+            mt.h = it.h;
+            mt.count = counts[j];
+            mt.i0 = it.i0;
+            mt.rend = it.rend;
+            mt.key0 = key0s[j];
+            mt.sbase = wb_j * 32;
+            mt.vmask = uint64_t(vb0) | (uint64_t(vb1) << 32);
+          }
+          publish();
+          if (lane == 0) {
+            trace_mark(p, T, 0);
+            const int bk = T % NK;
+            const uint32_t phk = (T / NK) & 1;
+            tc::mbar_wait(k_empty + bk, phk ^ 1);
+            tc::mbar_expect_tx(k_full + bk, kKStage);
+            uint8_t* kdst = smem + OFF_K + bk * kKStage;
+            const CUtensorMap* mh = kinds[j] == T_VERT ? &map_kc_hi : &map_k_hi;
+            const CUtensorMap* ml = kinds[j] == T_VERT ? &map_kc_lo : &map_k_lo;
+            const int tile = kinds[j] == T_VERT
+                                 ? int((int64_t(it.h) * (p.capp / 64) + key0s[j] / 64) * 2)
+                                 : int((int64_t(it.g) * p.ntiles_k + key0s[j] / 64) * 2);
+            tc::tma_load_3d(kdst + 0 * kKHalf, mh, k_full + bk, 0, 0, tile);
+            tc::tma_load_3d(kdst + 1 * kKHalf, mh, k_full + bk, 0, 0, tile + 1);
+            tc::tma_load_3d(kdst + 2 * kKHalf, ml, k_full + bk, 0, 0, tile);
+            tc::tma_load_3d(kdst + 3 * kKHalf, ml, k_full + bk, 0, 0, tile + 1);
+            trace_mark(p, T, 1);
+          }
+          __syncwarp();
+          ++T;
         }
       }
     }
-  } else if (warp == 1) {
-    // =================================================== MMA issuer ====
-    if (lane == 0) {
-      uint32_t T = 0, E = 0;
-      auto issue_pv = [&](uint32_t Tp, bool first) {
-        const int b = Tp & 1;
-        const uint32_t ph = (Tp >> 1) & 1;
-        tc::mbar_wait(p_full + b, ph);
-        tc::mbar_wait(v_full + b, ph);
-        tc::tc_fence_after();
-        const uint32_t pa = tc::smem_u32(smem + OFF_P + b * kPBuf);
-        const uint32_t va = tc::smem_u32(smem + OFF_V + b * kVStage);
-#pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk)
-          tc::mma_f16_ss(tmem + COL_O, tc::sdesc_sw128(pa + kk * 32), tc::sdesc_sw128(va + kk * 32),
-                         IDESC_PV, (first && kk == 0) ? 0u : 1u);
-        tc::mma_commit(v_empty + b);
-        tc::mma_commit(p_free + b);
-      };
-      for (int item = blockIdx.x; item < p.nitems; item += gridDim.x) {
-        Item it;
-        setup_item(p, item, it);
-        int prev_grp = -1;
-        for (int t = 0; t < it.ntiles; ++t, ++T) {
-          const Tile tl = get_tile(p, it, t);
-          if (tl.grp != prev_grp) {
-            tc::mbar_wait(q_ready, E & 1);
-            ++E;
-            prev_grp = tl.grp;
-          }
-          const int b = T & 1;
-          const uint32_t ph = (T >> 1) & 1;
-          tc::mbar_wait(k_full + b, ph);
-          tc::mbar_wait(s_free + b, ph ^ 1);
-          tc::tc_fence_after();
-          const uint32_t qh = tc::smem_u32(smem + OFF_QHI), ql = tc::smem_u32(smem + OFF_QLO);
-          const uint32_t kb = tc::smem_u32(smem + OFF_K + b * kKStage);
-          const uint32_t dS = tmem + b * BN;
-          uint32_t acc = 0;
-#pragma unroll
-          for (int combo = 0; combo < 3; ++combo) {
-            const uint32_t qa = combo == 2 ? ql : qh;            // hi.hi, hi.lo, lo.hi
-            const uint32_t ka = kb + (combo == 1 ? 2 * kKHalf : 0);
-#pragma unroll
-            for (int half = 0; half < 2; ++half)
-#pragma unroll
-              for (int kk = 0; kk < 4; ++kk) {
-                tc::mma_f16_ss(dS, tc::sdesc_sw128(qa + half * kQHalf + kk * 32),
-                               tc::sdesc_sw128(ka + half * kKHalf + kk * 32), IDESC_QK, acc);
-                acc = 1;
-              }
-          }
-          tc::mma_commit(k_empty + b);
-          tc::mma_commit(s_full + b);
-          if (t > 0) issue_pv(T - 1, t - 1 == 0);
-        }
-        if (it.ntiles > 0) issue_pv(T - 1, it.ntiles == 1);
-      }
+    {
+      TileMeta& mt = next_slot();
+      if (lane == 0) mt.kind = T_END;
+      publish();
     }
-  } else if (warp >= 4) {
+  } else if (warp == kWarpMma) {
+    // ==================================================== QK issuer ====
+    uint32_t T = 0, E = 0, M = 0;
+    // QK issuer: all 32 lanes run this loop (warp-uniform); one elected lane issues
+    const uint64_t dk0 = tc::sdesc_sw128(tc::smem_u32(smem + OFF_K));
+    for (;;) {
+      const int slot = M % kMetaSlots;
+      tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1);
+      const int kind = metas[slot].kind;
+      const int flags = metas[slot].flags;
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(m_empty + slot);
+      ++M;
+      if (kind == T_END) break;
+      if (kind == T_EMPTY) continue;
+      if (flags & F_EPOCH) {
+        tc::mbar_wait(q_ready, E & 1);
+        ++E;
+      }
+      const int bk = T % NK, bs = T % NS;
+      tc::mbar_wait(k_full + bk, (T / NK) & 1);
+      tc::mbar_wait(s_free + bs, ((T / NS) & 1) ^ 1);  // PV(T - NS) released S/P buffer
+      tc::tc_fence_after();
+      if (lane == 0) trace_mark(p, T, 7);
+      const uint64_t dk = dk0 + ((bk * kKStage) >> 4);
+      const uint32_t dS = tmem + bs * BN;
+#pragma unroll
+      for (int combo = 0; combo < 3; ++combo) {
+        const uint32_t qa = tmem + (combo == 2 ? COL_QLO : COL_QHI);  // hi.hi, hi.lo, lo.hi
+        const uint64_t ka = dk + (combo == 1 ? ((2 * kKHalf) >> 4) : 0);
+#pragma unroll
+        for (int half = 0; half < 2; ++half)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc::mma_f16_ts_warp(dS, qa + half * 32 + kk * 8,
+                                ka + ((half * kKHalf + kk * 32) >> 4), IDESC_QK,
+                                (combo | half | kk) ? 1u : 0u);
+      }
+      tc::mma_commit_warp(k_empty + bk);
+      tc::mma_commit_warp(s_full + bs);
+      if (lane == 0) trace_mark(p, T, 3);
+      ++T;
+    }
+  } else if (warp == kWarpV) {
+    // ===================================================== V TMA loads ====
+    uint32_t T = 0, M = 0;
+    for (;;) {
+      const int slot = M % kMetaSlots;
+      tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1);
+      const int kind = metas[slot].kind;
+      const int h = metas[slot].h;
+      const int key0 = int(metas[slot].key0);
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(m_empty + slot);
+      ++M;
+      if (kind == T_END) break;
+      if (kind == T_EMPTY) continue;
+      if (lane == 0) {
+        const int bv = T % NV;
+        tc::mbar_wait(v_empty + bv, ((T / NV) & 1) ^ 1);
+        tc::mbar_expect_tx(v_full + bv, kVStage);
+        uint8_t* vdst = smem + OFF_V + bv * kVStage;
+        if (kind == T_VERT)
+          tc::tma_load_3d(vdst, &map_vct, v_full + bv, 0, 0,
+                          int(int64_t(h) * (p.capp / 64) + key0 / 64));
+        else
+          tc::tma_load_3d(vdst, &map_vt, v_full + bv, 0, 0,
+                          int(int64_t(h / p.group) * p.ntiles_k + key0 / 64));
+        trace_mark(p, T, 2);
+      }
+      __syncwarp();
+      ++T;
+    }
+  } else if (warp == kWarpPv) {
+    // ============================================== PV issuer (O += P V) ====
+    uint32_t T = 0, M = 0;
+    const uint64_t dv0 = tc::sdesc_sw128(tc::smem_u32(smem + OFF_V));
+    for (;;) {
+      const int slot = M % kMetaSlots;
+      tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1);
+      const int kind = metas[slot].kind;
+      const int flags = metas[slot].flags;
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(m_empty + slot);
+      ++M;
+      if (kind == T_END) break;
+      if (kind == T_EMPTY) continue;
+      const int bs = T % NS, bv = T % NV;
+      tc::mbar_wait(p_full + bs, (T / NS) & 1);
+      tc::mbar_wait(v_full + bv, (T / NV) & 1);
+      tc::tc_fence_after();
+      const uint64_t dv = dv0 + ((bv * kVStage) >> 4);
+      const bool first = (flags & F_FIRST) != 0;
+#pragma unroll
+      for (int kk = 0; kk < BN / 16; ++kk)  // P (fp16, 2 per column) aliases S buffer bs
+        tc::mma_f16_ts_warp(tmem + COL_O, tmem + bs * BN + kk * 8, dv + ((kk * 32) >> 4),
+                            IDESC_PV, (first && kk == 0) ? 0u : 1u);
+      tc::mma_commit_warp(v_empty + bv);
+      tc::mma_commit_warp(s_free + bs);
+      if (lane == 0) trace_mark(p, T, 4);
+      ++T;
+    }
+  } else {
     // ============================= softmax / correction / epilogue ====
-    const int wq = warp & 3;  // TMEM lane quadrant
+    // Two warps per TMEM lane quadrant split each tile's 64 columns (32 each) and
+    // the 128 O columns (64 each); the row max is exchanged through shared memory
+    // with a 64-thread named barrier per quadrant.
+    const int wq = warp & 3;       // TMEM lane quadrant
+    const int part = warp >> 2;    // column half
     const int r = wq * 32 + lane;
     const uint32_t lane_base = uint32_t(wq * 32) << 16;
-    uint32_t T = 0;
-    for (int item = blockIdx.x; item < p.nitems; item += gridDim.x) {
-      Item it;
-      setup_item(p, item, it);
-      const int64_t i = it.i0 + r;
-      const bool row_ok = i < it.rend;
-      if (it.ntiles == 0) {
+    float* red = reinterpret_cast<float*>(smem + OFF_RED);  // [2 buf][2 part][128]
+    const uint32_t bar_id = 1 + wq;
+    uint32_t T = 0, M = 0;
+    float m = -INFINITY, l = 0.f;
+    Item qi{};  // only i0 / rend / h used by rotate_q
+    for (;;) {
+      const int slot = M % kMetaSlots;
+      tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1);
+      const TileMeta& mt = metas[slot];
+      const int kind = mt.kind, flags = mt.flags;
+      if (kind == T_END) break;
+      const int64_t i0 = mt.i0, rend = mt.rend;
+      const int h = mt.h;
+      const int64_t i = i0 + r;
+      const bool row_ok = i < rend;
+      if (kind == T_EMPTY) {
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(m_empty + slot);
+        ++M;
         if (row_ok) {
-          float4* o = reinterpret_cast<float4*>(p.out + (i * p.hq + it.h) * int64_t(HD));
-          for (int x = 0; x < HD / 4; ++x) o[x] = make_float4(0.f, 0.f, 0.f, 0.f);
-          p.lse[int64_t(it.h) * p.lse_stride + i] = -INFINITY;
+          float4* o = reinterpret_cast<float4*>(p.out + (i * p.hq + h) * int64_t(HD)) + part * 16;
+          for (int x = 0; x < 16; ++x) o[x] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (part == 0) p.lse[int64_t(h) * p.lse_stride + i] = -INFINITY;
         }
         continue;
       }
-      Tile tl = get_tile(p, it, 0);
-      rotate_q(p, it, it.grp[tl.grp].pattern, r, smem);
-      tc::fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(q_ready);
-
-      float m = -INFINITY, l = 0.f;
-      const int32_t* vh = p.verts ? p.verts + int64_t(it.h) * p.cap_v : nullptr;
-      const uint32_t* sb = p.sbits ? p.sbits + int64_t(it.h) * p.words : nullptr;
-      const uint32_t* vb = p.vbits ? p.vbits + int64_t(it.h) * p.words : nullptr;
-      for (int t = 0; t < it.ntiles; ++t, ++T) {
-        const int b = T & 1;
-        const uint32_t ph = (T >> 1) & 1;
-        float sv[64];
-        tc::mbar_wait(s_full + b, ph);
-        tc::tc_fence_after();
-        tc::tmem_ld32(tmem + lane_base + b * BN, sv);
-        tc::tmem_ld32(tmem + lane_base + b * BN + 32, sv + 32);
-        tc::tmem_wait_ld();
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(s_free + b);
-        Tile nxt{};
-        if (t + 1 < it.ntiles) {
-          nxt = get_tile(p, it, t + 1);
-          if (nxt.grp != tl.grp) {  // all QK of the old pattern are complete
-            rotate_q(p, it, it.grp[nxt.grp].pattern, r, smem);
-            tc::fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(q_ready);
+      // ---- admission mask of this warp's 32 columns ----
+      uint32_t mask = 0;
+      if (row_ok) {
+        uint64_t m64;
+        if (kind == T_VERT) {
+          int cnt = mt.nfar;
+          while (cnt < mt.count) {
+            const int32_t kk = mt.keys[cnt];
+            if (kk < 0 || int64_t(kk) > i) break;
+            ++cnt;
           }
+          m64 = cnt >= 64 ? ~0ull : ((1ull << cnt) - 1);
+        } else if (kind == T_SLASH) {
+          const int off = int(i - mt.key0 - 63 - mt.sbase);
+          m64 = __brevll(window64(mt.sw, off)) & ~mt.vmask;
+        } else {
+          const int64_t lim = i - mt.key0;
+          m64 = lim >= 63 ? ~0ull : (lim < 0 ? 0ull : ((2ull << lim) - 1));
         }
-        // ---- admission mask (bit c = key c of the tile) ----
-        uint64_t mask = 0;
-        if (row_ok) {
-          if (tl.kind == T_VERT) {
-            mask = tl.count >= 64 ? ~0ull : ((1ull << tl.count) - 1);
-            // real keys form an ascending prefix of the tile (pads = -1 at the tail)
-            const int32_t* ck = p.ckeys + int64_t(it.h) * p.capp + tl.key0;
-            int lo = 0, hi = tl.count;  // count of c with 0 <= ck[c] <= i
-            while (lo < hi) {
-              const int mid = (lo + hi) >> 1;
-              const int32_t kk = ck[mid];
-              if (kk >= 0 && int64_t(kk) <= i) lo = mid + 1;
-              else hi = mid;
-            }
-            mask = lo >= 64 ? ~0ull : ((1ull << lo) - 1);
-          } else if (tl.kind == T_SLASH) {
-            const uint64_t win = bits64(sb, p.words, i - tl.key0 - 63);  // bit k <-> d = lo + k
-            const uint64_t vm = bits64(vb, p.words, tl.key0);
-            mask = __brevll(win) & ~vm;
-          } else {
-            const int64_t lim = i - tl.key0;  // keys key0 + c <= i
-            mask = lim >= 63 ? ~0ull : (lim < 0 ? 0ull : ((2ull << lim) - 1));
-          }
-        }
-        float tmax = -INFINITY;
-#pragma unroll
-        for (int cc = 0; cc < 64; ++cc) {
-          sv[cc] *= p.scale_log2;
-          if ((mask >> cc) & 1ull) tmax = fmaxf(tmax, sv[cc]);
-        }
-        // lazy rescale (warp-uniform TMEM access)
-        const bool need = tmax > m + kRescaleThresh;
-        const bool warp_need = __any_sync(0xffffffffu, need && t > 0 && m != -INFINITY);
-        float m_new = need ? tmax : m;
-        if (warp_need) {
-          const uint32_t Tp = T - 1;
-          tc::mbar_wait(p_free + (Tp & 1), (Tp >> 1) & 1);
-          tc::tc_fence_after();
-          const float f = (need && m != -INFINITY) ? exp2f(m - m_new) : 1.f;
-          float ov[32];
-#pragma unroll
-          for (int q4 = 0; q4 < 4; ++q4) {
-            tc::tmem_ld32(tmem + lane_base + COL_O + q4 * 32, ov);
-            tc::tmem_wait_ld();
-#pragma unroll
-            for (int x = 0; x < 32; ++x) ov[x] *= f;
-            tc::tmem_st32(tmem + lane_base + COL_O + q4 * 32, ov);
-          }
-          tc::tmem_wait_st();
-          l *= f;
-        } else if (need && m != -INFINITY) {
-          // first tile of the item: O is overwritten by this tile's PV
-          l *= exp2f(m - m_new);
-        }
-        m = m_new;
-        // ---- P = exp2(x - m) in fp16, row sum from the rounded values ----
-        tc::mbar_wait(p_free + b, ph ^ 1);  // PV(T-2) has consumed this P buffer
-        uint8_t* pb = smem + OFF_P + b * kPBuf;
-        float rs = 0.f;
-#pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
-          uint32_t w[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int c0 = ch * 8 + 2 * k;
-            const float p0 = ((mask >> c0) & 1ull) ? exp2f(sv[c0] - m) : 0.f;
-            const float p1 = ((mask >> (c0 + 1)) & 1ull) ? exp2f(sv[c0 + 1] - m) : 0.f;
-            const __half2 h2 = __floats2half2_rn(p0, p1);
-            const float2 hf = __half22float2(h2);
-            rs += hf.x + hf.y;
-            w[k] = *reinterpret_cast<const uint32_t*>(&h2);
-          }
-          *reinterpret_cast<uint4*>(pb + tc::sw128_off(r, ch)) = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-        l += rs;
-        tc::fence_proxy_async();
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(p_full + b);
-        tl = nxt;
+        mask = uint32_t(m64 >> (32 * part));
       }
-      // ---- epilogue: wait for the last PV, normalize, store ----
-      {
-        const uint32_t Tp = T - 1;
-        tc::mbar_wait(p_free + (Tp & 1), (Tp >> 1) & 1);
-        tc::tc_fence_after();
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-        float4* o = reinterpret_cast<float4*>(p.out + (i * p.hq + it.h) * int64_t(HD));
+      const int pattern = mt.pattern, next_pattern = mt.next_pattern;
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(m_empty + slot);
+      ++M;
+      if (flags & F_FIRST) {
+        qi.i0 = i0;
+        qi.rend = rend;
+        qi.h = h;
+        m = -INFINITY;
+        l = 0.f;
+        rotate_q(p, qi, pattern, r, part, tmem + lane_base);
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(q_ready);
+      }
+      const int b = T % NS;
+      const uint32_t ph = (T / NS) & 1;
+      float sv[32];
+      tc::mbar_wait(s_full + b, ph);
+      tc::tc_fence_after();
+      tc::tmem_ld32(tmem + lane_base + b * BN + part * 32, sv);
+      tc::tmem_wait_ld();
+      if (threadIdx.x == 0) trace_mark(p, T, 5);
+      if (flags & F_EPOCH_AFTER) {  // all QK of the old pattern are complete
+        rotate_q(p, qi, next_pattern, r, part, tmem + lane_base);
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(q_ready);
+      }
+      // masked logits -> -inf (ex2(-inf) = 0), scaled to log2 units
+      float tmax = -INFINITY;
 #pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
+      for (int cc = 0; cc < 32; ++cc) {
+        sv[cc] = ((mask >> cc) & 1u) ? sv[cc] * p.scale_log2 : -INFINITY;
+        tmax = fmaxf(tmax, sv[cc]);
+      }
+      float* rb = red + (T & 1) * 256;
+      rb[part * 128 + r] = tmax;
+      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+      tmax = fmaxf(tmax, rb[(part ^ 1) * 128 + r]);
+      // lazy rescale (warp-uniform TMEM access); both halves take the same decision
+      const bool first = (flags & F_FIRST) != 0;
+      const bool need = tmax > m + kRescaleThresh;
+      const bool warp_need = __any_sync(0xffffffffu, need && !first && m != -INFINITY);
+      const float m_new = need ? tmax : m;
+      if (warp_need) {
+        const uint32_t Tp = T - 1;  // O must hold PV(T-1) before rescaling
+        tc::mbar_wait(s_free + (Tp % NS), (Tp / NS) & 1);
+        tc::tc_fence_after();
+        const float f = (need && m != -INFINITY) ? ex2(m - m_new) : 1.f;
+        for (int q4 = 0; q4 < 2; ++q4) {
           float ov[32];
-          tc::tmem_ld32(tmem + lane_base + COL_O + q4 * 32, ov);
+          const uint32_t ta = tmem + lane_base + COL_O + part * 64 + q4 * 32;
+          tc::tmem_ld32(ta, ov);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int x = 0; x < 32; ++x) ov[x] *= f;
+          tc::tmem_st32(ta, ov);
+        }
+        tc::tmem_wait_st();
+        l *= f;
+      } else if (need && m != -INFINITY) {
+        l *= ex2(m - m_new);
+      }
+      m = m_new;
+      // ---- P = exp2(x - m) in fp16, written over this tile's S columns in TMEM:
+      // key c -> column c / 2 (two fp16 per 32-bit column).  Both column halves of
+      // the row finished reading S before the max-exchange barrier above.
+      float rs = 0.f;
+      const float mm = m == -INFINITY ? 0.f : m;
+      uint32_t pw[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float p0 = ex2(sv[2 * k] - mm), p1 = ex2(sv[2 * k + 1] - mm);
+        rs += p0 + p1;
+        const __half2 h2 = __floats2half2_rn(p0, p1);
+        pw[k] = *reinterpret_cast<const uint32_t*>(&h2);
+      }
+      tc::tmem_st16(tmem + lane_base + b * BN + part * 16, pw);
+      tc::tmem_wait_st();
+      l += rs;
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(p_full + b);
+      if (threadIdx.x == 0) trace_mark(p, T, 6);
+      if (flags & F_LAST) {
+        // ---- epilogue: wait for this item's last PV, normalize, store ----
+        float* rl = red + 512;  // separated from the next tile's max exchange by its barrier
+        rl[part * 128 + r] = l;
+        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
+        const float lt = l + rl[(part ^ 1) * 128 + r];
+        tc::mbar_wait(s_free + b, ph);  // this item's last PV is complete
+        tc::tc_fence_after();
+        const float inv = lt > 0.f ? 1.f / lt : 0.f;
+        float4* o = reinterpret_cast<float4*>(p.out + (i * p.hq + h) * int64_t(HD)) + part * 16;
+#pragma unroll
+        for (int q4 = 0; q4 < 2; ++q4) {
+          float ov[32];
+          tc::tmem_ld32(tmem + lane_base + COL_O + part * 64 + q4 * 32, ov);
           tc::tmem_wait_ld();
           if (row_ok) {
 #pragma unroll
@@ -541,20 +753,26 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
                                           ov[4 * x + 2] * inv, ov[4 * x + 3] * inv);
           }
         }
-        if (row_ok)
-          p.lse[int64_t(it.h) * p.lse_stride + i] =
-              l > 0.f ? (m + log2f(l)) * 0.69314718055994530942f : -INFINITY;
+        if (row_ok && part == 0)
+          p.lse[int64_t(h) * p.lse_stride + i] =
+              lt > 0.f ? (m + log2f(lt)) * 0.69314718055994530942f : -INFINITY;
         tc::tc_fence_before();
       }
-      if (p.tile_count && threadIdx.x == 128)
-        atomicAdd(reinterpret_cast<unsigned long long*>(p.tile_count),
-                  (unsigned long long)it.ntiles);
+      ++T;
     }
   }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  if (warp == 2) tc::tmem_dealloc(tmem, kTmemCols);
+  if (warp == kWarpMma) tc::tmem_dealloc(tmem, kTmemCols);
+}
+
+__global__ void plan_items_kernel(const TcParams p, Item* __restrict__ plans) {
+  const int item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= p.nitems) return;
+  Item it;
+  setup_item(p, item, it);
+  plans[item] = it;
 }
 
 // ---------------------------------------------------------------- prep --
@@ -576,8 +794,13 @@ __global__ void k_prep_kernel(const __nv_bfloat16* __restrict__ k, int64_t n, in
   const float rx = xy.x * c.x - xy.y * c.y, ry = xy.x * c.y + xy.y * c.x;
   const __nv_bfloat162 h2 = __floats2bfloat162_rn(rx, ry);
   const float2 hf = __bfloat1622float2(h2);
-  reinterpret_cast<__nv_bfloat162*>(khi)[idx] = h2;
-  reinterpret_cast<__nv_bfloat162*>(klo)[idx] = __floats2bfloat162_rn(rx - hf.x, ry - hf.y);
+  // tiled [hkv][n/64][half][64 keys][64 dims]: each TMA box is one contiguous 8 KB block
+  const int g = int(rowhead % hkv);
+  const int64_t nt = (n + 63) / 64;
+  const int d = 2 * pr;
+  const int64_t o = ((((int64_t(g) * nt + j / 64) * 2 + d / 64) * 64 + j % 64) * 64 + d % 64) / 2;
+  reinterpret_cast<__nv_bfloat162*>(khi)[o] = h2;
+  reinterpret_cast<__nv_bfloat162*>(klo)[o] = __floats2bfloat162_rn(rx - hf.x, ry - hf.y);
 }
 
 // V^T [hkv][128][npad] fp16 from V [n][hkv][128] bf16 (smem-tiled transpose)
@@ -592,10 +815,11 @@ __global__ void vt_prep_kernel(const __nv_bfloat16* __restrict__ v, int64_t n, i
     tile[jj][d] = j < n ? __float2half(__bfloat162float(v[(j * hkv + g) * HD + d])) : __half(0.f);
   }
   __syncthreads();
+  const int64_t nt = npad / 64;
+  __half* dst = vt + (int64_t(g) * nt + blockIdx.x) * (HD * 64);  // [128 dims][64 keys]
   for (int x = threadIdx.x; x < 64 * HD; x += blockDim.x) {
     const int d = x / 64, jj = x % 64;
-    const int64_t j = j0 + jj;
-    if (j < npad) vt[(int64_t(g) * HD + d) * npad + j] = tile[jj][d];
+    dst[d * 64 + jj] = tile[jj][d];
   }
 }
 
@@ -629,7 +853,7 @@ __global__ void compact_kernel(const __nv_bfloat16* __restrict__ khi,
                                const int32_t* __restrict__ verts, const int32_t* __restrict__ nv,
                                int64_t cap_v, int64_t capp, int nseg_k,
                                const int32_t* __restrict__ vbase,
-                               const int32_t* __restrict__ vfirst,
+                               const int32_t* __restrict__ vfirst, int64_t nt,
                                __nv_bfloat16* __restrict__ kchi, __nv_bfloat16* __restrict__ kclo,
                                __half* __restrict__ vct, int32_t* __restrict__ ckeys) {
   __shared__ __half tile[64][HD + 8];
@@ -651,29 +875,30 @@ __global__ void compact_kernel(const __nv_bfloat16* __restrict__ khi,
     if (c < capp) ckeys[int64_t(h) * capp + c] = key;
   }
   __syncthreads();
+  const int64_t ct = capp / 64;
   for (int x = threadIdx.x; x < 64 * (HD / 8); x += blockDim.x) {
     const int cc = x / (HD / 8), ch = x % (HD / 8);
-    const int64_t c = c0 + cc;
     uint4 a = make_uint4(0, 0, 0, 0), b = a, vv = a;
     const int32_t j = keys[cc];
+    const int half = ch / 8, c8 = ch % 8;
     if (j >= 0) {
-      a = reinterpret_cast<const uint4*>(khi + (int64_t(j) * hkv + g) * HD)[ch];
-      b = reinterpret_cast<const uint4*>(klo + (int64_t(j) * hkv + g) * HD)[ch];
+      const int64_t src = (((int64_t(g) * nt + j / 64) * 2 + half) * 64 + j % 64) * 64 + c8 * 8;
+      a = *reinterpret_cast<const uint4*>(khi + src);
+      b = *reinterpret_cast<const uint4*>(klo + src);
       vv = reinterpret_cast<const uint4*>(v + (int64_t(j) * hkv + g) * HD)[ch];
     }
-    if (c < capp) {
-      reinterpret_cast<uint4*>(kchi + (int64_t(h) * capp + c) * HD)[ch] = a;
-      reinterpret_cast<uint4*>(kclo + (int64_t(h) * capp + c) * HD)[ch] = b;
-    }
+    const int64_t dst = (((int64_t(h) * ct + blockIdx.x) * 2 + half) * 64 + cc) * 64 + c8 * 8;
+    *reinterpret_cast<uint4*>(kchi + dst) = a;
+    *reinterpret_cast<uint4*>(kclo + dst) = b;
     const __nv_bfloat16* vbf = reinterpret_cast<const __nv_bfloat16*>(&vv);
 #pragma unroll
     for (int k = 0; k < 8; ++k) tile[cc][ch * 8 + k] = __float2half(__bfloat162float(vbf[k]));
   }
   __syncthreads();
+  __half* vdst = vct + (int64_t(h) * ct + blockIdx.x) * (HD * 64);  // [128 dims][64 slots]
   for (int x = threadIdx.x; x < 64 * HD; x += blockDim.x) {
     const int d = x / 64, cc = x % 64;
-    const int64_t c = c0 + cc;
-    if (c < capp) vct[(int64_t(h) * HD + d) * capp + c] = tile[cc][d];
+    vdst[d * 64 + cc] = tile[cc][d];
   }
 }
 
@@ -864,16 +1089,14 @@ int tc_prepare(const void* k, const void* v, int64_t n, int hq, int hkv, const i
       reinterpret_cast<const __nv_bfloat16*>(v), n, hkv, B.npad, B.vt);
   LCX_CHECK_LAUNCH();
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, F16 = CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  LCX_TRY(make_map3(&B.m_khi, BF, B.khi, HD, hkv, n, HD * 2, uint64_t(hkv) * HD * 2, 64, 1, 64));
-  LCX_TRY(make_map3(&B.m_klo, BF, B.klo, HD, hkv, n, HD * 2, uint64_t(hkv) * HD * 2, 64, 1, 64));
-  LCX_TRY(make_map3(&B.m_vt, F16, B.vt, B.npad, HD, hkv, B.npad * 2, uint64_t(HD) * B.npad * 2,
-                    64, HD, 1));
-  LCX_TRY(make_map3(&B.m_kchi, BF, B.kchi, HD, capp, hq, HD * 2, uint64_t(capp) * HD * 2, 64, 64,
-                    1));
-  LCX_TRY(make_map3(&B.m_kclo, BF, B.kclo, HD, capp, hq, HD * 2, uint64_t(capp) * HD * 2, 64, 64,
-                    1));
-  LCX_TRY(make_map3(&B.m_vct, F16, B.vct, capp, HD, hq, capp * 2, uint64_t(HD) * capp * 2, 64, HD,
-                    1));
+  const uint64_t nt = uint64_t(B.npad / 64), ct = uint64_t(capp / 64);
+  // tiled operands: every box is one contiguous block (8 KB K half-tile, 16 KB V^T tile)
+  LCX_TRY(make_map3(&B.m_khi, BF, B.khi, 64, 64, hkv * nt * 2, 128, 8192, 64, 64, 1));
+  LCX_TRY(make_map3(&B.m_klo, BF, B.klo, 64, 64, hkv * nt * 2, 128, 8192, 64, 64, 1));
+  LCX_TRY(make_map3(&B.m_vt, F16, B.vt, 64, HD, hkv * nt, 128, 16384, 64, HD, 1));
+  LCX_TRY(make_map3(&B.m_kchi, BF, B.kchi, 64, 64, hq * ct * 2, 128, 8192, 64, 64, 1));
+  LCX_TRY(make_map3(&B.m_kclo, BF, B.kclo, 64, 64, hq * ct * 2, 128, 8192, 64, 64, 1));
+  LCX_TRY(make_map3(&B.m_vct, F16, B.vct, 64, HD, hq * ct, 128, 16384, 64, HD, 1));
   return LCX_OK;
 }
 
@@ -884,7 +1107,7 @@ int tc_compact(const void* v, int hq, int hkv, const int32_t* verts, const int32
   dim3 grid(unsigned(B.capp / 64), unsigned(hq));
   compact_kernel<<<grid, 256, 0, st>>>(B.khi, B.klo, reinterpret_cast<const __nv_bfloat16*>(v),
                                        hkv, hq / hkv, verts, nv, cap_v, B.capp, B.nseg_k, B.vbase,
-                                       B.vfirst, B.kchi, B.kclo, B.vct, B.ckeys);
+                                       B.vfirst, B.npad / 64, B.kchi, B.kclo, B.vct, B.ckeys);
   LCX_CHECK_LAUNCH();
   return LCX_OK;
 }
@@ -898,6 +1121,8 @@ int tc_classify(const int32_t* slashes, const int32_t* ns, int64_t cap_s, int hq
   return LCX_OK;
 }
 
+size_t tc_plan_bytes() { return sizeof(Item); }
+
 int tc_attention(const TcParams& p, const TcBuffers& B, int sm_count, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
@@ -908,6 +1133,8 @@ int tc_attention(const TcParams& p, const TcBuffers& B, int sm_count, cudaStream
   }
   if (p.nitems <= 0) return LCX_OK;
   const int grid = std::min(p.nitems, sm_count);
+  plan_items_kernel<<<(p.nitems + 127) / 128, 128, 0, st>>>(p, reinterpret_cast<Item*>(p.plans));
+  LCX_CHECK_LAUNCH();
   attn_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(p, B.m_khi, B.m_klo, B.m_vt, B.m_kchi,
                                                      B.m_kclo, B.m_vct);
   LCX_CHECK_LAUNCH();

@@ -25,10 +25,13 @@ struct TcParams {
   // compacted verticals: per DCA key chunk m a 64-aligned segment starting at vbase[h][m]
   const int32_t* ckeys; const int32_t* vbase; const int32_t* vfirst; int64_t capp; int nseg_k;
   int64_t seg_len;     // key-chunk length used for the segments (s, or >= n when standard)
+  int64_t ntiles_k;    // 64-key tiles of the prepared K / V^T (npad / 64)
   const int32_t* tc_u; const int32_t* n_tc_u; int64_t cap_u;
   const uint32_t* sbits; const uint32_t* vbits; int64_t words;
   float* out; float* lse; int64_t lse_stride;
   int64_t* tile_count;  // optional: executed tiles (atomicAdd)
+  long long* trace;     // optional: CTA-0 per-tile timestamps [kTraceTiles][8]
+  void* plans;          // workspace: per-item tile plans (filled by plan_items_kernel)
 };
 
 struct TcBuffers {
@@ -67,6 +70,7 @@ int tc_classify(const int32_t* slashes, const int32_t* ns, int64_t cap_s, int hq
                 int min_entries, int32_t* hist_ws, int32_t* tc_u, int32_t* n_tc_u, int64_t cap_u,
                 int4* segs, int32_t* nseg, int64_t cap_seg, cudaStream_t st);
 int tc_attention(const TcParams& p, const TcBuffers& B, int sm_count, cudaStream_t st);
+size_t tc_plan_bytes();  // bytes per work item for the tile plans
 int admitted_counts(const int32_t* verts, const int32_t* nv, int64_t cap_v,
                     const int32_t* slashes, const int32_t* ns, int64_t cap_s, int hq,
                     int64_t t0, int64_t t1, int64_t* out, cudaStream_t st);

@@ -19,6 +19,7 @@
 namespace lcx {
 
 thread_local std::string g_err;
+thread_local long long g_launches = 0;
 void set_error(const std::string& msg) { g_err = msg; }
 
 int build_rope_table(const double* thetas_dev, int P, int64_t npos, float2* out,
@@ -192,6 +193,7 @@ struct AttnWS {
   int32_t* n_tc_u = nullptr;
   int4* segs = nullptr;
   int32_t* nseg = nullptr;
+  void* plans = nullptr;
   TcBuffers B;
 };
 
@@ -214,7 +216,12 @@ void attn_layout(A& ar, const lcx_attention_input* in, bool tc, bool sparse, int
       w.nseg = ar.template take<int32_t>(size_t(in->hq));
     }
   }
-  if (tc) tc_layout(ar, in->n, in->hq, in->hkv, sparse ? cap_v : 0, seg_len, w.B);
+  if (tc) {
+    tc_layout(ar, in->n, in->hq, in->hkv, sparse ? cap_v : 0, seg_len, w.B);
+    // one plan per (head, 128-row block) of the largest chunk (<= the whole input)
+    w.plans = ar.template take<uint8_t>(size_t(in->hq) * ((in->n + 127) / 128 + 1) *
+                                        tc_plan_bytes());
+  }
 }
 
 bool tc_eligible(const lcx_attention_input* in, int64_t chunk_len, bool dca, int64_t s) {
@@ -241,7 +248,8 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
                     int64_t t1, bool sparse, const int32_t* verts, const int32_t* nv,
                     int64_t cap_v, const int32_t* slashes, const int32_t* ns, int64_t cap_s,
                     bool dca, int64_t s, int64_t c, int tc_min_entries, float* out, float* lse,
-                    int64_t lse_stride, int64_t* admitted, cudaStream_t st) {
+                    int64_t lse_stride, int64_t* admitted, cudaStream_t st,
+                    cudaEvent_t ev_tc0 = nullptr, cudaEvent_t ev_tc1 = nullptr) {
   const int hq = in->hq;
   if (sparse) LCX_TRY(build_bitmaps(verts, nv, cap_v, hq, w.words, w.vbits, st));
   if (!w.tc) {
@@ -265,6 +273,7 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
     a.lse = lse;
     a.lse_stride = lse_stride;
     a.admitted = admitted;
+    a.simt_count = ctx->profiling ? ctx->tile_counter + 1 : nullptr;
     return attention_simt(a, st);
   }
   if (sparse) {
@@ -300,6 +309,7 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
   p.capp = w.B.capp;
   p.nseg_k = w.B.nseg_k;
   p.seg_len = w.B.seg_len;
+  p.ntiles_k = w.B.npad / 64;
   p.tc_u = sparse ? w.tc_u : nullptr;
   p.n_tc_u = w.n_tc_u;
   p.cap_u = w.cap_u;
@@ -309,8 +319,12 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
   p.out = out;
   p.lse = lse;
   p.lse_stride = lse_stride;
-  p.tile_count = ctx->tile_counter;
+  p.tile_count = ctx->profiling ? ctx->tile_counter : nullptr;
+  p.trace = ctx->trace;
+  p.plans = w.plans;
+  if (ev_tc0) LCX_CHECK_CUDA(cudaEventRecord(ev_tc0, st));
   LCX_TRY(tc_attention(p, w.B, ctx->sm_count, st));
+  if (ev_tc1) LCX_CHECK_CUDA(cudaEventRecord(ev_tc1, st));
   if (sparse) {
     // isolated slashes + self-fallback rows on the CUDA-core path, merged in place
     AttnArgs a = base_attn(in, ctx);
@@ -337,6 +351,7 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
     a.out = out;
     a.lse = lse;
     a.lse_stride = lse_stride;
+    a.simt_count = ctx->profiling ? ctx->tile_counter + 1 : nullptr;
     LCX_TRY(attention_simt(a, st));
     if (admitted)
       LCX_TRY(admitted_counts(verts, nv, cap_v, slashes, ns, cap_s, hq, t0, t1, admitted, st));
@@ -380,8 +395,8 @@ int lcx_context_create(int device, lcx_context** out) {
   auto* ctx = new lcx_context();
   ctx->device = device;
   ctx->sm_count = prop.multiProcessorCount;
-  LCX_CHECK_CUDA(cudaMalloc(&ctx->tile_counter, sizeof(int64_t)));
-  LCX_CHECK_CUDA(cudaMemset(ctx->tile_counter, 0, sizeof(int64_t)));
+  LCX_CHECK_CUDA(cudaMalloc(&ctx->tile_counter, 2 * sizeof(int64_t)));
+  LCX_CHECK_CUDA(cudaMemset(ctx->tile_counter, 0, 2 * sizeof(int64_t)));
   *out = ctx;
   return LCX_OK;
 }
@@ -398,6 +413,23 @@ int lcx_context_destroy(lcx_context* ctx) {
 
 int lcx_set_profiling(lcx_context* ctx, int enabled) {
   ctx->profiling = enabled;
+  return LCX_OK;
+}
+
+int lcx_debug_trace(lcx_context* ctx, int enable, long long* host_out) {
+  const size_t bytes = 512 * 8 * sizeof(long long);
+  if (enable && !ctx->trace) {
+    LCX_CHECK_CUDA(cudaMalloc(&ctx->trace, bytes));
+    LCX_CHECK_CUDA(cudaMemset(ctx->trace, 0, bytes));
+  }
+  if (host_out && ctx->trace) {
+    LCX_CHECK_CUDA(cudaDeviceSynchronize());
+    LCX_CHECK_CUDA(cudaMemcpy(host_out, ctx->trace, bytes, cudaMemcpyDeviceToHost));
+  }
+  if (!enable && ctx->trace) {
+    LCX_CHECK_CUDA(cudaFree(ctx->trace));
+    ctx->trace = nullptr;
+  }
   return LCX_OK;
 }
 
@@ -626,13 +658,15 @@ int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
   if (tc)
     LCX_TRY(tc_prepare(in->k, in->v, n, hq, in->hkv, in->positions_k, dca ? 1 : 0, s, ctx->rope,
                        w.B, st));
-  if (ctx->tile_counter) LCX_CHECK_CUDA(cudaMemsetAsync(ctx->tile_counter, 0, 8, st));
-
-  cudaEvent_t ev[5];
   const bool prof = ctx->profiling != 0;
-  double ms_est = 0, ms_sel = 0, ms_att = 0;
-  if (prof)
+  const long long launches0 = g_launches;
+  std::vector<cudaEvent_t> ev;
+  if (prof) {
+    LCX_CHECK_CUDA(cudaMemsetAsync(ctx->tile_counter, 0, 2 * sizeof(int64_t), st));
+    ev.resize(size_t(6 * nchunks + 1));
     for (auto& x : ev) LCX_CHECK_CUDA(cudaEventCreate(&x));
+    LCX_CHECK_CUDA(cudaEventRecord(ev[6 * nchunks], st));
+  }
 
   for (int64_t ci = 0; ci < nchunks; ++ci) {
     const int64_t t0 = ci * L, t1 = std::min(n, t0 + L);
@@ -641,51 +675,64 @@ int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
     int32_t* vcnt = out->sel_nv ? out->sel_nv + ci * hq : inv;
     int32_t* slist = out->sel_slashes ? out->sel_slashes + ci * hq * cap_s : is;
     int32_t* scnt = out->sel_ns ? out->sel_ns + ci * hq : ins;
-    if (prof) LCX_CHECK_CUDA(cudaEventRecord(ev[0], st));
+    cudaEvent_t* e = prof ? &ev[6 * ci] : nullptr;
+    if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[0], st));
     if (sparse) {
-      EstimateArgs e = base_est(in, ctx, t0, t1 - t0, t1, cfg->last_q, dca ? 1 : 0, c);
-      e.col = col;
-      e.slash = sl;
-      e.slash_mean = cfg->opts.slash_mean;
+      EstimateArgs es = base_est(in, ctx, t0, t1 - t0, t1, cfg->last_q, dca ? 1 : 0, c);
+      es.col = col;
+      es.slash = sl;
+      es.slash_mean = cfg->opts.slash_mean;
       Arena a2 = est_ar;
-      LCX_TRY(estimate_simt(ctx, e, a2, st));
-      if (prof) LCX_CHECK_CUDA(cudaEventRecord(ev[1], st));
+      LCX_TRY(estimate_simt(ctx, es, a2, st));
+      if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[1], st));
       LCX_TRY(select_lines(col, hq, t1, cfg->budget_vertical, cfg->opts.force_sink_column, 1,
                            vlist, vcnt, cap_v, st));
       LCX_TRY(select_lines(sl, hq, t1, cfg->budget_slash, cfg->opts.force_local_band, block,
                            slist, scnt, cap_s, st));
-      if (prof) LCX_CHECK_CUDA(cudaEventRecord(ev[2], st));
+      if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[2], st));
     }
     LCX_TRY(attention_chunk(ctx, in, w, t0, t1, sparse, vlist, vcnt, cap_v, slist, scnt, cap_s,
                             dca, s, dca ? c : 1, tc_min, out->out, out->lse, n,
-                            out->admitted ? out->admitted + ci * hq : nullptr, st));
-    if (prof) {
-      LCX_CHECK_CUDA(cudaEventRecord(ev[3], st));
-      LCX_CHECK_CUDA(cudaEventSynchronize(ev[3]));
-      float t = 0;
-      if (sparse) {
-        cudaEventElapsedTime(&t, ev[0], ev[1]);
-        ms_est += t;
-        cudaEventElapsedTime(&t, ev[1], ev[2]);
-        ms_sel += t;
-        cudaEventElapsedTime(&t, ev[2], ev[3]);
-      } else {
-        cudaEventElapsedTime(&t, ev[0], ev[3]);
-      }
-      ms_att += t;
-    }
+                            out->admitted ? out->admitted + ci * hq : nullptr, st,
+                            (prof && tc) ? e[4] : nullptr, (prof && tc) ? e[5] : nullptr));
+    if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[3], st));
   }
-  if (prof)
-    for (auto& x : ev) cudaEventDestroy(x);
   ctx->stats = lcx_prefill_stats{};
   ctx->stats.chunks = nchunks;
-  ctx->stats.ms_estimate = ms_est;
-  ctx->stats.ms_select = ms_sel;
-  ctx->stats.ms_attention = ms_att;
-  if (prof && ctx->tile_counter) {
-    long long tiles = 0;
-    LCX_CHECK_CUDA(cudaMemcpy(&tiles, ctx->tile_counter, 8, cudaMemcpyDeviceToHost));
-    ctx->stats.tc_tiles = tiles;
+  ctx->stats.launches = g_launches - launches0;
+  if (prof) {
+    LCX_CHECK_CUDA(cudaEventSynchronize(ev[6 * (nchunks - 1) + 3]));
+    double ms_est = 0, ms_sel = 0, ms_att = 0, ms_tc = 0;
+    for (int64_t ci = 0; ci < nchunks; ++ci) {
+      cudaEvent_t* e = &ev[6 * ci];
+      float t = 0;
+      if (sparse) {
+        cudaEventElapsedTime(&t, e[0], e[1]);
+        ms_est += t;
+        cudaEventElapsedTime(&t, e[1], e[2]);
+        ms_sel += t;
+        cudaEventElapsedTime(&t, e[2], e[3]);
+      } else {
+        cudaEventElapsedTime(&t, e[0], e[3]);
+      }
+      ms_att += t;
+      if (tc) {
+        cudaEventElapsedTime(&t, e[4], e[5]);
+        ms_tc += t;
+      }
+    }
+    float tot = 0;
+    cudaEventElapsedTime(&tot, ev[6 * nchunks], ev[6 * (nchunks - 1) + 3]);
+    long long cnt[2] = {0, 0};
+    LCX_CHECK_CUDA(cudaMemcpy(cnt, ctx->tile_counter, sizeof(cnt), cudaMemcpyDeviceToHost));
+    ctx->stats.tc_tiles = cnt[0];
+    ctx->stats.simt_entries = cnt[1];
+    ctx->stats.ms_estimate = ms_est;
+    ctx->stats.ms_select = ms_sel;
+    ctx->stats.ms_attention = ms_att;
+    ctx->stats.ms_tc_kernel = ms_tc;
+    ctx->stats.ms_total = tot;
+    for (auto& x : ev) cudaEventDestroy(x);
   }
   return LCX_OK;
 }

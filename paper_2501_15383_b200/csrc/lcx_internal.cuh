@@ -27,8 +27,11 @@ struct Status {
     }                                                                               \
   } while (0)
 
+extern thread_local long long g_launches;  // kernels launched by this thread (stats)
+
 #define LCX_CHECK_LAUNCH()                                                          \
   do {                                                                              \
+    ++::lcx::g_launches;                                                            \
     cudaError_t _e = cudaGetLastError();                                            \
     if (_e != cudaSuccess) {                                                        \
       ::lcx::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e));    \
@@ -115,7 +118,8 @@ struct lcx_context {
   size_t ws_bytes = 0;
   // persistent device scratch (counters)
   int profiling = 0;
-  int64_t* tile_counter = nullptr;  // device: executed tcgen05 tiles of the last call
+  int64_t* tile_counter = nullptr;  // device: [0] executed tcgen05 tiles, [1] CUDA-core entries
+  long long* trace = nullptr;        // device: optional tcgen05 pipeline trace (debug)
   lcx_prefill_stats stats{};
 };
 
@@ -184,6 +188,7 @@ struct AttnArgs {
   float* lse;                // [hq][lse_stride]
   int64_t lse_stride;
   int64_t* admitted;         // optional [hq] counts (atomicAdd)
+  int64_t* simt_count;       // optional scalar: entries processed here (atomicAdd)
 };
 int attention_simt(const AttnArgs& a, cudaStream_t st);
 
