@@ -1,0 +1,475 @@
+#!/usr/bin/env python
+"""bench.py -- sparse + DCA chunked prefill of one attention layer at 1M tokens.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1: one rank per GPU)
+
+One "step" is one full layer prefill of the workload below through
+lcx_chunked_prefill (include/longctx_b200.h): for each of the 32 chunks the
+Vertical-Slash estimator (K1) + selection (K2) over the chunk's t1-key context,
+then the block-sparse attention of the chunk's rows (K3 index build, K4 tcgen05
+tiles + CUDA-core slash gather) with the DCA remap fused into RoPE, for all 28
+query heads.  Inputs: seeded synthetic Q/K/V generated on the device ("structured":
+local + heavy-hitter attention structure, paper_2501_15383_b200/synth.py), 9.5 GB
+of bf16 inputs -- far larger than the 126 MB L2, so no flush is needed between
+steps.
+
+Printed JSON (rank 0, one line): `value` = whole-job tokens/s with inputs resident
+in HBM (device-timed, max over ranks); `e2e` = the same operator through the host
+entry lcx_chunked_prefill_host from pinned host buffers (H2D of Q/K/V and D2H of
+O/lse/selections inside the timed region); `roofline` for the dominant kernel with
+the per-kernel stage times measured by CUDA events on the launching stream;
+`cpu_baseline` = the reference CPU implementation (oracle/_ref, compiled from the
+reference sources; else the C restatement) timed on this host's cores on a bounded
+sample and projected onto the exact entry counts of this workload.
+
+--impl reference: times the reference's own CPU implementation on the same config
+(rank 0 only; other ranks exit 0) and prints the same JSON line with
+"impl": "reference".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sparse-attn prefill tokens/s at 1M ctx, Qwen2.5-7B geometry; % of TC roofline"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1 << 20)
+    ap.add_argument("--hq", type=int, default=28)
+    ap.add_argument("--hkv", type=int, default=4)
+    ap.add_argument("--chunk", type=int, default=32768)
+    ap.add_argument("--last-q", type=int, default=64)
+    ap.add_argument("--budget", type=int, nargs=2, default=[1000, 6096])
+    ap.add_argument("--dca", type=int, nargs=2, default=[131072, 262144],
+                    help="DCA chunk size s and training length c")
+    ap.add_argument("--rope-base", type=float, default=1e7)
+    ap.add_argument("--kind", default="structured", choices=["structured", "iid"])
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-reps", type=int, default=3)
+    ap.add_argument("--shard", default="auto", choices=["auto", "head", "seq"])
+    return ap.parse_args()
+
+
+def workload(a):
+    s, c = a.dca
+    scale = a.n / c
+    return {
+        "workload": f"sparse+DCA chunked prefill, {a.n} tokens, 1 layer, Qwen2.5-7B heads "
+                    f"({a.hq}Q/{a.hkv}KV, d=128), {a.chunk}-token chunks",
+        "n": a.n, "hq": a.hq, "hkv": a.hkv, "head_dim": 128, "chunk_len": a.chunk,
+        "last_q": a.last_q, "budget_vertical": a.budget[0], "budget_slash": a.budget[1],
+        "dca": {"chunk_size": s, "train_len": c, "local_window": min(s, c - s)},
+        "yarn_scale": scale, "rope_base": a.rope_base, "inputs": a.kind, "seed": a.seed,
+        "l2": "inputs (9.5 GB bf16) >> 126 MB L2; no flush needed",
+    }
+
+
+def yarn_t(scale):
+    if scale <= 1.0:
+        return 1.0
+    r = 0.1 * math.log(scale) + 1.0
+    return 1.0 / (r * r)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            d = json.load(open(p))
+            return d, "measured"
+        except Exception:
+            pass
+    return dict(FALLBACK_PEAKS), "fallback"
+
+
+def peak_value(peaks, key, default):
+    v = peaks.get(key, default)
+    if isinstance(v, dict):
+        v = v.get("value", default)
+    return float(v)
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of each kernel from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p))
+        except Exception:
+            return {}
+    return {}
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.out = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.out.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, pw, reasons = [], 0, [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+                pw.append(float(f[3]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        load = sorted(sm)
+        med = load[len(load) // 2]
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "power_w_median": sorted(pw)[len(pw) // 2] if pw else None,
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU baseline --
+def cpu_reference(a, est_full, e_full, reps, threads=None):
+    """Time the reference CPU path on this host's cores on a bounded sample and
+    project it onto this workload's exact entry counts.
+
+    Sample (per worker thread, one head each, concurrent -- SPEC.md:87): the
+    reference's own chunked_prefill (sparse mode, DcaContinuous selection, DCA
+    remapped attention) on n_s = 4096 tokens in 1024-token chunks, budget (64, 128),
+    plus one estimate_block of 64 rows x 4096 keys.  The estimate-only phase gives the
+    per-entry estimator rate; the chunked phase minus its estimator share gives the
+    per-admitted-entry attention rate.  Projected seconds for the workload =
+    r_est * (estimator entries) + r_att * (admitted entries), both exact counts of the
+    GPU run."""
+    import numpy as np
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from oracle import Oracle, ref_available
+    kind = "reference" if ref_available() else "port"
+    orc = Oracle(kind)
+    cnt = Oracle("port") if kind == "reference" else orc
+    threads = threads or os.cpu_count() or 1
+    ns, chunk, lq, bud = 4096, 1024, 64, (64, 128)
+    cfg = (1024, 2048, 1024)
+    rng = np.random.default_rng(a.seed)
+    heads = [tuple(rng.standard_normal((ns, 128)).astype(np.float32).astype(np.float64)
+                   for _ in range(3)) for _ in range(threads)]
+    est_entries_one = sum(ns - lq + r + 1 for r in range(lq))
+
+    def run_pool(fn):
+        res = [None] * threads
+        ts = [threading.Thread(target=lambda i=i: res.__setitem__(i, fn(i)))
+              for i in range(threads)]
+        t0 = time.perf_counter()
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        return time.perf_counter() - t0, res
+
+    t_est, t_cp, est_cp, e_cp = 0.0, 0.0, 0, 0
+    for _ in range(reps):
+        dt, _ = run_pool(lambda i: orc.estimate_block(heads[i][0][ns - lq:], heads[i][1], lq, 1,
+                                                      cfg, a.rope_base))
+        t_est += dt
+
+        def cp(i):
+            q, k, v = heads[i]
+            _, _, sels = orc.chunked_prefill(q, k, v, chunk, lq, bud, "sparse", 1, cfg,
+                                             rope_base=a.rope_base, temperature=1.0)
+            e = 0
+            for s in sels:
+                cv, cs = s.critical.verticals, s.critical.slashes
+                e += cnt.admitted_count(cv, cs, s.end) - (
+                    cnt.admitted_count(cv, cs, s.begin) if s.begin else 0)
+            est = sum(sum(s.end - min(lq, s.end - s.begin) + r + 1
+                          for r in range(min(lq, s.end - s.begin))) for s in sels)
+            return e, est
+
+        dt, res = run_pool(cp)
+        t_cp += dt
+        e_cp += sum(r[0] for r in res)
+        est_cp += sum(r[1] for r in res)
+    r_est = t_est / (reps * threads * est_entries_one)          # wall s per entry, all threads
+    r_att = max(t_cp - r_est * est_cp, 1e-12) / max(e_cp, 1)
+    secs = r_est * est_full + r_att * e_full
+    return {
+        "value": a.n / secs, "unit": "tokens/s", "cores": threads, "kind": kind,
+        "projected_seconds": secs,
+        "rates_us_per_entry_wall": {"estimate": r_est * 1e6, "attention": r_att * 1e6},
+        "sample": (f"{reps} reps x {threads} threads (one head each): reference chunked_prefill "
+                   f"n=4096, chunk 1024, lastQ 64, budget (64,128), DcaContinuous, DCA "
+                   f"(1024,2048,1024) + estimate_block 64x4096; projected onto this workload's "
+                   f"{est_full:.3e} estimator entries and {e_full:.3e} admitted entries"),
+        "sample_seconds": t_est + t_cp,
+    }
+
+
+def exact_estimator_entries(a):
+    """sum over chunks and query heads of the causal (row, key) entries K1 scores."""
+    tot = 0
+    for t0 in range(0, a.n, a.chunk):
+        t1 = min(a.n, t0 + a.chunk)
+        b = min(a.last_q, t1 - t0)
+        tot += b * (t1 - b) + b * (b + 1) // 2
+    return tot * a.hq
+
+
+def approx_admitted(a):
+    """Upper-bound estimate of admitted entries (for --impl reference without a GPU run):
+    every row admits min(i+1, V+1 + S+B) entries."""
+    per = a.budget[0] + 1 + a.budget[1] + a.last_q
+    tot = 0
+    for i0 in range(0, a.n, 4096):
+        i = i0 + 2048
+        tot += 4096 * min(i + 1, per)
+    return tot * a.hq
+
+
+# ------------------------------------------------------------ reference arm --
+def run_reference(a, rank):
+    if rank != 0:
+        return
+    est_full = exact_estimator_entries(a)
+    e_full = approx_admitted(a)
+    steps = []
+    for w in range(a.warmup + a.steps):
+        r = cpu_reference(a, est_full, e_full, reps=1)
+        if w >= a.warmup:
+            steps.append(r)
+    secs = sorted(s["projected_seconds"] for s in steps)[len(steps) // 2]
+    last = steps[-1]
+    val = a.n / secs
+    line = {
+        "metric": METRIC, "impl": "reference", "value": val, "unit": "tokens/s",
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": secs * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload(a),
+        "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": last["cores"],
+                         "kind": last["kind"], "sample": last["sample"],
+                         "rates_us_per_entry_wall": last["rates_us_per_entry_wall"]},
+        "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "note": "admitted entries projected as min(i+1, V+1+S+lastQ) per row (upper bound); "
+                "the main arm's cpu_baseline uses the exact count of its GPU run",
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------- ours --
+def main():
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        run_reference(a, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2501_15383_b200 import device as D
+    from paper_2501_15383_b200 import shard as SH
+    from paper_2501_15383_b200._lib import context
+    from paper_2501_15383_b200.synth import make_qkv
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    s, c = a.dca
+    dca = (s, c, min(s, c - s))
+    temp = yarn_t(a.n / c)
+    # every rank generates the same seeded full inputs, then keeps its shard
+    q, k, v = make_qkv(a.n, a.hq, a.hkv, kind=a.kind, seed=a.seed, rope_base=a.rope_base,
+                       device=dev)
+    plan = SH.plan(a.n, a.hq, a.hkv, world, rank, a.shard)
+    qs, ks, vs = SH.take(plan, q, k, v)
+    del q, k, v
+    torch.cuda.empty_cache()
+    ctx = context(local)
+    ctx.set_profiling(True)
+    kw = dict(chunk_len=a.chunk, last_q=a.last_q, budget=tuple(a.budget),
+              position_mode="dca_continuous", dca=dca, temperature=temp, rope_base=a.rope_base)
+    stream = torch.cuda.current_stream()
+
+    def step(return_admitted=False):
+        return SH.prefill(plan, qs, ks, vs, return_admitted=return_admitted, **kw)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(a.warmup):
+        step()
+    # exact admitted-entry count of this workload (untimed extra run)
+    r = step(return_admitted=True)
+    E_local = int(r["admitted"].sum()) if "admitted" in r else 0
+    del r
+    barrier()
+
+    sampler = ClockSampler(local) if local == 0 else None
+    if sampler:
+        sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stage = {"ms_estimate": 0.0, "ms_select": 0.0, "ms_attention": 0.0, "ms_tc_kernel": 0.0,
+             "ms_total": 0.0, "simt_entries": 0, "launches": 0, "chunks": 0}
+    barrier()
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+        st = ctx.stats()
+        for key in stage:
+            stage[key] += st[key]
+    e1.record(stream)
+    barrier()
+    clocks = sampler.stop() if sampler else None
+    ms_local = e0.elapsed_time(e1)
+    ms = ms_local
+    t_all = torch.tensor([ms_local, float(E_local)], dtype=torch.float64, device=dev)
+    if world > 1:
+        mx = t_all.clone()
+        dist.all_reduce(mx[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t_all[1:], op=dist.ReduceOp.SUM)
+        ms = float(mx[0])
+    E_total = int(t_all[1].item())
+    ms_step = ms / a.steps
+    value = a.n / (ms_step / 1e3)
+
+    # ---- end to end through the host entry (pinned host buffers) ----
+    e2e = None
+    if not a.no_e2e:
+        e2e = SH.e2e(plan, qs, ks, vs, a.steps, barrier, world, dev, **kw)
+        if e2e is not None:
+            e2e["value"] = a.n / (e2e.pop("ms_per_step") / 1e3)
+
+    # ---- roofline of the dominant kernel (this rank's stage times) ----
+    peaks, src = load_peaks()
+    K = a.steps
+    ch = max(stage["chunks"], 1)
+    ch = ch // K  # chunks per step (stats accumulate over the K steps)
+    simt = stage["simt_entries"] / K
+    E_rank = E_local
+    tc_entries = max(E_rank - simt, 0)
+    t_tc = stage["ms_tc_kernel"] / K / 1e3
+    t_est = stage["ms_estimate"] / K / 1e3
+    t_simt = max(stage["ms_attention"] - stage["ms_tc_kernel"], 0.0) / K / 1e3
+    est_bytes = 0
+    for t0 in range(plan.row0, plan.row0 + plan.n, a.chunk):
+        t1 = min(plan.n, t0 - plan.row0 + a.chunk)
+        est_bytes += plan.hkv * t1 * 128 * 2 + plan.hq * min(a.last_q, t1) * 128 * 2 \
+            + 2 * plan.hq * t1 * 4
+    tflops_peak = peak_value(peaks, "bf16_tflops_sustained", 1400.0)
+    hbm_peak = peak_value(peaks, "hbm_gbs", 6650.0)
+    traffic = ncu_traffic()
+    kernels = {
+        "attn_tc": {"bound": "tensor", "ms_per_step": t_tc * 1e3, "launches_per_step": ch,
+                    "achieved": 4 * 128 * tc_entries / max(t_tc, 1e-12) / 1e12,
+                    "unit": "TFLOP/s", "entries": tc_entries,
+                    "note": "4*D FLOPs per admitted entry on the tcgen05 tiles "
+                            "(verticals, band, dense slash tiles)"},
+        "attn_simt": {"bound": "hbm", "ms_per_step": t_simt * 1e3,
+                      "achieved": 2 * 128 * 2 * simt / max(t_simt, 1e-12) / 1e9,
+                      "unit": "GB/s", "entries": simt,
+                      "note": "isolated-slash gather: K and V row (2*D*2 B) per entry; "
+                              "includes the per-chunk index build"},
+        "estimate": {"bound": "hbm", "ms_per_step": t_est * 1e3,
+                     "achieved": est_bytes / max(t_est, 1e-12) / 1e9, "unit": "GB/s",
+                     "note": "K once + Q rows + 2 fp32 score arrays per chunk"},
+    }
+    for kname, kv in kernels.items():
+        kv["peak"] = tflops_peak if kv["bound"] == "tensor" else hbm_peak
+        kv["frac"] = kv["achieved"] / kv["peak"]
+    dom = max(kernels, key=lambda x: kernels[x]["ms_per_step"])
+    kd = kernels[dom]
+    tr = traffic.get(dom)
+    roofline = {"kernel": dom, "bound": kd["bound"], "achieved": kd["achieved"],
+                "peak": kd["peak"], "unit": kd["unit"], "frac": kd["frac"],
+                "traffic": tr, "peak_source": src,
+                "peak_note": ("sustained bf16 (kernel timed inside a long step)"
+                              if kd["bound"] == "tensor" else "HBM copy bandwidth")}
+    alg_tflops = 4 * 128 * E_total / (ms_step / 1e3) / 1e12
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        try:
+            cpu = cpu_reference(a, exact_estimator_entries(a), E_total, reps=a.cpu_reps)
+        except Exception as ex:  # the baseline must not hide the GPU number
+            cpu = {"error": str(ex)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (seeded structured Q/K/V generated on device)",
+            "config": {**workload(a), "parallelism": plan.describe()},
+            "roofline": roofline, "kernels": kernels,
+            "algorithmic_tflops_whole_step": alg_tflops,
+            "pct_tc_roofline_whole_step": alg_tflops / tflops_peak,
+            "admitted_entries": E_total,
+            "density": E_total / (a.hq * a.n * (a.n + 1) / 2),
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": int(stage["launches"]),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -17,6 +17,8 @@
  *   lcx_sparse_attention    <- longctx::sparse_attention    core/include/longctx/sparse.hpp:87-88
  *   lcx_full_attention      <- longctx::full_attention      core/include/longctx/attention.hpp:57-58
  *   lcx_chunked_prefill     <- longctx::chunked_prefill     core/include/longctx/sparse.hpp:125-129
+ *   lcx_chunked_prefill_host <- the same operator on HOST buffers (the reference
+ *                              API's by-value matrices), chunk-pipelined copies
  *   lcx_attention_recall    <- longctx::attention_recall    core/include/longctx/refine.hpp:25-26
  *   lcx_lse_merge           <- (new) log-sum-exp merge of KV-sequence shards (north star (e))
  *
@@ -206,6 +208,19 @@ int lcx_full_attention(lcx_context* ctx, const lcx_attention_input* in, int32_t 
 /* The operator: chunked prefill over all heads and chunks of one layer. */
 int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
                         const lcx_prefill_config* cfg, lcx_prefill_output* out, void* stream);
+
+/* Host-buffer entry of the operator -- what the reference's by-value API
+ * (chunked_prefill taking host matrices, sparse.hpp:125-129) maps onto.
+ * in->q / k / v / positions_* and every out-> pointer are HOST pointers
+ * (page-locked memory gives full copy / compute overlap; pageable works).
+ * Chunk c's Q/K/V rows are copied host-to-device on a copy stream while
+ * earlier chunks compute; chunk c's output rows, lse and selections are copied
+ * back on a second stream as soon as chunk c is final.  Device staging is
+ * owned by the context.  Synchronous: returns once every host output is
+ * written (or on the first error). */
+int lcx_chunked_prefill_host(lcx_context* ctx, const lcx_attention_input* in,
+                             const lcx_prefill_config* cfg, lcx_prefill_output* out,
+                             void* stream);
 
 /* ---- recall (part d) ----------------------------------------------------- */
 /* per_query[i] = min(1, exp(lse_s - lse_f)); LCX_ERR_DOMAIN if any value

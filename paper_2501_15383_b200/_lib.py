@@ -72,7 +72,8 @@ EXPORTS = [
     "lcx_context_create", "lcx_context_destroy", "lcx_last_error", "lcx_version",
     "lcx_device_ok", "lcx_set_profiling", "lcx_get_stats", "lcx_estimate_block",
     "lcx_line_scores", "lcx_select_from_scores", "lcx_select_critical", "lcx_sparse_attention",
-    "lcx_full_attention", "lcx_chunked_prefill", "lcx_attention_recall", "lcx_lse_merge",
+    "lcx_full_attention", "lcx_chunked_prefill", "lcx_chunked_prefill_host",
+    "lcx_attention_recall", "lcx_lse_merge",
 ]
 
 _lib = None
@@ -111,6 +112,8 @@ def lib() -> C.CDLL:
                                              vp, vp, vp]
             L.lcx_chunked_prefill.argtypes = [vp, P(AttentionInputC), P(PrefillConfigC),
                                               P(PrefillOutputC), vp]
+            L.lcx_chunked_prefill_host.argtypes = [vp, P(AttentionInputC), P(PrefillConfigC),
+                                                   P(PrefillOutputC), vp]
             L.lcx_attention_recall.argtypes = [vp, vp, vp, i64, dbl, vp, P(dbl), vp]
             L.lcx_lse_merge.argtypes = [vp, vp, vp, i32, i64, i32, vp, vp, vp]
             _lib = L

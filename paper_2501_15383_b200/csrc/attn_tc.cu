@@ -778,12 +778,13 @@ __global__ void plan_items_kernel(const TcParams p, Item* __restrict__ plans) {
 // ---------------------------------------------------------------- prep --
 // K_hi / K_lo [n][hkv][128] bf16 = split(rope(k_j, kpos(j))), kpos = pos_k[j]
 // (standard) or j mod s (DCA).
-__global__ void k_prep_kernel(const __nv_bfloat16* __restrict__ k, int64_t n, int hkv,
-                              const int64_t* __restrict__ pos_k, int rel_mode, int64_t s,
-                              const float2* __restrict__ rope, __nv_bfloat16* __restrict__ khi,
-                              __nv_bfloat16* __restrict__ klo) {
-  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // pair index
-  const int64_t total = n * hkv * (HD / 2);
+__global__ void k_prep_kernel(const __nv_bfloat16* __restrict__ k, int64_t n, int64_t r0,
+                              int64_t r1, int hkv, const int64_t* __restrict__ pos_k,
+                              int rel_mode, int64_t s, const float2* __restrict__ rope,
+                              __nv_bfloat16* __restrict__ khi, __nv_bfloat16* __restrict__ klo) {
+  // pair index over rows [r0, r1)
+  const int64_t idx = r0 * hkv * (HD / 2) + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t total = r1 * hkv * (HD / 2);
   if (idx >= total) return;
   const int pr = int(idx % (HD / 2));
   const int64_t rowhead = idx / (HD / 2);
@@ -804,11 +805,12 @@ __global__ void k_prep_kernel(const __nv_bfloat16* __restrict__ k, int64_t n, in
 }
 
 // V^T [hkv][128][npad] fp16 from V [n][hkv][128] bf16 (smem-tiled transpose)
-__global__ void vt_prep_kernel(const __nv_bfloat16* __restrict__ v, int64_t n, int hkv,
-                               int64_t npad, __half* __restrict__ vt) {
+__global__ void vt_prep_kernel(const __nv_bfloat16* __restrict__ v, int64_t n, int64_t tile0,
+                               int hkv, int64_t npad, __half* __restrict__ vt) {
   __shared__ __half tile[64][HD + 8];
   const int g = blockIdx.y;
-  const int64_t j0 = int64_t(blockIdx.x) * 64;
+  const int64_t jt = tile0 + blockIdx.x;
+  const int64_t j0 = jt * 64;
   for (int x = threadIdx.x; x < 64 * HD; x += blockDim.x) {
     const int jj = x / HD, d = x % HD;
     const int64_t j = j0 + jj;
@@ -816,7 +818,7 @@ __global__ void vt_prep_kernel(const __nv_bfloat16* __restrict__ v, int64_t n, i
   }
   __syncthreads();
   const int64_t nt = npad / 64;
-  __half* dst = vt + (int64_t(g) * nt + blockIdx.x) * (HD * 64);  // [128 dims][64 keys]
+  __half* dst = vt + (int64_t(g) * nt + jt) * (HD * 64);  // [128 dims][64 keys]
   for (int x = threadIdx.x; x < 64 * HD; x += blockDim.x) {
     const int d = x / 64, jj = x % 64;
     dst[d * 64 + jj] = tile[jj][d];
@@ -1077,17 +1079,28 @@ int make_map3(CUtensorMap* m, CUtensorMapDataType dt, void* base, uint64_t d0, u
 }  // namespace
 
 // ------------------------------------------------------------ host API --
-int tc_prepare(const void* k, const void* v, int64_t n, int hq, int hkv, const int64_t* pos_k,
-               int rel_mode, int64_t s, const float2* rope, TcBuffers& B, cudaStream_t st) {
+int tc_prepare_rows(const void* k, const void* v, int64_t n, int64_t r0, int64_t r1, int hkv,
+                    const int64_t* pos_k, int rel_mode, int64_t s, const float2* rope,
+                    const TcBuffers& B, cudaStream_t st) {
+  r1 = lcx_min64(r1, n);
+  if (r1 <= r0) return LCX_OK;
+  const int64_t pairs = (r1 - r0) * hkv * (HD / 2);
+  k_prep_kernel<<<unsigned((pairs + 255) / 256), 256, 0, st>>>(
+      reinterpret_cast<const __nv_bfloat16*>(k), n, r0, r1, hkv, pos_k, rel_mode, s, rope, B.khi,
+      B.klo);
+  LCX_CHECK_LAUNCH();
+  // V^T tiles covering [r0, r1); a partial trailing tile is rewritten (zero-padded) by the
+  // range that completes it, so ranges must be handed in ascending order
+  const int64_t tile0 = r0 / 64, tile1 = r1 == n ? B.npad / 64 : (r1 + 63) / 64;
+  vt_prep_kernel<<<dim3(unsigned(tile1 - tile0), unsigned(hkv)), 256, 0, st>>>(
+      reinterpret_cast<const __nv_bfloat16*>(v), r1, tile0, hkv, B.npad, B.vt);
+  LCX_CHECK_LAUNCH();
+  return LCX_OK;
+}
+
+int tc_prepare_maps(int hq, int hkv, TcBuffers& B) {
   const int64_t capp = B.capp;
   if (capp >= (int64_t(1) << 31)) return fail(LCX_ERR_DIMENSION, "vertical capacity too large");
-  const int64_t pairs = n * hkv * (HD / 2);
-  k_prep_kernel<<<unsigned((pairs + 255) / 256), 256, 0, st>>>(
-      reinterpret_cast<const __nv_bfloat16*>(k), n, hkv, pos_k, rel_mode, s, rope, B.khi, B.klo);
-  LCX_CHECK_LAUNCH();
-  vt_prep_kernel<<<dim3(unsigned(B.npad / 64), unsigned(hkv)), 256, 0, st>>>(
-      reinterpret_cast<const __nv_bfloat16*>(v), n, hkv, B.npad, B.vt);
-  LCX_CHECK_LAUNCH();
   const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, F16 = CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   const uint64_t nt = uint64_t(B.npad / 64), ct = uint64_t(capp / 64);
   // tiled operands: every box is one contiguous block (8 KB K half-tile, 16 KB V^T tile)
@@ -1098,6 +1111,12 @@ int tc_prepare(const void* k, const void* v, int64_t n, int hq, int hkv, const i
   LCX_TRY(make_map3(&B.m_kclo, BF, B.kclo, 64, 64, hq * ct * 2, 128, 8192, 64, 64, 1));
   LCX_TRY(make_map3(&B.m_vct, F16, B.vct, 64, HD, hq * ct, 128, 16384, 64, HD, 1));
   return LCX_OK;
+}
+
+int tc_prepare(const void* k, const void* v, int64_t n, int hq, int hkv, const int64_t* pos_k,
+               int rel_mode, int64_t s, const float2* rope, TcBuffers& B, cudaStream_t st) {
+  LCX_TRY(tc_prepare_maps(hq, hkv, B));
+  return tc_prepare_rows(k, v, n, 0, n, hkv, pos_k, rel_mode, s, rope, B, st);
 }
 
 int tc_compact(const void* v, int hq, int hkv, const int32_t* verts, const int32_t* nv,

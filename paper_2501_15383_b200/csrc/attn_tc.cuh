@@ -64,6 +64,11 @@ void tc_layout(A& ar, int64_t n, int hq, int hkv, int64_t cap_v, int64_t seg_len
 
 int tc_prepare(const void* k, const void* v, int64_t n, int hq, int hkv, const int64_t* pos_k,
                int rel_mode, int64_t s, const float2* rope, TcBuffers& B, cudaStream_t st);
+int tc_prepare_maps(int hq, int hkv, TcBuffers& B);
+// rotated K (hi/lo) and V^T for key rows [r0, r1) only (chunk-incremental preparation)
+int tc_prepare_rows(const void* k, const void* v, int64_t n, int64_t r0, int64_t r1, int hkv,
+                    const int64_t* pos_k, int rel_mode, int64_t s, const float2* rope,
+                    const TcBuffers& B, cudaStream_t st);
 int tc_compact(const void* v, int hq, int hkv, const int32_t* verts, const int32_t* nv,
                int64_t cap_v, TcBuffers& B, cudaStream_t st);
 int tc_classify(const int32_t* slashes, const int32_t* ns, int64_t cap_s, int hq, int64_t U,

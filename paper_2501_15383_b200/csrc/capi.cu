@@ -367,6 +367,11 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 int64_t words_for(int64_t n) { return (n + 31) / 32 + 1; }
 
 }  // namespace
+
+int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_prefill_config* cfg,
+                 lcx_prefill_output* out, cudaStream_t st, const cudaEvent_t* ready,
+                 const cudaEvent_t* done);
+
 }  // namespace lcx
 
 using namespace lcx;
@@ -407,6 +412,10 @@ int lcx_context_destroy(lcx_context* ctx) {
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->rope) cudaFree(ctx->rope);
   if (ctx->tile_counter) cudaFree(ctx->tile_counter);
+  if (ctx->trace) cudaFree(ctx->trace);
+  if (ctx->stage) cudaFree(ctx->stage);
+  if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
+  if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
   delete ctx;
   return LCX_OK;
 }
@@ -584,6 +593,158 @@ int lcx_full_attention(lcx_context* ctx, const lcx_attention_input* in, int32_t 
 
 int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
                         const lcx_prefill_config* cfg, lcx_prefill_output* out, void* stream) {
+  return prefill_impl(ctx, in, cfg, out, S(stream), nullptr, nullptr);
+}
+
+// Host-buffer entry: chunk-pipelined H2D / compute / D2H over three streams.
+int lcx_chunked_prefill_host(lcx_context* ctx, const lcx_attention_input* hin,
+                             const lcx_prefill_config* cfg, lcx_prefill_output* hout,
+                             void* stream) {
+  LCX_TRY(validate_input(hin));
+  if (!cfg || !hout || !hout->out || !hout->lse)
+    return fail(LCX_ERR_DIMENSION, "null config/output");
+  if (cfg->chunk_len <= 0) return fail(LCX_ERR_CONFIG, "chunkLen must be positive");
+  cudaStream_t st = S(stream);
+  const int64_t n = hin->n, L = cfg->chunk_len, nch = (n + L - 1) / L;
+  const int hq = hin->hq, hkv = hin->hkv, dim = hin->dim;
+  const size_t es = hin->dtype == LCX_BF16 ? 2 : 4;
+  const bool sel = hout->sel_verticals && hout->sel_nv && hout->sel_slashes && hout->sel_ns;
+  const int64_t cap_v = sel ? hout->cap_v : 0, cap_s = sel ? hout->cap_s : 0;
+  // device staging (context-owned, grown on demand)
+  auto plan = [&](auto& A, void** q, void** k, void** v, int64_t** pq, int64_t** pk, float** o,
+                  float** l, int32_t** sv, int32_t** snv, int32_t** ss, int32_t** sns,
+                  int64_t** adm) {
+    *q = A.template take<char>(size_t(n) * hq * dim * es);
+    *k = A.template take<char>(size_t(n) * hkv * dim * es);
+    *v = A.template take<char>(size_t(n) * hkv * dim * es);
+    *pq = hin->positions_q ? A.template take<int64_t>(size_t(n)) : nullptr;
+    *pk = hin->positions_k ? A.template take<int64_t>(size_t(n)) : nullptr;
+    *o = A.template take<float>(size_t(n) * hq * dim);
+    *l = A.template take<float>(size_t(hq) * n);
+    *sv = sel ? A.template take<int32_t>(size_t(nch) * hq * cap_v) : nullptr;
+    *snv = sel ? A.template take<int32_t>(size_t(nch) * hq) : nullptr;
+    *ss = sel ? A.template take<int32_t>(size_t(nch) * hq * cap_s) : nullptr;
+    *sns = sel ? A.template take<int32_t>(size_t(nch) * hq) : nullptr;
+    *adm = hout->admitted ? A.template take<int64_t>(size_t(nch) * hq) : nullptr;
+  };
+  void *dq, *dk, *dv;
+  int64_t *dpq, *dpk, *dadm;
+  float *dout, *dlse;
+  int32_t *dsv, *dsnv, *dss, *dsns;
+  Sizer sz;
+  plan(sz, &dq, &dk, &dv, &dpq, &dpk, &dout, &dlse, &dsv, &dsnv, &dss, &dsns, &dadm);
+  if (sz.off > ctx->stage_bytes) {
+    if (ctx->stage) LCX_CHECK_CUDA(cudaFree(ctx->stage));
+    ctx->stage = nullptr;
+    ctx->stage_bytes = 0;
+    LCX_CHECK_CUDA(cudaMalloc(&ctx->stage, sz.off));
+    ctx->stage_bytes = sz.off;
+  }
+  Arena ar{ctx->stage, ctx->stage_bytes, 0};
+  plan(ar, &dq, &dk, &dv, &dpq, &dpk, &dout, &dlse, &dsv, &dsnv, &dss, &dsns, &dadm);
+  if (!ctx->h2d) LCX_CHECK_CUDA(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
+  if (!ctx->d2h) LCX_CHECK_CUDA(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
+  // positions are validated before the chunk loop: upload them first
+  if (dpq) LCX_CHECK_CUDA(cudaMemcpy(dpq, hin->positions_q, 8 * n, cudaMemcpyHostToDevice));
+  if (dpk) LCX_CHECK_CUDA(cudaMemcpy(dpk, hin->positions_k, 8 * n, cudaMemcpyHostToDevice));
+  std::vector<cudaEvent_t> ready(nch), done(nch);
+  for (int64_t c = 0; c < nch; ++c) {
+    LCX_CHECK_CUDA(cudaEventCreateWithFlags(&ready[c], cudaEventDisableTiming));
+    LCX_CHECK_CUDA(cudaEventCreateWithFlags(&done[c], cudaEventDisableTiming));
+  }
+  cudaEvent_t start;
+  LCX_CHECK_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  LCX_CHECK_CUDA(cudaEventRecord(start, st));
+  LCX_CHECK_CUDA(cudaStreamWaitEvent(ctx->h2d, start, 0));
+  int rc = LCX_OK;
+  // H2D: token-major rows [t0, t1) of q, k, v are contiguous slabs
+  for (int64_t c = 0; c < nch && rc == LCX_OK; ++c) {
+    const int64_t t0 = c * L, t1 = std::min(n, t0 + L);
+    auto cp = [&](void* d, const void* h, size_t row_bytes) {
+      return cudaMemcpyAsync(static_cast<char*>(d) + t0 * row_bytes,
+                             static_cast<const char*>(h) + t0 * row_bytes,
+                             (t1 - t0) * row_bytes, cudaMemcpyHostToDevice, ctx->h2d);
+    };
+    if (cp(dq, hin->q, size_t(hq) * dim * es) != cudaSuccess ||
+        cp(dk, hin->k, size_t(hkv) * dim * es) != cudaSuccess ||
+        cp(dv, hin->v, size_t(hkv) * dim * es) != cudaSuccess ||
+        cudaEventRecord(ready[c], ctx->h2d) != cudaSuccess)
+      rc = fail(LCX_ERR_CUDA, "host-to-device copy failed");
+  }
+  if (rc == LCX_OK) {
+    lcx_attention_input din = *hin;
+    din.q = dq;
+    din.k = dk;
+    din.v = dv;
+    din.positions_q = dpq;
+    din.positions_k = dpk;
+    lcx_prefill_output dout_s{dout, dlse, dsv, dsnv, dss, dsns, cap_v, cap_s, dadm};
+    rc = prefill_impl(ctx, &din, cfg, &dout_s, st, ready.data(), done.data());
+  }
+  // D2H of each chunk's rows as soon as the chunk is final
+  const int64_t nrec = rc == LCX_OK ? nch : 0;
+  for (int64_t c = 0; c < nrec && rc == LCX_OK; ++c) {
+    const int64_t t0 = c * L, t1 = std::min(n, t0 + L);
+    cudaError_t e = cudaStreamWaitEvent(ctx->d2h, done[c], 0);
+    const size_t orow = size_t(hq) * dim * sizeof(float);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(reinterpret_cast<char*>(hout->out) + t0 * orow,
+                          reinterpret_cast<char*>(dout) + t0 * orow, (t1 - t0) * orow,
+                          cudaMemcpyDeviceToHost, ctx->d2h);
+    if (e == cudaSuccess)
+      e = cudaMemcpy2DAsync(hout->lse + t0, sizeof(float) * n, dlse + t0, sizeof(float) * n,
+                            sizeof(float) * (t1 - t0), hq, cudaMemcpyDeviceToHost, ctx->d2h);
+    if (e == cudaSuccess && sel) {
+      e = cudaMemcpyAsync(hout->sel_verticals + c * hq * cap_v, dsv + c * hq * cap_v,
+                          sizeof(int32_t) * hq * cap_v, cudaMemcpyDeviceToHost, ctx->d2h);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(hout->sel_slashes + c * hq * cap_s, dss + c * hq * cap_s,
+                            sizeof(int32_t) * hq * cap_s, cudaMemcpyDeviceToHost, ctx->d2h);
+    }
+    if (e != cudaSuccess) rc = fail(LCX_ERR_CUDA, "device-to-host copy failed");
+  }
+  if (rc == LCX_OK && sel) {
+    if (cudaMemcpyAsync(hout->sel_nv, dsnv, sizeof(int32_t) * nch * hq, cudaMemcpyDeviceToHost,
+                        ctx->d2h) != cudaSuccess ||
+        cudaMemcpyAsync(hout->sel_ns, dsns, sizeof(int32_t) * nch * hq, cudaMemcpyDeviceToHost,
+                        ctx->d2h) != cudaSuccess)
+      rc = fail(LCX_ERR_CUDA, "device-to-host copy failed");
+  }
+  if (rc == LCX_OK && hout->admitted) {
+    if (cudaMemcpyAsync(hout->admitted, dadm, sizeof(int64_t) * nch * hq, cudaMemcpyDeviceToHost,
+                        ctx->d2h) != cudaSuccess)
+      rc = fail(LCX_ERR_CUDA, "device-to-host copy failed");
+  }
+  // the caller's stream observes completion of every copy
+  cudaEvent_t fin;
+  cudaEventCreateWithFlags(&fin, cudaEventDisableTiming);
+  cudaEventRecord(fin, ctx->d2h);
+  cudaStreamWaitEvent(st, fin, 0);
+  const cudaError_t e1 = cudaStreamSynchronize(ctx->h2d);
+  const cudaError_t e2 = cudaStreamSynchronize(ctx->d2h);
+  const cudaError_t e3 = cudaStreamSynchronize(st);
+  for (auto& x : ready) cudaEventDestroy(x);
+  for (auto& x : done) cudaEventDestroy(x);
+  cudaEventDestroy(start);
+  cudaEventDestroy(fin);
+  if (rc != LCX_OK) return rc;
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)
+    return fail(LCX_ERR_CUDA, std::string("host prefill: ") +
+                                  cudaGetErrorString(e1 != cudaSuccess ? e1
+                                                     : e2 != cudaSuccess ? e2 : e3));
+  return LCX_OK;
+}
+
+}  // extern "C"
+
+namespace lcx {
+
+// The operator body.  ready[c] (optional) is waited on before chunk c touches its
+// rows (host-pipelined entry: Q/K/V rows of chunk c arrive on a copy stream);
+// done[c] (optional) is recorded once chunk c's output rows and lse are final.
+int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_prefill_config* cfg,
+                 lcx_prefill_output* out, cudaStream_t st, const cudaEvent_t* ready,
+                 const cudaEvent_t* done) {
   LCX_TRY(validate_input(in));
   if (!cfg || !out || !out->out || !out->lse) return fail(LCX_ERR_DIMENSION, "null config/output");
   if (cfg->chunk_len <= 0) return fail(LCX_ERR_CONFIG, "chunkLen must be positive");
@@ -596,7 +757,6 @@ int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
   if (cfg->budget_vertical < 0 || cfg->budget_slash < 0)
     return fail(LCX_ERR_CONFIG, "budgets must be non-negative");
 
-  cudaStream_t st = S(stream);
   const int64_t n = in->n;
   const int hq = in->hq;
   const int64_t L = cfg->chunk_len;
@@ -655,9 +815,7 @@ int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
   Arena ar{ctx->ws, ctx->ws_bytes, 0};
   layout(ar, w, &col, &sl, &iv, &inv, &is, &ins, &est_off);
   Arena est_ar{ctx->ws, ctx->ws_bytes, est_off};
-  if (tc)
-    LCX_TRY(tc_prepare(in->k, in->v, n, hq, in->hkv, in->positions_k, dca ? 1 : 0, s, ctx->rope,
-                       w.B, st));
+  if (tc) LCX_TRY(tc_prepare_maps(hq, in->hkv, w.B));
   const bool prof = ctx->profiling != 0;
   const long long launches0 = g_launches;
   std::vector<cudaEvent_t> ev;
@@ -676,7 +834,12 @@ int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
     int32_t* slist = out->sel_slashes ? out->sel_slashes + ci * hq * cap_s : is;
     int32_t* scnt = out->sel_ns ? out->sel_ns + ci * hq : ins;
     cudaEvent_t* e = prof ? &ev[6 * ci] : nullptr;
+    if (ready) LCX_CHECK_CUDA(cudaStreamWaitEvent(st, ready[ci], 0));
     if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[0], st));
+    // rotated K / V^T of this chunk's new key rows (chunks only ever append keys)
+    if (tc)
+      LCX_TRY(tc_prepare_rows(in->k, in->v, n, t0, t1, in->hkv, in->positions_k, dca ? 1 : 0, s,
+                              ctx->rope, w.B, st));
     if (sparse) {
       EstimateArgs es = base_est(in, ctx, t0, t1 - t0, t1, cfg->last_q, dca ? 1 : 0, c);
       es.col = col;
@@ -696,6 +859,7 @@ int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
                             out->admitted ? out->admitted + ci * hq : nullptr, st,
                             (prof && tc) ? e[4] : nullptr, (prof && tc) ? e[5] : nullptr));
     if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[3], st));
+    if (done) LCX_CHECK_CUDA(cudaEventRecord(done[ci], st));
   }
   ctx->stats = lcx_prefill_stats{};
   ctx->stats.chunks = nchunks;
@@ -736,6 +900,10 @@ int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
   }
   return LCX_OK;
 }
+
+}  // namespace lcx
+
+extern "C" {
 
 int lcx_attention_recall(lcx_context* ctx, const float* lse_sparse, const float* lse_full,
                          int64_t n, double slack, float* per_query, double* aggregate,

@@ -121,6 +121,10 @@ struct lcx_context {
   int64_t* tile_counter = nullptr;  // device: [0] executed tcgen05 tiles, [1] CUDA-core entries
   long long* trace = nullptr;        // device: optional tcgen05 pipeline trace (debug)
   lcx_prefill_stats stats{};
+  // host-buffer entry: device staging + copy streams (created lazily)
+  char* stage = nullptr;
+  size_t stage_bytes = 0;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
 };
 
 namespace lcx {

@@ -256,3 +256,50 @@ def lse_merge(o_parts, lse_parts, *, stream=None, ctx=None):
     check(lib().lcx_lse_merge(ctx.ptr, _ptr(o_parts), _ptr(lse_parts), g, rows, dim, _ptr(out),
                               _ptr(lse), _stream(stream)))
     return out, lse
+
+
+def chunked_prefill_host(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
+                         position_mode="standard", dca=None, opts: Options | None = None,
+                         rope_base=1e4, temperature=1.0, kernel_path="auto", out=None, lse=None,
+                         return_selections=False, stream=None, ctx=None, device=0):
+    """chunked_prefill on HOST tensors (CPU, ideally pinned) through
+    lcx_chunked_prefill_host: chunk-pipelined H2D / compute / D2H inside the library.
+    Returns host tensors (out [n, hq, dim] fp32, lse [hq, n] fp32, selections)."""
+    for nm, t in (("q", q), ("k", k), ("v", v)):
+        if not isinstance(t, torch.Tensor) or t.is_cuda:
+            raise Error("dimension", f"{nm} must be a host tensor for the host entry")
+        if t.dtype not in (torch.float32, torch.bfloat16) or not t.is_contiguous():
+            raise Error("config", f"{nm} must be contiguous float32 / bfloat16")
+    n, hq, dim = q.shape
+    dt = 0 if q.dtype == torch.float32 else 1
+    inp = AttentionInputC(n, hq, k.shape[1], dim, dt, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                          None, None, float(rope_base), float(temperature))
+    opts = opts or Options()
+    bv, bs = int(budget[0]), int(budget[1])
+    nchunks = max(1, -(-n // max(int(chunk_len), 1)))
+    block = min(int(last_q), int(chunk_len))
+    cap_v, cap_s = bv + 2, bs + block + 1
+    if out is None:
+        out = torch.empty((n, hq, dim), dtype=torch.float32, pin_memory=True)
+    if lse is None:
+        lse = torch.empty((hq, n), dtype=torch.float32, pin_memory=True)
+    sel = {}
+    if return_selections and mode == "sparse":
+        sel["verticals"] = torch.zeros((nchunks, hq, cap_v), dtype=torch.int32)
+        sel["nv"] = torch.zeros((nchunks, hq), dtype=torch.int32)
+        sel["slashes"] = torch.zeros((nchunks, hq, cap_s), dtype=torch.int32)
+        sel["ns"] = torch.zeros((nchunks, hq), dtype=torch.int32)
+    pm = POSITION_MODES[position_mode] if isinstance(position_mode, str) else int(position_mode)
+    cfg = PrefillConfigC(int(chunk_len), int(last_q), bv, bs, PREFILL_MODES[mode], pm,
+                         _chunk(dca) or ChunkConfigC(0, 0, 0), opts.c(),
+                         KERNEL_PATHS[kernel_path], 0)
+    o = PrefillOutputC(out.data_ptr(), lse.data_ptr(),
+                       sel["verticals"].data_ptr() if sel else None,
+                       sel["nv"].data_ptr() if sel else None,
+                       sel["slashes"].data_ptr() if sel else None,
+                       sel["ns"].data_ptr() if sel else None, cap_v, cap_s, None)
+    ctx = ctx or context(device)
+    with torch.cuda.device(device):
+        check(lib().lcx_chunked_prefill_host(ctx.ptr, C.byref(inp), C.byref(cfg), C.byref(o),
+                                             _stream(stream)))
+    return dict(out=out, lse=lse, **sel)

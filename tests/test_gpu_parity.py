@@ -468,3 +468,27 @@ def test_tc_sparse_attention_custom_positions(D, port):
                                   positions_k=torch.tensor(pk).cuda(), kernel_path="tc")
     assert row_rel_err(out[:, 0].double().cpu().numpy(), ref[0]) <= 2e-3
     assert lse_rel_err(lse[0].double().cpu().numpy(), ref[1]) <= 2e-3
+
+
+# ------------------------------------------------------------ host entry --
+@pytest.mark.parametrize("precision,dca", [("bf16", (256, 768, 256)), ("fp32", None)])
+def test_host_entry_equals_device_entry(D, port, precision, dca):
+    """lcx_chunked_prefill_host (host buffers, chunk-pipelined copies) computes exactly
+    what the device entry computes: same kernels, bitwise-equal outputs and selections;
+    and the oracle agrees."""
+    import torch
+    n, hq, hkv = 1280, 4, 2
+    q, k, v = _mh_inputs(n, hq, hkv, 128, precision, 21)
+    dt = torch.float32 if precision == "fp32" else torch.bfloat16
+    H = lambda x: torch.tensor(x).to(dt).contiguous().pin_memory()  # noqa: E731
+    kw = dict(chunk_len=256, last_q=64, budget=(40, 120), temperature=0.9,
+              position_mode="dca_continuous" if dca else "standard", dca=dca)
+    rh = D.chunked_prefill_host(H(q), H(k), H(v), return_selections=True, **kw)
+    rd = D.chunked_prefill(H(q).cuda(), H(k).cuda(), H(v).cuda(), **kw)
+    assert torch.equal(rh["out"], rd["out"].cpu())
+    assert torch.equal(rh["lse"], rd["lse"].cpu())
+    for key in ("verticals", "nv", "slashes", "ns"):
+        assert torch.equal(rh[key], rd[key].cpu()), key
+    o_ref, l_ref, _ = port.chunked_prefill(q[:, 3], k[:, 1], v[:, 1], 256, 64, (40, 120),
+                                           "sparse", 1 if dca else 0, dca, temperature=0.9)
+    assert row_rel_err(rh["out"][:, 3].double().numpy(), o_ref) <= TOL[precision]
