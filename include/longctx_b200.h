@@ -16,6 +16,8 @@
  *   lcx_select_critical     <- longctx::select_critical     core/include/longctx/sparse.hpp:81-82
  *   lcx_sparse_attention    <- longctx::sparse_attention    core/include/longctx/sparse.hpp:87-88
  *   lcx_full_attention      <- longctx::full_attention      core/include/longctx/attention.hpp:57-58
+ *   lcx_attention_rel       <- full_attention / sparse_attention with a RelPositionMatrix
+ *                                                         override (attention.cpp:173-183)
  *   lcx_chunked_prefill     <- longctx::chunked_prefill     core/include/longctx/sparse.hpp:125-129
  *   lcx_chunked_prefill_host <- the same operator on HOST buffers (the reference
  *                              API's by-value matrices), chunk-pipelined copies
@@ -204,6 +206,16 @@ int lcx_sparse_attention(lcx_context* ctx, const lcx_attention_input* in,
 int lcx_full_attention(lcx_context* ctx, const lcx_attention_input* in, int32_t use_dca,
                        const lcx_chunk_config* dca, int32_t kernel_path, float* out, float* lse,
                        void* stream);
+
+/* Attention with an explicit relative-position matrix rel [n][n] (device int64):
+ * logit(i, j) = rope(q_i, rel[i][j]) . k_j (the reference's RelPositionMatrix
+ * override, attention.cpp:173-183 / sparse.cpp:400-413).  verticals == NULL: dense
+ * causal (full_attention); else the sparse lists as in lcx_sparse_attention.
+ * Exact fp32 CUDA-core path. */
+int lcx_attention_rel(lcx_context* ctx, const lcx_attention_input* in, const int32_t* verticals,
+                      const int32_t* nv, int64_t cap_v, const int32_t* slashes,
+                      const int32_t* ns, int64_t cap_s, const int64_t* rel, float* out,
+                      float* lse, void* stream);
 
 /* The operator: chunked prefill over all heads and chunks of one layer. */
 int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,

@@ -43,7 +43,8 @@ def compile_one(src, hdr_t, verbose):
         return obj, False
     cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
     if src.endswith(".cpp"):
-        cmd = [NVCC, *FLAGS, "-x", "c++", "-c", src, "-o", obj]
+        cmd = [NVCC, *[("-std=c++20" if f == "-std=c++17" else f) for f in FLAGS], "-x", "c++",
+               "-c", src, "-o", obj]
     if verbose:
         print(" ".join(cmd))
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -17,9 +17,8 @@
 //   on both a vertical and a selected diagonal is counted once, by the
 //   vertical path; sparse.cpp:95-108 dedupe),
 //   no admitted entry -> the self entry j = i (sparse.cpp:111).
-// In tcgen05 mode the slash entries come from per-head SIMT segments
-// (d, first row, last row) and the partial result of the tensor-core tiles is
-// folded in as one extra "entry" with logit lse_tc and value o_tc.
+// This is the complete exact-fp32 path (fp32 storage, any head dim <= 128, any
+// positions); in tensor-core mode the isolated slash entries go to attn_gather.cu.
 #include "lcx_internal.cuh"
 
 namespace lcx {
@@ -42,6 +41,8 @@ __device__ __forceinline__ void process_entry(const AttnArgs& a, RowState<T, PPL
   int64_t rel;
   if (a.rel_mode == 1) {
     rel = dca_relative(i, j, a.s, a.c);
+  } else if (a.rel_mode == 2) {
+    rel = a.rel_mat[i * a.rel_n + j];  // explicit RelPositionMatrix (attention.cpp:173-183)
   } else {
     const int64_t pk = a.pos_k ? a.pos_k[j] : j;
     rel = pq_i - pk;
@@ -110,22 +111,6 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(AttnArgs a) {
   }
   s.m = -INFINITY;
   s.l = 0.f;
-  if (a.o_part) {
-    const float lp = a.lse_part[int64_t(h) * a.lse_stride + i];
-    if (lp != -INFINITY) {
-      s.m = lp;
-      s.l = 1.f;
-      const float* op = a.o_part + (i * a.hq + h) * int64_t(a.dim);
-#pragma unroll
-      for (int t = 0; t < PPL; ++t) {
-        const int p = lane4 + 4 * t;
-        if (p < P) {
-          s.o[2 * t] = op[2 * p];
-          s.o[2 * t + 1] = op[2 * p + 1];
-        }
-      }
-    }
-  }
   const int64_t pq_i = a.pos_q ? a.pos_q[i] : i;
   int64_t entries = 0;
 
@@ -138,54 +123,24 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(AttnArgs a) {
     const int nv = a.nv[h], ns = a.ns[h];
     const uint32_t* vb = a.vbits + int64_t(h) * a.bit_words;
     bool any = (nv > 0 && verts[0] <= i) || (ns > 0 && sl[0] <= i);
-    if (!a.skip_verticals) {
-      for (int x = 0; x < nv; ++x) {
-        const int64_t v = verts[x];
-        if (v > i) break;
-        process_entry<T, PPL>(a, s, i, v, pq_i, g, lane4, qmask);
-        ++entries;
-      }
-    } else {
-      // the tensor-core tiles own the verticals; count them for the statistics
-      int lo = 0, hi = nv;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (verts[mid] <= i) lo = mid + 1;
-        else hi = mid;
-      }
-      (void)lo;
+    for (int x = 0; x < nv; ++x) {
+      const int64_t v = verts[x];
+      if (v > i) break;
+      process_entry<T, PPL>(a, s, i, v, pq_i, g, lane4, qmask);
+      ++entries;
     }
-    if (a.segs) {
-      // tcgen05 mode: only the slash entries routed to the CUDA-core path
-      const int4* sg = a.segs + int64_t(h) * a.cap_seg;
-      const int nseg = a.nseg[h];
-      const int64_t r = i & 127;  // row within its 128-row block
-      for (int x = 0; x < nseg; ++x) {
-        const int4 e = sg[x];     // (d, r0, r1, -), ascending d
-        const int64_t d = e.x;
-        if (d > i) break;
-        if (r < e.y || r >= e.z) continue;
-        const int64_t j = i - d;
-        if (is_vertical(vb, j)) continue;
-        process_entry<T, PPL>(a, s, i, j, pq_i, g, lane4, qmask);
-        ++entries;
-      }
-    } else {
-      for (int x = 0; x < ns; ++x) {
-        const int64_t d = sl[x];
-        if (d > i) break;
-        const int64_t j = i - d;
-        if (is_vertical(vb, j)) continue;
-        process_entry<T, PPL>(a, s, i, j, pq_i, g, lane4, qmask);
-        ++entries;
-      }
+    for (int x = 0; x < ns; ++x) {
+      const int64_t d = sl[x];
+      if (d > i) break;
+      const int64_t j = i - d;
+      if (is_vertical(vb, j)) continue;
+      process_entry<T, PPL>(a, s, i, j, pq_i, g, lane4, qmask);
+      ++entries;
     }
     if (!any) {  // self fallback (sparse.cpp:111)
       process_entry<T, PPL>(a, s, i, i, pq_i, g, lane4, qmask);
       entries = 1;
     }
-    // tcgen05 mode: nothing on this path for the row -> the tile result stands
-    if (a.segs && entries == 0) return;
   }
 
   const float inv_l = 1.f / s.l;

@@ -488,6 +488,8 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       if (lane == 0) mt.kind = T_END;
       publish();
     }
+    if (lane == 0 && p.tile_count)
+      atomicAdd(reinterpret_cast<unsigned long long*>(p.tile_count), (unsigned long long)T);
   } else if (warp == kWarpMma) {
     // ==================================================== QK issuer ====
     uint32_t T = 0, E = 0, M = 0;
@@ -924,7 +926,8 @@ classify_kernel(const int32_t* __restrict__ slashes, const int32_t* __restrict__
   __syncthreads();
   for (int x = threadIdx.x; x < cnt; x += blockDim.x) {
     const int64_t d = sl[x];
-    for (int64_t u = -((d + 63) >> 6) - 1; u <= 1; ++u) {  // floor(-d/64) .. 1
+    const int64_t u_lo = -((d + 63) >> 6) - 1;  // rows [0, 128) meet at most 3 tiles
+    for (int64_t u = u_lo; u <= u_lo + 4 && u <= 1; ++u) {
       const int64_t r0 = lcx_max64(0, d + 64 * u), r1 = lcx_min64(128, d + 64 * u + 64);
       if (r1 > r0 && 1 - u >= 0 && 1 - u < U) atomicAdd(hist + (1 - u), int(r1 - r0));
     }
@@ -969,40 +972,45 @@ classify_kernel(const int32_t* __restrict__ slashes, const int32_t* __restrict__
   }
   if (threadIdx.x == 0) n_tc_u[h] = int32_t(base < cap_u ? base : cap_u);
   __syncthreads();
-  // segments (the hist array now doubles as the class lookup)
-  int sbase = 0;
-  for (int s0 = 0; s0 < cnt || s0 == 0; s0 += blockDim.x) {
-    const int x = s0 + threadIdx.x;
-    int4 sg[2];
-    int nsg = 0;
-    if (x < cnt) {
-      const int64_t d = sl[x];
-      int cur0 = -1, cur1 = -1;
-      for (int64_t u = -((d + 63) >> 6) - 1; u <= 1; ++u) {
-        const int64_t r0 = lcx_max64(0, d + 64 * u), r1 = lcx_min64(128, d + 64 * u + 64);
-        if (r1 <= r0) continue;
-        const int64_t idx = 1 - u;
-        const bool tcu = idx >= 0 && idx < U && hist[idx] >= min_entries && hist[idx] > 0;
-        if (!tcu) {
-          if (cur1 == int(r0)) {
-            cur1 = int(r1);
-          } else {
-            if (cur0 >= 0 && nsg < 2) sg[nsg++] = make_int4(int(d), cur0, cur1, 0);
-            cur0 = int(r0);
-            cur1 = int(r1);
-          }
+  // CUDA-core segments, one list per 64-row half of the block: for every diagonal d the
+  // rows of the half whose key lands in a non-tcgen05 relative tile form one contiguous
+  // range (a half spans at most two relative tiles).  The hist array doubles as the
+  // class lookup.
+  for (int hf = 0; hf < 2; ++hf) {
+    int sbase = 0;
+    for (int s0 = 0; s0 < cnt || s0 == 0; s0 += blockDim.x) {
+      const int x = s0 + threadIdx.x;
+      int4 sg = make_int4(0, 0, 0, 0);
+      int nsg = 0;
+      if (x < cnt) {
+        const int64_t d = sl[x];
+        int cur0 = -1, cur1 = -1;
+        const int64_t u_lo = -((d + 63) >> 6) - 1;
+        for (int64_t u = u_lo; u <= u_lo + 4 && u <= 1; ++u) {
+          const int64_t r0 = lcx_max64(64 * hf, d + 64 * u);
+          const int64_t r1 = lcx_min64(64 * hf + 64, d + 64 * u + 64);
+          if (r1 <= r0) continue;
+          const int64_t idx = 1 - u;
+          const bool tcu = idx >= 0 && idx < U && hist[idx] >= min_entries && hist[idx] > 0;
+          if (tcu) continue;
+          if (cur0 < 0) cur0 = int(r0);
+          cur1 = int(r1);  // non-TC pieces of one half are adjacent
+        }
+        if (cur0 >= 0) {
+          sg = make_int4(int(d), cur0, cur1, 0);
+          nsg = 1;
         }
       }
-      if (cur0 >= 0 && nsg < 2) sg[nsg++] = make_int4(int(d), cur0, cur1, 0);
+      const int pos = scan(nsg);
+      const int tot = total;
+      if (nsg && sbase + pos < cap_seg)
+        segs[(int64_t(h) * 2 + hf) * cap_seg + sbase + pos] = sg;
+      sbase += tot;
+      if (s0 + int(blockDim.x) >= cnt) break;
     }
-    const int pos = scan(nsg);
-    const int tot = total;
-    for (int k = 0; k < nsg; ++k)
-      if (sbase + pos + k < cap_seg) segs[int64_t(h) * cap_seg + sbase + pos + k] = sg[k];
-    sbase += tot;
-    if (s0 + int(blockDim.x) >= cnt) break;
+    if (threadIdx.x == 0) nseg[h * 2 + hf] = int32_t(sbase < cap_seg ? sbase : cap_seg);
+    __syncthreads();
   }
-  if (threadIdx.x == 0) nseg[h] = int32_t(sbase < cap_seg ? sbase : cap_seg);
 }
 
 // Exact admitted-entry count of rows [t0, t1) per head (CriticalSet::admitted_count

@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "attn_gather.cuh"
 #include "attn_tc.cuh"
 #include "lcx_internal.cuh"
 
@@ -42,7 +43,7 @@ int ensure_rope(lcx_context* ctx, double base, int dim, int64_t P, cudaStream_t 
   if (ctx->rope) LCX_CHECK_CUDA(cudaFree(ctx->rope));
   ctx->rope = nullptr;
   const int pairs = dim / 2;
-  const int64_t npos = std::max<int64_t>(P, 1);
+  const int64_t npos = std::max<int64_t>(P, 128);  // the gather's low table needs 64 rows
   std::vector<double> th(pairs);
   for (int p = 0; p < pairs; ++p) th[p] = std::pow(base, -double(2 * p) / double(dim));
   double* th_dev = nullptr;
@@ -81,6 +82,14 @@ __global__ void max_pos_kernel(const int64_t* a, const int64_t* b, int64_t n,
     if (x < 0 || y < 0) atomicExch(neg, 1);
     const int64_t m = x > y ? x : y;
     atomicMax(out, (unsigned long long)(m < 0 ? 0 : m));
+  }
+}
+
+__global__ void max_abs_kernel(const int64_t* a, int64_t n, unsigned long long* out) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t x = a[i] < 0 ? -a[i] : a[i];
+    atomicMax(out, (unsigned long long)x);
   }
 }
 
@@ -208,12 +217,12 @@ void attn_layout(A& ar, const lcx_attention_input* in, bool tc, bool sparse, int
       w.sbits = ar.template take<uint32_t>(size_t(in->hq) * w.words);
       w.U = in->n / 64 + 4;
       w.cap_u = w.U;
-      w.cap_seg = 2 * cap_s;
+      w.cap_seg = cap_s;  // per 64-row half: at most one segment per diagonal
       w.hist = ar.template take<int32_t>(size_t(in->hq) * w.U);
       w.tc_u = ar.template take<int32_t>(size_t(in->hq) * w.cap_u);
       w.n_tc_u = ar.template take<int32_t>(size_t(in->hq));
-      w.segs = ar.template take<int4>(size_t(in->hq) * w.cap_seg);
-      w.nseg = ar.template take<int32_t>(size_t(in->hq));
+      w.segs = ar.template take<int4>(size_t(in->hq) * 2 * w.cap_seg);
+      w.nseg = ar.template take<int32_t>(size_t(in->hq) * 2);
     }
   }
   if (tc) {
@@ -326,14 +335,23 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
   LCX_TRY(tc_attention(p, w.B, ctx->sm_count, st));
   if (ev_tc1) LCX_CHECK_CUDA(cudaEventRecord(ev_tc1, st));
   if (sparse) {
-    // isolated slashes + self-fallback rows on the CUDA-core path, merged in place
-    AttnArgs a = base_attn(in, ctx);
-    a.n = t1;
+    // isolated slashes + self-fallback rows on the CUDA-core gather, merged in place
+    GatherArgs a{};
+    a.q = reinterpret_cast<const __nv_bfloat16*>(in->q);
+    a.k = reinterpret_cast<const __nv_bfloat16*>(in->k);
+    a.v = reinterpret_cast<const __nv_bfloat16*>(in->v);
+    a.hq = hq;
+    a.hkv = in->hkv;
+    a.group = hq / in->hkv;
     a.row_begin = t0;
     a.row_end = t1;
     a.rel_mode = dca ? 1 : 0;
     a.s = dca ? s : 1;
     a.c = dca ? c : 1;
+    a.pos_q = in->positions_q;
+    a.pos_k = in->positions_k;
+    a.rope = ctx->rope;
+    a.scale_log2 = p.scale_log2;
     a.verts = verts;
     a.nv = nv;
     a.cap_v = cap_v;
@@ -341,18 +359,15 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
     a.ns = ns;
     a.cap_s = cap_s;
     a.vbits = w.vbits;
-    a.bit_words = w.words;
-    a.skip_verticals = 1;
+    a.words = w.words;
     a.segs = w.segs;
     a.nseg = w.nseg;
     a.cap_seg = w.cap_seg;
-    a.o_part = out;
-    a.lse_part = lse;
     a.out = out;
     a.lse = lse;
     a.lse_stride = lse_stride;
     a.simt_count = ctx->profiling ? ctx->tile_counter + 1 : nullptr;
-    LCX_TRY(attention_simt(a, st));
+    LCX_TRY(attention_gather(a, st));
     if (admitted)
       LCX_TRY(admitted_counts(verts, nv, cap_v, slashes, ns, cap_s, hq, t0, t1, admitted, st));
   } else if (admitted) {
@@ -561,6 +576,56 @@ int lcx_sparse_attention(lcx_context* ctx, const lcx_attention_input* in,
   return attention_chunk(ctx, in, w, 0, n, true, verticals, nv, cap_v, slashes, ns, cap_s,
                          use_dca != 0, use_dca ? dca->chunk_size : 1,
                          use_dca ? dca->train_len : 1, kDefaultTcMin, out, lse, n, nullptr, st);
+}
+
+int lcx_attention_rel(lcx_context* ctx, const lcx_attention_input* in, const int32_t* verticals,
+                      const int32_t* nv, int64_t cap_v, const int32_t* slashes,
+                      const int32_t* ns, int64_t cap_s, const int64_t* rel, float* out,
+                      float* lse, void* stream) {
+  LCX_TRY(validate_input(in));
+  if (!rel) return fail(LCX_ERR_DIMENSION, "relative-position override must be n x n");
+  const bool sparse = verticals != nullptr;
+  if (sparse && (!nv || !slashes || !ns)) return fail(LCX_ERR_DIMENSION, "null index list");
+  cudaStream_t st = S(stream);
+  const int64_t n = in->n;
+  unsigned long long* dmax = nullptr;
+  LCX_CHECK_CUDA(cudaMallocAsync(&dmax, sizeof(unsigned long long), st));
+  LCX_CHECK_CUDA(cudaMemsetAsync(dmax, 0, sizeof(unsigned long long), st));
+  max_abs_kernel<<<256, 256, 0, st>>>(rel, n * n, dmax);
+  LCX_CHECK_LAUNCH();
+  unsigned long long hmax = 0;
+  LCX_CHECK_CUDA(cudaMemcpyAsync(&hmax, dmax, sizeof(hmax), cudaMemcpyDeviceToHost, st));
+  LCX_CHECK_CUDA(cudaStreamSynchronize(st));
+  LCX_CHECK_CUDA(cudaFreeAsync(dmax, st));
+  LCX_TRY(ensure_rope(ctx, in->rope_base, in->dim, std::max<int64_t>(int64_t(hmax) + 1, n), st));
+  AttnWS w;
+  Sizer sz;
+  attn_layout(sz, in, false, sparse, cap_v, cap_s, n, w);
+  LCX_TRY(ensure_workspace(ctx, sz.off));
+  Arena ar{ctx->ws, ctx->ws_bytes, 0};
+  attn_layout(ar, in, false, sparse, cap_v, cap_s, n, w);
+  if (sparse) LCX_TRY(build_bitmaps(verticals, nv, cap_v, in->hq, w.words, w.vbits, st));
+  AttnArgs a = base_attn(in, ctx);
+  a.n = n;
+  a.row_begin = 0;
+  a.row_end = n;
+  a.rel_mode = 2;
+  a.rel_mat = rel;
+  a.rel_n = n;
+  a.s = a.c = 1;
+  a.dense = sparse ? 0 : 1;
+  a.verts = verticals;
+  a.nv = nv;
+  a.cap_v = cap_v;
+  a.slashes = slashes;
+  a.ns = ns;
+  a.cap_s = cap_s;
+  a.vbits = w.vbits;
+  a.bit_words = w.words;
+  a.out = out;
+  a.lse = lse;
+  a.lse_stride = n;
+  return attention_simt(a, st);
 }
 
 int lcx_full_attention(lcx_context* ctx, const lcx_attention_input* in, int32_t use_dca,

@@ -172,7 +172,9 @@ struct AttnArgs {
   int64_t row_begin, row_end;
   const int64_t* pos_q;      // nullptr = iota
   const int64_t* pos_k;
-  int rel_mode;              // 0 standard positions, 1 dca remap
+  int rel_mode;              // 0 standard positions, 1 dca remap, 2 explicit matrix
+  const int64_t* rel_mat;    // rel_mode 2: [rel_n][rel_n] relative positions
+  int64_t rel_n;
   int64_t s, c;
   float scale;               // 1 / (temperature * sqrt(dim))
   const float2* rope;
@@ -183,11 +185,6 @@ struct AttnArgs {
   const int32_t* slashes; const int32_t* ns; int64_t cap_s;
   const uint32_t* vbits;     // [hq][words] keys that are verticals (skip on the slash path)
   int64_t bit_words;
-  int skip_verticals;        // 1: verticals handled elsewhere (tcgen05 path)
-  // optional SIMT segments (TC mode): per head list of (d, r0, r1) relative to block rows
-  const int4* segs; const int32_t* nseg; int64_t cap_seg;
-  // merge-in partial (TC mode): o_part [n_rows][hq][dim] normalized + lse_part [hq][n]
-  const float* o_part; const float* lse_part;
   float* out;                // [.][hq][dim] rows indexed by absolute row
   float* lse;                // [hq][lse_stride]
   int64_t lse_stride;
