@@ -23,6 +23,8 @@
  *                              API's by-value matrices), chunk-pipelined copies
  *   lcx_attention_recall    <- longctx::attention_recall    core/include/longctx/refine.hpp:25-26
  *   lcx_lse_merge           <- (new) log-sum-exp merge of KV-sequence shards (north star (e))
+ *   lcx_lse_scale_partial   <- (new) per-shard scaling step of that merge when the sum
+ *                              runs as an NCCL collective
  *
  * Conventions
  *   - All tensor pointers are DEVICE pointers; every call takes an explicit
@@ -112,6 +114,15 @@ typedef struct {
   lcx_selection_options opts;
   int32_t kernel_path;     /* lcx_kernel_path */
   int32_t tc_min_entries;  /* slash entries per 64-key tile to route it to tcgen05 (0 = default) */
+  /* KV-line sharding (north star (e)): with shard_count > 1 this call computes, for every
+   * row, the partial attention over shard shard_rank's part of each head's selected
+   * lines (contiguous parts of the sorted vertical and slash lists); the estimator and
+   * selection run in full on every shard (identical lists, no exchange).  out / lse are
+   * then partials (o normalised within the shard, lse = -inf where the shard has no
+   * entry) to be combined with lcx_lse_scale_partial + a sum over shards.  Sparse mode
+   * only.  0 / 1 = unsharded. */
+  int32_t shard_rank;
+  int32_t shard_count;
 } lcx_prefill_config;
 
 typedef struct {
@@ -248,6 +259,15 @@ int lcx_attention_recall(lcx_context* ctx, const float* lse_sparse, const float*
  * Writes the merged output/lse into out / lse_out. */
 int lcx_lse_merge(lcx_context* ctx, const float* o_parts, const float* lse_parts, int32_t parts,
                   int64_t rows, int32_t dim, float* out, float* lse_out, void* stream);
+
+/* Shard-side half of the log-sum-exp merge of KV-line shards: given this shard's partial
+ * o [n][hq][dim] (normalised) and the lse of ALL shards lse_all [parts][hq][n], writes
+ * lse_out [hq][n] = logsumexp_g lse_g and scales o in place by exp(lse_own - lse_out)
+ * (0 where lse_own = -inf), so that summing the scaled partials over shards (an NCCL
+ * reduce-scatter / all-reduce) yields the exact attention output. */
+int lcx_lse_scale_partial(lcx_context* ctx, float* o, const float* lse_own, const float* lse_all,
+                          int32_t parts, int64_t n, int32_t hq, int32_t dim, float* lse_out,
+                          void* stream);
 
 #ifdef __cplusplus
 }

@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 3) attn_gather_kernel(const GatherAr
   const int nvh = a.nv[h], nsh = a.ns[h];
   const bool any = (nvh > 0 && int64_t(a.verts[int64_t(h) * a.cap_v]) <= i) ||
                    (nsh > 0 && int64_t(a.slashes[int64_t(h) * a.cap_s]) <= i);
-  if (!any) {
+  if (!any && a.do_fallback) {
     m = -INFINITY;
     l = 0.f;
 #pragma unroll

@@ -16,8 +16,10 @@ struct GatherArgs {
   const int64_t* pos_q; const int64_t* pos_k;     // standard mode (nullptr = iota)
   const float2* rope;                              // fp64-derived table, >= 64 rows
   float scale_log2;                                // log2(e) / (temperature sqrt(D))
+  // the FULL selection (self-fallback decision) and whether this shard owns fallbacks
   const int32_t* verts; const int32_t* nv; int64_t cap_v;
   const int32_t* slashes; const int32_t* ns; int64_t cap_s;
+  int do_fallback;
   const uint32_t* vbits; int64_t words;
   const int4* segs; const int32_t* nseg; int64_t cap_seg;  // [hq][2 halves][cap_seg]
   float* out; float* lse; int64_t lse_stride;      // tensor-core partial in, merged out

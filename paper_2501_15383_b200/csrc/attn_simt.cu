@@ -122,7 +122,9 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(AttnArgs a) {
     const int32_t* sl = a.slashes + int64_t(h) * a.cap_s;
     const int nv = a.nv[h], ns = a.ns[h];
     const uint32_t* vb = a.vbits + int64_t(h) * a.bit_words;
-    bool any = (nv > 0 && verts[0] <= i) || (ns > 0 && sl[0] <= i);
+    const int fnv = a.fnv[h], fns = a.fns[h];
+    const bool any = (fnv > 0 && a.fverts[int64_t(h) * a.cap_v] <= i) ||
+                     (fns > 0 && a.fslashes[int64_t(h) * a.cap_s] <= i);
     for (int x = 0; x < nv; ++x) {
       const int64_t v = verts[x];
       if (v > i) break;
@@ -137,13 +139,13 @@ __global__ void __launch_bounds__(128) attn_simt_kernel(AttnArgs a) {
       process_entry<T, PPL>(a, s, i, j, pq_i, g, lane4, qmask);
       ++entries;
     }
-    if (!any) {  // self fallback (sparse.cpp:111)
+    if (!any && a.do_fallback) {  // self fallback (sparse.cpp:111)
       process_entry<T, PPL>(a, s, i, i, pq_i, g, lane4, qmask);
       entries = 1;
     }
   }
 
-  const float inv_l = 1.f / s.l;
+  const float inv_l = s.l > 0.f ? 1.f / s.l : 0.f;  // no entry on this shard: o = 0, lse = -inf
   float* orow = a.out + (i * a.hq + h) * int64_t(a.dim);
 #pragma unroll
   for (int t = 0; t < PPL; ++t) {

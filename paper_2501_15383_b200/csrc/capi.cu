@@ -68,6 +68,28 @@ __global__ void dense_count_kernel(int hq, int64_t t0, int64_t t1, int64_t* out)
   if (h < hq) out[h] = (t1 * (t1 + 1) - t0 * (t0 + 1)) / 2;  // sum_{i=t0}^{t1-1} (i + 1)
 }
 
+// Line sharding: shard r of G keeps the contiguous part [r cnt / G, (r+1) cnt / G) of each
+// head's sorted vertical and slash lists (clustered slashes stay together, so dense slash
+// runs still become tensor-core tiles on their shard).
+__global__ void shard_lists_kernel(const int32_t* __restrict__ v, const int32_t* __restrict__ nv,
+                                   int64_t cap_v, const int32_t* __restrict__ sl,
+                                   const int32_t* __restrict__ ns, int64_t cap_s, int rank,
+                                   int shards, int32_t* __restrict__ ov, int32_t* __restrict__ onv,
+                                   int32_t* __restrict__ os, int32_t* __restrict__ ons) {
+  const int h = blockIdx.x;
+  const int64_t cv = nv[h], cs = ns[h];
+  const int64_t v0 = cv * rank / shards, v1 = cv * (rank + 1) / shards;
+  const int64_t s0 = cs * rank / shards, s1 = cs * (rank + 1) / shards;
+  for (int64_t x = threadIdx.x; x < v1 - v0; x += blockDim.x)
+    ov[h * cap_v + x] = v[h * cap_v + v0 + x];
+  for (int64_t x = threadIdx.x; x < s1 - s0; x += blockDim.x)
+    os[h * cap_s + x] = sl[h * cap_s + s0 + x];
+  if (threadIdx.x == 0) {
+    onv[h] = int32_t(v1 - v0);
+    ons[h] = int32_t(s1 - s0);
+  }
+}
+
 int dense_counts(int hq, int64_t t0, int64_t t1, int64_t* out, cudaStream_t st) {
   dense_count_kernel<<<(hq + 127) / 128, 128, 0, st>>>(hq, t0, t1, out);
   LCX_CHECK_LAUNCH();
@@ -192,6 +214,11 @@ EstimateArgs base_est(const lcx_attention_input* in, lcx_context* ctx, int64_t q
 // Path: tcgen05 tiles (+ CUDA-core gather for isolated slashes) when the input is
 // bf16 with dim 128, the chunk boundaries are 128-aligned and DCA chunks are
 // multiples of 128; otherwise the exact CUDA-core path for every entry.
+struct FullLists {
+  const int32_t* verts; const int32_t* nv; const int32_t* slashes; const int32_t* ns;
+  int do_fallback;
+};
+
 struct AttnWS {
   bool tc = false;
   int64_t words = 0, U = 0, cap_u = 0, cap_seg = 0;
@@ -258,9 +285,17 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
                     int64_t cap_v, const int32_t* slashes, const int32_t* ns, int64_t cap_s,
                     bool dca, int64_t s, int64_t c, int tc_min_entries, float* out, float* lse,
                     int64_t lse_stride, int64_t* admitted, cudaStream_t st,
-                    cudaEvent_t ev_tc0 = nullptr, cudaEvent_t ev_tc1 = nullptr) {
+                    cudaEvent_t ev_tc0 = nullptr, cudaEvent_t ev_tc1 = nullptr,
+                    const FullLists* full = nullptr) {
   const int hq = in->hq;
-  if (sparse) LCX_TRY(build_bitmaps(verts, nv, cap_v, hq, w.words, w.vbits, st));
+  // line sharding: (verts, slashes) are this rank's lines; the full selection decides
+  // V∩S ownership (vertical bitmap) and the self-fallback rows (rank 0 only)
+  const int32_t* fv = full ? full->verts : verts;
+  const int32_t* fnv = full ? full->nv : nv;
+  const int32_t* fs = full ? full->slashes : slashes;
+  const int32_t* fns = full ? full->ns : ns;
+  const int do_fallback = full ? full->do_fallback : 1;
+  if (sparse) LCX_TRY(build_bitmaps(fv, fnv, cap_v, hq, w.words, w.vbits, st));
   if (!w.tc) {
     AttnArgs a = base_attn(in, ctx);
     a.n = t1;
@@ -278,12 +313,24 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
     a.cap_s = cap_s;
     a.vbits = w.vbits;
     a.bit_words = w.words;
+    a.fverts = fv;
+    a.fnv = fnv;
+    a.fslashes = fs;
+    a.fns = fns;
+    a.do_fallback = do_fallback;
     a.out = out;
     a.lse = lse;
     a.lse_stride = lse_stride;
-    a.admitted = admitted;
+    a.admitted = full && admitted ? nullptr : admitted;
     a.simt_count = ctx->profiling ? ctx->tile_counter + 1 : nullptr;
-    return attention_simt(a, st);
+    LCX_TRY(attention_simt(a, st));
+    if (full && admitted) {
+      if (do_fallback)
+        LCX_TRY(admitted_counts(fv, fnv, cap_v, fs, fns, cap_s, hq, t0, t1, admitted, st));
+      else
+        LCX_CHECK_CUDA(cudaMemsetAsync(admitted, 0, sizeof(int64_t) * hq, st));
+    }
+    return LCX_OK;
   }
   if (sparse) {
     LCX_TRY(build_bitmaps(slashes, ns, cap_s, hq, w.words, w.sbits, st));
@@ -352,12 +399,13 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
     a.pos_k = in->positions_k;
     a.rope = ctx->rope;
     a.scale_log2 = p.scale_log2;
-    a.verts = verts;
-    a.nv = nv;
+    a.verts = fv;
+    a.nv = fnv;
     a.cap_v = cap_v;
-    a.slashes = slashes;
-    a.ns = ns;
+    a.slashes = fs;
+    a.ns = fns;
     a.cap_s = cap_s;
+    a.do_fallback = do_fallback;
     a.vbits = w.vbits;
     a.words = w.words;
     a.segs = w.segs;
@@ -368,8 +416,12 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
     a.lse_stride = lse_stride;
     a.simt_count = ctx->profiling ? ctx->tile_counter + 1 : nullptr;
     LCX_TRY(attention_gather(a, st));
-    if (admitted)
-      LCX_TRY(admitted_counts(verts, nv, cap_v, slashes, ns, cap_s, hq, t0, t1, admitted, st));
+    if (admitted) {
+      if (do_fallback)  // exact count of the full selection, reported once (rank 0)
+        LCX_TRY(admitted_counts(fv, fnv, cap_v, fs, fns, cap_s, hq, t0, t1, admitted, st));
+      else
+        LCX_CHECK_CUDA(cudaMemsetAsync(admitted, 0, sizeof(int64_t) * hq, st));
+    }
   } else if (admitted) {
     // dense rows: entries = i + 1
     LCX_TRY(dense_counts(hq, t0, t1, admitted, st));
@@ -821,6 +873,11 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
   if (dca) LCX_TRY(validate_chunk(&cfg->dca));
   if (cfg->budget_vertical < 0 || cfg->budget_slash < 0)
     return fail(LCX_ERR_CONFIG, "budgets must be non-negative");
+  const int shards = cfg->shard_count > 1 ? cfg->shard_count : 1;
+  if (shards > 1 && (cfg->shard_rank < 0 || cfg->shard_rank >= shards))
+    return fail(LCX_ERR_CONFIG, "shard rank out of range");
+  if (shards > 1 && !sparse)
+    return fail(LCX_ERR_CONFIG, "line sharding applies to sparse prefill");
 
   const int64_t n = in->n;
   const int hq = in->hq;
@@ -848,6 +905,7 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
                                 dca ? 1 : 0, c);
   e_max.col = reinterpret_cast<float*>(1);
   e_max.slash = reinterpret_cast<float*>(1);
+  int32_t *ov = nullptr, *onv = nullptr, *os = nullptr, *ons = nullptr;
   auto layout = [&](auto& A, AttnWS& w, float** col, float** sl, int32_t** iv, int32_t** inv,
                     int32_t** is, int32_t** ins, size_t* est_off) {
     *est_off = A.off;
@@ -864,6 +922,12 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
       if (!out->sel_slashes) {
         *is = A.template take<int32_t>(size_t(hq) * cap_s);
         *ins = A.template take<int32_t>(size_t(hq));
+      }
+      if (shards > 1) {  // this shard's lines
+        ov = A.template take<int32_t>(size_t(hq) * cap_v);
+        onv = A.template take<int32_t>(size_t(hq));
+        os = A.template take<int32_t>(size_t(hq) * cap_s);
+        ons = A.template take<int32_t>(size_t(hq));
       }
     }
     attn_layout(A, in, tc, sparse, cap_v, cap_s, dca ? s : n, w);
@@ -919,10 +983,21 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
                            slist, scnt, cap_s, st));
       if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[2], st));
     }
-    LCX_TRY(attention_chunk(ctx, in, w, t0, t1, sparse, vlist, vcnt, cap_v, slist, scnt, cap_s,
+    const int32_t *avl = vlist, *avc = vcnt, *asl = slist, *asc = scnt;
+    FullLists full{vlist, vcnt, slist, scnt, cfg->shard_rank == 0 ? 1 : 0};
+    if (shards > 1) {
+      shard_lists_kernel<<<hq, 256, 0, st>>>(vlist, vcnt, cap_v, slist, scnt, cap_s,
+                                             cfg->shard_rank, shards, ov, onv, os, ons);
+      LCX_CHECK_LAUNCH();
+      avl = ov;
+      avc = onv;
+      asl = os;
+      asc = ons;
+    }
+    LCX_TRY(attention_chunk(ctx, in, w, t0, t1, sparse, avl, avc, cap_v, asl, asc, cap_s,
                             dca, s, dca ? c : 1, tc_min, out->out, out->lse, n,
                             out->admitted ? out->admitted + ci * hq : nullptr, st,
-                            (prof && tc) ? e[4] : nullptr, (prof && tc) ? e[5] : nullptr));
+                            (prof && tc) ? e[4] : nullptr, (prof && tc) ? e[5] : nullptr, shards > 1 ? &full : nullptr));
     if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[3], st));
     if (done) LCX_CHECK_CUDA(cudaEventRecord(done[ci], st));
   }
@@ -991,6 +1066,15 @@ int lcx_attention_recall(lcx_context* ctx, const float* lse_sparse, const float*
   if (hbad) return fail(LCX_ERR_DOMAIN, "recall above 1: sparse lse exceeds full lse");
   if (aggregate) *aggregate = hsum / double(n);
   return LCX_OK;
+}
+
+int lcx_lse_scale_partial(lcx_context* ctx, float* o, const float* lse_own, const float* lse_all,
+                          int32_t parts, int64_t n, int32_t hq, int32_t dim, float* lse_out,
+                          void* stream) {
+  (void)ctx;
+  if (parts <= 0 || n <= 0 || hq <= 0 || dim <= 0)
+    return fail(LCX_ERR_DIMENSION, "merge needs at least one part, row, head and dim");
+  return lse_scale_launch(o, lse_own, lse_all, parts, n, hq, dim, lse_out, S(stream));
 }
 
 int lcx_lse_merge(lcx_context* ctx, const float* o_parts, const float* lse_parts, int32_t parts,

@@ -185,6 +185,9 @@ struct AttnArgs {
   const int32_t* slashes; const int32_t* ns; int64_t cap_s;
   const uint32_t* vbits;     // [hq][words] keys that are verticals (skip on the slash path)
   int64_t bit_words;
+  // full selection (== the lists above unless line-sharded): self-fallback decision
+  const int32_t* fverts; const int32_t* fnv; const int32_t* fslashes; const int32_t* fns;
+  int do_fallback;           // this shard computes the self-fallback rows
   float* out;                // [.][hq][dim] rows indexed by absolute row
   float* lse;                // [hq][lse_stride]
   int64_t lse_stride;
@@ -204,6 +207,8 @@ int build_bitmaps(const int32_t* lists, const int32_t* counts, int64_t cap, int 
 // misc.cu
 int recall_kernel_launch(const float* ls, const float* lf, int64_t n, double slack,
                          float* per, double* sum_dev, int* bad_dev, cudaStream_t st);
+int lse_scale_launch(float* o, const float* lse_own, const float* lse_all, int parts, int64_t n,
+                     int hq, int dim, float* lse_out, cudaStream_t st);
 int lse_merge_launch(const float* o_parts, const float* lse_parts, int parts, int64_t rows,
                      int dim, float* out, float* lse_out, cudaStream_t st);
 

@@ -68,7 +68,41 @@ __global__ void lse_merge_kernel(const float* __restrict__ o_parts,
   if (threadIdx.x == 0) lse_out[row] = m + logf(den);
 }
 
+// lse_out = logsumexp_g lse_all[g]; o *= exp(lse_own - lse_out) (0 where lse_own = -inf)
+__global__ void lse_scale_kernel(float* __restrict__ o, const float* __restrict__ lse_own,
+                                 const float* __restrict__ lse_all, int parts, int64_t n, int hq,
+                                 int dim, float* __restrict__ lse_out) {
+  const int64_t idx = int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5);  // (i, h)
+  if (idx >= n * hq) return;
+  const int64_t i = idx / hq;
+  const int h = int(idx - i * hq);
+  const int64_t li = int64_t(h) * n + i;
+  float m = -INFINITY;
+  for (int g = 0; g < parts; ++g) m = fmaxf(m, lse_all[int64_t(g) * hq * n + li]);
+  float den = 0.f;
+  for (int g = 0; g < parts; ++g) {
+    const float l = lse_all[int64_t(g) * hq * n + li];
+    if (l != -INFINITY) den += expf(l - m);
+  }
+  const float tot = m == -INFINITY ? -INFINITY : m + logf(den);
+  const float own = lse_own[li];
+  const float w = own == -INFINITY ? 0.f : expf(own - tot);
+  float* row = o + idx * dim;
+  for (int d = threadIdx.x & 31; d < dim; d += 32) row[d] *= w;
+  if ((threadIdx.x & 31) == 0 && lse_out) lse_out[li] = tot;
+}
+
 }  // namespace
+
+int lse_scale_launch(float* o, const float* lse_own, const float* lse_all, int parts, int64_t n,
+                     int hq, int dim, float* lse_out, cudaStream_t st) {
+  const int64_t rows = n * hq;
+  if (rows <= 0) return LCX_OK;
+  lse_scale_kernel<<<unsigned((rows + 7) / 8), 256, 0, st>>>(o, lse_own, lse_all, parts, n, hq,
+                                                             dim, lse_out);
+  LCX_CHECK_LAUNCH();
+  return LCX_OK;
+}
 
 int build_rope_table(const double* thetas_dev, int P, int64_t npos, float2* out,
                      cudaStream_t st) {

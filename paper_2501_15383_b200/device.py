@@ -87,8 +87,11 @@ def chunked_prefill(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
                     position_mode="standard", dca=None, opts: Options | None = None,
                     positions_q=None, positions_k=None, rope_base=1e4, temperature=1.0,
                     kernel_path="auto", return_selections=True, return_admitted=False,
-                    tc_min_entries=0, out=None, lse=None, stream=None, ctx=None):
-    """longctx::chunked_prefill (sparse.hpp:125-129) over all heads of one layer."""
+                    tc_min_entries=0, out=None, lse=None, stream=None, ctx=None, shard=None):
+    """longctx::chunked_prefill (sparse.hpp:125-129) over all heads of one layer.
+
+    shard=(rank, count): KV-line sharding -- out / lse are this shard's partials
+    (see lse_scale_partial and paper_2501_15383_b200/shard.py)."""
     inp = make_input(q, k, v, positions_q, positions_k, rope_base, temperature)
     opts = opts or Options()
     n, hq, dim = q.shape
@@ -111,9 +114,10 @@ def chunked_prefill(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
     admitted = torch.zeros((nchunks, hq), dtype=torch.int64, device=dev) \
         if return_admitted else None
     pm = POSITION_MODES[position_mode] if isinstance(position_mode, str) else int(position_mode)
+    sr, sc = shard if shard is not None else (0, 1)
     cfg = PrefillConfigC(int(chunk_len), int(last_q), bv, bs, PREFILL_MODES[mode], pm,
                          _chunk(dca) or ChunkConfigC(0, 0, 0), opts.c(),
-                         KERNEL_PATHS[kernel_path], int(tc_min_entries))
+                         KERNEL_PATHS[kernel_path], int(tc_min_entries), int(sr), int(sc))
     o = PrefillOutputC(out.data_ptr(), lse.data_ptr(),
                        sel["verticals"].data_ptr() if sel else None,
                        sel["nv"].data_ptr() if sel else None,
@@ -245,6 +249,23 @@ def attention_recall(lse_sparse, lse_full, *, slack=1e-5, stream=None, ctx=None)
     return per, agg.value
 
 
+def lse_scale_partial(o, lse_own, lse_all, *, stream=None, ctx=None):
+    """This shard's half of the KV-line LSE merge: o [n, hq, dim] scaled in place by
+    exp(lse_own - lse_tot); returns lse_tot [hq, n] (lse_all [G, hq, n])."""
+    _check_tensor("o", o, (torch.float32,))
+    _check_tensor("lse_own", lse_own, (torch.float32,))
+    _check_tensor("lse_all", lse_all, (torch.float32,))
+    n, hq, dim = o.shape
+    g = lse_all.shape[0]
+    if lse_all.shape[1:] != (hq, n) or lse_own.shape != (hq, n):
+        raise Error("dimension", "lse shapes must be [G, hq, n] and [hq, n]")
+    tot = torch.empty((hq, n), dtype=torch.float32, device=o.device)
+    ctx = ctx or context(o.device.index)
+    check(lib().lcx_lse_scale_partial(ctx.ptr, _ptr(o), _ptr(lse_own), _ptr(lse_all), g, n, hq,
+                                      dim, _ptr(tot), _stream(stream)))
+    return tot
+
+
 def lse_merge(o_parts, lse_parts, *, stream=None, ctx=None):
     """Merge G shard partials: o_parts [G, rows, dim], lse_parts [G, rows]."""
     _check_tensor("o_parts", o_parts, (torch.float32,))
@@ -292,7 +313,7 @@ def chunked_prefill_host(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
     pm = POSITION_MODES[position_mode] if isinstance(position_mode, str) else int(position_mode)
     cfg = PrefillConfigC(int(chunk_len), int(last_q), bv, bs, PREFILL_MODES[mode], pm,
                          _chunk(dca) or ChunkConfigC(0, 0, 0), opts.c(),
-                         KERNEL_PATHS[kernel_path], 0)
+                         KERNEL_PATHS[kernel_path], 0, 0, 1)
     o = PrefillOutputC(out.data_ptr(), lse.data_ptr(),
                        sel["verticals"].data_ptr() if sel else None,
                        sel["nv"].data_ptr() if sel else None,

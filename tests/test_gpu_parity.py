@@ -492,3 +492,50 @@ def test_host_entry_equals_device_entry(D, port, precision, dca):
     o_ref, l_ref, _ = port.chunked_prefill(q[:, 3], k[:, 1], v[:, 1], 256, 64, (40, 120),
                                            "sparse", 1 if dca else 0, dca, temperature=0.9)
     assert row_rel_err(rh["out"][:, 3].double().numpy(), o_ref) <= TOL[precision]
+
+
+# ------------------------------------------------------- KV-line sharding --
+@pytest.mark.parametrize("shards", [2, 3])
+@pytest.mark.parametrize("path,precision,dca", [("tc", "bf16", (256, 768, 256)),
+                                                ("simt", "fp32", None)])
+def test_line_sharded_prefill_merges_to_unsharded(D, port, shards, path, precision, dca):
+    """North star (e): every shard attends over its part of the selected lines; the LSE
+    merge of the partials (on-device merge of stacked partials, and the collective path's
+    per-shard scaling + sum) equals the unsharded operator and the oracle; admitted
+    counts add up (rank 0 reports the exact count, sparse.cpp:115-119)."""
+    import torch
+    n, hq, hkv = 1024, 4, 2
+    q, k, v = _mh_inputs(n, hq, hkv, 128, precision, 31, "peaked")
+    dt = torch.float32 if precision == "fp32" else torch.bfloat16
+    T = lambda x: torch.tensor(x).to(dt).cuda().contiguous()  # noqa: E731
+    qt, kt, vt = T(q), T(k), T(v)
+    kw = dict(chunk_len=256, last_q=64, budget=(40, 200), temperature=0.9, kernel_path=path,
+              position_mode="dca_continuous" if dca else "standard", dca=dca,
+              return_admitted=True)
+    full = D.chunked_prefill(qt, kt, vt, **kw)
+    parts = [D.chunked_prefill(qt, kt, vt, shard=(r, shards), **kw) for r in range(shards)]
+    for p in parts:  # every shard logs the full selection
+        assert torch.equal(p["verticals"], full["verticals"])
+        assert torch.equal(p["slashes"], full["slashes"])
+    assert int(sum(p["admitted"].sum() for p in parts)) == int(full["admitted"].sum())
+    o = torch.stack([p["out"] for p in parts]).reshape(shards, n * hq, 128)
+    ls = torch.stack([p["lse"] for p in parts]).transpose(1, 2).reshape(shards, n * hq)
+    mo, ml = D.lse_merge(o.contiguous(), ls.contiguous())
+    mo = mo.reshape(n, hq, 128).double().cpu().numpy()
+    ml = ml.reshape(n, hq).t().double().cpu().numpy()
+    tol = TOL[precision]
+    ref_o, ref_l = full["out"].double().cpu().numpy(), full["lse"].double().cpu().numpy()
+    assert row_rel_err(mo.reshape(n * hq, -1), ref_o.reshape(n * hq, -1)) <= tol
+    assert lse_rel_err(ml, ref_l) <= tol
+    # collective form: scale each partial by exp(lse_g - lse_tot), then sum over shards
+    lse_all = torch.stack([p["lse"] for p in parts]).contiguous()
+    acc = torch.zeros_like(parts[0]["out"])
+    for p in parts:
+        tot = D.lse_scale_partial(p["out"], p["lse"], lse_all)
+        acc += p["out"]
+    assert row_rel_err(acc.double().cpu().numpy().reshape(n * hq, -1),
+                       ref_o.reshape(n * hq, -1)) <= tol
+    assert lse_rel_err(tot.double().cpu().numpy(), ref_l) <= tol
+    o_ref, l_ref, _ = port.chunked_prefill(q[:, 1], k[:, 0], v[:, 0], 256, 64, (40, 200),
+                                           "sparse", 1 if dca else 0, dca, temperature=0.9)
+    assert row_rel_err(mo[:, 1], o_ref) <= tol
