@@ -1050,6 +1050,14 @@ admitted_kernel(const int32_t* __restrict__ verts, const int32_t* __restrict__ n
   }
 }
 
+int make_map3(CUtensorMap* m, CUtensorMapDataType dt, void* base, uint64_t d0, uint64_t d1,
+              uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0,
+              uint32_t b1, uint32_t b2) {
+  return make_tmap3(m, dt, base, d0, d1, d2, stride1_bytes, stride2_bytes, b0, b1, b2);
+}
+
+}  // namespace
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -1068,7 +1076,7 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-int make_map3(CUtensorMap* m, CUtensorMapDataType dt, void* base, uint64_t d0, uint64_t d1,
+int make_tmap3(CUtensorMap* m, CUtensorMapDataType dt, void* base, uint64_t d0, uint64_t d1,
               uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0,
               uint32_t b1, uint32_t b2) {
   EncodeTiledFn fn = encode_fn();
@@ -1084,7 +1092,6 @@ int make_map3(CUtensorMap* m, CUtensorMapDataType dt, void* base, uint64_t d0, u
   return LCX_OK;
 }
 
-}  // namespace
 
 // ------------------------------------------------------------ host API --
 int tc_prepare_rows(const void* k, const void* v, int64_t n, int64_t r0, int64_t r1, int hkv,

@@ -62,6 +62,11 @@ void tc_layout(A& ar, int64_t n, int hq, int hkv, int64_t cap_v, int64_t seg_len
   B.vct = ar.template take<__half>(size_t(hq) * 128 * capp);
 }
 
+// 3-D tiled tensor map, SWIZZLE_128B, L2 promotion 256 B
+int make_tmap3(CUtensorMap* m, CUtensorMapDataType dt, void* base, uint64_t d0, uint64_t d1,
+               uint64_t d2, uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t b0,
+               uint32_t b1, uint32_t b2);
+
 int tc_prepare(const void* k, const void* v, int64_t n, int hq, int hkv, const int64_t* pos_k,
                int rel_mode, int64_t s, const float2* rope, TcBuffers& B, cudaStream_t st);
 int tc_prepare_maps(int hq, int hkv, TcBuffers& B);

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "attn_gather.cuh"
+#include "est_tc.cuh"
 #include "attn_tc.cuh"
 #include "lcx_internal.cuh"
 
@@ -555,10 +556,22 @@ int lcx_line_scores(lcx_context* ctx, const lcx_attention_input* in, int64_t q_r
   e.col = col_score;
   e.slash = slash_score;
   e.slash_mean = slash_mean;
+  const bool est_tc = est_tc_eligible(in->dtype, in->dim, e.block);
+  const int64_t k3_tiles = (nk + 63) / 64;
+  if (est_tc) {
+    e.k3 = reinterpret_cast<void*>(1);
+    e.k3_tiles = k3_tiles;
+  }
   Sizer sz;
+  if (est_tc) sz.take<uint8_t>(est_tc_k3_bytes(nk, in->hkv));
   estimate_simt_size(e, sz, ctx->sm_count);
   LCX_TRY(ensure_workspace(ctx, sz.off));
   Arena ar{ctx->ws, ctx->ws_bytes, 0};
+  if (est_tc) {
+    void* k3 = ar.take<uint8_t>(est_tc_k3_bytes(nk, in->hkv));
+    LCX_TRY(est_tc_prepare_keys(in->k, 0, nk, in->hkv, k3_tiles, ctx->rope, k3, st));
+    e.k3 = k3;
+  }
   return estimate_simt(ctx, e, ar, st);
 }
 
@@ -905,6 +918,15 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
                                 dca ? 1 : 0, c);
   e_max.col = reinterpret_cast<float*>(1);
   e_max.slash = reinterpret_cast<float*>(1);
+  // tensor-core estimator: keys rotated by their token index and split into 3 bf16 terms,
+  // prepared once per chunk for the chunk's new keys (chunks only append keys)
+  const bool est_tc = sparse && est_tc_eligible(in->dtype, in->dim, block_max);
+  const int64_t k3_tiles = (n + 63) / 64;
+  void* k3 = nullptr;
+  if (est_tc) {
+    e_max.k3 = reinterpret_cast<void*>(1);
+    e_max.k3_tiles = k3_tiles;
+  }
   int32_t *ov = nullptr, *onv = nullptr, *os = nullptr, *ons = nullptr;
   auto layout = [&](auto& A, AttnWS& w, float** col, float** sl, int32_t** iv, int32_t** inv,
                     int32_t** is, int32_t** ins, size_t* est_off) {
@@ -923,6 +945,7 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
         *is = A.template take<int32_t>(size_t(hq) * cap_s);
         *ins = A.template take<int32_t>(size_t(hq));
       }
+      if (est_tc) k3 = A.template take<uint8_t>(est_tc_k3_bytes(n, in->hkv));
       if (shards > 1) {  // this shard's lines
         ov = A.template take<int32_t>(size_t(hq) * cap_v);
         onv = A.template take<int32_t>(size_t(hq));
@@ -970,7 +993,11 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
       LCX_TRY(tc_prepare_rows(in->k, in->v, n, t0, t1, in->hkv, in->positions_k, dca ? 1 : 0, s,
                               ctx->rope, w.B, st));
     if (sparse) {
+      if (est_tc)
+        LCX_TRY(est_tc_prepare_keys(in->k, t0, t1, in->hkv, k3_tiles, ctx->rope, k3, st));
       EstimateArgs es = base_est(in, ctx, t0, t1 - t0, t1, cfg->last_q, dca ? 1 : 0, c);
+      es.k3 = k3;
+      es.k3_tiles = k3_tiles;
       es.col = col;
       es.slash = sl;
       es.slash_mean = cfg->opts.slash_mean;

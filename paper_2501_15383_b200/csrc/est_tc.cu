@@ -1,0 +1,448 @@
+// K1 on tcgen05 -- the Vertical-Slash estimator for bf16 inputs, head dim 128.
+//
+// Same semantics as the exact CUDA-core estimator (estimate.cu; reference
+// core/src/sparse.cpp:142-217): rows gi = t1 - B + r of the chunk, keys [0, t1),
+// logit = rope(q, rel) . k / sqrt(D), rel = gi - j (near) or c - 1 (DcaContinuous far
+// region, gi - j > c - 1), token-index positions, causal softmax, then column sums and
+// per-diagonal sums of the probabilities.  Near logits are rope(q_gi, gi) .
+// rope(k_j, j); far logits rope(q_gi, c - 1) . k_raw_j.
+//
+// The two matmul passes (pass 1: per-row max / sum-exp; pass 2: probabilities reduced
+// into column and diagonal partials) run on the tensor cores with fp32-level accuracy:
+// the fp32-rotated operands are split into three bf16 terms (x = h + m + l, 24
+// significant bits) and the six products of order <= 2^-16 are accumulated in fp32
+// TMEM (hh, hm, mh, hl, lh, mm; the far region's raw keys are exact in bf16, so it
+// needs three).  A CTA owns one pair of query heads of one KV head (M = 128 = 2 x 64
+// estimator rows, its Q terms resident in shared memory) and a range of 64-key tiles
+// streamed by TMA (N = 64); tiles whose rows straddle the near / far boundary go to the
+// CUDA-core kernel (at most two per chunk).
+//
+// Warp roles (384 threads): warp 0 TMA producer, warp 1 MMA issuer + TMEM owner,
+// warps 4-11 epilogue (TMEM lane quadrant = warp % 4, column half = (warp - 4) / 4).
+// Pass 2 transposes each tile's probabilities through shared memory so that column
+// sums (over a head's 64 rows) and diagonal sums (127 per head and tile) are
+// conflict-free strided reads.
+#include <cuda.h>
+
+#include "attn_tc.cuh"
+#include "est_tc.cuh"
+#include "lcx_internal.cuh"
+#include "tc_ptx.cuh"
+
+namespace lcx {
+namespace {
+
+constexpr int BN = 64;             // keys per tile
+constexpr int kQBox = 128 * 64 * 2;   // one [128 rows][64 dims] bf16 box = 16 KB
+constexpr int kKBox = 64 * 64 * 2;    // one [64 keys][64 dims] box = 8 KB
+constexpr int kQBytes = 6 * kQBox;    // 3 terms x 2 halves = 96 KB
+constexpr int kKStage = 6 * kKBox;    // near: 3 terms x 2 halves = 48 KB
+constexpr int NKS = 2;
+constexpr int OFF_Q = 0;
+constexpr int OFF_K = OFF_Q + kQBytes;
+constexpr int OFF_T = OFF_K + NKS * kKStage;      // pass-2 transpose [128][65] fp32
+constexpr int OFF_BAR = OFF_T + 128 * 65 * 4;
+constexpr int kSmem = OFF_BAR + 256 + 1024;
+constexpr int kThreads = 384;
+constexpr uint32_t IDESC = tc::idesc_f16(128, BN, 1, 1);
+
+struct Item {
+  int pair;      // head pair index
+  int far;       // 1: far tiles (raw K, Q at c - 1)
+  int t0, t1;    // 64-key tiles [t0, t1)
+  int split;     // stats split slot
+};
+
+// CTA -> (pair, phase, tile range): far tiles [0, far_end) then near tiles
+// [near_begin, ntiles), each cut into `per`-tile pieces; split = piece index of the pair
+__device__ __forceinline__ Item decode_item(const EstTcParams& p, int idx) {
+  const int nf = int((p.far_end + p.per - 1) / p.per);
+  const int nn = int((p.ntiles - p.near_begin + p.per - 1) / p.per);
+  Item it;
+  it.pair = idx / (nf + nn);
+  const int k = idx - it.pair * (nf + nn);
+  it.split = k;
+  if (k < nf) {
+    it.far = 1;
+    it.t0 = k * p.per;
+    it.t1 = int(lcx_min64(p.far_end, int64_t(it.t0) + p.per));
+  } else {
+    it.far = 0;
+    it.t0 = int(p.near_begin + int64_t(k - nf) * p.per);
+    it.t1 = int(lcx_min64(p.ntiles, int64_t(it.t0) + p.per));
+  }
+  return it;
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(kThreads, 1)
+est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k3,
+              const __grid_constant__ CUtensorMap map_kraw) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;          // [NKS]
+  uint64_t* k_empty = k_full + NKS;     // [NKS]
+  uint64_t* s_full = k_empty + NKS;     // [2]
+  uint64_t* s_empty = s_full + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_empty + 2);
+  float* T = reinterpret_cast<float*>(smem + OFF_T);
+
+  const Item it = decode_item(p, blockIdx.x);
+  const int ntl = it.t1 - it.t0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    tc::mbar_init(q_full, 1);
+    for (int b = 0; b < NKS; ++b) {
+      tc::mbar_init(k_full + b, 1);
+      tc::mbar_init(k_empty + b, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(s_full + b, 1);
+      tc::mbar_init(s_empty + b, 8);
+    }
+    tc::fence_barrier_init();
+    tc::fence_proxy_async();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 128);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int g = it.pair / p.pairs_per_group;   // kv head
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // resident Q terms of the pair (near: rope(q, gi); far: rope(q, c - 1))
+      tc::mbar_expect_tx(q_full, kQBytes);
+      const int qbox0 = ((it.far * p.npairs + it.pair) * 6);
+      for (int b = 0; b < 6; ++b)
+        tc::tma_load_3d(smem + OFF_Q + b * kQBox, &map_q, q_full, 0, 0, qbox0 + b);
+      for (int t = 0; t < ntl; ++t) {
+        const int st = t % NKS;
+        tc::mbar_wait(k_empty + st, ((t / NKS) & 1) ^ 1);
+        const int kt = it.t0 + t;
+        uint8_t* dst = smem + OFF_K + st * kKStage;
+        if (it.far) {
+          tc::mbar_expect_tx(k_full + st, 2 * kKBox);
+          tc::tma_load_3d(dst, &map_kraw, k_full + st, 0, g, kt * 64);
+          tc::tma_load_3d(dst + kKBox, &map_kraw, k_full + st, 64, g, kt * 64);
+        } else {
+          tc::mbar_expect_tx(k_full + st, 6 * kKBox);
+          const int b0 = int((int64_t(g) * p.ntiles_k + kt) * 6);
+          for (int b = 0; b < 6; ++b)
+            tc::tma_load_3d(dst + b * kKBox, &map_k3, k_full + st, 0, 0, b0 + b);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    tc::mbar_wait(q_full, 0);
+    const uint64_t dq = tc::sdesc_sw128(tc::smem_u32(smem + OFF_Q));
+    const uint64_t dk0 = tc::sdesc_sw128(tc::smem_u32(smem + OFF_K));
+    // (q term, k term) products of order <= 2^-16: hh hm mh hl lh mm (near), h. m. l. (far)
+    const int qt_near[6] = {0, 0, 1, 0, 2, 1}, kt_near[6] = {0, 1, 0, 2, 0, 1};
+    for (int t = 0; t < ntl; ++t) {
+      const int st = t % NKS, sb = t & 1;
+      tc::mbar_wait(k_full + st, (t / NKS) & 1);
+      tc::mbar_wait(s_empty + sb, ((t >> 1) & 1) ^ 1);
+      tc::tc_fence_after();
+      const uint64_t dk = dk0 + ((st * kKStage) >> 4);
+      const uint32_t dS = tmem + sb * BN;
+      const int nprod = it.far ? 3 : 6;
+      for (int x = 0; x < nprod; ++x) {
+        const int qt = it.far ? x : qt_near[x];
+        const int kt = it.far ? 0 : kt_near[x];
+#pragma unroll
+        for (int half = 0; half < 2; ++half)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc::mma_f16_ss_warp(dS, dq + (((qt * 2 + half) * kQBox + kk * 32) >> 4),
+                                dk + (((kt * 2 + half) * kKBox + kk * 32) >> 4), IDESC,
+                                (x | half | kk) ? 1u : 0u);
+      }
+      tc::mma_commit_warp(k_empty + st);
+      tc::mma_commit_warp(s_full + sb);
+    }
+  } else if (warp >= 4) {
+    const int wq = warp & 3, part = (warp - 4) >> 2;
+    const int r = wq * 32 + lane;            // TMEM lane = row of the pair tile
+    const int hh = r >> 6, rr = r & 63;      // head within the pair, estimator row
+    const int h = g * p.group + (it.pair % p.pairs_per_group) * 2 + hh;
+    const bool head_ok = (it.pair % p.pairs_per_group) * 2 + hh < p.group;
+    const bool row_ok = head_ok && rr < p.block;
+    const int64_t gi = p.nk - p.block + rr;
+    const uint32_t lane_base = uint32_t(wq * 32) << 16;
+    float m = -INFINITY, s = 0.f, rm = 0.f, rinv = 0.f;
+    if (PASS == 2 && row_ok) {
+      const float2 ms = p.rowstat[int64_t(h) * p.block + rr];
+      rm = ms.x * 1.4426950408889634f;  // natural -> log2 domain
+      rinv = ms.y > 0.f ? 1.f / ms.y : 0.f;
+    }
+    const float sc = p.scale_log2;
+    for (int t = 0; t < ntl; ++t) {
+      const int sb = t & 1;
+      const int64_t j0 = int64_t(it.t0 + t) * BN;
+      tc::mbar_wait(s_full + sb, (t >> 1) & 1);
+      tc::tc_fence_after();
+      float v[32];
+      tc::tmem_ld32(tmem + lane_base + sb * BN + part * 32, v);
+      tc::tmem_wait_ld();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(s_empty + sb);
+      const int64_t jb = j0 + part * 32;
+      if (PASS == 1) {
+        float tmax = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const bool ok = row_ok && jb + c <= gi && jb + c < p.nk;
+          v[c] = ok ? v[c] * sc : -INFINITY;
+          tmax = fmaxf(tmax, v[c]);
+        }
+        if (tmax != -INFINITY) {
+          float ts = 0.f;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) ts += ex2(v[c] - tmax);
+          const float nm = fmaxf(m, tmax);
+          s = s * ex2(m - nm) + ts * ex2(tmax - nm);
+          m = nm;
+        }
+      } else {
+        float* Tr = T + r * 65 + part * 32;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const bool ok = row_ok && jb + c <= gi && jb + c < p.nk;
+          Tr[c] = ok ? ex2(v[c] * sc - rm) * rinv : 0.f;
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        const int et = threadIdx.x - 128;    // 0..255
+        // column sums: thread et < 128 -> (head et / 64, key et % 64)
+        if (et < 128) {
+          const int ch = et >> 6, c = et & 63;
+          const int hc = g * p.group + (it.pair % p.pairs_per_group) * 2 + ch;
+          const int64_t j = j0 + c;
+          if ((it.pair % p.pairs_per_group) * 2 + ch < p.group && j < p.nk) {
+            float acc = 0.f;
+            for (int q = 0; q < p.block; ++q) acc += T[(ch * 64 + q) * 65 + c];
+            p.col_part[int64_t(hc) * p.nk + j] = acc;
+          }
+        }
+        // diagonal sums: thread et -> (head et / 128, e = et % 128), e = r - c + 63
+        {
+          const int dh = et >> 7, e = et & 127;
+          const int hd = g * p.group + (it.pair % p.pairs_per_group) * 2 + dh;
+          if ((it.pair % p.pairs_per_group) * 2 + dh < p.group && e < 127) {
+            float acc = 0.f;
+            const int q0 = e > 63 ? e - 63 : 0;
+            const int q1 = min(p.block - 1, e);
+            for (int q = q0; q <= q1; ++q) acc += T[(dh * 64 + q) * 65 + (q - e + 63)];
+            p.diag_part[(int64_t(hd) * p.ntiles + it.t0 + t) * 128 + e] = acc;
+          }
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+      }
+    }
+    if (PASS == 1) {
+      // combine the two column halves of the row, then write this split's stats
+      float* red = T;  // [2][128] (m, s) exchange, pass 1 does not use the transpose
+      red[part * 256 + r * 2] = m;
+      red[part * 256 + r * 2 + 1] = s;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (part == 0 && row_ok) {
+        const float m2 = red[256 + r * 2], s2 = red[256 + r * 2 + 1];
+        const float nm = fmaxf(m, m2);
+        float tot = 0.f;
+        if (nm != -INFINITY) tot = s * ex2(m - nm) + s2 * ex2(m2 - nm);
+        // natural-log domain (m, sum), as the CUDA-core estimator writes them
+        p.stats[(int64_t(h) * p.nsplit + it.split) * p.block + rr] =
+            make_float2(nm == -INFINITY ? -INFINITY : nm * 0.6931471805599453f, tot);
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 1) tc::tmem_dealloc(tmem, 128);
+}
+
+// ------------------------------------------------------------- prep --
+// K3 [hkv][ntiles][3 terms][2 halves][64 keys][64 dims] = split(rope(k_j, j)), rows [r0, r1)
+__global__ void est_k3_kernel(const __nv_bfloat16* __restrict__ k, int64_t r0, int64_t r1,
+                              int hkv, int64_t ntiles, const float2* __restrict__ rope,
+                              __nv_bfloat16* __restrict__ k3) {
+  const int64_t idx = r0 * hkv * 64 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // pair
+  if (idx >= r1 * hkv * 64) return;
+  const int pr = int(idx & 63);
+  const int64_t rowhead = idx >> 6;
+  const int64_t j = rowhead / hkv;
+  const int gg = int(rowhead % hkv);
+  const float2 xy = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(k)[idx]);
+  const float2 cs = rope[j * 64 + pr];
+  const float rx = xy.x * cs.x - xy.y * cs.y, ry = xy.x * cs.y + xy.y * cs.x;
+  const int d = 2 * pr, half = d >> 6;
+  const __nv_bfloat162 h2 = __floats2bfloat162_rn(rx, ry);
+  const float2 hf = __bfloat1622float2(h2);
+  const __nv_bfloat162 m2 = __floats2bfloat162_rn(rx - hf.x, ry - hf.y);
+  const float2 mf = __bfloat1622float2(m2);
+  const __nv_bfloat162 l2 = __floats2bfloat162_rn(rx - hf.x - mf.x, ry - hf.y - mf.y);
+  const __nv_bfloat162 terms[3] = {h2, m2, l2};
+#pragma unroll
+  for (int tm = 0; tm < 3; ++tm) {
+    const int64_t o = (((((int64_t(gg) * ntiles + (j >> 6)) * 3 + tm) * 2 + half) * 64 + (j & 63)) *
+                           64 + (d & 63)) >> 1;
+    reinterpret_cast<__nv_bfloat162*>(k3)[o] = terms[tm];
+  }
+}
+
+// Q3 [far 0/1][npairs][3 terms][2 halves][128 rows][64 dims]: row = 64 * (head in pair) + r
+__global__ void est_q3_kernel(const __nv_bfloat16* __restrict__ q, int hq, int group,
+                              int pairs_per_group, int npairs, int64_t nk, int64_t block,
+                              int far_too, int64_t c, const float2* __restrict__ rope,
+                              __nv_bfloat16* __restrict__ q3) {
+  const int row = blockIdx.x;        // 0..127
+  const int pair = blockIdx.y;
+  const int far = blockIdx.z;
+  if (far && !far_too) return;
+  const int pr = threadIdx.x;        // 0..63
+  const int hh = row >> 6, r = row & 63;
+  const int hig = (pair % pairs_per_group) * 2 + hh;
+  const int h = (pair / pairs_per_group) * group + hig;
+  float rx = 0.f, ry = 0.f;
+  if (hig < group && r < block) {
+    const int64_t gi = nk - block + r;
+    const float2 xy = __bfloat1622float2(
+        reinterpret_cast<const __nv_bfloat162*>(q + (gi * hq + h) * 128)[pr]);
+    const float2 cs = rope[(far ? c - 1 : gi) * 64 + pr];
+    rx = xy.x * cs.x - xy.y * cs.y;
+    ry = xy.x * cs.y + xy.y * cs.x;
+  }
+  const __nv_bfloat162 h2 = __floats2bfloat162_rn(rx, ry);
+  const float2 hf = __bfloat1622float2(h2);
+  const __nv_bfloat162 m2 = __floats2bfloat162_rn(rx - hf.x, ry - hf.y);
+  const float2 mf = __bfloat1622float2(m2);
+  const __nv_bfloat162 l2 = __floats2bfloat162_rn(rx - hf.x - mf.x, ry - hf.y - mf.y);
+  const __nv_bfloat162 terms[3] = {h2, m2, l2};
+  const int d = 2 * pr, half = d >> 6;
+#pragma unroll
+  for (int tm = 0; tm < 3; ++tm) {
+    const int64_t o = (((((int64_t(far) * npairs + pair) * 3 + tm) * 2 + half) * 128 + row) * 64 +
+                       (d & 63)) >> 1;
+    reinterpret_cast<__nv_bfloat162*>(q3)[o] = terms[tm];
+  }
+}
+
+}  // namespace
+
+size_t est_tc_k3_bytes(int64_t n, int hkv) {
+  return size_t((n + 63) / 64) * hkv * 6 * kKBox;
+}
+
+int est_tc_prepare_keys(const void* k, int64_t r0, int64_t r1, int hkv, int64_t ntiles,
+                        const float2* rope, void* k3, cudaStream_t st) {
+  if (r1 <= r0) return LCX_OK;
+  const int64_t pairs = (r1 - r0) * hkv * 64;
+  est_k3_kernel<<<unsigned((pairs + 255) / 256), 256, 0, st>>>(
+      reinterpret_cast<const __nv_bfloat16*>(k), r0, r1, hkv, ntiles, rope,
+      reinterpret_cast<__nv_bfloat16*>(k3));
+  LCX_CHECK_LAUNCH();
+  return LCX_OK;
+}
+
+bool est_tc_eligible(int dtype, int dim, int64_t block) {
+  return dtype == LCX_BF16 && dim == 128 && block <= 64;
+}
+
+void est_tc_size(int hq, int hkv, Sizer& sz) {
+  const int group = hq / hkv, ppg = (group + 1) / 2, npairs = hkv * ppg;
+  sz.take<uint8_t>(size_t(2) * npairs * 6 * kQBox);  // q3
+}
+
+void est_tc_plan(const EstTcArgs& a, EstTcPlan& pl) {
+  const int group = a.hq / a.hkv, ppg = (group + 1) / 2;
+  pl.npairs = a.hkv * ppg;
+  pl.ntiles = (a.nk + 63) / 64;
+  pl.far_end = 0;
+  pl.near_begin = 0;
+  if (a.pos_mode == 1) {
+    // near iff gi - j <= c - 1 (sparse.cpp:169-178), gi in [nk - block, nk):
+    // keys < nk - block - c + 1 are far for every row, keys >= nk - c near for every row
+    const int64_t lim_far = a.nk - a.block - a.c + 1;
+    pl.far_end = lim_far > 0 ? std::min<int64_t>(pl.ntiles, lim_far / 64) : 0;
+    const int64_t near_key = a.nk - a.c;
+    pl.near_begin = near_key <= 0 ? 0 : std::min<int64_t>(pl.ntiles, (near_key + 63) / 64);
+    if (pl.near_begin < pl.far_end) pl.near_begin = pl.far_end;
+  }
+  const int64_t tc_tiles = pl.far_end + (pl.ntiles - pl.near_begin);
+  pl.per = int(std::max<int64_t>(4, (tc_tiles * pl.npairs + 4 * a.sm_count - 1) /
+                                        (4 * int64_t(a.sm_count))));
+  // at most 64 pieces per phase and pair: bounds the stats slots (64 + 2 incl. partials)
+  pl.per = int(std::max<int64_t>(pl.per, (tc_tiles + 63) / 64));
+  const int nf = int((pl.far_end + pl.per - 1) / pl.per);
+  const int nn = int((pl.ntiles - pl.near_begin + pl.per - 1) / pl.per);
+  pl.tc_splits = nf + nn;
+  pl.items = pl.npairs * (nf + nn);
+}
+
+// One pass of the estimator for one chunk on the tensor cores over the far and near
+// tiles of every head pair; writes the same stats / column / diagonal partials as the
+// CUDA-core estimator (which covers the mixed tiles [far_end, near_begin)).
+int est_tc_run(const EstTcArgs& a, const EstTcPlan& pl, Arena& ar, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    LCX_CHECK_CUDA(cudaFuncSetAttribute(est_tc_kernel<1>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    LCX_CHECK_CUDA(cudaFuncSetAttribute(est_tc_kernel<2>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+    attr = true;
+  }
+  const int group = a.hq / a.hkv, ppg = (group + 1) / 2, npairs = pl.npairs;
+  uint8_t* q3 = ar.take<uint8_t>(size_t(2) * npairs * 6 * kQBox);
+  if (pl.items == 0) return LCX_OK;
+  const bool dca = a.pos_mode == 1;
+  if (a.pass == 1) {  // operands: rotated, 3-term split query rows (near and far)
+    dim3 grid(128, unsigned(npairs), 2);
+    est_q3_kernel<<<grid, 64, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(a.q), a.hq, group,
+                                       ppg, npairs, a.nk, a.block, dca ? 1 : 0, a.c, a.rope,
+                                       reinterpret_cast<__nv_bfloat16*>(q3));
+    LCX_CHECK_LAUNCH();
+  }
+  CUtensorMap mq, mk3, mkr;
+  const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  LCX_TRY(make_tmap3(&mq, BF, q3, 64, 128, uint64_t(2) * npairs * 6, 128, kQBox, 64, 128, 1));
+  LCX_TRY(make_tmap3(&mk3, BF, const_cast<void*>(a.k3), 64, 64, uint64_t(a.hkv) * a.k3_tiles * 6, 128, kKBox, 64,
+                     64, 1));
+  LCX_TRY(make_tmap3(&mkr, BF, const_cast<void*>(a.k), 128, uint64_t(a.hkv), uint64_t(a.nk), 256,
+                     uint64_t(a.hkv) * 256, 64, 1, 64));
+  EstTcParams p{};
+  p.group = group;
+  p.pairs_per_group = ppg;
+  p.npairs = npairs;
+  p.nk = a.nk;
+  p.block = int(a.block);
+  p.ntiles_k = a.k3_tiles;
+  p.ntiles = pl.ntiles;
+  p.far_end = pl.far_end;
+  p.near_begin = pl.near_begin;
+  p.per = pl.per;
+  p.scale_log2 = float(1.4426950408889634 / std::sqrt(128.0));
+  p.nsplit = a.nsplit;
+  p.stats = a.stats;
+  p.rowstat = a.rowstat;
+  p.col_part = a.col_part;
+  p.diag_part = a.diag_part;
+  if (a.pass == 1)
+    est_tc_kernel<1><<<unsigned(pl.items), kThreads, kSmem, st>>>(p, mq, mk3, mkr);
+  else
+    est_tc_kernel<2><<<unsigned(pl.items), kThreads, kSmem, st>>>(p, mq, mk3, mkr);
+  LCX_CHECK_LAUNCH();
+  return LCX_OK;
+}
+
+}  // namespace lcx

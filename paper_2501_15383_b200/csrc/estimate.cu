@@ -18,6 +18,7 @@
 // sums (over rows, ascending) and the 127 diagonal partial sums; a combine
 // kernel adds the two tiles that share each diagonal in ascending tile order.
 // All reductions are in a fixed order (bitwise deterministic).
+#include "est_tc.cuh"
 #include "lcx_internal.cuh"
 
 namespace lcx {
@@ -43,6 +44,8 @@ struct EstDev {
   int tiles_per_split;
   int nsplit;
   int nrt;           // row tiles
+  int64_t tile0, tile_end;  // key tiles this launch covers
+  int split0, nsplit_total; // stats slot of split 0, slots per head
 };
 
 // ---- prep: rotate the estimator query rows and the keys ------------------
@@ -69,10 +72,10 @@ __global__ void est_prep_q(EstDev a) {
 }
 
 template <typename T>
-__global__ void est_prep_k(const T* __restrict__ k, int64_t nk, int hkv, int dim,
+__global__ void est_prep_k(const T* __restrict__ k, int64_t j0, int64_t nk, int hkv, int dim,
                            const float2* __restrict__ rope, float* __restrict__ kn) {
-  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // pair index
   const int P = dim / 2;
+  const int64_t idx = j0 * hkv * P + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // pair
   const int64_t total = nk * hkv * P;
   if (idx >= total) return;
   const int p = int(idx % P);
@@ -129,8 +132,8 @@ est_tile_kernel(EstDev a, float2* __restrict__ stats, const float2* __restrict__
     }
   }
   const float inv_sqrt = rsqrtf(float(a.dim));
-  const int64_t t_begin = int64_t(split) * a.tiles_per_split;
-  const int64_t t_end = lcx_min64(a.ntiles, t_begin + a.tiles_per_split);
+  const int64_t t_begin = a.tile0 + int64_t(split) * a.tiles_per_split;
+  const int64_t t_end = lcx_min64(a.tile_end, t_begin + a.tiles_per_split);
   const T* kraw = reinterpret_cast<const T*>(a.k);
 
   for (int64_t t = t_begin; t < t_end; ++t) {
@@ -257,7 +260,7 @@ est_tile_kernel(EstDev a, float2* __restrict__ stats, const float2* __restrict__
     for (int i = 0; i < 4; ++i) {
       const int r = ty * 4 + i;
       if (r < rows)
-        stats[((int64_t(h) * a.nsplit) + split) * a.block + row0 + r] =
+        stats[((int64_t(h) * a.nsplit_total) + a.split0 + split) * a.block + row0 + r] =
             make_float2(run_m[i], run_s[i]);
     }
   }
@@ -315,37 +318,86 @@ __global__ void est_combine_lines(const float* __restrict__ col_part,
   }
 }
 
-void plan(const EstimateArgs& a, int sm_count, int64_t& ntiles, int& nsplit, int& tps,
-          int& nrt) {
-  ntiles = (a.nk + kKeys - 1) / kKeys;
+void plan(const EstimateArgs& a, int sm_count, int64_t tiles, int& nsplit, int& tps, int& nrt) {
   nrt = int((a.block + kRows - 1) / kRows);
   const int64_t want = std::max<int64_t>(1, (int64_t(sm_count) * 4) / std::max(1, a.hq * nrt));
-  tps = int(std::max<int64_t>(1, (ntiles + want - 1) / want));
-  nsplit = int((ntiles + tps - 1) / tps);
+  tps = int(std::max<int64_t>(1, (tiles + want - 1) / want));
+  nsplit = tiles > 0 ? int((tiles + tps - 1) / tps) : 0;
+}
+
+bool use_tc(const EstimateArgs& a) {
+  return a.k3 != nullptr && a.est == nullptr && est_tc_eligible(a.dtype, a.dim, a.block);
+}
+
+EstTcArgs tc_args(const EstimateArgs& a, int sm_count) {
+  EstTcArgs t{};
+  t.q = a.q;
+  t.k = a.k;
+  t.hq = a.hq;
+  t.hkv = a.hkv;
+  t.nk = a.nk;
+  t.block = a.block;
+  t.pos_mode = a.pos_mode;
+  t.c = a.c;
+  t.rope = a.rope;
+  t.k3 = a.k3;
+  t.k3_tiles = a.k3_tiles;
+  t.sm_count = sm_count;
+  return t;
+}
+
+// CUDA-core tile range of this launch: all tiles, or the mixed near / far tiles left
+// over by the tensor-core estimator
+void simt_range(const EstimateArgs& a, int sm_count, int64_t& t0, int64_t& t1, int& tc_splits) {
+  const int64_t ntiles = (a.nk + kKeys - 1) / kKeys;
+  t0 = 0;
+  t1 = ntiles;
+  tc_splits = 0;
+  if (use_tc(a)) {
+    EstTcArgs t = tc_args(a, sm_count);
+    EstTcPlan pl;
+    est_tc_plan(t, pl);
+    t0 = pl.far_end;
+    t1 = pl.near_begin;
+    tc_splits = pl.tc_splits;
+  }
 }
 
 }  // namespace
 
 void estimate_simt_size(const EstimateArgs& a, Sizer& sz, int sm_count) {
-  int64_t ntiles;
-  int nsplit, tps, nrt;
-  plan(a, sm_count, ntiles, nsplit, tps, nrt);
+  int64_t t0, t1;
+  int tc_splits, nsplit, tps, nrt;
+  simt_range(a, sm_count, t0, t1, tc_splits);
+  plan(a, sm_count, t1 - t0, nsplit, tps, nrt);
+  const int64_t ntiles = (a.nk + kKeys - 1) / kKeys;
+  // stats slots: the worst case over chunk sizes (CUDA-core splits of every tile, or the
+  // tensor-core estimator's <= 2 x 66 pieces plus the mixed tiles' splits)
+  int nsplit_all, tps_all, nrt_all;
+  plan(a, sm_count, ntiles, nsplit_all, tps_all, nrt_all);
+  const int nst = std::max(nsplit_all, nsplit + 136) + 1;
   sz.take<float>(size_t(a.hq) * a.block * a.dim);                       // qn
   if (a.pos_mode == 1) sz.take<float>(size_t(a.hq) * a.block * a.dim);  // qf
   sz.take<float>(size_t(a.nk) * a.hkv * a.dim);                         // kn
-  sz.take<float2>(size_t(a.hq) * nsplit * a.block);                     // stats
+  sz.take<float2>(size_t(a.hq) * nst * a.block);                        // stats
   sz.take<float2>(size_t(a.hq) * a.block);                              // rowstat
   if (a.col || a.slash) {
     sz.take<float>(size_t(nrt) * a.hq * a.nk);                 // col_part
     sz.take<float>(size_t(nrt) * a.hq * ntiles * 128);         // diag_part
   }
+  if (use_tc(a)) est_tc_size(a.hq, a.hkv, sz);
 }
 
 int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream_t st) {
   if (a.dim > kMaxDim) return fail(LCX_ERR_CONFIG, "estimator supports head dim <= 128");
-  int64_t ntiles;
-  int nsplit, tps, nrt;
-  plan(a, ctx->sm_count, ntiles, nsplit, tps, nrt);
+  const bool tc = use_tc(a);
+  int64_t s0, s1;
+  int tc_splits, nsplit, tps, nrt;
+  simt_range(a, ctx->sm_count, s0, s1, tc_splits);
+  plan(a, ctx->sm_count, s1 - s0, nsplit, tps, nrt);
+  if (tc && nrt != 1) return fail(LCX_ERR_INTERNAL, "tensor-core estimator needs block <= 64");
+  const int64_t ntiles = (a.nk + kKeys - 1) / kKeys;
+  const int nst = std::max(1, nsplit + tc_splits);
   EstDev d{};
   d.q = a.q;
   d.k = a.k;
@@ -363,10 +415,14 @@ int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream
   d.tiles_per_split = tps;
   d.nsplit = nsplit;
   d.nrt = nrt;
+  d.tile0 = s0;
+  d.tile_end = s1;
+  d.split0 = tc_splits;
+  d.nsplit_total = nst;
   float* qn = ar.take<float>(size_t(a.hq) * a.block * a.dim);
   float* qf = a.pos_mode == 1 ? ar.take<float>(size_t(a.hq) * a.block * a.dim) : nullptr;
   float* kn = ar.take<float>(size_t(a.nk) * a.hkv * a.dim);
-  float2* stats = ar.take<float2>(size_t(a.hq) * nsplit * a.block);
+  float2* stats = ar.take<float2>(size_t(a.hq) * nst * a.block);
   float2* rowstat = ar.take<float2>(size_t(a.hq) * a.block);
   float* col_part = nullptr;
   float* diag_part = nullptr;
@@ -377,22 +433,37 @@ int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream
   d.qn = qn;
   d.qf = qf;
   d.kn = kn;
+  Arena tc_ar = ar;  // the tensor-core estimator's operands (same offsets in both passes)
+  EstTcArgs ta = tc_args(a, ctx->sm_count);
+  EstTcPlan pl{};
+  if (tc) {
+    est_tc_plan(ta, pl);
+    ta.nsplit = nst;
+    ta.stats = stats;
+    ta.rowstat = rowstat;
+    ta.col_part = col_part;
+    ta.diag_part = diag_part;
+  }
 
   const bool bf = a.dtype == LCX_BF16;
-  {
+  const bool simt = nsplit > 0;
+  if (simt) {
     dim3 grid(unsigned(a.block), unsigned(a.hq));
     if (bf) est_prep_q<__nv_bfloat16><<<grid, 64, 0, st>>>(d);
     else est_prep_q<float><<<grid, 64, 0, st>>>(d);
     LCX_CHECK_LAUNCH();
-    const int64_t pairs = a.nk * a.hkv * (a.dim / 2);
+    const int64_t j0 = s0 * kKeys, j1 = std::min<int64_t>(a.nk, s1 * kKeys);
+    const int64_t pairs = (j1 - j0) * a.hkv * (a.dim / 2);
     const unsigned blocks = unsigned((pairs + 255) / 256);
-    if (bf)
-      est_prep_k<__nv_bfloat16><<<blocks, 256, 0, st>>>(
-          reinterpret_cast<const __nv_bfloat16*>(a.k), a.nk, a.hkv, a.dim, a.rope, kn);
-    else
-      est_prep_k<float><<<blocks, 256, 0, st>>>(reinterpret_cast<const float*>(a.k), a.nk,
-                                                 a.hkv, a.dim, a.rope, kn);
-    LCX_CHECK_LAUNCH();
+    if (pairs > 0) {
+      if (bf)
+        est_prep_k<__nv_bfloat16><<<blocks, 256, 0, st>>>(
+            reinterpret_cast<const __nv_bfloat16*>(a.k), j0, j1, a.hkv, a.dim, a.rope, kn);
+      else
+        est_prep_k<float><<<blocks, 256, 0, st>>>(reinterpret_cast<const float*>(a.k), j0, j1,
+                                                   a.hkv, a.dim, a.rope, kn);
+      LCX_CHECK_LAUNCH();
+    }
   }
   const int DP = a.dim + 1;
   const size_t smem = sizeof(float) * (size_t(2 * kRows + 2 * kKeys) * DP + kRows * 65);
@@ -406,32 +477,48 @@ int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream
     }
     return LCX_OK;
   };
-  dim3 grid(unsigned(nsplit), unsigned(a.hq), unsigned(nrt));
-  if (bf) {
-    LCX_TRY(set_attr((const void*)est_tile_kernel<__nv_bfloat16, 1>, 0));
-    LCX_TRY(set_attr((const void*)est_tile_kernel<__nv_bfloat16, 2>, 1));
-    est_tile_kernel<__nv_bfloat16, 1><<<grid, kThreads, smem, st>>>(d, stats, nullptr, nullptr,
-                                                                     nullptr, nullptr);
-  } else {
-    LCX_TRY(set_attr((const void*)est_tile_kernel<float, 1>, 2));
-    LCX_TRY(set_attr((const void*)est_tile_kernel<float, 2>, 3));
-    est_tile_kernel<float, 1><<<grid, kThreads, smem, st>>>(d, stats, nullptr, nullptr, nullptr,
-                                                             nullptr);
+  dim3 grid(unsigned(std::max(nsplit, 1)), unsigned(a.hq), unsigned(nrt));
+  // ---- pass 1: row max / sum-exp ----
+  if (tc) {
+    Arena ta_ar = tc_ar;
+    ta.pass = 1;
+    LCX_TRY(est_tc_run(ta, pl, ta_ar, st));
   }
-  LCX_CHECK_LAUNCH();
-  {
-    const int64_t rows = int64_t(a.hq) * a.block;
-    est_combine_stats<<<unsigned((rows + 255) / 256), 256, 0, st>>>(stats, a.hq, nsplit,
-                                                                    a.block, rowstat);
+  if (simt) {
+    if (bf) {
+      LCX_TRY(set_attr((const void*)est_tile_kernel<__nv_bfloat16, 1>, 0));
+      LCX_TRY(set_attr((const void*)est_tile_kernel<__nv_bfloat16, 2>, 1));
+      est_tile_kernel<__nv_bfloat16, 1><<<grid, kThreads, smem, st>>>(d, stats, nullptr, nullptr,
+                                                                       nullptr, nullptr);
+    } else {
+      LCX_TRY(set_attr((const void*)est_tile_kernel<float, 1>, 2));
+      LCX_TRY(set_attr((const void*)est_tile_kernel<float, 2>, 3));
+      est_tile_kernel<float, 1><<<grid, kThreads, smem, st>>>(d, stats, nullptr, nullptr,
+                                                               nullptr, nullptr);
+    }
     LCX_CHECK_LAUNCH();
   }
-  if (bf)
-    est_tile_kernel<__nv_bfloat16, 2><<<grid, kThreads, smem, st>>>(d, nullptr, rowstat, a.est,
-                                                                     col_part, diag_part);
-  else
-    est_tile_kernel<float, 2><<<grid, kThreads, smem, st>>>(d, nullptr, rowstat, a.est, col_part,
-                                                             diag_part);
-  LCX_CHECK_LAUNCH();
+  {
+    const int64_t rows = int64_t(a.hq) * a.block;
+    est_combine_stats<<<unsigned((rows + 255) / 256), 256, 0, st>>>(stats, a.hq, nst, a.block,
+                                                                    rowstat);
+    LCX_CHECK_LAUNCH();
+  }
+  // ---- pass 2: probabilities -> column / diagonal partials ----
+  if (tc) {
+    Arena ta_ar = tc_ar;
+    ta.pass = 2;
+    LCX_TRY(est_tc_run(ta, pl, ta_ar, st));
+  }
+  if (simt) {
+    if (bf)
+      est_tile_kernel<__nv_bfloat16, 2><<<grid, kThreads, smem, st>>>(d, nullptr, rowstat,
+                                                                       a.est, col_part, diag_part);
+    else
+      est_tile_kernel<float, 2><<<grid, kThreads, smem, st>>>(d, nullptr, rowstat, a.est,
+                                                               col_part, diag_part);
+    LCX_CHECK_LAUNCH();
+  }
   if (a.col || a.slash) {
     const int64_t total = int64_t(a.hq) * a.nk;
     est_combine_lines<<<unsigned((total + 255) / 256), 256, 0, st>>>(

@@ -150,6 +150,10 @@ struct EstimateArgs {
   float* col;      // optional [hq][nk]
   float* slash;    // optional [hq][nk]
   int slash_mean;
+  // tensor-core estimator (bf16, dim 128): rotated 3-term keys prepared up to nk
+  // (est_tc_prepare_keys); nullptr = CUDA-core estimator for every tile
+  const void* k3;
+  int64_t k3_tiles;
 };
 int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream_t st);
 void estimate_simt_size(const EstimateArgs& a, Sizer& sz, int sm_count);

@@ -23,3 +23,25 @@ def lse_rel_err(lse, ref):
 
 
 TOL = {"fp32": 1e-5, "bf16": 2e-3}
+
+
+def check_selection(port, got_v, got_s, col32, sl32, col64, sl64, t1, block, budget,
+                    sink=True, band=True, rel=1e-5):
+    """The index contract: (1) the device selection is identical to the reference ranking
+    of the device's own fp32 scores (ties -> lowest index); (2) where it differs from the
+    selection of the fp64 reference scores, the differing lines are near-ties: their fp64
+    score lies within `rel` (relative to the largest score) of the selection threshold."""
+    crit = port.select_from_scores(col32, sl32, t1, block, budget, sink, band)
+    assert list(got_v) == crit.verticals, "verticals differ from the ranking of own scores"
+    assert list(got_s) == crit.slashes, "slashes differ from the ranking of own scores"
+    ref = port.select_from_scores(col64, sl64, t1, block, budget, sink, band)
+    for got, want, score, k in ((got_v, ref.verticals, col64, budget[0]),
+                                (got_s, ref.slashes, sl64, budget[1])):
+        diff = set(got) ^ set(want)
+        if not diff:
+            continue
+        finite = np.where(np.isfinite(score), score, -np.inf)
+        thresh = np.sort(finite)[::-1][min(k, len(finite)) - 1]
+        scale = np.abs(finite[np.isfinite(finite)]).max()
+        for x in diff:
+            assert abs(score[x] - thresh) <= rel * scale, (x, score[x], thresh)
