@@ -7,10 +7,11 @@ namespace lcx {
 
 struct GatherArgs {
   const __nv_bfloat16* q;                          // [n][hq][128]
-  const __nv_bfloat16* k;                          // [n][hkv][128] raw (unrotated)
+  const float* kf;                                 // [n][hkv][128] rope(k_j, kpos(j)) fp32
   const __nv_bfloat16* v;                          // [n][hkv][128]
   int hq, hkv, group;
   int64_t row_begin, row_end;                      // rows (row_begin % 128 == 0)
+  int64_t key_lo, key_hi;                          // only entries with key in [key_lo, key_hi)
   int rel_mode;                                    // 0 standard, 1 DCA
   int64_t s, c;
   const int64_t* pos_q; const int64_t* pos_k;     // standard mode (nullptr = iota)

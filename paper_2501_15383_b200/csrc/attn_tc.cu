@@ -81,6 +81,7 @@ struct Group {
   int vlo, vhi;  // compact positions [vlo, vhi) (64-aligned start)
   int ulo, uhi;
   int nvt, nst;
+  int soff;     // slash tiles start at list position soff (cyclic), see setup_item
   int64_t kt0;  // dense: first key tile
 };
 
@@ -160,6 +161,20 @@ __device__ void setup_item(const TcParams& p, int item, Item& it) {
       G.ulo = lower_bound32(uh, nuh, (G.klo >> 6) - ib);
       G.uhi = lower_bound32(uh, nuh, ceil_div64(G.khi) - ib);
       G.nst = G.uhi - G.ulo;
+      // Key-aligned schedule: block b's relative tile u is key tile 2b + u.  Every block of
+      // a head shares the same u list, so a block starts its cyclic walk at the first
+      // u >= u_first + (-2b mod span): the blocks running concurrently then read the SAME
+      // key tile at the same time (one DRAM read per wave, the rest L2 hits) instead of
+      // distinct tiles 2 apart.
+      G.soff = 0;
+      if (G.nst > 1) {
+        const int32_t* ul = uh + G.ulo;
+        const int64_t span = int64_t(ul[G.nst - 1]) - ul[0] + 1;
+        const int64_t shift = (2 * (it.i0 >> 7)) % span;
+        const int64_t target = ul[0] + (span - shift) % span;
+        G.soff = lower_bound32(ul, G.nst, target);
+        if (G.soff >= G.nst) G.soff = 0;
+      }
     }
     if (G.nvt + G.nst == 0) continue;
     it.grp[it.ng++] = G;
@@ -187,7 +202,9 @@ __device__ Tile get_tile(const TcParams& p, const Item& it, int t) {
         T.key0 = (G.kt0 + t) * 64;
       } else {
         T.kind = T_SLASH;
-        T.key0 = it.i0 + int64_t(p.tc_u[int64_t(it.h) * p.cap_u + G.ulo + t]) * 64;
+        int tt = t + G.soff;
+        if (tt >= G.nst) tt -= G.nst;
+        T.key0 = it.i0 + int64_t(p.tc_u[int64_t(it.h) * p.cap_u + G.ulo + tt]) * 64;
       }
       return T;
     }
@@ -783,7 +800,8 @@ __global__ void plan_items_kernel(const TcParams p, Item* __restrict__ plans) {
 __global__ void k_prep_kernel(const __nv_bfloat16* __restrict__ k, int64_t n, int64_t r0,
                               int64_t r1, int hkv, const int64_t* __restrict__ pos_k,
                               int rel_mode, int64_t s, const float2* __restrict__ rope,
-                              __nv_bfloat16* __restrict__ khi, __nv_bfloat16* __restrict__ klo) {
+                              __nv_bfloat16* __restrict__ khi, __nv_bfloat16* __restrict__ klo,
+                              float2* __restrict__ kf) {
   // pair index over rows [r0, r1)
   const int64_t idx = r0 * hkv * (HD / 2) + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int64_t total = r1 * hkv * (HD / 2);
@@ -795,6 +813,7 @@ __global__ void k_prep_kernel(const __nv_bfloat16* __restrict__ k, int64_t n, in
   const float2 xy = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(k)[idx]);
   const float2 c = rope[kp * (HD / 2) + pr];
   const float rx = xy.x * c.x - xy.y * c.y, ry = xy.x * c.y + xy.y * c.x;
+  kf[idx] = make_float2(rx, ry);
   const __nv_bfloat162 h2 = __floats2bfloat162_rn(rx, ry);
   const float2 hf = __bfloat1622float2(h2);
   // tiled [hkv][n/64][half][64 keys][64 dims]: each TMA box is one contiguous 8 KB block
@@ -1102,7 +1121,7 @@ int tc_prepare_rows(const void* k, const void* v, int64_t n, int64_t r0, int64_t
   const int64_t pairs = (r1 - r0) * hkv * (HD / 2);
   k_prep_kernel<<<unsigned((pairs + 255) / 256), 256, 0, st>>>(
       reinterpret_cast<const __nv_bfloat16*>(k), n, r0, r1, hkv, pos_k, rel_mode, s, rope, B.khi,
-      B.klo);
+      B.klo, reinterpret_cast<float2*>(B.kf));
   LCX_CHECK_LAUNCH();
   // V^T tiles covering [r0, r1); a partial trailing tile is rewritten (zero-padded) by the
   // range that completes it, so ranges must be handed in ascending order

@@ -36,6 +36,7 @@ struct TcParams {
 
 struct TcBuffers {
   __nv_bfloat16 *khi = nullptr, *klo = nullptr, *kchi = nullptr, *kclo = nullptr;
+  float* kf = nullptr;  // [n][hkv][128] rope(k_j, kpos(j)) in fp32 (CUDA-core gather)
   __half *vt = nullptr, *vct = nullptr;
   int32_t *ckeys = nullptr, *vbase = nullptr, *vfirst = nullptr;
   int64_t npad = 0, capp = 0, seg_len = 0;
@@ -54,8 +55,9 @@ void tc_layout(A& ar, int64_t n, int hq, int hkv, int64_t cap_v, int64_t seg_len
   B.ckeys = ar.template take<int32_t>(size_t(hq) * capp);
   B.vbase = ar.template take<int32_t>(size_t(hq) * (B.nseg_k + 1));
   B.vfirst = ar.template take<int32_t>(size_t(hq) * (B.nseg_k + 1));
-  B.khi = ar.template take<__nv_bfloat16>(size_t(n) * hkv * 128);
-  B.klo = ar.template take<__nv_bfloat16>(size_t(n) * hkv * 128);
+  B.khi = ar.template take<__nv_bfloat16>(size_t(B.npad) * hkv * 128);  // tiled: whole tiles
+  B.klo = ar.template take<__nv_bfloat16>(size_t(B.npad) * hkv * 128);
+  B.kf = ar.template take<float>(size_t(n) * hkv * 128);  // rotated K, fp32, row-major
   B.vt = ar.template take<__half>(size_t(hkv) * 128 * B.npad);
   B.kchi = ar.template take<__nv_bfloat16>(size_t(hq) * capp * 128);
   B.kclo = ar.template take<__nv_bfloat16>(size_t(hq) * capp * 128);

@@ -63,6 +63,7 @@ int ensure_rope(lcx_context* ctx, double base, int dim, int64_t P, cudaStream_t 
 namespace {
 
 constexpr int kDefaultTcMin = 96;  // slash entries per 64-key tile to use tcgen05
+constexpr int64_t kGatherSegment = 32768;  // keys per gather pass (L2-resident K / V)
 
 __global__ void dense_count_kernel(int hq, int64_t t0, int64_t t1, int64_t* out) {
   const int h = blockIdx.x * blockDim.x + threadIdx.x;
@@ -386,7 +387,7 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
     // isolated slashes + self-fallback rows on the CUDA-core gather, merged in place
     GatherArgs a{};
     a.q = reinterpret_cast<const __nv_bfloat16*>(in->q);
-    a.k = reinterpret_cast<const __nv_bfloat16*>(in->k);
+    a.kf = w.B.kf;
     a.v = reinterpret_cast<const __nv_bfloat16*>(in->v);
     a.hq = hq;
     a.hkv = in->hkv;
@@ -416,7 +417,15 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
     a.lse = lse;
     a.lse_stride = lse_stride;
     a.simt_count = ctx->profiling ? ctx->tile_counter + 1 : nullptr;
-    LCX_TRY(attention_gather(a, st));
+    // key-segment passes: the rows of all heads sweep one key segment at a time, so the
+    // K / V rows a pass gathers (kGatherSegment keys x Hkv x 512 B) stay L2-resident
+    // while every diagonal of every row reads them; the running (o, lse) state of each row
+    // is carried in out / lse between passes
+    for (int64_t k0 = 0; k0 < t1; k0 += kGatherSegment) {
+      a.key_lo = k0;
+      a.key_hi = std::min<int64_t>(t1, k0 + kGatherSegment);
+      LCX_TRY(attention_gather(a, st));
+    }
     if (admitted) {
       if (do_fallback)  // exact count of the full selection, reported once (rank 0)
         LCX_TRY(admitted_counts(fv, fnv, cap_v, fs, fns, cap_s, hq, t0, t1, admitted, st));
