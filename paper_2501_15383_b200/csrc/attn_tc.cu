@@ -81,7 +81,6 @@ struct Group {
   int vlo, vhi;  // compact positions [vlo, vhi) (64-aligned start)
   int ulo, uhi;
   int nvt, nst;
-  int soff;     // slash tiles start at list position soff (cyclic), see setup_item
   int64_t kt0;  // dense: first key tile
 };
 
@@ -157,24 +156,16 @@ __device__ void setup_item(const TcParams& p, int item, Item& it) {
         const int m_hi = int(G.khi / p.seg_len);  // intra group ends inside chunk m_hi
         G.vhi = vb[m_hi] + (lower_bound32(vh, nvh, G.khi) - vf[m_hi]);
       }
-      G.nvt = (G.vhi - G.vlo + 63) >> 6;
-      G.ulo = lower_bound32(uh, nuh, (G.klo >> 6) - ib);
-      G.uhi = lower_bound32(uh, nuh, ceil_div64(G.khi) - ib);
-      G.nst = G.uhi - G.ulo;
-      // Key-aligned schedule: block b's relative tile u is key tile 2b + u.  Every block of
-      // a head shares the same u list, so a block starts its cyclic walk at the first
-      // u >= u_first + (-2b mod span): the blocks running concurrently then read the SAME
-      // key tile at the same time (one DRAM read per wave, the rest L2 hits) instead of
-      // distinct tiles 2 apart.
-      G.soff = 0;
-      if (G.nst > 1) {
-        const int32_t* ul = uh + G.ulo;
-        const int64_t span = int64_t(ul[G.nst - 1]) - ul[0] + 1;
-        const int64_t shift = (2 * (it.i0 >> 7)) % span;
-        const int64_t target = ul[0] + (span - shift) % span;
-        G.soff = lower_bound32(ul, G.nst, target);
-        if (G.soff >= G.nst) G.soff = 0;
+      G.nvt = p.vert_pass ? (G.vhi - G.vlo + 63) >> 6 : 0;
+      // slash tiles of this pass's key window [key_lo, key_hi) (64-aligned)
+      const int64_t wlo = lcx_max64(G.klo, p.key_lo), whi = lcx_min64(G.khi, p.key_hi);
+      if (whi > wlo) {
+        G.ulo = lower_bound32(uh, nuh, (wlo >> 6) - ib);
+        G.uhi = lower_bound32(uh, nuh, ceil_div64(whi) - ib);
+      } else {
+        G.ulo = G.uhi = 0;
       }
+      G.nst = G.uhi - G.ulo;
     }
     if (G.nvt + G.nst == 0) continue;
     it.grp[it.ng++] = G;
@@ -202,9 +193,7 @@ __device__ Tile get_tile(const TcParams& p, const Item& it, int t) {
         T.key0 = (G.kt0 + t) * 64;
       } else {
         T.kind = T_SLASH;
-        int tt = t + G.soff;
-        if (tt >= G.nst) tt -= G.nst;
-        T.key0 = it.i0 + int64_t(p.tc_u[int64_t(it.h) * p.cap_u + G.ulo + tt]) * 64;
+        T.key0 = it.i0 + int64_t(p.tc_u[int64_t(it.h) * p.cap_u + G.ulo + t]) * 64;
       }
       return T;
     }
@@ -603,7 +592,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #pragma unroll
       for (int kk = 0; kk < BN / 16; ++kk)  // P (fp16, 2 per column) aliases S buffer bs
         tc::mma_f16_ts_warp(tmem + COL_O, tmem + bs * BN + kk * 8, dv + ((kk * 32) >> 4),
-                            IDESC_PV, (first && kk == 0) ? 0u : 1u);
+                            IDESC_PV, (first && !p.init && kk == 0) ? 0u : 1u);
       tc::mma_commit_warp(v_empty + bv);
       tc::mma_commit_warp(s_free + bs);
       if (lane == 0) trace_mark(p, T, 4);
@@ -637,7 +626,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(m_empty + slot);
         ++M;
-        if (row_ok) {
+        if (row_ok && !p.init) {  // init passes keep the running state of an empty item
           float4* o = reinterpret_cast<float4*>(p.out + (i * p.hq + h) * int64_t(HD)) + part * 16;
           for (int x = 0; x < 16; ++x) o[x] = make_float4(0.f, 0.f, 0.f, 0.f);
           if (part == 0) p.lse[int64_t(h) * p.lse_stride + i] = -INFINITY;
@@ -675,6 +664,30 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         qi.h = h;
         m = -INFINITY;
         l = 0.f;
+        if (p.init) {
+          // key-window pass > 0: continue from the row's running (o, lse) -- O goes back
+          // into TMEM (the previous item's last PV completed before its epilogue read O)
+          const float lp = row_ok ? p.lse[int64_t(h) * p.lse_stride + i] : -INFINITY;
+          const bool live = lp != -INFINITY;
+          m = live ? lp * 1.4426950408889634f : -INFINITY;
+          l = (live && part == 0) ? 1.f : 0.f;
+          const float4* o =
+              reinterpret_cast<const float4*>(p.out + (i * p.hq + h) * int64_t(HD)) + part * 16;
+#pragma unroll
+          for (int q4 = 0; q4 < 2; ++q4) {
+            float ov[32];
+#pragma unroll
+            for (int x = 0; x < 8; ++x) {
+              const float4 v = live ? o[q4 * 8 + x] : make_float4(0.f, 0.f, 0.f, 0.f);
+              ov[4 * x] = v.x;
+              ov[4 * x + 1] = v.y;
+              ov[4 * x + 2] = v.z;
+              ov[4 * x + 3] = v.w;
+            }
+            tc::tmem_st32(tmem + lane_base + COL_O + part * 64 + q4 * 32, ov);
+          }
+          tc::tmem_wait_st();
+        }
         rotate_q(p, qi, pattern, r, part, tmem + lane_base);
         tc::tc_fence_before();
         __syncwarp();
@@ -706,9 +719,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
       tmax = fmaxf(tmax, rb[(part ^ 1) * 128 + r]);
       // lazy rescale (warp-uniform TMEM access); both halves take the same decision
-      const bool first = (flags & F_FIRST) != 0;
+      // (first tile: O holds either nothing (m = -inf) or the loaded running state)
       const bool need = tmax > m + kRescaleThresh;
-      const bool warp_need = __any_sync(0xffffffffu, need && !first && m != -INFINITY);
+      const bool warp_need = __any_sync(0xffffffffu, need && m != -INFINITY);
       const float m_new = need ? tmax : m;
       if (warp_need) {
         const uint32_t Tp = T - 1;  // O must hold PV(T-1) before rescaling

@@ -32,6 +32,10 @@ struct TcParams {
   int64_t* tile_count;  // optional: executed tiles (atomicAdd)
   long long* trace;     // optional: CTA-0 per-tile timestamps [kTraceTiles][8]
   void* plans;          // workspace: per-item tile plans (filled by plan_items_kernel)
+  // key-window pass: slash tiles with keys in [key_lo, key_hi) only; vertical tiles only
+  // when vert_pass; init = continue from the running (out, lse) of the rows
+  int64_t key_lo, key_hi;
+  int vert_pass, init;
 };
 
 struct TcBuffers {

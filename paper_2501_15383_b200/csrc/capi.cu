@@ -64,6 +64,7 @@ namespace {
 
 constexpr int kDefaultTcMin = 96;  // slash entries per 64-key tile to use tcgen05
 constexpr int64_t kGatherSegment = 32768;  // keys per gather pass (L2-resident K / V)
+constexpr int64_t kTcSegment = 32768;      // keys per tcgen05 slash pass (K hi/lo + V^T)
 
 __global__ void dense_count_kernel(int hq, int64_t t0, int64_t t1, int64_t* out) {
   const int h = blockIdx.x * blockDim.x + threadIdx.x;
@@ -381,7 +382,25 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
   p.trace = ctx->trace;
   p.plans = w.plans;
   if (ev_tc0) LCX_CHECK_CUDA(cudaEventRecord(ev_tc0, st));
-  LCX_TRY(tc_attention(p, w.B, ctx->sm_count, st));
+  if (!sparse) {
+    p.key_lo = 0;
+    p.key_hi = INT64_MAX;
+    p.vert_pass = 1;
+    p.init = 0;
+    LCX_TRY(tc_attention(p, w.B, ctx->sm_count, st));
+  } else {
+    // key-window passes: the slash tiles of all (head, block) items sweep one window of
+    // keys at a time so that its K hi/lo + V^T tiles stay L2-resident (every block's
+    // diagonals hit them); pass 0 also runs the vertical tiles (compacted per head and
+    // shared by all blocks of a head), later passes continue from the running state
+    for (int64_t k0 = 0, pass = 0; k0 < t1; k0 += kTcSegment, ++pass) {
+      p.key_lo = k0;
+      p.key_hi = std::min<int64_t>(t1, k0 + kTcSegment);
+      p.vert_pass = pass == 0;
+      p.init = pass > 0;
+      LCX_TRY(tc_attention(p, w.B, ctx->sm_count, st));
+    }
+  }
   if (ev_tc1) LCX_CHECK_CUDA(cudaEventRecord(ev_tc1, st));
   if (sparse) {
     // isolated slashes + self-fallback rows on the CUDA-core gather, merged in place
