@@ -65,6 +65,7 @@ namespace {
 constexpr int kDefaultTcMin = 96;  // slash entries per 64-key tile to use tcgen05
 constexpr int64_t kGatherSegment = 32768;  // keys per gather pass (L2-resident K / V)
 constexpr int64_t kTcSegment = 32768;      // keys per tcgen05 slash pass (K hi/lo + V^T)
+constexpr int64_t kWindowMinSlashes = 512;  // slash capacity from which windows are used
 
 __global__ void dense_count_kernel(int hq, int64_t t0, int64_t t1, int64_t* out) {
   const int h = blockIdx.x * blockDim.x + threadIdx.x;
@@ -393,9 +394,11 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
     // keys at a time so that its K hi/lo + V^T tiles stay L2-resident (every block's
     // diagonals hit them); pass 0 also runs the vertical tiles (compacted per head and
     // shared by all blocks of a head), later passes continue from the running state
-    for (int64_t k0 = 0, pass = 0; k0 < t1; k0 += kTcSegment, ++pass) {
+    // (few slash lines -> one pass: the windows only pay off when slash tiles dominate)
+    const int64_t seg = cap_s > kWindowMinSlashes ? kTcSegment : t1;
+    for (int64_t k0 = 0, pass = 0; k0 < t1; k0 += seg, ++pass) {
       p.key_lo = k0;
-      p.key_hi = std::min<int64_t>(t1, k0 + kTcSegment);
+      p.key_hi = std::min<int64_t>(t1, k0 + seg);
       p.vert_pass = pass == 0;
       p.init = pass > 0;
       LCX_TRY(tc_attention(p, w.B, ctx->sm_count, st));
@@ -440,9 +443,10 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
     // K / V rows a pass gathers (kGatherSegment keys x Hkv x 512 B) stay L2-resident
     // while every diagonal of every row reads them; the running (o, lse) state of each row
     // is carried in out / lse between passes
-    for (int64_t k0 = 0; k0 < t1; k0 += kGatherSegment) {
+    const int64_t gseg = cap_s > kWindowMinSlashes ? kGatherSegment : t1;
+    for (int64_t k0 = 0; k0 < t1; k0 += gseg) {
       a.key_lo = k0;
-      a.key_hi = std::min<int64_t>(t1, k0 + kGatherSegment);
+      a.key_hi = std::min<int64_t>(t1, k0 + gseg);
       LCX_TRY(attention_gather(a, st));
     }
     if (admitted) {
