@@ -345,8 +345,9 @@ def main():
               position_mode="dca_continuous", dca=dca, temperature=temp, rope_base=a.rope_base)
     stream = torch.cuda.current_stream()
 
-    def step(return_admitted=False):
-        return SH.prefill(plan, qs, ks, vs, return_admitted=return_admitted, **kw)
+    def step(return_admitted=False, return_recall=False):
+        return SH.prefill(plan, qs, ks, vs, return_admitted=return_admitted,
+                          return_recall=return_recall, **kw)
 
     def barrier():
         torch.cuda.synchronize()
@@ -356,9 +357,16 @@ def main():
 
     for _ in range(a.warmup):
         step()
-    # exact admitted-entry count of this workload (untimed extra run)
-    r = step(return_admitted=True)
+    # exact admitted-entry count and the recall check (north star (d): dense vs sparse
+    # LSE of every chunk's last lastQ rows) of this workload -- an untimed extra run
+    r = step(return_admitted=True, return_recall=plan.kind != "seq")
     E_local = int(r["admitted"].sum()) if "admitted" in r else 0
+    recall = None
+    if "recall" in r:
+        rc = r["recall"].float()
+        recall = {"mean": float(rc.mean()), "min": float(rc.min()),
+                  "rows": f"last {a.last_q} rows of each chunk, all heads on this rank",
+                  "definition": "mean min(1, exp(lse_sparse - lse_dense)) (refine.cpp:51-72)"}
     del r
     barrier()
 
@@ -486,6 +494,7 @@ def main():
             "admitted_entries": E_total,
             "density": E_total / (a.hq * a.n * (a.n + 1) / 2),
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "budget_1000_64": extra,
+            "recall_check": recall,
             "gpu_launches": int(stage["launches"]),
         }
         print(json.dumps(line), flush=True)

@@ -137,6 +137,12 @@ typedef struct {
   /* optional exact admitted-entry counts per (chunk, head) (CriticalSet::admitted_count
    * restricted to the chunk's rows), device int64 [nchunks][hq], may be NULL */
   int64_t* admitted;
+  /* optional sparsity-refinement recall check (north star (d); refine.cpp:51-85 on the
+   * chunk's last queries): recall[chunk][head] = mean over the chunk's last
+   * min(lastQ, rows) rows of min(1, exp(lse_sparse - lse_full)), lse_full from a dense
+   * pass over those rows against keys [0, t1) with the same positions / DCA remap /
+   * temperature.  Device float [nchunks][hq], may be NULL; unsharded calls only. */
+  float* recall;
 } lcx_prefill_output;
 
 /* Execution statistics of the last lcx_chunked_prefill on a context (host side).

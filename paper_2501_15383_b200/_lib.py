@@ -59,7 +59,8 @@ class PrefillConfigC(C.Structure):
 class PrefillOutputC(C.Structure):
     _fields_ = [("out", C.c_void_p), ("lse", C.c_void_p), ("sel_verticals", C.c_void_p),
                 ("sel_nv", C.c_void_p), ("sel_slashes", C.c_void_p), ("sel_ns", C.c_void_p),
-                ("cap_v", C.c_int64), ("cap_s", C.c_int64), ("admitted", C.c_void_p)]
+                ("cap_v", C.c_int64), ("cap_s", C.c_int64), ("admitted", C.c_void_p),
+                ("recall", C.c_void_p)]
 
 
 class PrefillStatsC(C.Structure):

@@ -840,7 +840,7 @@ int lcx_chunked_prefill_host(lcx_context* ctx, const lcx_attention_input* hin,
     din.v = dv;
     din.positions_q = dpq;
     din.positions_k = dpk;
-    lcx_prefill_output dout_s{dout, dlse, dsv, dsnv, dss, dsns, cap_v, cap_s, dadm};
+    lcx_prefill_output dout_s{dout, dlse, dsv, dsnv, dss, dsns, cap_v, cap_s, dadm, nullptr};
     rc = prefill_impl(ctx, &din, cfg, &dout_s, st, ready.data(), done.data());
   }
   // D2H of each chunk's rows as soon as the chunk is final
@@ -960,6 +960,9 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
     e_max.k3_tiles = k3_tiles;
   }
   int32_t *ov = nullptr, *onv = nullptr, *os = nullptr, *ons = nullptr;
+  float *rec_o = nullptr, *rec_l = nullptr;
+  if (out->recall && shards > 1)
+    return fail(LCX_ERR_CONFIG, "the recall check needs the merged (unsharded) lse");
   auto layout = [&](auto& A, AttnWS& w, float** col, float** sl, int32_t** iv, int32_t** inv,
                     int32_t** is, int32_t** ins, size_t* est_off) {
     *est_off = A.off;
@@ -978,6 +981,10 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
         *ins = A.template take<int32_t>(size_t(hq));
       }
       if (est_tc) k3 = A.template take<uint8_t>(est_tc_k3_bytes(n, in->hkv));
+      if (out->recall) {  // dense rows of the recall check: [128][hq][dim] O + [hq][128] lse
+        rec_o = A.template take<float>(size_t(128) * hq * in->dim);
+        rec_l = A.template take<float>(size_t(hq) * 128);
+      }
       if (shards > 1) {  // this shard's lines
         ov = A.template take<int32_t>(size_t(hq) * cap_v);
         onv = A.template take<int32_t>(size_t(hq));
@@ -1057,6 +1064,18 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
                             dca, s, dca ? c : 1, tc_min, out->out, out->lse, n,
                             out->admitted ? out->admitted + ci * hq : nullptr, st,
                             (prof && tc) ? e[4] : nullptr, (prof && tc) ? e[5] : nullptr, shards > 1 ? &full : nullptr));
+    if (sparse && out->recall) {
+      // dense LSE of the chunk's last rows (the TC path needs a 128-aligned row block)
+      const int64_t b = std::min(cfg->last_q, t1 - t0);
+      const int64_t r0 = tc ? std::max<int64_t>(t0, t1 - 128) : t1 - b;
+      float* o_base = rec_o - r0 * hq * in->dim;  // rows [r0, t1) -> scratch rows
+      float* l_base = rec_l - r0;                 // lse[h * 128 + i - r0]
+      LCX_TRY(attention_chunk(ctx, in, w, r0, t1, false, nullptr, nullptr, 0, nullptr, nullptr,
+                              0, dca, s, dca ? c : 1, tc_min, o_base, l_base, 128, nullptr,
+                              st));
+      LCX_TRY(chunk_recall_launch(out->lse, n, rec_l, 128, r0, t1 - b, t1, hq,
+                                  out->recall + ci * hq, st));
+    }
     if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[3], st));
     if (done) LCX_CHECK_CUDA(cudaEventRecord(done[ci], st));
   }

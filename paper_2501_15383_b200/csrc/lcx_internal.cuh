@@ -211,6 +211,9 @@ int build_bitmaps(const int32_t* lists, const int32_t* counts, int64_t cap, int 
 // misc.cu
 int recall_kernel_launch(const float* ls, const float* lf, int64_t n, double slack,
                          float* per, double* sum_dev, int* bad_dev, cudaStream_t st);
+int chunk_recall_launch(const float* lse_s, int64_t s_stride, const float* lse_f,
+                        int64_t f_stride, int64_t f0, int64_t i0, int64_t i1, int hq, float* out,
+                        cudaStream_t st);
 int lse_scale_launch(float* o, const float* lse_own, const float* lse_all, int parts, int64_t n,
                      int hq, int dim, float* lse_out, cudaStream_t st);
 int lse_merge_launch(const float* o_parts, const float* lse_parts, int parts, int64_t rows,

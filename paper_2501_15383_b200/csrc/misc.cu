@@ -92,7 +92,37 @@ __global__ void lse_scale_kernel(float* __restrict__ o, const float* __restrict_
   if ((threadIdx.x & 31) == 0 && lse_out) lse_out[li] = tot;
 }
 
+// recall[h] = mean over rows [i0, i1) of min(1, exp(lse_s[h][i] - lse_f[h][i - f0]))
+// (refine.cpp:51-72 with the clamp; one block per head)
+__global__ void chunk_recall_kernel(const float* __restrict__ lse_s, int64_t s_stride,
+                                    const float* __restrict__ lse_f, int64_t f_stride,
+                                    int64_t f0, int64_t i0, int64_t i1, float* __restrict__ out) {
+  __shared__ float red[32];
+  const int h = blockIdx.x;
+  float acc = 0.f;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    const float d = lse_s[int64_t(h) * s_stride + i] - lse_f[int64_t(h) * f_stride + (i - f0)];
+    acc += fminf(1.f, expf(d));
+  }
+  for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) t += red[w];
+    out[h] = i1 > i0 ? t / float(i1 - i0) : 1.f;
+  }
+}
+
 }  // namespace
+
+int chunk_recall_launch(const float* lse_s, int64_t s_stride, const float* lse_f,
+                        int64_t f_stride, int64_t f0, int64_t i0, int64_t i1, int hq, float* out,
+                        cudaStream_t st) {
+  chunk_recall_kernel<<<hq, 256, 0, st>>>(lse_s, s_stride, lse_f, f_stride, f0, i0, i1, out);
+  LCX_CHECK_LAUNCH();
+  return LCX_OK;
+}
 
 int lse_scale_launch(float* o, const float* lse_own, const float* lse_all, int parts, int64_t n,
                      int hq, int dim, float* lse_out, cudaStream_t st) {

@@ -87,11 +87,14 @@ def chunked_prefill(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
                     position_mode="standard", dca=None, opts: Options | None = None,
                     positions_q=None, positions_k=None, rope_base=1e4, temperature=1.0,
                     kernel_path="auto", return_selections=True, return_admitted=False,
-                    tc_min_entries=0, out=None, lse=None, stream=None, ctx=None, shard=None):
+                    tc_min_entries=0, out=None, lse=None, stream=None, ctx=None, shard=None,
+                    return_recall=False):
     """longctx::chunked_prefill (sparse.hpp:125-129) over all heads of one layer.
 
     shard=(rank, count): KV-line sharding -- out / lse are this shard's partials
-    (see lse_scale_partial and paper_2501_15383_b200/shard.py)."""
+    (see lse_scale_partial and paper_2501_15383_b200/shard.py).
+    return_recall: the recall check (north star (d)) -- recall [chunks, hq] = mean over
+    each chunk's last min(last_q, rows) rows of min(1, exp(lse_sparse - lse_full))."""
     inp = make_input(q, k, v, positions_q, positions_k, rope_base, temperature)
     opts = opts or Options()
     n, hq, dim = q.shape
@@ -113,6 +116,8 @@ def chunked_prefill(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
         sel["ns"] = torch.zeros((nchunks, hq), dtype=torch.int32, device=dev)
     admitted = torch.zeros((nchunks, hq), dtype=torch.int64, device=dev) \
         if return_admitted else None
+    recall = torch.zeros((nchunks, hq), dtype=torch.float32, device=dev) \
+        if return_recall else None
     pm = POSITION_MODES[position_mode] if isinstance(position_mode, str) else int(position_mode)
     sr, sc = shard if shard is not None else (0, 1)
     cfg = PrefillConfigC(int(chunk_len), int(last_q), bv, bs, PREFILL_MODES[mode], pm,
@@ -123,13 +128,16 @@ def chunked_prefill(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
                        sel["nv"].data_ptr() if sel else None,
                        sel["slashes"].data_ptr() if sel else None,
                        sel["ns"].data_ptr() if sel else None, cap_v, cap_s,
-                       admitted.data_ptr() if admitted is not None else None)
+                       admitted.data_ptr() if admitted is not None else None,
+                       recall.data_ptr() if recall is not None else None)
     ctx = ctx or context(dev.index)
     check(lib().lcx_chunked_prefill(ctx.ptr, C.byref(inp), C.byref(cfg), C.byref(o),
                                     _stream(stream)))
     res = dict(out=out, lse=lse, **sel)
     if admitted is not None:
         res["admitted"] = admitted
+    if recall is not None:
+        res["recall"] = recall
     return res
 
 
@@ -318,7 +326,7 @@ def chunked_prefill_host(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
                        sel["verticals"].data_ptr() if sel else None,
                        sel["nv"].data_ptr() if sel else None,
                        sel["slashes"].data_ptr() if sel else None,
-                       sel["ns"].data_ptr() if sel else None, cap_v, cap_s, None)
+                       sel["ns"].data_ptr() if sel else None, cap_v, cap_s, None, None)
     ctx = ctx or context(device)
     with torch.cuda.device(device):
         check(lib().lcx_chunked_prefill_host(ctx.ptr, C.byref(inp), C.byref(cfg), C.byref(o),

@@ -587,3 +587,33 @@ def test_line_sharded_prefill_merges_to_unsharded(D, port, shards, path, precisi
     o_ref, l_ref, _ = port.chunked_prefill(q[:, 1], k[:, 0], v[:, 0], 256, 64, (40, 200),
                                            "sparse", 1 if dca else 0, dca, temperature=0.9)
     assert row_rel_err(mo[:, 1], o_ref) <= tol
+
+
+# ------------------------------------------------------------- recall check --
+@pytest.mark.parametrize("precision,dca", [("bf16", (256, 768, 256)), ("fp32", None),
+                                           ("bf16", None)])
+def test_prefill_recall_check(D, port, precision, dca):
+    """North star (d): the operator's recall check (dense LSE of each chunk's last lastQ
+    rows vs the sparse LSE) equals the reference's attention_recall on the oracle's
+    sparse and dense LSE of the same rows (refine.cpp:51-72); full budget -> recall 1."""
+    import torch
+    n, hq, hkv, chunk, lq = 1024, 2, 1, 256, 64
+    q, k, v = _mh_inputs(n, hq, hkv, 128, precision, 41, "peaked")
+    dt = torch.float32 if precision == "fp32" else torch.bfloat16
+    T = lambda x: torch.tensor(x).to(dt).cuda().contiguous()  # noqa: E731
+    kw = dict(chunk_len=chunk, last_q=lq, temperature=0.9,
+              position_mode="dca_continuous" if dca else "standard", dca=dca)
+    r = D.chunked_prefill(T(q), T(k), T(v), budget=(8, 16), return_recall=True, **kw)
+    rec = r["recall"].double().cpu().numpy()
+    tol = 1e-4 if precision == "fp32" else 4e-3
+    for h in range(hq):
+        o_s, l_s, _ = port.chunked_prefill(q[:, h], k[:, 0], v[:, 0], chunk, lq, (8, 16),
+                                           "sparse", 1 if dca else 0, dca, temperature=0.9)
+        o_f, l_f, _ = port.chunked_prefill(q[:, h], k[:, 0], v[:, 0], chunk, lq, (8, 16),
+                                           "full", 1 if dca else 0, dca, temperature=0.9)
+        for ci in range(n // chunk):
+            rows = slice((ci + 1) * chunk - lq, (ci + 1) * chunk)
+            per, agg = port.attention_recall(l_s[rows], l_f[rows], slack=1e-9)
+            assert abs(rec[ci, h] - agg) <= tol, (ci, h, rec[ci, h], agg)
+    full = D.chunked_prefill(T(q), T(k), T(v), budget=(n, n), return_recall=True, **kw)
+    assert float(full["recall"].min()) >= 1.0 - tol
