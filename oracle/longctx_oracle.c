@@ -454,6 +454,59 @@ int lco_sparse_attention(const double* q, const double* k, const double* v, int6
                         slashes, ns, 0, rel_mode, s, c, 0, n, out, lse);
 }
 
+/* Listed rows only (row-sampled parity at 128K-1M, where whole-sequence oracle runs are
+ * infeasible): the same per-row computation as attention_rows / sparse_attention
+ * (sparse.cpp:232-284; DCA override sparse.cpp:385-393), out [nrows][dim], lse [nrows].
+ * dense != 0: every key j <= i (full_attention). */
+int lco_attention_row_list(const double* q, const double* k, const double* v, int64_t n,
+                           int64_t dim, const int64_t* pos_q, const int64_t* pos_k,
+                           double rope_base, double temperature, const int64_t* verts,
+                           int64_t nv, const int64_t* slashes, int64_t ns, int dense,
+                           int rel_mode, int64_t s, int64_t c, const int64_t* rows,
+                           int64_t nrows, double* out, double* lse) {
+  const double inv_scale = 1.0 / (temperature * sqrt((double)dim));
+  double* thetas = (double*)malloc(sizeof(double) * (size_t)(dim / 2));
+  lco_rope_thetas(dim, rope_base, thetas);
+  double* logits = (double*)malloc(sizeof(double) * (size_t)n);
+  int64_t* adm = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + nv + ns + 1));
+  double* q_rot = (double*)malloc(sizeof(double) * (size_t)dim);
+  double* k_rot = (double*)malloc(sizeof(double) * (size_t)dim);
+  for (int64_t x = 0; x < nrows; ++x) {
+    const int64_t i = rows[x];
+    if (i < 0 || i >= n) {
+      free(thetas); free(logits); free(adm); free(q_rot); free(k_rot);
+      return LCO_E_DIMENSION;
+    }
+    int64_t cnt;
+    if (dense) {
+      for (int64_t j = 0; j <= i; ++j) adm[j] = j;
+      cnt = i + 1;
+    } else {
+      cnt = lco_admitted_row(verts, nv, slashes, ns, i, adm);
+    }
+    if (rel_mode == 0) lco_rope_rotate_row(q + i * dim, dim, pos_q[i], thetas, q_rot);
+    for (int64_t a = 0; a < cnt; ++a) {
+      const int64_t j = adm[a];
+      double acc = 0.0;
+      if (rel_mode == 0) {
+        lco_rope_rotate_row(k + j * dim, dim, pos_k[j], thetas, k_rot);
+        for (int64_t d = 0; d < dim; ++d) acc += q_rot[d] * k_rot[d];
+      } else {
+        lco_rope_rotate_row(q + i * dim, dim, lco_dca_relative(i, j, s, c), thetas, q_rot);
+        for (int64_t d = 0; d < dim; ++d) acc += q_rot[d] * k[j * dim + d];
+      }
+      logits[j] = acc * inv_scale;
+    }
+    lse[x] = attend_admitted(logits, adm, cnt, v, dim, out + x * dim);
+  }
+  free(thetas);
+  free(logits);
+  free(adm);
+  free(q_rot);
+  free(k_rot);
+  return LCO_OK;
+}
+
 int lco_full_attention(const double* q, const double* k, const double* v, int64_t n,
                        int64_t dim, const int64_t* pos_q, const int64_t* pos_k,
                        double rope_base, double temperature, int rel_mode, int64_t s,

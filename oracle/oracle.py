@@ -246,6 +246,26 @@ class Oracle:
         self._check(st)
         return out, lse
 
+    def attention_rows(self, q, k, v, rows, crit: Critical | None = None, pos_q=None,
+                       pos_k=None, rope_base=1e4, temperature=1.0, dca=None):
+        """Port only: sparse (crit) or dense (crit None) attention of the listed rows."""
+        q, k, v = _d(q), _d(k), _d(v)
+        n, dim = q.shape
+        pq, pk = self._pos(n, pos_q), self._pos(n, pos_k)
+        rows = _i(rows)
+        vv = _i(crit.verticals if crit else [0])
+        ss = _i(crit.slashes if crit else [0])
+        out, lse = np.zeros((len(rows), dim)), np.zeros(len(rows))
+        s, c, w = dca if dca else (0, 0, 0)
+        fn = self.lib.lco_attention_row_list
+        self._check(fn(_pd(q), _pd(k), _pd(v), C.c_int64(n), C.c_int64(dim), _pi(pq), _pi(pk),
+                       C.c_double(rope_base), C.c_double(temperature), _pi(vv),
+                       C.c_int64(len(crit.verticals) if crit else 0), _pi(ss),
+                       C.c_int64(len(crit.slashes) if crit else 0), C.c_int(crit is None),
+                       C.c_int(dca is not None), C.c_int64(s), C.c_int64(c), _pi(rows),
+                       C.c_int64(len(rows)), _pd(out), _pd(lse)))
+        return out, lse
+
     def dca_attention(self, q, k, v, cfg, scale_factor, rope_base=1e4):
         q, k, v = _d(q), _d(k), _d(v)
         n, dim = q.shape

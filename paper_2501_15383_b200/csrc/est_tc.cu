@@ -379,11 +379,11 @@ void est_tc_plan(const EstTcArgs& a, EstTcPlan& pl) {
     pl.near_begin = near_key <= 0 ? 0 : std::min<int64_t>(pl.ntiles, (near_key + 63) / 64);
     if (pl.near_begin < pl.far_end) pl.near_begin = pl.far_end;
   }
+  // pieces of 1/32 of the chunk's tensor-core tiles (>= 4 tiles): a function of the key
+  // range only, so a head's row statistics (combined over pieces in a fixed order) are
+  // bitwise the same whichever heads a call covers; <= 2 x 33 stats slots
   const int64_t tc_tiles = pl.far_end + (pl.ntiles - pl.near_begin);
-  pl.per = int(std::max<int64_t>(4, (tc_tiles * pl.npairs + 4 * a.sm_count - 1) /
-                                        (4 * int64_t(a.sm_count))));
-  // at most 64 pieces per phase and pair: bounds the stats slots (64 + 2 incl. partials)
-  pl.per = int(std::max<int64_t>(pl.per, (tc_tiles + 63) / 64));
+  pl.per = int(std::max<int64_t>(4, (tc_tiles + 31) / 32));
   const int nf = int((pl.far_end + pl.per - 1) / pl.per);
   const int nn = int((pl.ntiles - pl.near_begin + pl.per - 1) / pl.per);
   pl.tc_splits = nf + nn;

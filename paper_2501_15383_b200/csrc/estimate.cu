@@ -318,10 +318,13 @@ __global__ void est_combine_lines(const float* __restrict__ col_part,
   }
 }
 
+// Split plan of the CUDA-core estimator: a function of the key tiles only (not of the head
+// count or the device), so a head's scores -- and therefore its selection -- are bitwise
+// the same whichever subset of heads a call covers (head-sharded multi-GPU runs).
 void plan(const EstimateArgs& a, int sm_count, int64_t tiles, int& nsplit, int& tps, int& nrt) {
+  (void)sm_count;
   nrt = int((a.block + kRows - 1) / kRows);
-  const int64_t want = std::max<int64_t>(1, (int64_t(sm_count) * 4) / std::max(1, a.hq * nrt));
-  tps = int(std::max<int64_t>(1, (tiles + want - 1) / want));
+  tps = int(std::max<int64_t>(1, (tiles + 63) / 64));
   nsplit = tiles > 0 ? int((tiles + tps - 1) / tps) : 0;
 }
 

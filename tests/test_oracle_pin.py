@@ -159,3 +159,17 @@ def test_errors_match_reference_kinds(port, ref):
         with pytest.raises(OracleError) as e:
             o.estimate_block(q, k, 0)
         assert e.value.kind == "config"
+
+
+@pytest.mark.parametrize("dca", [None, (64, 192, 64)])
+def test_row_list_oracle_equals_whole_sequence_oracle(port, dca):
+    """lco_attention_row_list (row-sampled parity at 128K-1M) computes exactly the rows
+    sparse_attention / full_attention compute (same per-row arithmetic)."""
+    q, k, v = port.random_input(3, 300, 16)
+    crit = port.select_critical(port.estimate_block(q, k, 64), (10, 20), 300)
+    rows = [0, 5, 150, 299]
+    for c in (crit, None):
+        fo, fl = (port.sparse_attention(q, k, v, c, dca=dca, temperature=0.8) if c else
+                  port.full_attention(q, k, v, dca=dca, temperature=0.8))
+        ro, rl = port.attention_rows(q, k, v, rows, c, dca=dca, temperature=0.8)
+        assert np.array_equal(ro, fo[rows]) and np.array_equal(rl, fl[rows])
