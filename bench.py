@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--dca", type=int, nargs=2, default=[131072, 262144],
                     help="DCA chunk size s and training length c")
     ap.add_argument("--rope-base", type=float, default=1e7)
-    ap.add_argument("--kind", default="structured", choices=["structured", "iid"])
+    ap.add_argument("--kind", default="planted", choices=["planted", "structured", "iid"])
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -474,6 +474,34 @@ def main():
         extra = {"budget": [a.budget[0], 64], "value": a.n / (ms2 / a.steps / 1e3),
                  "unit": "tokens/s", "ms_per_step": ms2 / a.steps}
 
+    # the same budget on the "structured" inputs, whose selected slashes scatter over the
+    # whole context (recall ~0.1: no vertical-slash structure to find) -- the adversarial
+    # case for the kernels, device-timed, reported beside the headline
+    scattered = None
+    if not a.no_extra and a.kind == "planted":
+        del qs, ks, vs
+        torch.cuda.empty_cache()
+        q2, k2, v2 = make_qkv(a.n, a.hq, a.hkv, kind="structured", seed=a.seed,
+                              rope_base=a.rope_base, device=dev)
+        qs, ks, vs = SH.take(plan, q2, k2, v2)
+        del q2, k2, v2
+        step()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(a.steps):
+            step()
+        f1.record(stream)
+        barrier()
+        ms3 = f0.elapsed_time(f1)
+        if world > 1:
+            t3 = torch.tensor([ms3], dtype=torch.float64, device=dev)
+            dist.all_reduce(t3, op=dist.ReduceOp.MAX)
+            ms3 = float(t3[0])
+        scattered = {"inputs": "structured (scattered slashes)", "budget": list(a.budget),
+                     "value": a.n / (ms3 / a.steps / 1e3), "unit": "tokens/s",
+                     "ms_per_step": ms3 / a.steps}
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         try:
@@ -486,7 +514,10 @@ def main():
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "bf16", "data": "synthetic (seeded structured Q/K/V generated on device)",
+            "dtype": "bf16",
+            "data": f"synthetic, seeded, generated on device ({a.kind}: "
+                    + ("vertical + local-band slash structure, synth.make_planted" if
+                       a.kind == "planted" else "synth.make_qkv") + ")",
             "config": {**workload(a), "parallelism": plan.describe()},
             "roofline": roofline, "kernels": kernels,
             "algorithmic_tflops_whole_step": alg_tflops,
@@ -494,7 +525,7 @@ def main():
             "admitted_entries": E_total,
             "density": E_total / (a.hq * a.n * (a.n + 1) / 2),
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "budget_1000_64": extra,
-            "recall_check": recall,
+            "recall_check": recall, "scattered_inputs": scattered,
             "gpu_launches": int(stage["launches"]),
         }
         print(json.dumps(line), flush=True)

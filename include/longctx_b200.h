@@ -241,7 +241,8 @@ int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
 /* Host-buffer entry of the operator -- what the reference's by-value API
  * (chunked_prefill taking host matrices, sparse.hpp:125-129) maps onto.
  * in->q / k / v / positions_* and every out-> pointer are HOST pointers
- * (page-locked memory gives full copy / compute overlap; pageable works).
+ * (page-locked memory gives full copy / compute overlap; a pageable output buffer
+ * works but makes each chunk's copy-out block the enqueue of the next chunk).
  * Chunk c's Q/K/V rows are copied host-to-device on a copy stream while
  * earlier chunks compute; chunk c's output rows, lse and selections are copied
  * back on a second stream as soon as chunk c is final.  Device staging is

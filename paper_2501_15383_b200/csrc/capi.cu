@@ -9,6 +9,7 @@
 // back-to-back on one stream, each launch covering every head.
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -470,7 +471,8 @@ int64_t words_for(int64_t n) { return (n + 31) / 32 + 1; }
 
 int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_prefill_config* cfg,
                  lcx_prefill_output* out, cudaStream_t st, const cudaEvent_t* ready,
-                 const cudaEvent_t* done);
+                 const cudaEvent_t* done,
+                 const std::function<int(int64_t)>* on_chunk = nullptr);
 
 }  // namespace lcx
 
@@ -841,29 +843,29 @@ int lcx_chunked_prefill_host(lcx_context* ctx, const lcx_attention_input* hin,
     din.positions_q = dpq;
     din.positions_k = dpk;
     lcx_prefill_output dout_s{dout, dlse, dsv, dsnv, dss, dsns, cap_v, cap_s, dadm, nullptr};
-    rc = prefill_impl(ctx, &din, cfg, &dout_s, st, ready.data(), done.data());
-  }
-  // D2H of each chunk's rows as soon as the chunk is final
-  const int64_t nrec = rc == LCX_OK ? nch : 0;
-  for (int64_t c = 0; c < nrec && rc == LCX_OK; ++c) {
-    const int64_t t0 = c * L, t1 = std::min(n, t0 + L);
-    cudaError_t e = cudaStreamWaitEvent(ctx->d2h, done[c], 0);
-    const size_t orow = size_t(hq) * dim * sizeof(float);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(reinterpret_cast<char*>(hout->out) + t0 * orow,
-                          reinterpret_cast<char*>(dout) + t0 * orow, (t1 - t0) * orow,
-                          cudaMemcpyDeviceToHost, ctx->d2h);
-    if (e == cudaSuccess)
-      e = cudaMemcpy2DAsync(hout->lse + t0, sizeof(float) * n, dlse + t0, sizeof(float) * n,
-                            sizeof(float) * (t1 - t0), hq, cudaMemcpyDeviceToHost, ctx->d2h);
-    if (e == cudaSuccess && sel) {
-      e = cudaMemcpyAsync(hout->sel_verticals + c * hq * cap_v, dsv + c * hq * cap_v,
-                          sizeof(int32_t) * hq * cap_v, cudaMemcpyDeviceToHost, ctx->d2h);
+    // D2H of each chunk's rows, enqueued as soon as the chunk's kernels are (so the copy
+    // of chunk c overlaps the compute of chunks c+1, ...)
+    const std::function<int(int64_t)> d2h = [&](int64_t c) -> int {
+      const int64_t t0 = c * L, t1 = std::min(n, t0 + L);
+      cudaError_t e = cudaStreamWaitEvent(ctx->d2h, done[c], 0);
+      const size_t orow = size_t(hq) * dim * sizeof(float);
       if (e == cudaSuccess)
-        e = cudaMemcpyAsync(hout->sel_slashes + c * hq * cap_s, dss + c * hq * cap_s,
-                            sizeof(int32_t) * hq * cap_s, cudaMemcpyDeviceToHost, ctx->d2h);
-    }
-    if (e != cudaSuccess) rc = fail(LCX_ERR_CUDA, "device-to-host copy failed");
+        e = cudaMemcpyAsync(reinterpret_cast<char*>(hout->out) + t0 * orow,
+                            reinterpret_cast<char*>(dout) + t0 * orow, (t1 - t0) * orow,
+                            cudaMemcpyDeviceToHost, ctx->d2h);
+      if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync(hout->lse + t0, sizeof(float) * n, dlse + t0, sizeof(float) * n,
+                              sizeof(float) * (t1 - t0), hq, cudaMemcpyDeviceToHost, ctx->d2h);
+      if (e == cudaSuccess && sel) {
+        e = cudaMemcpyAsync(hout->sel_verticals + c * hq * cap_v, dsv + c * hq * cap_v,
+                            sizeof(int32_t) * hq * cap_v, cudaMemcpyDeviceToHost, ctx->d2h);
+        if (e == cudaSuccess)
+          e = cudaMemcpyAsync(hout->sel_slashes + c * hq * cap_s, dss + c * hq * cap_s,
+                              sizeof(int32_t) * hq * cap_s, cudaMemcpyDeviceToHost, ctx->d2h);
+      }
+      return e == cudaSuccess ? LCX_OK : fail(LCX_ERR_CUDA, "device-to-host copy failed");
+    };
+    rc = prefill_impl(ctx, &din, cfg, &dout_s, st, ready.data(), done.data(), &d2h);
   }
   if (rc == LCX_OK && sel) {
     if (cudaMemcpyAsync(hout->sel_nv, dsnv, sizeof(int32_t) * nch * hq, cudaMemcpyDeviceToHost,
@@ -906,7 +908,7 @@ namespace lcx {
 // done[c] (optional) is recorded once chunk c's output rows and lse are final.
 int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_prefill_config* cfg,
                  lcx_prefill_output* out, cudaStream_t st, const cudaEvent_t* ready,
-                 const cudaEvent_t* done) {
+                 const cudaEvent_t* done, const std::function<int(int64_t)>* on_chunk) {
   LCX_TRY(validate_input(in));
   if (!cfg || !out || !out->out || !out->lse) return fail(LCX_ERR_DIMENSION, "null config/output");
   if (cfg->chunk_len <= 0) return fail(LCX_ERR_CONFIG, "chunkLen must be positive");
@@ -1078,6 +1080,7 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
     }
     if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[3], st));
     if (done) LCX_CHECK_CUDA(cudaEventRecord(done[ci], st));
+    if (on_chunk) LCX_TRY((*on_chunk)(ci));  // e.g. enqueue this chunk's D2H now
   }
   ctx->stats = lcx_prefill_stats{};
   ctx->stats.chunks = nchunks;

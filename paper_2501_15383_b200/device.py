@@ -314,10 +314,11 @@ def chunked_prefill_host(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
         lse = torch.empty((hq, n), dtype=torch.float32, pin_memory=True)
     sel = {}
     if return_selections and mode == "sparse":
-        sel["verticals"] = torch.zeros((nchunks, hq, cap_v), dtype=torch.int32)
-        sel["nv"] = torch.zeros((nchunks, hq), dtype=torch.int32)
-        sel["slashes"] = torch.zeros((nchunks, hq, cap_s), dtype=torch.int32)
-        sel["ns"] = torch.zeros((nchunks, hq), dtype=torch.int32)
+        # page-locked: a copy into pageable memory would block the enqueue of later chunks
+        sel["verticals"] = torch.zeros((nchunks, hq, cap_v), dtype=torch.int32, pin_memory=True)
+        sel["nv"] = torch.zeros((nchunks, hq), dtype=torch.int32, pin_memory=True)
+        sel["slashes"] = torch.zeros((nchunks, hq, cap_s), dtype=torch.int32, pin_memory=True)
+        sel["ns"] = torch.zeros((nchunks, hq), dtype=torch.int32, pin_memory=True)
     pm = POSITION_MODES[position_mode] if isinstance(position_mode, str) else int(position_mode)
     cfg = PrefillConfigC(int(chunk_len), int(last_q), bv, bs, PREFILL_MODES[mode], pm,
                          _chunk(dca) or ChunkConfigC(0, 0, 0), opts.c(),

@@ -5,7 +5,7 @@ sys.path.insert(0, ".")
 from paper_2501_15383_b200 import device as D  # noqa: E402
 from paper_2501_15383_b200.synth import make_qkv, yarn_temperature  # noqa: E402
 n, bv, bs = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
-kind = sys.argv[4] if len(sys.argv) > 4 else "structured"
+kind = sys.argv[4] if len(sys.argv) > 4 else "planted"
 chunk = int(sys.argv[5]) if len(sys.argv) > 5 else 32768
 q, k, v = make_qkv(n, 28, 4, kind=kind, seed=1)
 s, c = 131072, 262144

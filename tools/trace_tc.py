@@ -8,7 +8,7 @@ from paper_2501_15383_b200 import device as D  # noqa: E402
 from paper_2501_15383_b200._lib import context, lib  # noqa: E402
 from paper_2501_15383_b200.synth import make_qkv, yarn_temperature  # noqa: E402
 n, bv, bs = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3])
-kind = sys.argv[4] if len(sys.argv) > 4 else "structured"
+kind = sys.argv[4] if len(sys.argv) > 4 else "planted"
 ctx = context(0)
 L = lib()
 L.lcx_debug_trace.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
