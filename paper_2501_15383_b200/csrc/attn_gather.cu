@@ -68,6 +68,8 @@ __device__ __forceinline__ int64_t qpos_of(const GatherArgs& a, int pattern, int
 }
 
 __global__ void __launch_bounds__(kThreads, 2) attn_gather_kernel(const GatherArgs a) {
+  // a window with no segment (and before the chunk's rows: no self-fallback rows) is empty
+  if (a.win_flags && !a.win_flags[a.win] && a.key_hi <= a.row_begin) return;
   const int lane = threadIdx.x & (kLanes - 1);
   const int rw = threadIdx.x / kLanes;
   const int64_t i = a.row_begin + int64_t(blockIdx.x) * kRows + rw;

@@ -12,6 +12,7 @@ struct GatherArgs {
   int hq, hkv, group;
   int64_t row_begin, row_end;                      // rows (row_begin % 128 == 0)
   int64_t key_lo, key_hi;                          // only entries with key in [key_lo, key_hi)
+  const int* win_flags; int win;                   // optional: skip an empty key window
   int rel_mode;                                    // 0 standard, 1 DCA
   int64_t s, c;
   const int64_t* pos_q; const int64_t* pos_k;     // standard mode (nullptr = iota)

@@ -311,6 +311,8 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
                const __grid_constant__ CUtensorMap map_kc_hi,
                const __grid_constant__ CUtensorMap map_kc_lo,
                const __grid_constant__ CUtensorMap map_vct) {
+  // key-window pass with no slash tile anywhere in it (and no vertical pass): nothing to do
+  if (!p.vert_pass && p.win_flags && !p.win_flags[p.win]) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // stay in the shared address space (LDS/STS, not generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -1059,6 +1061,36 @@ classify_kernel(const int32_t* __restrict__ slashes, const int32_t* __restrict__
   }
 }
 
+// Per key window w = [w W, (w+1) W): 1 if some head has a tcgen05 slash tile or a
+// CUDA-core segment whose keys meet it for some row of the chunk [t0, t1) (relative tile
+// u covers keys [t0 + 64u, t1 + 64u); segment (d, r0, r1) of half h keys
+// [t0 + 64h + r0 - d, t1 - d)), so passes over empty windows exit at once.
+__global__ void window_flags_kernel(const int32_t* __restrict__ tc_u,
+                                    const int32_t* __restrict__ n_tc_u, int64_t cap_u,
+                                    const int4* __restrict__ segs, const int32_t* __restrict__ nseg,
+                                    int64_t cap_seg, int64_t t0, int64_t t1, int64_t W, int nwin,
+                                    int* __restrict__ tc_flags, int* __restrict__ g_flags) {
+  const int h = blockIdx.x;
+  auto mark = [&](int* f, int64_t lo, int64_t hi) {  // keys [lo, hi)
+    lo = lcx_max64(lo, 0);
+    hi = lcx_min64(hi, t1);
+    if (hi <= lo) return;
+    for (int64_t w = lo / W; w <= (hi - 1) / W && w < nwin; ++w) f[w] = 1;
+  };
+  const int nu = n_tc_u[h];
+  for (int x = threadIdx.x; x < nu; x += blockDim.x) {
+    const int64_t u = tc_u[int64_t(h) * cap_u + x];
+    mark(tc_flags, t0 + 64 * u, t1 + 64 * u + 64);
+  }
+  for (int hf = 0; hf < 2; ++hf) {
+    const int ns = nseg[h * 2 + hf];
+    for (int x = threadIdx.x; x < ns; x += blockDim.x) {
+      const int4 e = segs[(int64_t(h) * 2 + hf) * cap_seg + x];
+      mark(g_flags, t0 + e.y - e.x, t1 - e.x);
+    }
+  }
+}
+
 // Exact admitted-entry count of rows [t0, t1) per head (CriticalSet::admitted_count
 // restricted to the chunk rows, sparse.cpp:115-119), in O(nv log ns + ns):
 //   sum_v (t1 - max(t0, v)) + sum_d (t1 - max(t0, d)) - #{(v, d) : t0 <= v + d < t1}
@@ -1202,6 +1234,17 @@ int tc_classify(const int32_t* slashes, const int32_t* ns, int64_t cap_s, int hq
 }
 
 size_t tc_plan_bytes() { return sizeof(Item); }
+
+int tc_window_flags(const int32_t* tc_u, const int32_t* n_tc_u, int64_t cap_u, const int4* segs,
+                    const int32_t* nseg, int64_t cap_seg, int hq, int64_t t0, int64_t t1,
+                    int64_t W, int nwin, int* tc_flags, int* g_flags, cudaStream_t st) {
+  LCX_CHECK_CUDA(cudaMemsetAsync(tc_flags, 0, sizeof(int) * nwin, st));
+  LCX_CHECK_CUDA(cudaMemsetAsync(g_flags, 0, sizeof(int) * nwin, st));
+  window_flags_kernel<<<hq, 256, 0, st>>>(tc_u, n_tc_u, cap_u, segs, nseg, cap_seg, t0, t1, W,
+                                          nwin, tc_flags, g_flags);
+  LCX_CHECK_LAUNCH();
+  return LCX_OK;
+}
 
 int tc_attention(const TcParams& p, const TcBuffers& B, int sm_count, cudaStream_t st) {
   static bool attr = false;

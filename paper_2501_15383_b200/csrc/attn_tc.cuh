@@ -36,6 +36,7 @@ struct TcParams {
   // when vert_pass; init = continue from the running (out, lse) of the rows
   int64_t key_lo, key_hi;
   int vert_pass, init;
+  const int* win_flags; int win;  // optional: skip the pass when win_flags[win] == 0
 };
 
 struct TcBuffers {
@@ -87,6 +88,10 @@ int tc_classify(const int32_t* slashes, const int32_t* ns, int64_t cap_s, int hq
                 int4* segs, int32_t* nseg, int64_t cap_seg, cudaStream_t st);
 int tc_attention(const TcParams& p, const TcBuffers& B, int sm_count, cudaStream_t st);
 size_t tc_plan_bytes();  // bytes per work item for the tile plans
+// per-key-window work flags of a chunk's slash tiles (tc_flags) and segments (g_flags)
+int tc_window_flags(const int32_t* tc_u, const int32_t* n_tc_u, int64_t cap_u, const int4* segs,
+                    const int32_t* nseg, int64_t cap_seg, int hq, int64_t t0, int64_t t1,
+                    int64_t W, int nwin, int* tc_flags, int* g_flags, cudaStream_t st);
 int admitted_counts(const int32_t* verts, const int32_t* nv, int64_t cap_v,
                     const int32_t* slashes, const int32_t* ns, int64_t cap_s, int hq,
                     int64_t t0, int64_t t1, int64_t* out, cudaStream_t st);

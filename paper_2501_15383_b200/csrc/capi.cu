@@ -9,6 +9,7 @@
 // back-to-back on one stream, each launch covering every head.
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 #include <functional>
 #include <mutex>
 #include <string>
@@ -93,6 +94,21 @@ __global__ void shard_lists_kernel(const int32_t* __restrict__ v, const int32_t*
     onv[h] = int32_t(v1 - v0);
     ons[h] = int32_t(s1 - s0);
   }
+}
+
+// far[0] += slashes with d >= far_d, far[1] += all slashes (over heads)
+__global__ void far_count_kernel(const int32_t* __restrict__ sl, const int32_t* __restrict__ ns,
+                                 int64_t cap_s, int hq, int64_t far_d, int* far) {
+  int f = 0, t = 0;
+  for (int h = 0; h < hq; ++h) {
+    const int cnt = ns[h];
+    for (int x = threadIdx.x; x < cnt; x += blockDim.x) {
+      f += sl[int64_t(h) * cap_s + x] >= far_d;
+      ++t;
+    }
+  }
+  atomicAdd(far, f);
+  atomicAdd(far + 1, t);
 }
 
 int dense_counts(int hq, int64_t t0, int64_t t1, int64_t* out, cudaStream_t st) {
@@ -234,6 +250,10 @@ struct AttnWS {
   int32_t* n_tc_u = nullptr;
   int4* segs = nullptr;
   int32_t* nseg = nullptr;
+  bool windows = false;      // key-window passes for this chunk (see prefill_impl)
+  int* tc_flags = nullptr;   // per key window: slash tiles present
+  int* g_flags = nullptr;    // per key window: gather segments present
+  int nwin = 0;
   void* plans = nullptr;
   TcBuffers B;
 };
@@ -255,6 +275,9 @@ void attn_layout(A& ar, const lcx_attention_input* in, bool tc, bool sparse, int
       w.n_tc_u = ar.template take<int32_t>(size_t(in->hq));
       w.segs = ar.template take<int4>(size_t(in->hq) * 2 * w.cap_seg);
       w.nseg = ar.template take<int32_t>(size_t(in->hq) * 2);
+      w.nwin = int(in->n / kTcSegment + 2);
+      w.tc_flags = ar.template take<int>(size_t(w.nwin));
+      w.g_flags = ar.template take<int>(size_t(w.nwin));
     }
   }
   if (tc) {
@@ -343,6 +366,9 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
     const int64_t U = t1 / 64 + 4;
     LCX_TRY(tc_classify(slashes, ns, cap_s, hq, std::min(U, w.U), tc_min_entries, w.hist,
                         w.tc_u, w.n_tc_u, w.cap_u, w.segs, w.nseg, w.cap_seg, st));
+    if (w.windows)
+      LCX_TRY(tc_window_flags(w.tc_u, w.n_tc_u, w.cap_u, w.segs, w.nseg, w.cap_seg, hq, t0, t1,
+                              kTcSegment, w.nwin, w.tc_flags, w.g_flags, st));
   }
   TcParams p{};
   p.q = reinterpret_cast<const __nv_bfloat16*>(in->q);
@@ -396,12 +422,14 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
     // diagonals hit them); pass 0 also runs the vertical tiles (compacted per head and
     // shared by all blocks of a head), later passes continue from the running state
     // (few slash lines -> one pass: the windows only pay off when slash tiles dominate)
-    const int64_t seg = cap_s > kWindowMinSlashes ? kTcSegment : t1;
+    const int64_t seg = w.windows ? kTcSegment : t1;
     for (int64_t k0 = 0, pass = 0; k0 < t1; k0 += seg, ++pass) {
       p.key_lo = k0;
       p.key_hi = std::min<int64_t>(t1, k0 + seg);
       p.vert_pass = pass == 0;
       p.init = pass > 0;
+      p.win_flags = seg == kTcSegment ? w.tc_flags : nullptr;
+      p.win = int(pass);
       LCX_TRY(tc_attention(p, w.B, ctx->sm_count, st));
     }
   }
@@ -444,10 +472,12 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
     // K / V rows a pass gathers (kGatherSegment keys x Hkv x 512 B) stay L2-resident
     // while every diagonal of every row reads them; the running (o, lse) state of each row
     // is carried in out / lse between passes
-    const int64_t gseg = cap_s > kWindowMinSlashes ? kGatherSegment : t1;
+    const int64_t gseg = w.windows ? kGatherSegment : t1;
+    a.win_flags = gseg == kGatherSegment ? w.g_flags : nullptr;
     for (int64_t k0 = 0; k0 < t1; k0 += gseg) {
       a.key_lo = k0;
       a.key_hi = std::min<int64_t>(t1, k0 + gseg);
+      a.win = int(k0 / gseg);
       LCX_TRY(attention_gather(a, st));
     }
     if (admitted) {
@@ -503,6 +533,9 @@ int lcx_context_create(int device, lcx_context** out) {
   ctx->device = device;
   ctx->sm_count = prop.multiProcessorCount;
   LCX_CHECK_CUDA(cudaMalloc(&ctx->tile_counter, 2 * sizeof(int64_t)));
+  LCX_CHECK_CUDA(cudaMalloc(&ctx->far_dev, 2 * sizeof(int)));
+  LCX_CHECK_CUDA(cudaMallocHost(&ctx->far_host, 4 * sizeof(int)));
+  for (auto& e : ctx->far_ev) LCX_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   LCX_CHECK_CUDA(cudaMemset(ctx->tile_counter, 0, 2 * sizeof(int64_t)));
   *out = ctx;
   return LCX_OK;
@@ -515,6 +548,10 @@ int lcx_context_destroy(lcx_context* ctx) {
   if (ctx->rope) cudaFree(ctx->rope);
   if (ctx->tile_counter) cudaFree(ctx->tile_counter);
   if (ctx->trace) cudaFree(ctx->trace);
+  if (ctx->far_dev) cudaFree(ctx->far_dev);
+  if (ctx->far_host) cudaFreeHost(ctx->far_host);
+  for (auto& e : ctx->far_ev)
+    if (e) cudaEventDestroy(e);
   if (ctx->stage) cudaFree(ctx->stage);
   if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
   if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
@@ -1050,6 +1087,27 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
       LCX_TRY(select_lines(sl, hq, t1, cfg->budget_slash, cfg->opts.force_local_band, block,
                            slist, scnt, cap_s, st));
       if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[2], st));
+      if (tc) {  // how many selected slashes reach beyond one key window (see below)
+        LCX_CHECK_CUDA(cudaMemsetAsync(ctx->far_dev, 0, 2 * sizeof(int), st));
+        far_count_kernel<<<1, 256, 0, st>>>(slist, scnt, cap_s, hq, kTcSegment, ctx->far_dev);
+        LCX_CHECK_LAUNCH();
+        LCX_CHECK_CUDA(cudaMemcpyAsync(ctx->far_host + 2 * (ci & 1), ctx->far_dev, 2 * sizeof(int),
+                                       cudaMemcpyDeviceToHost, st));
+        LCX_CHECK_CUDA(cudaEventRecord(ctx->far_ev[ci & 1], st));
+      }
+    }
+    // Key-window passes pay off when most slash work lies far from the diagonal (scattered
+    // lines: L2-resident windows) and cost a pass per window otherwise.  Decided from the
+    // PREVIOUS chunk's selection (the host waits for that selection only, so chunk ci-1's
+    // attention still overlaps this enqueue), which keeps the choice -- and the
+    // floating-point accumulation order -- deterministic.
+    if (sparse && tc) {
+      w.windows = false;
+      if (ci > 0 && cap_s > kWindowMinSlashes) {
+        LCX_CHECK_CUDA(cudaEventSynchronize(ctx->far_ev[(ci - 1) & 1]));
+        const int* fh = ctx->far_host + 2 * ((ci - 1) & 1);
+        w.windows = fh[1] > 0 && 2 * int64_t(fh[0]) > int64_t(fh[1]);
+      }
     }
     const int32_t *avl = vlist, *avc = vcnt, *asl = slist, *asc = scnt;
     FullLists full{vlist, vcnt, slist, scnt, cfg->shard_rank == 0 ? 1 : 0};

@@ -125,6 +125,10 @@ struct lcx_context {
   char* stage = nullptr;
   size_t stage_bytes = 0;
   cudaStream_t h2d = nullptr, d2h = nullptr;
+  // key-window decision of chunked prefill: far-slash counts of the last two chunks
+  int* far_dev = nullptr;        // device [2]
+  int* far_host = nullptr;       // pinned [2][2]
+  cudaEvent_t far_ev[2] = {nullptr, nullptr};
 };
 
 namespace lcx {
