@@ -7,11 +7,17 @@
 // [0, prefix_len) (column 0 for forceSink, offsets [0, block) for
 // forceLocalBand), sorted unique.
 //
-// One CTA per (head, line kind): MSB-first 8-bit radix select on the
-// order-preserving uint32 image of the fp32 score finds the k-th largest key T
-// and how many keys equal to T must be taken; a chunked block scan then emits,
-// in ascending index order, every index with key > T and the first `need`
-// indices with key == T.  Output is sorted by construction.
+// One thread-block CLUSTER of 8 CTAs per head (each CTA one contiguous eighth of the
+// scores): MSB-first 8-bit radix select on the order-preserving uint32 image of the
+// fp32 score finds the k-th largest key T and how many keys equal to T must be taken --
+// the per-CTA digit histograms are combined through distributed shared memory between
+// cluster barriers, so the 4 passes + the emission are one launch that reads the scores
+// at full-chip bandwidth instead of one SM's; the emission then writes, in ascending
+// index order, every index with key > T and the first `need` indices with key == T
+// (CTA r after CTAs < r: offsets from the other CTAs' counts via DSMEM).  Output is
+// sorted by construction.
+#include <cooperative_groups.h>
+
 #include "lcx_internal.cuh"
 
 namespace lcx {
@@ -30,7 +36,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_sums, int* total
   if (lane == 31) warp_sums[wid] = x;
   __syncthreads();
   if (wid == 0) {
-    int w = warp_sums[lane];
+    int w = lane < int(blockDim.x >> 5) ? warp_sums[lane] : 0;
     int ws = w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -122,6 +128,141 @@ select_kernel(const float* __restrict__ scores, int64_t n, int64_t k, int64_t pr
   if (tid == 0) count[h] = int32_t(prefix_len + out_seen);
 }
 
+constexpr int kCl = 8;      // CTAs per head (cluster)
+constexpr int kCT = 512;    // threads per CTA
+
+// distributed shared memory: address of `p` in cluster CTA `rank`, loads, cluster barrier
+__device__ __forceinline__ uint32_t dsmem(const void* p, int rank) {
+  uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p)), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ int ld_dsmem_i32(uint32_t a) {
+  int v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ long long ld_dsmem_i64(uint32_t a) {
+  long long v;
+  asm volatile("ld.shared::cluster.s64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+__device__ __forceinline__ int cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return int(r);
+}
+
+__global__ void __launch_bounds__(kCT)
+select_cluster_kernel(const float* __restrict__ scores, int64_t n, int64_t k,
+                      int64_t prefix_len, int32_t* __restrict__ out,
+                      int32_t* __restrict__ count, int64_t cap) {
+  __shared__ int hist[256];
+  __shared__ int warp_sums[32];
+  __shared__ int total;
+  __shared__ uint32_t sh_prefix;
+  __shared__ long long sh_remaining;
+  __shared__ long long sh_cnt[2];  // [0] emitted by this CTA, [1] its equal count
+  const int rank = cluster_rank();
+  const int h = blockIdx.x / kCl;
+  const float* sc = scores + int64_t(h) * n;
+  int32_t* o = out + int64_t(h) * cap;
+  const int tid = threadIdx.x;
+  const int64_t lo = n * rank / kCl, hi = n * (rank + 1) / kCl;
+  // (the k >= n and k <= 0 cases are handled by the single-CTA kernel)
+  if (rank == 0)
+    for (int64_t i = tid; i < prefix_len; i += kCT) o[i] = int32_t(i);
+  uint32_t prefix = 0, mask = 0;
+  long long remaining = k;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int b = tid; b < 256; b += kCT) hist[b] = 0;
+    __syncthreads();
+    for (int64_t i = lo + tid; i < hi; i += kCT) {
+      const uint32_t u = float_to_ordered(sc[i]);
+      if ((u & mask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1);
+    }
+    cluster_sync();  // all eighths histogrammed
+    if (tid == 0) {
+      long long cum = 0;
+      int chosen = 0;
+      for (int dgt = 255; dgt >= 0; --dgt) {
+        long long c = 0;
+        for (int r = 0; r < kCl; ++r) c += ld_dsmem_i32(dsmem(&hist[dgt], r));
+        if (cum + c >= remaining) {
+          chosen = dgt;
+          break;
+        }
+        cum += c;
+      }
+      sh_remaining = remaining - cum;
+      sh_prefix = prefix | (uint32_t(chosen) << shift);
+    }
+    cluster_sync();  // every CTA read every histogram before the next pass clears its own
+    prefix = sh_prefix;
+    remaining = sh_remaining;
+    mask |= 255u << shift;
+  }
+  const uint32_t T = prefix;
+  const long long need_eq = remaining;
+  // phase 1: this eighth's equal count and its emitted greater-than count
+  int gt_c = 0, eq_c = 0;
+  for (int64_t i = lo + tid; i < hi; i += kCT) {
+    const uint32_t u = float_to_ordered(sc[i]);
+    gt_c += (u > T) && (i >= prefix_len);
+    eq_c += (u == T);
+  }
+  block_excl_scan(gt_c, warp_sums, &total);
+  gt_c = total;
+  block_excl_scan(eq_c, warp_sums, &total);
+  eq_c = total;
+  if (tid == 0) sh_cnt[1] = eq_c;
+  cluster_sync();
+  // ties go to the lowest indices: this eighth takes the equals ranked
+  // [eq_before, eq_before + take) in index order
+  long long eq_before = 0;
+  for (int r = 0; r < rank; ++r) eq_before += ld_dsmem_i64(dsmem(&sh_cnt[1], r));
+  long long take = need_eq - eq_before;
+  take = take < 0 ? 0 : (take > eq_c ? eq_c : take);
+  if (tid == 0) {
+    // taken equals inside the forced prefix are already written
+    long long pref = 0, seen = 0;
+    const int64_t pe = hi < prefix_len ? hi : prefix_len;
+    for (int64_t i = lo; i < pe && seen < take; ++i)
+      if (float_to_ordered(sc[i]) == T) {
+        ++seen;
+        ++pref;
+      }
+    sh_cnt[0] = gt_c + take - pref;  // emitted by this eighth
+  }
+  cluster_sync();
+  long long base = prefix_len;
+  for (int r = 0; r < rank; ++r) base += ld_dsmem_i64(dsmem(&sh_cnt[0], r));
+  // phase 2: emit in ascending index order
+  long long eq_seen = 0, out_seen = 0;
+  for (int64_t b0 = lo; b0 < hi; b0 += kCT) {
+    const int64_t i = b0 + tid;
+    uint32_t u = 0;
+    if (i < hi) u = float_to_ordered(sc[i]);
+    const int g = (i < hi) && (u > T);
+    const int e = (i < hi) && (u == T);
+    const int e_rank = block_excl_scan(e, warp_sums, &total);
+    const int e_total = total;
+    const int sel = g || (e && (eq_seen + e_rank) < take);
+    const int emit = sel && (i >= prefix_len);
+    const int pos = block_excl_scan(emit, warp_sums, &total);
+    const int emit_total = total;
+    if (emit) o[base + out_seen + pos] = int32_t(i);
+    eq_seen += e_total;
+    out_seen += emit_total;
+  }
+  if (rank == kCl - 1 && tid == 0) count[h] = int32_t(base + out_seen);
+  cluster_sync();  // keep every CTA's shared memory alive until all DSMEM reads are done
+}
+
 // col[h][j] = sum_r est[h][r][j]; slash[h][d] = (sum_r est[h][r][gi_r - d]) / cnt
 // (sparse.cpp:198-217), ascending r.
 __global__ void est_line_scores(const float* __restrict__ est, int heads, int64_t block,
@@ -155,7 +296,22 @@ int select_lines(const float* scores, int heads, int64_t n, int64_t k, int force
   if (pl + std::min<int64_t>(k, n) > cap && std::min<int64_t>(k, n) < n)
     return fail(LCX_ERR_DIMENSION, "selection capacity too small for budget + forced lines");
   if (k >= n && n > cap) return fail(LCX_ERR_DIMENSION, "selection capacity too small");
-  select_kernel<<<heads, kT, 0, st>>>(scores, n, k, pl, out, count, cap);
+  if (n >= int64_t(kCl) * kCT && k > 0 && k < n) {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(unsigned(heads * kCl));
+    lc.blockDim = dim3(kCT);
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kCl;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    LCX_CHECK_CUDA(cudaLaunchKernelEx(&lc, select_cluster_kernel, scores, n, k, pl, out, count,
+                                      cap));
+  } else
+    select_kernel<<<heads, kT, 0, st>>>(scores, n, k, pl, out, count, cap);
   LCX_CHECK_LAUNCH();
   return LCX_OK;
 }

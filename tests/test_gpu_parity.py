@@ -119,6 +119,30 @@ def test_selection_identical_given_identical_scores(D, port, seed):
             assert s[h, :int(ns[h])].tolist() == exp.slashes
 
 
+@pytest.mark.parametrize("n,bud", [(4096, (100, 300)), (33333, (1000, 6096)),
+                                   (262144, (1000, 6096)), (100000, (50000, 99990))])
+def test_selection_cluster_path_large_n(D, port, n, bud):
+    """The clustered radix select (8 CTAs per head, DSMEM histograms) on large score
+    arrays with heavy ties and ties straddling the CTA slices: identical to the reference
+    ranking (score desc, index asc) + forced lines."""
+    import torch
+    rng = np.random.default_rng(n)
+    heads = 3
+    col = rng.random((heads, n)).astype(np.float32)
+    sl = rng.random((heads, n)).astype(np.float32)
+    col[:, rng.integers(0, n, n // 3)] = 0.75  # a tie class spanning every slice
+    sl[:, :] = np.round(sl * 64) / 64           # 65 tie classes
+    block = 64
+    T = lambda x: torch.tensor(x).cuda().contiguous()  # noqa: E731
+    v, nv, s, ns = D.select_from_scores(T(col), T(sl), block=block, budget=bud)
+    v, nv, s, ns = v.cpu().numpy(), nv.cpu().numpy(), s.cpu().numpy(), ns.cpu().numpy()
+    for h in range(heads):
+        exp = port.select_from_scores(col[h].astype(np.float64), sl[h].astype(np.float64), n,
+                                      block, bud)
+        assert v[h, :int(nv[h])].tolist() == exp.verticals
+        assert s[h, :int(ns[h])].tolist() == exp.slashes
+
+
 def test_select_critical_one_row_trick(L, ref):
     """Drive the REAL reference select_critical with a 1-row estimate (count 1 => mean =
     value) built from fp32 scores; the device selection must agree."""
