@@ -38,10 +38,12 @@ constexpr int kKBox = 64 * 64 * 2;    // one [64 keys][64 dims] box = 8 KB
 constexpr int kQBytes = 6 * kQBox;    // 3 terms x 2 halves = 96 KB
 constexpr int kKStage = 6 * kKBox;    // near: 3 terms x 2 halves = 48 KB
 constexpr int NKS = 2;
-constexpr int OFF_Q = 0;
+constexpr int OFF_Q = 0;     // Q terms (TMA), then reused: pass-2 transposes [2][128][65]
 constexpr int OFF_K = OFF_Q + kQBytes;
-constexpr int OFF_T = OFF_K + NKS * kKStage;      // pass-2 transpose [128][65] fp32
-constexpr int OFF_BAR = OFF_T + 128 * 65 * 4;
+constexpr int OFF_BAR = OFF_K + NKS * kKStage;
+constexpr int kTBuf = 128 * 65;                   // floats per transpose buffer
+static_assert(2 * kTBuf * 4 <= kQBytes, "transpose buffers must fit the Q staging area");
+constexpr uint32_t QCOL = 128;                    // TMEM: S [0, 128), Q terms [128, 320)
 constexpr int kSmem = OFF_BAR + 256 + 1024;
 constexpr int kThreads = 384;
 constexpr uint32_t IDESC = tc::idesc_f16(128, BN, 1, 1);
@@ -92,8 +94,9 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
   uint64_t* k_empty = k_full + NKS;     // [NKS]
   uint64_t* s_full = k_empty + NKS;     // [2]
   uint64_t* s_empty = s_full + 2;       // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_empty + 2);
-  float* T = reinterpret_cast<float*>(smem + OFF_T);
+  uint64_t* q_tmem = s_empty + 2;       // epilogue warps copied Q into TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_tmem + 1);
+  float* T = reinterpret_cast<float*>(smem + OFF_Q);
 
   const Item it = decode_item(p, blockIdx.x);
   const int ntl = it.t1 - it.t0;
@@ -108,10 +111,11 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
       tc::mbar_init(s_full + b, 1);
       tc::mbar_init(s_empty + b, 8);
     }
+    tc::mbar_init(q_tmem, 8);
     tc::fence_barrier_init();
     tc::fence_proxy_async();
   }
-  if (warp == 1) tc::tmem_alloc(tmem_slot, 128);
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -143,8 +147,9 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
       }
     }
   } else if (warp == 1) {
-    tc::mbar_wait(q_full, 0);
-    const uint64_t dq = tc::sdesc_sw128(tc::smem_u32(smem + OFF_Q));
+    // Q is the A operand from TMEM: with N = 64 an A operand in shared memory makes each
+    // M128 N64 K16 MMA shared-memory-bound (48 vs 32 cycles, tools/micro/mma_rate.cu)
+    tc::mbar_wait(q_tmem, 0);
     const uint64_t dk0 = tc::sdesc_sw128(tc::smem_u32(smem + OFF_K));
     // (q term, k term) products of order <= 2^-16: hh hm mh hl lh mm (near), h. m. l. (far)
     const int qt_near[6] = {0, 0, 1, 0, 2, 1}, kt_near[6] = {0, 1, 0, 2, 0, 1};
@@ -163,7 +168,7 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
         for (int half = 0; half < 2; ++half)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            tc::mma_f16_ss_warp(dS, dq + (((qt * 2 + half) * kQBox + kk * 32) >> 4),
+            tc::mma_f16_ts_warp(dS, tmem + QCOL + qt * 64 + half * 32 + kk * 8,
                                 dk + (((kt * 2 + half) * kKBox + kk * 32) >> 4), IDESC,
                                 (x | half | kk) ? 1u : 0u);
       }
@@ -186,6 +191,29 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
       rinv = ms.y > 0.f ? 1.f / ms.y : 0.f;
     }
     const float sc = p.scale_log2;
+    {  // Q terms: shared memory (TMA, SW128) -> TMEM, this thread's row and dim half
+      tc::mbar_wait(q_full, 0);
+#pragma unroll
+      for (int tm = 0; tm < 3; ++tm) {
+        const uint8_t* box = smem + OFF_Q + (tm * 2 + part) * kQBox;
+        uint32_t w[32];
+#pragma unroll
+        for (int c8 = 0; c8 < 8; ++c8) {
+          const uint4 x = *reinterpret_cast<const uint4*>(box + tc::sw128_off(r, c8));
+          w[c8 * 4] = x.x;
+          w[c8 * 4 + 1] = x.y;
+          w[c8 * 4 + 2] = x.z;
+          w[c8 * 4 + 3] = x.w;
+        }
+        tc::tmem_st32(tmem + lane_base + QCOL + tm * 64 + part * 32,
+                      reinterpret_cast<const float*>(w));
+      }
+      tc::tmem_wait_st();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(q_tmem);
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // Q staging area free for reuse
+    }
     for (int t = 0; t < ntl; ++t) {
       const int sb = t & 1;
       const int64_t j0 = int64_t(it.t0 + t) * BN;
@@ -215,7 +243,10 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
           m = nm;
         }
       } else {
-        float* Tr = T + r * 65 + part * 32;
+        // double-buffered transpose: one barrier per tile (tile t + 2 rewrites this buffer
+        // only after every thread passed tile t + 1's barrier, i.e. finished reading it)
+        float* Tb = T + (t & 1) * kTBuf;
+        float* Tr = Tb + r * 65 + part * 32;
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
           const bool ok = row_ok && jb + c <= gi && jb + c < p.nk;
@@ -230,7 +261,7 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
           const int64_t j = j0 + c;
           if ((it.pair % p.pairs_per_group) * 2 + ch < p.group && j < p.nk) {
             float acc = 0.f;
-            for (int q = 0; q < p.block; ++q) acc += T[(ch * 64 + q) * 65 + c];
+            for (int q = 0; q < p.block; ++q) acc += Tb[(ch * 64 + q) * 65 + c];
             p.col_part[int64_t(hc) * p.nk + j] = acc;
           }
         }
@@ -242,11 +273,10 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
             float acc = 0.f;
             const int q0 = e > 63 ? e - 63 : 0;
             const int q1 = min(p.block - 1, e);
-            for (int q = q0; q <= q1; ++q) acc += T[(dh * 64 + q) * 65 + (q - e + 63)];
+            for (int q = q0; q <= q1; ++q) acc += Tb[(dh * 64 + q) * 65 + (q - e + 63)];
             p.diag_part[(int64_t(hd) * p.ntiles + it.t0 + t) * 128 + e] = acc;
           }
         }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
       }
     }
     if (PASS == 1) {
@@ -269,7 +299,7 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  if (warp == 1) tc::tmem_dealloc(tmem, 128);
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
 // ------------------------------------------------------------- prep --
