@@ -98,17 +98,14 @@ __global__ void shard_lists_kernel(const int32_t* __restrict__ v, const int32_t*
 
 // far[0] += slashes with d >= far_d, far[1] += all slashes (over heads)
 __global__ void far_count_kernel(const int32_t* __restrict__ sl, const int32_t* __restrict__ ns,
-                                 int64_t cap_s, int hq, int64_t far_d, int* far) {
-  int f = 0, t = 0;
-  for (int h = 0; h < hq; ++h) {
-    const int cnt = ns[h];
-    for (int x = threadIdx.x; x < cnt; x += blockDim.x) {
-      f += sl[int64_t(h) * cap_s + x] >= far_d;
-      ++t;
-    }
-  }
-  atomicAdd(far, f);
-  atomicAdd(far + 1, t);
+                                 int64_t cap_s, int64_t far_d, int* far) {
+  const int h = blockIdx.x;  // one block per head
+  const int cnt = ns[h];
+  int f = 0;
+  for (int x = threadIdx.x; x < cnt; x += blockDim.x) f += sl[int64_t(h) * cap_s + x] >= far_d;
+  f = __reduce_add_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && f) atomicAdd(far, f);
+  if (threadIdx.x == 0) atomicAdd(far + 1, cnt);
 }
 
 int dense_counts(int hq, int64_t t0, int64_t t1, int64_t* out, cudaStream_t st) {
@@ -1089,7 +1086,7 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
       if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[2], st));
       if (tc) {  // how many selected slashes reach beyond one key window (see below)
         LCX_CHECK_CUDA(cudaMemsetAsync(ctx->far_dev, 0, 2 * sizeof(int), st));
-        far_count_kernel<<<1, 256, 0, st>>>(slist, scnt, cap_s, hq, kTcSegment, ctx->far_dev);
+        far_count_kernel<<<hq, 256, 0, st>>>(slist, scnt, cap_s, kTcSegment, ctx->far_dev);
         LCX_CHECK_LAUNCH();
         LCX_CHECK_CUDA(cudaMemcpyAsync(ctx->far_host + 2 * (ci & 1), ctx->far_dev, 2 * sizeof(int),
                                        cudaMemcpyDeviceToHost, st));

@@ -37,13 +37,15 @@ constexpr int kQBox = 128 * 64 * 2;   // one [128 rows][64 dims] bf16 box = 16 K
 constexpr int kKBox = 64 * 64 * 2;    // one [64 keys][64 dims] box = 8 KB
 constexpr int kQBytes = 6 * kQBox;    // 3 terms x 2 halves = 96 KB
 constexpr int kKStage = 6 * kKBox;    // near: 3 terms x 2 halves = 48 KB
-constexpr int NKS = 2;
+constexpr int NKS = 2;          // K stages in the K region
+constexpr int NKS_MAX = 4;      // pass 1 adds two stages in the Q staging area once Q is in TMEM
 constexpr int OFF_Q = 0;     // Q terms (TMA), then reused: pass-2 transposes [2][128][65]
 constexpr int OFF_K = OFF_Q + kQBytes;
 constexpr int OFF_BAR = OFF_K + NKS * kKStage;
 constexpr int kTBuf = 128 * 65;                   // floats per transpose buffer
 static_assert(2 * kTBuf * 4 <= kQBytes, "transpose buffers must fit the Q staging area");
-constexpr uint32_t QCOL = 128;                    // TMEM: S [0, 128), Q terms [128, 320)
+constexpr int NSB = 4;                            // S buffers in TMEM
+constexpr uint32_t QCOL = NSB * BN;               // TMEM: S [0, 256), Q terms [256, 448)
 constexpr int kSmem = OFF_BAR + 256 + 1024;
 constexpr int kThreads = 384;
 constexpr uint32_t IDESC = tc::idesc_f16(128, BN, 1, 1);
@@ -90,24 +92,30 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;          // [NKS]
-  uint64_t* k_empty = k_full + NKS;     // [NKS]
-  uint64_t* s_full = k_empty + NKS;     // [2]
-  uint64_t* s_empty = s_full + 2;       // [2]
-  uint64_t* q_tmem = s_empty + 2;       // epilogue warps copied Q into TMEM
+  uint64_t* k_full = bars + 1;          // [NKS_MAX]
+  uint64_t* k_empty = k_full + NKS_MAX; // [NKS_MAX]
+  uint64_t* s_full = k_empty + NKS_MAX; // [2]
+  uint64_t* s_empty = s_full + NSB;     // [NSB]
+  uint64_t* q_tmem = s_empty + NSB;     // epilogue warps copied Q into TMEM
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_tmem + 1);
   float* T = reinterpret_cast<float*>(smem + OFF_Q);
 
   const Item it = decode_item(p, blockIdx.x);
+  // pass 1 streams through 4 K stages (2 in the K region, 2 in the Q staging area after Q
+  // moved to TMEM); pass 2 keeps the Q area for its transposes
+  constexpr int kStages = PASS == 1 ? NKS_MAX : NKS;
+  auto stage_ptr = [&](int st) -> uint8_t* {
+    return st < NKS ? smem + OFF_K + st * kKStage : smem + OFF_Q + (st - NKS) * kKStage;
+  };
   const int ntl = it.t1 - it.t0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     tc::mbar_init(q_full, 1);
-    for (int b = 0; b < NKS; ++b) {
+    for (int b = 0; b < NKS_MAX; ++b) {
       tc::mbar_init(k_full + b, 1);
       tc::mbar_init(k_empty + b, 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NSB; ++b) {
       tc::mbar_init(s_full + b, 1);
       tc::mbar_init(s_empty + b, 8);
     }
@@ -130,10 +138,11 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
       for (int b = 0; b < 6; ++b)
         tc::tma_load_3d(smem + OFF_Q + b * kQBox, &map_q, q_full, 0, 0, qbox0 + b);
       for (int t = 0; t < ntl; ++t) {
-        const int st = t % NKS;
-        tc::mbar_wait(k_empty + st, ((t / NKS) & 1) ^ 1);
+        const int st = t % kStages;
+        tc::mbar_wait(k_empty + st, ((t / kStages) & 1) ^ 1);
+        if (st >= NKS && t < kStages) tc::mbar_wait(q_tmem, 0);  // Q staging area now free
         const int kt = it.t0 + t;
-        uint8_t* dst = smem + OFF_K + st * kKStage;
+        uint8_t* dst = stage_ptr(st);
         if (it.far) {
           tc::mbar_expect_tx(k_full + st, 2 * kKBox);
           tc::tma_load_3d(dst, &map_kraw, k_full + st, 0, g, kt * 64);
@@ -150,15 +159,14 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
     // Q is the A operand from TMEM: with N = 64 an A operand in shared memory makes each
     // M128 N64 K16 MMA shared-memory-bound (48 vs 32 cycles, tools/micro/mma_rate.cu)
     tc::mbar_wait(q_tmem, 0);
-    const uint64_t dk0 = tc::sdesc_sw128(tc::smem_u32(smem + OFF_K));
     // (q term, k term) products of order <= 2^-16: hh hm mh hl lh mm (near), h. m. l. (far)
     const int qt_near[6] = {0, 0, 1, 0, 2, 1}, kt_near[6] = {0, 1, 0, 2, 0, 1};
     for (int t = 0; t < ntl; ++t) {
-      const int st = t % NKS, sb = t & 1;
-      tc::mbar_wait(k_full + st, (t / NKS) & 1);
-      tc::mbar_wait(s_empty + sb, ((t >> 1) & 1) ^ 1);
+      const int st = t % kStages, sb = t % NSB;
+      tc::mbar_wait(k_full + st, (t / kStages) & 1);
+      tc::mbar_wait(s_empty + sb, ((t / NSB) & 1) ^ 1);
       tc::tc_fence_after();
-      const uint64_t dk = dk0 + ((st * kKStage) >> 4);
+      const uint64_t dk = tc::sdesc_sw128(tc::smem_u32(stage_ptr(st)));
       const uint32_t dS = tmem + sb * BN;
       const int nprod = it.far ? 3 : 6;
       for (int x = 0; x < nprod; ++x) {
@@ -215,9 +223,9 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
       asm volatile("bar.sync 1, 256;" ::: "memory");  // Q staging area free for reuse
     }
     for (int t = 0; t < ntl; ++t) {
-      const int sb = t & 1;
+      const int sb = t % NSB;
       const int64_t j0 = int64_t(it.t0 + t) * BN;
-      tc::mbar_wait(s_full + sb, (t >> 1) & 1);
+      tc::mbar_wait(s_full + sb, (t / NSB) & 1);
       tc::tc_fence_after();
       float v[32];
       tc::tmem_ld32(tmem + lane_base + sb * BN + part * 32, v);
@@ -226,12 +234,14 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(s_empty + sb);
       const int64_t jb = j0 + part * 32;
+      // valid columns of this row: c < nvalid (causal j <= gi, j < nk); int32 compares
+      const int64_t lim = (gi < p.nk - 1 ? gi : p.nk - 1) - jb + 1;
+      const int nvalid = !row_ok ? 0 : (lim >= 32 ? 32 : (lim < 0 ? 0 : int(lim)));
       if (PASS == 1) {
         float tmax = -INFINITY;
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
-          const bool ok = row_ok && jb + c <= gi && jb + c < p.nk;
-          v[c] = ok ? v[c] * sc : -INFINITY;
+          v[c] = c < nvalid ? v[c] * sc : -INFINITY;
           tmax = fmaxf(tmax, v[c]);
         }
         if (tmax != -INFINITY) {
@@ -248,10 +258,7 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
         float* Tb = T + (t & 1) * kTBuf;
         float* Tr = Tb + r * 65 + part * 32;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const bool ok = row_ok && jb + c <= gi && jb + c < p.nk;
-          Tr[c] = ok ? ex2(v[c] * sc - rm) * rinv : 0.f;
-        }
+        for (int c = 0; c < 32; ++c) Tr[c] = c < nvalid ? ex2(fmaf(v[c], sc, -rm)) * rinv : 0.f;
         asm volatile("bar.sync 1, 256;" ::: "memory");
         const int et = threadIdx.x - 128;    // 0..255
         // column sums: thread et < 128 -> (head et / 64, key et % 64)
@@ -261,7 +268,20 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
           const int64_t j = j0 + c;
           if ((it.pair % p.pairs_per_group) * 2 + ch < p.group && j < p.nk) {
             float acc = 0.f;
-            for (int q = 0; q < p.block; ++q) acc += Tb[(ch * 64 + q) * 65 + c];
+            const float* col = Tb + ch * 64 * 65 + c;
+            if (p.block == 64) {
+              float a2 = 0.f, a3 = 0.f, a4 = 0.f;  // fixed trip count: unrolled, 4 chains
+#pragma unroll 16
+              for (int q = 0; q < 64; q += 4) {
+                acc += col[q * 65];
+                a2 += col[(q + 1) * 65];
+                a3 += col[(q + 2) * 65];
+                a4 += col[(q + 3) * 65];
+              }
+              acc = (acc + a2) + (a3 + a4);
+            } else {
+              for (int q = 0; q < p.block; ++q) acc += col[q * 65];
+            }
             p.col_part[int64_t(hc) * p.nk + j] = acc;
           }
         }
@@ -273,7 +293,19 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
             float acc = 0.f;
             const int q0 = e > 63 ? e - 63 : 0;
             const int q1 = min(p.block - 1, e);
-            for (int q = q0; q <= q1; ++q) acc += Tb[(dh * 64 + q) * 65 + (q - e + 63)];
+            // diagonal e walks T with stride 66 (= row 65 + column 1); zeros past the
+            // estimator rows make the fixed-count form exact
+            const float* dg = Tb + (dh * 64 + q0) * 65 + (q0 - e + 63);
+            const int cnt = q1 - q0 + 1;
+            float a2 = 0.f;
+            int q = 0;
+#pragma unroll 4
+            for (; q + 1 < cnt; q += 2) {
+              acc += dg[q * 66];
+              a2 += dg[(q + 1) * 66];
+            }
+            if (q < cnt) acc += dg[q * 66];
+            acc += a2;
             p.diag_part[(int64_t(hd) * p.ntiles + it.t0 + t) * 128 + e] = acc;
           }
         }
