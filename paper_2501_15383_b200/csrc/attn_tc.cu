@@ -274,8 +274,16 @@ constexpr int kMetaSlots = 8;
 constexpr int kTraceTiles = 512;
 // trace columns: 0 meta ready (producer), 1 K TMA issued, 2 V TMA issued,
 // 3 QK issued (MMA), 4 PV issued, 5 softmax got S, 6 softmax P written, 7 kind
+// pipeline trace (tools/trace_tc.py): compiled in only with -DLCX_TC_TRACE -- the
+// per-tile checks cost ~3 % of the kernel's instructions
 __device__ __forceinline__ void trace_mark(const TcParams& p, uint32_t T, int col) {
+#ifdef LCX_TC_TRACE
   if (p.trace && blockIdx.x == 0 && T < kTraceTiles) p.trace[T * 8 + col] = clock64();
+#else
+  (void)p;
+  (void)T;
+  (void)col;
+#endif
 }
 static_assert(sizeof(TileMeta) <= 448, "tile metadata slot overflow");
 
@@ -283,17 +291,6 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
-}
-
-// 2^x on the FMA / ALU pipes: 2^floor(x) * p(x - floor(x)), p a degree-3 minimax fit of
-// 2^f on [0, 1) (max rel. error 8.6e-5, below the fp16 rounding of P); x <= 0 except
-// within the lazy-rescale threshold, -inf -> 0
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -127.f);
-  const float xi = floorf(x);
-  const float f = x - xi;
-  const float p = fmaf(fmaf(fmaf(0.07706616f, f, 0.22764521f), f, 0.69511718f), f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (int(xi) << 23));
 }
 
 __device__ __forceinline__ uint64_t window64(const uint32_t* sw, int off) {
@@ -766,8 +763,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       uint32_t pw[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) {
-        // half of the exponentials on the FMA pipe (MUFU ex2 is the per-tile limiter)
-        const float p0 = ex2(sv[2 * k] - mm), p1 = ex2_poly(sv[2 * k + 1] - mm);
+        const float p0 = ex2(sv[2 * k] - mm), p1 = ex2(sv[2 * k + 1] - mm);
         rs += p0 + p1;
         const __half2 h2 = __floats2half2_rn(p0, p1);
         pw[k] = *reinterpret_cast<const uint32_t*>(&h2);
