@@ -24,6 +24,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+# e.g. LCX_NVCC_EXTRA=-DLCX_TC_TRACE for tools/trace_tc.py (build with --clean)
+FLAGS += os.environ.get("LCX_NVCC_EXTRA", "").split()
 
 
 def sources():

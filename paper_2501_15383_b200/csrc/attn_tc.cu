@@ -59,8 +59,10 @@ constexpr uint32_t OFF_K = 0;
 constexpr uint32_t OFF_V = OFF_K + NK * kKStage;     // 128 KB
 constexpr uint32_t OFF_BAR = OFF_V + NV * kVStage;   // 192 KB
 constexpr uint32_t OFF_META = OFF_BAR + 512;
-constexpr uint32_t OFF_RED = OFF_META + 8 * 448;  // [2 buf][2 part][128] max, then [2][128] sum
-constexpr uint32_t kSmemBytes = OFF_RED + 3 * 2 * 128 * 4 + 1024;  // + alignment slack
+// softmax hand-off area: running max per tile parity [2][128], partial sums
+// (l, m) [2 slot][2 warp group][128]
+constexpr uint32_t OFF_RED = OFF_META + 8 * 448;
+constexpr uint32_t kSmemBytes = OFF_RED + 2 * 128 * 4 + 2 * 2 * 128 * 8 + 1024;  // + align slack
 // TMEM (512 columns x 128 lanes): S/P buffers [0, 256), O [256, 384), rotated
 // Q hi [384, 448) and lo [448, 512) as the A operand of every QK MMA (bf16 pairs
 // per 32-bit column), so all MMAs read only B from shared memory.
@@ -271,6 +273,13 @@ struct TileMeta {
   int32_t keys[64];
 };
 constexpr int kMetaSlots = 8;
+#ifndef LCX_TC_PREFETCH
+#define LCX_TC_PREFETCH 0
+#endif
+constexpr int kPrefetchLead = LCX_TC_PREFETCH;  // tiles (0 = off)
+#ifndef LCX_TC_BULK
+#define LCX_TC_BULK 1  // 1-D bulk copies of the pre-swizzled tiles (else 3-D tensor TMA)
+#endif
 constexpr int kTraceTiles = 512;
 // trace columns: 0 meta ready (producer), 1 K TMA issued, 2 V TMA issued,
 // 3 QK issued (MMA), 4 PV issued, 5 softmax got S, 6 softmax P written, 7 kind
@@ -313,18 +322,20 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // stay in the shared address space (LDS/STS, not generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
-  uint64_t* k_full = bars;                 // [NK] TMA -> MMA
-  uint64_t* k_empty = k_full + NK;         // [NK] QK commit -> producer
-  uint64_t* v_full = k_empty + NK;         // [NV]
-  uint64_t* v_empty = v_full + NV;         // [NV] PV commit -> producer
-  uint64_t* s_full = v_empty + NV;         // [NS] QK commit -> softmax
-  uint64_t* s_free = s_full + NS;          // [NS] PV commit (S/P buffer, O updated)
-  uint64_t* p_full = s_free + NS;          // [NS] softmax wrote P -> PV issuer
-  uint64_t* q_ready = p_full + NS;         // softmax rotated Q -> QK issuer
-  uint64_t* m_full = q_ready + 1;          // [kMetaSlots]
-  uint64_t* m_empty = m_full + kMetaSlots; // [kMetaSlots]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(m_empty + kMetaSlots);
+  // barriers as 32-bit shared addresses (no generic -> shared conversion per use)
+  const uint32_t smem_base = tc::smem_u32(smem);
+  const tc::SBar k_full{smem_base + OFF_BAR};  // [NK] TMA -> MMA
+  const tc::SBar k_empty = k_full + NK;        // [NK] QK commit -> producer
+  const tc::SBar v_full = k_empty + NK;        // [NV]
+  const tc::SBar v_empty = v_full + NV;        // [NV] PV commit -> producer
+  const tc::SBar s_full = v_empty + NV;        // [NS] QK commit -> softmax
+  const tc::SBar s_free = s_full + NS;         // [NS] PV commit (S/P buffer, O updated)
+  const tc::SBar p_full = s_free + NS;         // [NS] softmax wrote P -> PV issuer
+  const tc::SBar q_ready = p_full + NS;        // softmax rotated Q -> QK issuer
+  const tc::SBar m_full = q_ready + 1;         // [kMetaSlots]
+  const tc::SBar m_empty = m_full + kMetaSlots;  // [kMetaSlots]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR) +
+                        2 * (2 * NK + 2 * NV + 3 * NS + 1 + 2 * kMetaSlots);
   static_assert((2 * NK + 2 * NV + 3 * NS + 1 + 2 * kMetaSlots + 1) * 8 <= 512,
                 "barrier area overflow");
   TileMeta* metas = reinterpret_cast<TileMeta*>(smem + OFF_META);
@@ -342,9 +353,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     for (int b = 0; b < NS; ++b) {
       tc::mbar_init(s_full + b, 1);
       tc::mbar_init(s_free + b, 1);
-      tc::mbar_init(p_full + b, kSoftmaxWarps);
+      tc::mbar_init(p_full + b, kSoftmaxWarps / 2);  // the tile's warp group
     }
-    tc::mbar_init(q_ready, kSoftmaxWarps);
+    tc::mbar_init(q_ready, kSoftmaxWarps / 2);
     for (int b = 0; b < kMetaSlots; ++b) {
       tc::mbar_init(m_full + b, 1);
       tc::mbar_init(m_empty + b, kSoftmaxWarps + 3);  // softmax + QK + PV + V warps
@@ -381,8 +392,36 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       if (lane == 0) tc::mbar_arrive(m_full + (M % kMetaSlots));
       ++M;
     };
+    // L2 prefetch cursor kPrefetchLead tiles ahead of the load cursor (into the next
+    // item of this CTA near the end of an item): far slash tiles are single-use DRAM
+    // reads whose latency the 4 K / V stages alone do not cover
+    const Item* plans = reinterpret_cast<const Item*>(p.plans);
+    auto prefetch_tile = [&](const Item& pi, int t) {
+      const Tile pt = get_tile(p, pi, t);
+      if (pt.kind == T_VERT) {
+        const int tile = int((int64_t(pi.h) * (p.capp / 64) + pt.key0 / 64) * 2);
+        tc::tma_prefetch_l2_3d(&map_kc_hi, 0, 0, tile);
+        tc::tma_prefetch_l2_3d(&map_kc_hi, 0, 0, tile + 1);
+        tc::tma_prefetch_l2_3d(&map_kc_lo, 0, 0, tile);
+        tc::tma_prefetch_l2_3d(&map_kc_lo, 0, 0, tile + 1);
+        tc::tma_prefetch_l2_3d(&map_vct, 0, 0, tile / 2);
+      } else {
+        const int tile = int((int64_t(pi.g) * p.ntiles_k + pt.key0 / 64) * 2);
+        tc::tma_prefetch_l2_3d(&map_k_hi, 0, 0, tile);
+        tc::tma_prefetch_l2_3d(&map_k_hi, 0, 0, tile + 1);
+        tc::tma_prefetch_l2_3d(&map_k_lo, 0, 0, tile);
+        tc::tma_prefetch_l2_3d(&map_k_lo, 0, 0, tile + 1);
+        tc::tma_prefetch_l2_3d(&map_vt, 0, 0, tile / 2);
+      }
+    };
     for (int item = blockIdx.x; item < p.nitems; item += gridDim.x) {
-      const Item it = reinterpret_cast<const Item*>(p.plans)[item];
+      const Item it = plans[item];
+      const bool has_next = item + int(gridDim.x) < p.nitems;
+      Item nit{};
+      if (kPrefetchLead > 0 && has_next) nit = plans[item + gridDim.x];
+      if (kPrefetchLead > 0 && item == int(blockIdx.x) && lane < kPrefetchLead &&
+          lane < it.ntiles)
+        prefetch_tile(it, lane);  // first item: its head tiles
       if (it.ntiles == 0) {
         TileMeta& mt = next_slot();
         if (lane == 0) {
@@ -412,6 +451,12 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
             counts[j] = __shfl_sync(0xffffffffu, my.count, j);
             key0s[j] = __shfl_sync(0xffffffffu, (long long)my.key0, j);
           }
+        }
+        // L2 prefetch of tiles tb + kPrefetchLead + [0, 4) (lanes 8..11)
+        if (kPrefetchLead > 0 && lane >= 8 && lane < 12) {
+          const int t = tb + kPrefetchLead + (lane - 8);
+          if (t < it.ntiles) prefetch_tile(it, t);
+          else if (has_next && t - it.ntiles < nit.ntiles) prefetch_tile(nit, t - it.ntiles);
         }
         // B: all loads of the batch
         const int jj = lane >> 3, w = lane & 7;
@@ -479,22 +524,38 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           }
           publish();
           if (lane == 0) {
+#if !defined(LCX_TC_TRACE_PV) && !defined(LCX_TC_TRACE_SM)
             trace_mark(p, T, 0);
+#endif
             const int bk = T % NK;
             const uint32_t phk = (T / NK) & 1;
             tc::mbar_wait(k_empty + bk, phk ^ 1);
             tc::mbar_expect_tx(k_full + bk, kKStage);
-            uint8_t* kdst = smem + OFF_K + bk * kKStage;
-            const CUtensorMap* mh = kinds[j] == T_VERT ? &map_kc_hi : &map_k_hi;
-            const CUtensorMap* ml = kinds[j] == T_VERT ? &map_kc_lo : &map_k_lo;
+            const uint32_t kdst = smem_base + OFF_K + bk * kKStage;
             const int tile = kinds[j] == T_VERT
                                  ? int((int64_t(it.h) * (p.capp / 64) + key0s[j] / 64) * 2)
                                  : int((int64_t(it.g) * p.ntiles_k + key0s[j] / 64) * 2);
+#ifdef LCX_TC_FAKE_LOADS  // timing experiment only: every tile loads from a small L2-resident set
+            const_cast<int&>(tile) = (tile & 62);
+#endif
+#if LCX_TC_BULK
+            // pre-swizzled tiles: hi (2 halves) and lo are one contiguous 16 KB run each
+            const __nv_bfloat16* sh = kinds[j] == T_VERT ? p.kchi : p.khi;
+            const __nv_bfloat16* sl = kinds[j] == T_VERT ? p.kclo : p.klo;
+            tc::bulk_load(kdst, sh + int64_t(tile) * (kKHalf / 2), 2 * kKHalf, k_full + bk);
+            tc::bulk_load(kdst + 2 * kKHalf, sl + int64_t(tile) * (kKHalf / 2), 2 * kKHalf,
+                          k_full + bk);
+#else
+            const CUtensorMap* mh = kinds[j] == T_VERT ? &map_kc_hi : &map_k_hi;
+            const CUtensorMap* ml = kinds[j] == T_VERT ? &map_kc_lo : &map_k_lo;
             tc::tma_load_3d(kdst + 0 * kKHalf, mh, k_full + bk, 0, 0, tile);
             tc::tma_load_3d(kdst + 1 * kKHalf, mh, k_full + bk, 0, 0, tile + 1);
             tc::tma_load_3d(kdst + 2 * kKHalf, ml, k_full + bk, 0, 0, tile);
             tc::tma_load_3d(kdst + 3 * kKHalf, ml, k_full + bk, 0, 0, tile + 1);
+#endif
+#if !defined(LCX_TC_TRACE_PV) && !defined(LCX_TC_TRACE_SM)
             trace_mark(p, T, 1);
+#endif
           }
           __syncwarp();
           ++T;
@@ -531,11 +592,17 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       tc::mbar_wait(k_full + bk, (T / NK) & 1);
       tc::mbar_wait(s_free + bs, ((T / NS) & 1) ^ 1);  // PV(T - NS) released S/P buffer
       tc::tc_fence_after();
+#ifndef LCX_TC_TRACE_PV
       if (lane == 0) trace_mark(p, T, 7);
+#endif
       const uint64_t dk = dk0 + ((bk * kKStage) >> 4);
       const uint32_t dS = tmem + bs * BN;
 #pragma unroll
+#ifdef LCX_TC_ONE_TERM  // timing experiment only: hi.hi product alone
+      for (int combo = 0; combo < 1; ++combo) {
+#else
       for (int combo = 0; combo < 3; ++combo) {
+#endif
         const uint32_t qa = tmem + (combo == 2 ? COL_QLO : COL_QHI);  // hi.hi, hi.lo, lo.hi
         const uint64_t ka = dk + (combo == 1 ? ((2 * kKHalf) >> 4) : 0);
 #pragma unroll
@@ -548,7 +615,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       }
       tc::mma_commit_warp(k_empty + bk);
       tc::mma_commit_warp(s_full + bs);
+#ifndef LCX_TC_TRACE_PV
       if (lane == 0) trace_mark(p, T, 3);
+#endif
       ++T;
     }
   } else if (warp == kWarpV) {
@@ -569,14 +638,21 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         const int bv = T % NV;
         tc::mbar_wait(v_empty + bv, ((T / NV) & 1) ^ 1);
         tc::mbar_expect_tx(v_full + bv, kVStage);
-        uint8_t* vdst = smem + OFF_V + bv * kVStage;
-        if (kind == T_VERT)
-          tc::tma_load_3d(vdst, &map_vct, v_full + bv, 0, 0,
-                          int(int64_t(h) * (p.capp / 64) + key0 / 64));
-        else
-          tc::tma_load_3d(vdst, &map_vt, v_full + bv, 0, 0,
-                          int(int64_t(h / p.group) * p.ntiles_k + key0 / 64));
+        const uint32_t vdst = smem_base + OFF_V + bv * kVStage;
+        const int64_t vtile = kind == T_VERT ? int64_t(h) * (p.capp / 64) + key0 / 64
+                                             : int64_t(h / p.group) * p.ntiles_k + key0 / 64;
+#ifdef LCX_TC_FAKE_LOADS
+        const_cast<int64_t&>(vtile) = (vtile & 31);
+#endif
+#if LCX_TC_BULK
+        tc::bulk_load(vdst, (kind == T_VERT ? p.vct : p.vt) + vtile * (kVStage / 2), kVStage,
+                      v_full + bv);
+#else
+        tc::tma_load_3d(vdst, kind == T_VERT ? &map_vct : &map_vt, v_full + bv, 0, 0, int(vtile));
+#endif
+#ifndef LCX_TC_TRACE_PV
         trace_mark(p, T, 2);
+#endif
       }
       __syncwarp();
       ++T;
@@ -588,6 +664,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     for (;;) {
       const int slot = M % kMetaSlots;
       tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1);
+#ifdef LCX_TC_TRACE_PV
+      if (lane == 0) trace_mark(p, T, 0);
+#endif
       const int kind = metas[slot].kind;
       const int flags = metas[slot].flags;
       __syncwarp();
@@ -597,7 +676,13 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       if (kind == T_EMPTY) continue;
       const int bs = T % NS, bv = T % NV;
       tc::mbar_wait(p_full + bs, (T / NS) & 1);
+#ifdef LCX_TC_TRACE_PV  // columns 0 / 1 / 2: PV issuer passed the meta / P / V waits
+      if (lane == 0) trace_mark(p, T, 1);
+#endif
       tc::mbar_wait(v_full + bv, (T / NV) & 1);
+#ifdef LCX_TC_TRACE_PV
+      if (lane == 0) trace_mark(p, T, 2);
+#endif
       tc::tc_fence_after();
       const uint64_t dv = dv0 + ((bv * kVStage) >> 4);
       const bool first = (flags & F_FIRST) != 0;
@@ -612,43 +697,52 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     }
   } else {
     // ============================= softmax / correction / epilogue ====
-    // Two warps per TMEM lane quadrant split each tile's 64 columns (32 each) and
-    // the 128 O columns (64 each); the row max is exchanged through shared memory
-    // with a 64-thread named barrier per quadrant.
+    // Two warp groups take alternate tiles of the stream (group g: tiles T with
+    // T % 2 == g); within a group, warp = TMEM lane quadrant and thread = query row
+    // with all 64 columns of the tile.  The groups run out of phase -- one computes
+    // a tile's max while the other exponentiates the previous tile -- and hand the
+    // row's running max over per tile through shared memory with named barriers
+    // (quadrant q: id 1 + q for group 0 -> 1, id 5 + q for 1 -> 0; strictly
+    // alternating arrive / sync).  Each group keeps its own partial row sum l
+    // expressed at the max it last used; the owner of an item's last tile combines
+    // both (the other group's (l, m) published before its P release) in the epilogue.
     const int wq = warp & 3;       // TMEM lane quadrant
-    const int part = warp >> 2;    // column half
+    const int grp = warp >> 2;     // warp group: tiles of this parity
     const int r = wq * 32 + lane;
     const uint32_t lane_base = uint32_t(wq * 32) << 16;
-    float* red = reinterpret_cast<float*>(smem + OFF_RED);  // [2 buf][2 part][128]
-    const uint32_t bar_id = 1 + wq;
+    float* mbuf = reinterpret_cast<float*>(smem + OFF_RED);        // [2][128] m after tile T
+    float2* lbuf = reinterpret_cast<float2*>(smem + OFF_RED + 1024);  // [2][2][128] (l, m)
+    const uint32_t bar_in = grp == 0 ? 5 + wq : 1 + wq;   // other group -> this group
+    const uint32_t bar_out = grp == 0 ? 1 + wq : 5 + wq;  // this group -> other group
     uint32_t T = 0, M = 0;
-    float m = -INFINITY, l = 0.f;
+    float l = 0.f, m_used = -INFINITY;  // this group's partial sum, at max m_used
+    float m_init = -INFINITY;           // running max at the item start (key-window passes)
     Item qi{};  // only i0 / rend / h used by rotate_q
+    if (grp == 1) asm volatile("bar.arrive %0, 64;" ::"r"(bar_out) : "memory");  // T = 0 is g0's
+    auto rotate_row = [&](int pattern) {
+      rotate_q(p, qi, pattern, r, 0, tmem + lane_base);
+      rotate_q(p, qi, pattern, r, 1, tmem + lane_base);
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(q_ready);
+    };
     for (;;) {
       const int slot = M % kMetaSlots;
       tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1);
       const TileMeta& mt = metas[slot];
       const int kind = mt.kind, flags = mt.flags;
-      if (kind == T_END) break;
+      if (kind == T_END) {
+        if ((T & 1) == uint32_t(grp))  // match the last tile's hand-off (or the initial one)
+          asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
+        break;
+      }
       const int64_t i0 = mt.i0, rend = mt.rend;
       const int h = mt.h;
       const int64_t i = i0 + r;
       const bool row_ok = i < rend;
-      if (kind == T_EMPTY) {
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(m_empty + slot);
-        ++M;
-        if (row_ok && !p.init) {  // init passes keep the running state of an empty item
-          float4* o = reinterpret_cast<float4*>(p.out + (i * p.hq + h) * int64_t(HD)) + part * 16;
-          for (int x = 0; x < 16; ++x) o[x] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (part == 0) p.lse[int64_t(h) * p.lse_stride + i] = -INFINITY;
-        }
-        continue;
-      }
-      // ---- admission mask of this warp's 32 columns ----
-      uint32_t mask = 0;
-      if (row_ok) {
-        uint64_t m64;
+      const bool mine = kind != T_EMPTY && (T & 1) == uint32_t(grp);
+      uint64_t mask = 0;
+      if (mine && row_ok) {
         if (kind == T_VERT) {
           int cnt = mt.nfar;
           while (cnt < mt.count) {
@@ -656,37 +750,55 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
             if (kk < 0 || int64_t(kk) > i) break;
             ++cnt;
           }
-          m64 = cnt >= 64 ? ~0ull : ((1ull << cnt) - 1);
+          mask = cnt >= 64 ? ~0ull : ((1ull << cnt) - 1);
         } else if (kind == T_SLASH) {
           const int off = int(i - mt.key0 - 63 - mt.sbase);
-          m64 = __brevll(window64(mt.sw, off)) & ~mt.vmask;
+          mask = __brevll(window64(mt.sw, off)) & ~mt.vmask;
         } else {
           const int64_t lim = i - mt.key0;
-          m64 = lim >= 63 ? ~0ull : (lim < 0 ? 0ull : ((2ull << lim) - 1));
+          mask = lim >= 63 ? ~0ull : (lim < 0 ? 0ull : ((2ull << lim) - 1));
         }
-        mask = uint32_t(m64 >> (32 * part));
       }
       const int pattern = mt.pattern, next_pattern = mt.next_pattern;
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(m_empty + slot);
       ++M;
-      if (flags & F_FIRST) {
+      if (kind == T_EMPTY) {
+        if (grp == 0 && row_ok && !p.init) {  // init passes keep the running state
+          float4* o = reinterpret_cast<float4*>(p.out + (i * p.hq + h) * int64_t(HD));
+          for (int x = 0; x < 32; ++x) o[x] = make_float4(0.f, 0.f, 0.f, 0.f);
+          p.lse[int64_t(h) * p.lse_stride + i] = -INFINITY;
+        }
+        continue;
+      }
+      if (flags & F_FIRST) {  // both groups start the item (partial sums, Q rotation rows)
+        l = 0.f;
+        m_used = -INFINITY;
         qi.i0 = i0;
         qi.rend = rend;
         qi.h = h;
-        m = -INFINITY;
-        l = 0.f;
+      }
+      if (!mine) {
+        ++T;
+        continue;
+      }
+      if (flags & F_FIRST) {
+        // the other group's epilogue of the previous item (its last tile, T - 1) has read
+        // O and S(T - 1) is consumed, so O / Q of this CTA's TMEM are free
+        asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
+        tc::tc_fence_after();
+        m_init = -INFINITY;
         if (p.init) {
           // key-window pass > 0: continue from the row's running (o, lse) -- O goes back
           // into TMEM (the previous item's last PV completed before its epilogue read O)
           const float lp = row_ok ? p.lse[int64_t(h) * p.lse_stride + i] : -INFINITY;
           const bool live = lp != -INFINITY;
-          m = live ? lp * 1.4426950408889634f : -INFINITY;
-          l = (live && part == 0) ? 1.f : 0.f;
-          const float4* o =
-              reinterpret_cast<const float4*>(p.out + (i * p.hq + h) * int64_t(HD)) + part * 16;
-#pragma unroll
-          for (int q4 = 0; q4 < 2; ++q4) {
+          m_init = live ? lp * 1.4426950408889634f : -INFINITY;
+          l = live ? 1.f : 0.f;
+          m_used = m_init;
+          const float4* o = reinterpret_cast<const float4*>(p.out + (i * p.hq + h) * int64_t(HD));
+#pragma unroll 1
+          for (int q4 = 0; q4 < 4; ++q4) {
             float ov[32];
 #pragma unroll
             for (int x = 0; x < 8; ++x) {
@@ -696,53 +808,72 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
               ov[4 * x + 2] = v.z;
               ov[4 * x + 3] = v.w;
             }
-            tc::tmem_st32(tmem + lane_base + COL_O + part * 64 + q4 * 32, ov);
+            tc::tmem_st32(tmem + lane_base + COL_O + q4 * 32, ov);
           }
           tc::tmem_wait_st();
         }
-        rotate_q(p, qi, pattern, r, part, tmem + lane_base);
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(q_ready);
+        rotate_row(pattern);
       }
       const int b = T % NS;
       const uint32_t ph = (T / NS) & 1;
-      float sv[32];
+      float sv[64];
       tc::mbar_wait(s_full + b, ph);
       tc::tc_fence_after();
-      tc::tmem_ld32(tmem + lane_base + b * BN + part * 32, sv);
+      tc::tmem_ld32(tmem + lane_base + b * BN, sv);
+      tc::tmem_ld32(tmem + lane_base + b * BN + 32, sv + 32);
       tc::tmem_wait_ld();
+#ifdef LCX_TC_TRACE_SM  // owner group's quadrant-0 warp: 5 S got, 0 m handed over, 6 P put
+      if (wq == 0 && lane == 0) trace_mark(p, T, 5);
+#else
       if (threadIdx.x == 0) trace_mark(p, T, 5);
-      if (flags & F_EPOCH_AFTER) {  // all QK of the old pattern are complete
-        rotate_q(p, qi, next_pattern, r, part, tmem + lane_base);
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(q_ready);
-      }
-      // masked logits -> -inf (ex2(-inf) = 0), scaled to log2 units
-      float tmax = -INFINITY;
+#endif
+      if (flags & F_EPOCH_AFTER) rotate_row(next_pattern);  // the old pattern's QKs are done
+#ifdef LCX_TC_FAKE_SOFTMAX  // timing experiment only: no softmax math
+      for (int cc = 0; cc < 64; ++cc) sv[cc] = -INFINITY;
+      mask = ~0ull;
+#endif
+      // masked logits -> -inf (ex2(-inf) = 0), already in log2 units
+      if (!__all_sync(0xffffffffu, mask == ~0ull)) {  // fully admitted rows: no select
+        const uint32_t lo = uint32_t(mask), hi = uint32_t(mask >> 32);
 #pragma unroll
-      for (int cc = 0; cc < 32; ++cc) {
-        sv[cc] = ((mask >> cc) & 1u) ? sv[cc] : -INFINITY;
-        tmax = fmaxf(tmax, sv[cc]);
+        for (int cc = 0; cc < 32; ++cc) {
+          sv[cc] = ((lo >> cc) & 1u) ? sv[cc] : -INFINITY;
+          sv[32 + cc] = ((hi >> cc) & 1u) ? sv[32 + cc] : -INFINITY;
+        }
       }
-      float* rb = red + (T & 1) * 256;
-      rb[part * 128 + r] = tmax;
-      asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-      tmax = fmaxf(tmax, rb[(part ^ 1) * 128 + r]);
-      // lazy rescale (warp-uniform TMEM access); both halves take the same decision
-      // (first tile: O holds either nothing (m = -inf) or the loaded running state)
-      const bool need = tmax > m + kRescaleThresh;
-      const bool warp_need = __any_sync(0xffffffffu, need && m != -INFINITY);
-      const float m_new = need ? tmax : m;
-      if (warp_need) {
-        const uint32_t Tp = T - 1;  // O must hold PV(T-1) before rescaling
+      float t4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int cc = 0; cc < 64; cc += 8)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) t4[u] = fmaxf(t4[u], fmaxf(sv[cc + u], sv[cc + 4 + u]));
+      const float tmax = fmaxf(fmaxf(t4[0], t4[1]), fmaxf(t4[2], t4[3]));
+      // ---- running max: previous tile's (other group) unless the item starts here
+      if (!(flags & F_FIRST)) asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
+      const float m_prev = (flags & F_FIRST) ? m_init : mbuf[((T - 1) & 1) * 128 + r];
+      // lazy rescale: the max moves only past a threshold (P <= 2^8 in fp16)
+      const bool need = tmax > m_prev + kRescaleThresh;
+      const float m = need ? tmax : m_prev;
+      mbuf[(T & 1) * 128 + r] = m;
+#ifdef LCX_TC_TRACE_SM  // column 1: flags | kind << 8 | rescale << 12 (a value, not a time)
+      if (wq == 0 && lane == 0) {
+        trace_mark(p, T, 0);
+        const bool any_need = __any_sync(0x1u, need && m_prev != -INFINITY);
+        if (p.trace && blockIdx.x == 0 && T < kTraceTiles)
+          p.trace[T * 8 + 1] = flags | (kind << 8) | (int(any_need) << 12);
+      }
+#endif
+      // an item's last tile hands over only after its epilogue (next item's O / Q)
+      if (!(flags & F_LAST)) asm volatile("bar.arrive %0, 64;" ::"r"(bar_out) : "memory");
+      if (__any_sync(0xffffffffu, need && m_prev != -INFINITY)) {
+        // O holds PV up to tile T - 1 at max m_prev: complete it, then rescale
+        const uint32_t Tp = T - 1;
         tc::mbar_wait(s_free + (Tp % NS), (Tp / NS) & 1);
         tc::tc_fence_after();
-        const float f = (need && m != -INFINITY) ? ex2(m - m_new) : 1.f;
-        for (int q4 = 0; q4 < 2; ++q4) {
+        const float f = (need && m_prev != -INFINITY) ? ex2(m_prev - m) : 1.f;
+#pragma unroll 1
+        for (int q4 = 0; q4 < 4; ++q4) {
           float ov[32];
-          const uint32_t ta = tmem + lane_base + COL_O + part * 64 + q4 * 32;
+          const uint32_t ta = tmem + lane_base + COL_O + q4 * 32;
           tc::tmem_ld32(ta, ov);
           tc::tmem_wait_ld();
 #pragma unroll
@@ -750,45 +881,58 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           tc::tmem_st32(ta, ov);
         }
         tc::tmem_wait_st();
-        l *= f;
-      } else if (need && m != -INFINITY) {
-        l *= ex2(m - m_new);
       }
-      m = m_new;
-      // ---- P = exp2(x - m) in fp16, written over this tile's S columns in TMEM:
-      // key c -> column c / 2 (two fp16 per 32-bit column).  Both column halves of
-      // the row finished reading S before the max-exchange barrier above.
-      float rs = 0.f;
+      if (m != m_used) {  // this group's partial sum follows the row max
+        if (m_used != -INFINITY) l *= ex2(m_used - m);
+        m_used = m;
+      }
+      // ---- P = exp2(x - m) in fp16, written over the tile's S columns in TMEM:
+      // key c -> column c / 2 (two fp16 per 32-bit column).  Packed f32x2 subtract /
+      // accumulate (FADD2): half the FP32 instructions per key.
       const float mm = m == -INFINITY ? 0.f : m;
-      uint32_t pw[16];
+      const float2 nm2 = make_float2(-mm, -mm);
+      float2 rs2 = make_float2(0.f, 0.f);
+      uint32_t pw[32];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const float p0 = ex2(sv[2 * k] - mm), p1 = ex2(sv[2 * k + 1] - mm);
-        rs += p0 + p1;
-        const __half2 h2 = __floats2half2_rn(p0, p1);
+      for (int k = 0; k < 32; ++k) {
+        const float2 x = __fadd2_rn(make_float2(sv[2 * k], sv[2 * k + 1]), nm2);
+        const float2 pp = make_float2(ex2(x.x), ex2(x.y));
+        rs2 = __fadd2_rn(rs2, pp);
+        const __half2 h2 = __floats2half2_rn(pp.x, pp.y);
         pw[k] = *reinterpret_cast<const uint32_t*>(&h2);
       }
-      tc::tmem_st16(tmem + lane_base + b * BN + part * 16, pw);
+      tc::tmem_st16(tmem + lane_base + b * BN, pw);
+      tc::tmem_st16(tmem + lane_base + b * BN + 16, pw + 16);
       tc::tmem_wait_st();
-      l += rs;
+      l += rs2.x + rs2.y;
+      // partial (l, m) for the item's epilogue (ordered before the P release below)
+      lbuf[(((T >> 1) & 1) * 2 + grp) * 128 + r] = make_float2(l, m_used);
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(p_full + b);
+#ifdef LCX_TC_TRACE_SM
+      if (wq == 0 && lane == 0) trace_mark(p, T, 6);
+#else
       if (threadIdx.x == 0) trace_mark(p, T, 6);
+#endif
       if (flags & F_LAST) {
-        // ---- epilogue: wait for this item's last PV, normalize, store ----
-        float* rl = red + 512;  // separated from the next tile's max exchange by its barrier
-        rl[part * 128 + r] = l;
-        asm volatile("bar.sync %0, 64;" ::"r"(bar_id) : "memory");
-        const float lt = l + rl[(part ^ 1) * 128 + r];
+        // ---- epilogue: add the other group's partial sum, wait for the last PV,
+        // normalize, store ----
+        float lt = l;
+        if (!(flags & F_FIRST)) {
+          const uint32_t To = T - 1;  // the other group's last tile of this item
+          tc::mbar_wait(p_full + (To % NS), (To / NS) & 1);
+          const float2 lo = lbuf[(((To >> 1) & 1) * 2 + (grp ^ 1)) * 128 + r];
+          if (lo.x > 0.f) lt += lo.x * ex2(lo.y - m);
+        }
         tc::mbar_wait(s_free + b, ph);  // this item's last PV is complete
         tc::tc_fence_after();
         const float inv = lt > 0.f ? 1.f / lt : 0.f;
-        float4* o = reinterpret_cast<float4*>(p.out + (i * p.hq + h) * int64_t(HD)) + part * 16;
-#pragma unroll
-        for (int q4 = 0; q4 < 2; ++q4) {
+        float4* o = reinterpret_cast<float4*>(p.out + (i * p.hq + h) * int64_t(HD));
+#pragma unroll 1
+        for (int q4 = 0; q4 < 4; ++q4) {
           float ov[32];
-          tc::tmem_ld32(tmem + lane_base + COL_O + part * 64 + q4 * 32, ov);
+          tc::tmem_ld32(tmem + lane_base + COL_O + q4 * 32, ov);
           tc::tmem_wait_ld();
           if (row_ok) {
 #pragma unroll
@@ -797,10 +941,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
                                           ov[4 * x + 2] * inv, ov[4 * x + 3] * inv);
           }
         }
-        if (row_ok && part == 0)
+        if (row_ok)
           p.lse[int64_t(h) * p.lse_stride + i] =
               lt > 0.f ? (m + log2f(lt)) * 0.69314718055994530942f : -INFINITY;
         tc::tc_fence_before();
+        asm volatile("bar.arrive %0, 64;" ::"r"(bar_out) : "memory");
       }
       ++T;
     }
@@ -845,7 +990,9 @@ __global__ void k_prep_kernel(const __nv_bfloat16* __restrict__ k, int64_t n, in
   const int g = int(rowhead % hkv);
   const int64_t nt = (n + 63) / 64;
   const int d = 2 * pr;
-  const int64_t o = ((((int64_t(g) * nt + j / 64) * 2 + d / 64) * 64 + j % 64) * 64 + d % 64) / 2;
+  const int jr = int(j % 64), dd = d % 64;
+  const int64_t o = ((((int64_t(g) * nt + j / 64) * 2 + d / 64) * 64 + jr) * 64 +
+                     sw128_chunk(jr, dd / 8) * 8 + dd % 8) / 2;
   reinterpret_cast<__nv_bfloat162*>(khi)[o] = h2;
   reinterpret_cast<__nv_bfloat162*>(klo)[o] = __floats2bfloat162_rn(rx - hf.x, ry - hf.y);
 }
@@ -867,7 +1014,7 @@ __global__ void vt_prep_kernel(const __nv_bfloat16* __restrict__ v, int64_t n, i
   __half* dst = vt + (int64_t(g) * nt + jt) * (HD * 64);  // [128 dims][64 keys]
   for (int x = threadIdx.x; x < 64 * HD; x += blockDim.x) {
     const int d = x / 64, jj = x % 64;
-    dst[d * 64 + jj] = tile[jj][d];
+    dst[d * 64 + sw128_chunk(d, jj / 8) * 8 + jj % 8] = tile[jj][d];
   }
 }
 
@@ -930,12 +1077,14 @@ __global__ void compact_kernel(const __nv_bfloat16* __restrict__ khi,
     const int32_t j = keys[cc];
     const int half = ch / 8, c8 = ch % 8;
     if (j >= 0) {
-      const int64_t src = (((int64_t(g) * nt + j / 64) * 2 + half) * 64 + j % 64) * 64 + c8 * 8;
+      const int64_t src = (((int64_t(g) * nt + j / 64) * 2 + half) * 64 + j % 64) * 64 +
+                          sw128_chunk(j % 64, c8) * 8;
       a = *reinterpret_cast<const uint4*>(khi + src);
       b = *reinterpret_cast<const uint4*>(klo + src);
       vv = reinterpret_cast<const uint4*>(v + (int64_t(j) * hkv + g) * HD)[ch];
     }
-    const int64_t dst = (((int64_t(h) * ct + blockIdx.x) * 2 + half) * 64 + cc) * 64 + c8 * 8;
+    const int64_t dst =
+        (((int64_t(h) * ct + blockIdx.x) * 2 + half) * 64 + cc) * 64 + sw128_chunk(cc, c8) * 8;
     *reinterpret_cast<uint4*>(kchi + dst) = a;
     *reinterpret_cast<uint4*>(kclo + dst) = b;
     const __nv_bfloat16* vbf = reinterpret_cast<const __nv_bfloat16*>(&vv);
@@ -946,7 +1095,7 @@ __global__ void compact_kernel(const __nv_bfloat16* __restrict__ khi,
   __half* vdst = vct + (int64_t(h) * ct + blockIdx.x) * (HD * 64);  // [128 dims][64 slots]
   for (int x = threadIdx.x; x < 64 * HD; x += blockDim.x) {
     const int d = x / 64, cc = x % 64;
-    vdst[d * 64 + cc] = tile[cc][d];
+    vdst[d * 64 + sw128_chunk(d, cc / 8) * 8 + cc % 8] = tile[cc][d];
   }
 }
 
@@ -1254,7 +1403,14 @@ int tc_attention(const TcParams& p, const TcBuffers& B, int sm_count, cudaStream
   const int grid = std::min(p.nitems, sm_count);
   plan_items_kernel<<<(p.nitems + 127) / 128, 128, 0, st>>>(p, reinterpret_cast<Item*>(p.plans));
   LCX_CHECK_LAUNCH();
-  attn_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(p, B.m_khi, B.m_klo, B.m_vt, B.m_kchi,
+  TcParams q = p;
+  q.khi = B.khi;
+  q.klo = B.klo;
+  q.kchi = B.kchi;
+  q.kclo = B.kclo;
+  q.vt = B.vt;
+  q.vct = B.vct;
+  attn_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(q, B.m_khi, B.m_klo, B.m_vt, B.m_kchi,
                                                      B.m_kclo, B.m_vct);
   LCX_CHECK_LAUNCH();
   return LCX_OK;

@@ -37,6 +37,9 @@ struct TcParams {
   int64_t key_lo, key_hi;
   int vert_pass, init;
   const int* win_flags; int win;  // optional: skip the pass when win_flags[win] == 0
+  // pre-swizzled tiled operands (TcBuffers), loaded with 1-D bulk copies
+  const __nv_bfloat16 *khi, *klo, *kchi, *kclo;
+  const __half *vt, *vct;
 };
 
 struct TcBuffers {
@@ -67,6 +70,13 @@ void tc_layout(A& ar, int64_t n, int hq, int hkv, int64_t cap_v, int64_t seg_len
   B.kchi = ar.template take<__nv_bfloat16>(size_t(hq) * capp * 128);
   B.kclo = ar.template take<__nv_bfloat16>(size_t(hq) * capp * 128);
   B.vct = ar.template take<__half>(size_t(hq) * 128 * capp);
+}
+
+// Tiled operand layout: every 64-key tile is a run of 64-row x 128-byte blocks stored
+// already in the SWIZZLE_128B shared-memory image (16-byte chunk c of row r at chunk
+// c ^ (r & 7)), so one contiguous bulk copy lands a ready UMMA operand.
+__host__ __device__ __forceinline__ int sw128_chunk(int row, int chunk) {
+  return chunk ^ (row & 7);
 }
 
 // 3-D tiled tensor map, SWIZZLE_128B, L2 promotion 256 B

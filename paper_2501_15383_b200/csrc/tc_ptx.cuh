@@ -12,9 +12,20 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// mbarrier handle as a 32-bit shared-window address: kernels that touch barriers every
+// tile compute it once instead of converting a generic pointer per call
+struct SBar {
+  uint32_t a;
+  __device__ __forceinline__ SBar operator+(int i) const { return SBar{a + 8u * uint32_t(i)}; }
+};
+__device__ __forceinline__ SBar sbar(uint64_t* bar) { return SBar{smem_u32(bar)}; }
+
 // ------------------------------------------------------------ mbarrier --
+__device__ __forceinline__ void mbar_init(SBar bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar.a), "r"(count));
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  mbar_init(sbar(bar), count);
 }
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -22,38 +33,78 @@ __device__ __forceinline__ void fence_barrier_init() {
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void mbar_arrive(SBar bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar.a) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) { mbar_arrive(sbar(bar)); }
+__device__ __forceinline__ void mbar_expect_tx(SBar bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar.a), "r"(bytes)
+               : "memory");
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
+  mbar_expect_tx(sbar(bar), bytes);
 }
 // try_wait with a suspend-time hint: the waiting warp is parked by the hardware until the
 // phase completes (or the hint expires) instead of spinning -- spinning waiters steal
 // issue slots from the warps doing the work (ncu: 110 try_wait per tile without it)
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait(SBar bar, uint32_t parity) {
+#ifdef LCX_MBAR_NOHINT
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "LAB_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra LAB_WAIT_%=;\n\t}" ::"r"(bar.a),
+      "r"(parity)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "LAB_WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-      "@!p bra LAB_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "@!p bra LAB_WAIT_%=;\n\t}" ::"r"(bar.a),
       "r"(parity), "r"(0x989680u)
       : "memory");
+#endif
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  mbar_wait(sbar(bar), parity);
 }
 
 // ----------------------------------------------------------------- TMA --
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
-__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+// 1-D bulk copy global -> shared (contiguous, 16-byte multiples), completion on an mbarrier
+__device__ __forceinline__ void bulk_load(uint32_t smem_dst, const void* src, uint32_t bytes,
+                                          SBar bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_dst),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar.a)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+  bulk_load(smem_u32(smem_dst), src, bytes, sbar(bar));
+}
+// bring a TMA box into L2 ahead of its load (no shared memory, no completion)
+__device__ __forceinline__ void tma_prefetch_l2_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t smem_dst, const CUtensorMap* map, SBar bar,
                                             int c0, int c1, int c2) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar.a), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+  tma_load_3d(smem_u32(smem_dst), map, sbar(bar), c0, c1, c2);
 }
 
 // ------------------------------------------------------------- tcgen05 --
@@ -116,14 +167,15 @@ __device__ __forceinline__ void mma_f16_ts_warp(uint32_t d_tmem, uint32_t a_tmem
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-__device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
+__device__ __forceinline__ void mma_commit_warp(SBar bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
-          smem_u32(bar))
+          bar.a)
       : "memory");
 }
+__device__ __forceinline__ void mma_commit_warp(uint64_t* bar) { mma_commit_warp(sbar(bar)); }
 // arrive on an mbarrier when all previously issued tcgen05.mma of this thread complete
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile(

@@ -1,0 +1,30 @@
+"""Per-tile softmax timeline of CTA 0 (build with LCX_NVCC_EXTRA='-DLCX_TC_TRACE -DLCX_TC_TRACE_SM')."""
+import ctypes as C
+import sys
+import numpy as np
+sys.path.insert(0, ".")
+from paper_2501_15383_b200 import device as D  # noqa: E402
+from paper_2501_15383_b200._lib import context, lib  # noqa: E402
+from paper_2501_15383_b200.synth import make_qkv, yarn_temperature  # noqa: E402
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1048576
+ctx = context(0)
+L = lib()
+L.lcx_debug_trace.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+L.lcx_debug_trace(ctx.ptr, 1, None)
+q, k, v = make_qkv(n, 28, 4, kind="planted", seed=1)
+s, c = 131072, 262144
+D.chunked_prefill(q, k, v, chunk_len=32768, last_q=64, budget=(1000, 6096),
+                  position_mode="dca_continuous", dca=(s, c, min(s, c - s)),
+                  temperature=yarn_temperature(n / c), rope_base=1e7)
+buf = np.zeros((512, 8), np.int64)
+L.lcx_debug_trace(ctx.ptr, 1, buf.ctypes.data)
+t0 = buf[0, 7]
+print("tile grp flg kind resc   QKst  QKend  S_got  m_out  P_put  PV_is   d(S-QKend) d(P-S)")
+for t in range(1, 400):
+    b = buf[t]
+    if b[7] == 0:
+        break
+    f = int(b[1])
+    print(f"{t:4d} {t & 1:3d} {f & 15:3d} {(f >> 8) & 15:4d} {(f >> 12) & 1:4d} "
+          + " ".join(f"{(x - t0):6d}" for x in (b[7], b[3], b[5], b[0], b[6], b[4]))
+          + f"   {b[5] - b[3]:6d} {b[6] - b[5]:6d}")
