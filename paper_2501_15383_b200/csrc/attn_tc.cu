@@ -59,9 +59,10 @@ constexpr uint32_t OFF_K = 0;
 constexpr uint32_t OFF_V = OFF_K + NK * kKStage;     // 128 KB
 constexpr uint32_t OFF_BAR = OFF_V + NV * kVStage;   // 192 KB
 constexpr uint32_t OFF_META = OFF_BAR + 512;
+constexpr int kMetaSlots = 16;                      // tile metadata ring (448 B slots)
 // softmax hand-off area: running max per tile parity [2][128], partial sums
 // (l, m) [2 slot][2 warp group][128]
-constexpr uint32_t OFF_RED = OFF_META + 8 * 448;
+constexpr uint32_t OFF_RED = OFF_META + kMetaSlots * 448;
 constexpr uint32_t kSmemBytes = OFF_RED + 2 * 128 * 4 + 2 * 2 * 128 * 8 + 1024;  // + align slack
 // TMEM (512 columns x 128 lanes): S/P buffers [0, 256), O [256, 384), rotated
 // Q hi [384, 448) and lo [448, 512) as the A operand of every QK MMA (bf16 pairs
@@ -175,9 +176,11 @@ __device__ void setup_item(const TcParams& p, int item, Item& it) {
   }
 }
 
-__device__ Tile get_tile(const TcParams& p, const Item& it, int t) {
+__device__ __forceinline__ Tile get_tile(const TcParams& p, const Item& it, int t) {
   Tile T{};
-  for (int x = 0; x < it.ng; ++x) {
+#pragma unroll
+  for (int x = 0; x < 3; ++x) {  // compile-time group index: Item stays in registers
+    if (x >= it.ng) break;
     const Group& G = it.grp[x];
     if (t < G.nvt) {
       T.kind = T_VERT;
@@ -202,6 +205,10 @@ __device__ Tile get_tile(const TcParams& p, const Item& it, int t) {
     t -= G.nst;
   }
   return T;
+}
+
+__device__ __forceinline__ int grp_pattern(const Item& it, int g) {
+  return g == 0 ? it.grp[0].pattern : (g == 1 ? it.grp[1].pattern : it.grp[2].pattern);
 }
 
 // bits [lo, lo + 64) of a bitmap (zeros outside [0, 32 * words))
@@ -272,7 +279,6 @@ struct TileMeta {
   uint32_t sw[8];
   int32_t keys[64];
 };
-constexpr int kMetaSlots = 8;
 #ifndef LCX_TC_PREFETCH
 #define LCX_TC_PREFETCH 0
 #endif
@@ -295,6 +301,28 @@ __device__ __forceinline__ void trace_mark(const TcParams& p, uint32_t T, int co
 #endif
 }
 static_assert(sizeof(TileMeta) <= 448, "tile metadata slot overflow");
+// wait profile (LCX_TC_WAITPROF, tools/trace_wait.py): cycles each role spends per wait
+// site, summed over all CTAs into trace[4096 + role * 8 + site]
+#ifdef LCX_TC_WAITPROF
+#define WAITP(site, ...)                      \
+  do {                                        \
+    const long long _w0 = clock64();          \
+    __VA_ARGS__;                              \
+    wacc[site] += clock64() - _w0;            \
+  } while (0)
+#define WAITP_FLUSH(role)                                                                   \
+  do {                                                                                      \
+    if (lane == 0 && p.trace)                                                               \
+      for (int _j = 0; _j < 8; ++_j)                                                        \
+        atomicAdd(reinterpret_cast<unsigned long long*>(p.trace + 4096 + (role) * 8 + _j),  \
+                  (unsigned long long)wacc[_j]);                                            \
+  } while (0)
+#else
+#define WAITP(site, ...) __VA_ARGS__
+#define WAITP_FLUSH(role) \
+  do {                    \
+  } while (0)
+#endif
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -341,6 +369,10 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
   TileMeta* metas = reinterpret_cast<TileMeta*>(smem + OFF_META);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef LCX_TC_WAITPROF
+  long long wacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long t_start = clock64();
+#endif
   if (threadIdx.x == 0) {
     for (int b = 0; b < NK; ++b) {
       tc::mbar_init(k_full + b, 1);
@@ -378,52 +410,21 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
   const uint32_t tmem = *tmem_slot;
 
   if (warp == kWarpProducer) {
-    // ============================ producer: tile stream + metadata + TMA ====
-    // Tiles are processed in batches of 4 so that every global load of a batch
-    // (tile list entries, bitmap windows, compacted keys) is in flight at once.
+    // ============================ producer: tile stream + metadata + K loads ====
+    // Batches of 4 tiles, one lane per tile: lane j resolves tile j (tile-list entry,
+    // bitmap window), waits for nothing but its slot, writes the tile's record into the
+    // metadata ring, publishes it and issues its K loads -- the batch's global loads and
+    // its four ring slots are all in flight at once.
     uint32_t T = 0, M = 0;
-    auto next_slot = [&]() -> TileMeta& {
-      const int slot = M % kMetaSlots;
-      tc::mbar_wait(m_empty + slot, ((M / kMetaSlots) & 1) ^ 1);
-      return metas[slot];
-    };
-    auto publish = [&]() {
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(m_full + (M % kMetaSlots));
-      ++M;
-    };
-    // L2 prefetch cursor kPrefetchLead tiles ahead of the load cursor (into the next
-    // item of this CTA near the end of an item): far slash tiles are single-use DRAM
-    // reads whose latency the 4 K / V stages alone do not cover
     const Item* plans = reinterpret_cast<const Item*>(p.plans);
-    auto prefetch_tile = [&](const Item& pi, int t) {
-      const Tile pt = get_tile(p, pi, t);
-      if (pt.kind == T_VERT) {
-        const int tile = int((int64_t(pi.h) * (p.capp / 64) + pt.key0 / 64) * 2);
-        tc::tma_prefetch_l2_3d(&map_kc_hi, 0, 0, tile);
-        tc::tma_prefetch_l2_3d(&map_kc_hi, 0, 0, tile + 1);
-        tc::tma_prefetch_l2_3d(&map_kc_lo, 0, 0, tile);
-        tc::tma_prefetch_l2_3d(&map_kc_lo, 0, 0, tile + 1);
-        tc::tma_prefetch_l2_3d(&map_vct, 0, 0, tile / 2);
-      } else {
-        const int tile = int((int64_t(pi.g) * p.ntiles_k + pt.key0 / 64) * 2);
-        tc::tma_prefetch_l2_3d(&map_k_hi, 0, 0, tile);
-        tc::tma_prefetch_l2_3d(&map_k_hi, 0, 0, tile + 1);
-        tc::tma_prefetch_l2_3d(&map_k_lo, 0, 0, tile);
-        tc::tma_prefetch_l2_3d(&map_k_lo, 0, 0, tile + 1);
-        tc::tma_prefetch_l2_3d(&map_vt, 0, 0, tile / 2);
-      }
+    auto slot_wait = [&](uint32_t mm) {
+      WAITP(0, tc::mbar_wait(m_empty + int(mm % kMetaSlots), ((mm / kMetaSlots) & 1) ^ 1));
     };
     for (int item = blockIdx.x; item < p.nitems; item += gridDim.x) {
       const Item it = plans[item];
-      const bool has_next = item + int(gridDim.x) < p.nitems;
-      Item nit{};
-      if (kPrefetchLead > 0 && has_next) nit = plans[item + gridDim.x];
-      if (kPrefetchLead > 0 && item == int(blockIdx.x) && lane < kPrefetchLead &&
-          lane < it.ntiles)
-        prefetch_tile(it, lane);  // first item: its head tiles
       if (it.ntiles == 0) {
-        TileMeta& mt = next_slot();
+        slot_wait(M);
+        TileMeta& mt = metas[M % kMetaSlots];
         if (lane == 0) {
           mt.kind = T_EMPTY;
           mt.flags = F_FIRST | F_LAST;
@@ -431,144 +432,140 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           mt.i0 = it.i0;
           mt.rend = it.rend;
         }
-        publish();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(m_full + int(M % kMetaSlots));
+        ++M;
         continue;
       }
-      int prev_grp = -1;
+      int carry_grp = -1;
       for (int tb = 0; tb < it.ntiles; tb += 4) {
         const int nb = min(4, it.ntiles - tb);
-        // A: lane j (j <= nb) resolves tile tb + j (one tile-list load each, in parallel)
+        // A: lane j <= nb resolves tile tb + j (lane nb: the next tile's group)
         Tile my{};
         my.grp = -1;
+        my.kind = -1;
         if (lane <= nb && tb + lane < it.ntiles) my = get_tile(p, it, tb + lane);
-        int kinds[5], grps[5], counts[4];
-        int64_t key0s[4];
-#pragma unroll
-        for (int j = 0; j < 5; ++j) {
-          kinds[j] = __shfl_sync(0xffffffffu, my.kind, j);
-          grps[j] = __shfl_sync(0xffffffffu, my.grp, j);
-          if (j < 4) {
-            counts[j] = __shfl_sync(0xffffffffu, my.count, j);
-            key0s[j] = __shfl_sync(0xffffffffu, (long long)my.key0, j);
-          }
-        }
-        // L2 prefetch of tiles tb + kPrefetchLead + [0, 4) (lanes 8..11)
-        if (kPrefetchLead > 0 && lane >= 8 && lane < 12) {
-          const int t = tb + kPrefetchLead + (lane - 8);
-          if (t < it.ntiles) prefetch_tile(it, t);
-          else if (has_next && t - it.ntiles < nit.ntiles) prefetch_tile(nit, t - it.ntiles);
-        }
-        // B: all loads of the batch
-        const int jj = lane >> 3, w = lane & 7;
-        uint32_t swv = 0, vbv = 0;
-        int64_t wbase = 0;
-        if (jj < nb && kinds[jj] == T_SLASH) {
-          const int64_t lo = it.i0 - key0s[jj] - 63;
-          wbase = lo >= 0 ? (lo >> 5) : -((-lo + 31) >> 5);
-          const int64_t wi = wbase + w;
-          const uint32_t* sb = p.sbits + int64_t(it.h) * p.words;
-          swv = (wi >= 0 && wi < p.words) ? sb[wi] : 0u;
-          if (w < 2) {
-            const int64_t kw = (key0s[jj] >> 5) + w;
-            vbv = kw < p.words ? p.vbits[int64_t(it.h) * p.words + kw] : 0u;
-          }
-        }
-        int32_t ck[4][2];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          ck[j][0] = ck[j][1] = -1;
-          if (j < nb && kinds[j] == T_VERT) {
-            const int32_t* c = p.ckeys + int64_t(it.h) * p.capp + key0s[j];
-            if (lane < counts[j]) ck[j][0] = c[lane];
-            if (lane + 32 < counts[j]) ck[j][1] = c[lane + 32];
-          }
-        }
-        // C: publish the metadata, then issue the TMA loads
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (j >= nb) break;
-          const int t = tb + j;
-          int flags = 0;
+        const int up_grp = __shfl_up_sync(0xffffffffu, my.grp, 1);
+        const int dn_grp = __shfl_down_sync(0xffffffffu, my.grp, 1);
+        const int prev_grp = lane == 0 ? carry_grp : up_grp;
+        carry_grp = __shfl_sync(0xffffffffu, my.grp, nb - 1);
+        // B: lane j < nb builds its tile's record (SLASH: the 256-bit diagonal window)
+        const int t = tb + lane;
+        int flags = 0, pattern = 0, next_pattern = 0;
+        uint32_t swv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        uint64_t vmask = 0;
+        int64_t sbase = 0;
+        if (lane < nb) {
           if (t == 0) flags |= F_FIRST;
-          if (grps[j] != prev_grp) flags |= F_EPOCH;
+          if (my.grp != prev_grp) flags |= F_EPOCH;
           if (t + 1 == it.ntiles) flags |= F_LAST;
-          else if (grps[j + 1] != grps[j]) flags |= F_EPOCH_AFTER;
-          prev_grp = grps[j];
-          TileMeta& mt = next_slot();
-          const uint32_t sw_j = __shfl_sync(0xffffffffu, swv, 8 * j + (lane & 7));
-          const uint32_t vb0 = __shfl_sync(0xffffffffu, vbv, 8 * j);
-          const uint32_t vb1 = __shfl_sync(0xffffffffu, vbv, 8 * j + 1);
-          const long long wb_j = __shfl_sync(0xffffffffu, (long long)wbase, 8 * j);
-          if (kinds[j] == T_SLASH && lane < 8) mt.sw[lane] = sw_j;
-          if (kinds[j] == T_VERT) {
-            mt.keys[lane] = ck[j][0];
-            mt.keys[lane + 32] = ck[j][1];
-            const unsigned f0 =
-                __ballot_sync(0xffffffffu, ck[j][0] >= 0 && int64_t(ck[j][0]) < it.i0);
-            const unsigned f1 =
-                __ballot_sync(0xffffffffu, ck[j][1] >= 0 && int64_t(ck[j][1]) < it.i0);
-            if (lane == 0) mt.nfar = __popc(f0) + __popc(f1);
+          else if (dn_grp != my.grp) flags |= F_EPOCH_AFTER;
+          pattern = grp_pattern(it, my.grp);
+          next_pattern = (flags & F_EPOCH_AFTER) ? grp_pattern(it, dn_grp) : 0;
+          if (my.kind == T_SLASH) {
+            const int64_t lo = it.i0 - my.key0 - 63;
+            const int64_t wbase = lo >= 0 ? (lo >> 5) : -((-lo + 31) >> 5);
+            sbase = wbase * 32;
+            const uint32_t* sb = p.sbits + int64_t(it.h) * p.words;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+              const int64_t wi = wbase + w;
+              swv[w] = (wi >= 0 && wi < p.words) ? sb[wi] : 0u;
+            }
+            const uint32_t* vb = p.vbits + int64_t(it.h) * p.words;
+            const int64_t kw = my.key0 >> 5;
+            const uint32_t v0 = kw < p.words ? vb[kw] : 0u;
+            const uint32_t v1 = kw + 1 < p.words ? vb[kw + 1] : 0u;
+            vmask = uint64_t(v0) | (uint64_t(v1) << 32);
           }
-          if (lane == 0) {
-            mt.kind = kinds[j];
-            mt.flags = flags;
-            mt.pattern = it.grp[grps[j]].pattern;
-            mt.next_pattern = (flags & F_EPOCH_AFTER) ? it.grp[grps[j + 1]].pattern : 0;
-            mt.h = it.h;
-            mt.count = counts[j];
-            mt.i0 = it.i0;
-            mt.rend = it.rend;
-            mt.key0 = key0s[j];
-            mt.sbase = wb_j * 32;
-            mt.vmask = uint64_t(vb0) | (uint64_t(vb1) << 32);
+        }
+        // C: the batch's ring slots, then every lane writes its record; vertical tiles'
+        // key lists are written warp-wide
+        for (int j = 0; j < nb; ++j) slot_wait(M + j);
+        if (lane < nb) {
+          TileMeta& mt = metas[(M + lane) % kMetaSlots];
+          mt.kind = my.kind;
+          mt.flags = flags;
+          mt.pattern = pattern;
+          mt.next_pattern = next_pattern;
+          mt.h = it.h;
+          mt.count = my.count;
+          mt.i0 = it.i0;
+          mt.rend = it.rend;
+          mt.key0 = my.key0;
+          mt.sbase = sbase;
+          mt.vmask = vmask;
+          if (my.kind == T_SLASH) {
+#pragma unroll
+            for (int w = 0; w < 8; ++w) mt.sw[w] = swv[w];
           }
-          publish();
-          if (lane == 0) {
+        }
+        for (int j = 0; j < nb; ++j) {
+          if (__shfl_sync(0xffffffffu, my.kind, j) != T_VERT) continue;
+          const long long key0j = __shfl_sync(0xffffffffu, (long long)my.key0, j);
+          const int countj = __shfl_sync(0xffffffffu, my.count, j);
+          const int32_t* c = p.ckeys + int64_t(it.h) * p.capp + key0j;
+          const int32_t k0 = lane < countj ? c[lane] : -1;
+          const int32_t k1 = lane + 32 < countj ? c[lane + 32] : -1;
+          TileMeta& mt = metas[(M + j) % kMetaSlots];
+          mt.keys[lane] = k0;
+          mt.keys[lane + 32] = k1;
+          const unsigned f0 = __ballot_sync(0xffffffffu, k0 >= 0 && int64_t(k0) < it.i0);
+          const unsigned f1 = __ballot_sync(0xffffffffu, k1 >= 0 && int64_t(k1) < it.i0);
+          if (lane == 0) mt.nfar = __popc(f0) + __popc(f1);
+        }
+        // D: publish (lane j: slot of tile j), then lane j issues tile j's K loads
+        __syncwarp();
+        if (lane < nb) {
+          tc::mbar_arrive(m_full + int((M + lane) % kMetaSlots));
+          const uint32_t Tj = T + lane;
 #if !defined(LCX_TC_TRACE_PV) && !defined(LCX_TC_TRACE_SM)
-            trace_mark(p, T, 0);
+          trace_mark(p, Tj, 0);
 #endif
-            const int bk = T % NK;
-            const uint32_t phk = (T / NK) & 1;
-            tc::mbar_wait(k_empty + bk, phk ^ 1);
-            tc::mbar_expect_tx(k_full + bk, kKStage);
-            const uint32_t kdst = smem_base + OFF_K + bk * kKStage;
-            const int tile = kinds[j] == T_VERT
-                                 ? int((int64_t(it.h) * (p.capp / 64) + key0s[j] / 64) * 2)
-                                 : int((int64_t(it.g) * p.ntiles_k + key0s[j] / 64) * 2);
+          const int bk = Tj % NK;
+          WAITP(1, tc::mbar_wait(k_empty + bk, ((Tj / NK) & 1) ^ 1));
+          tc::mbar_expect_tx(k_full + bk, kKStage);
+          const uint32_t kdst = smem_base + OFF_K + bk * kKStage;
+          int tile = my.kind == T_VERT ? int((int64_t(it.h) * (p.capp / 64) + my.key0 / 64) * 2)
+                                       : int((int64_t(it.g) * p.ntiles_k + my.key0 / 64) * 2);
 #ifdef LCX_TC_FAKE_LOADS  // timing experiment only: every tile loads from a small L2-resident set
-            const_cast<int&>(tile) = (tile & 62);
+          tile &= 62;
 #endif
 #if LCX_TC_BULK
-            // pre-swizzled tiles: hi (2 halves) and lo are one contiguous 16 KB run each
-            const __nv_bfloat16* sh = kinds[j] == T_VERT ? p.kchi : p.khi;
-            const __nv_bfloat16* sl = kinds[j] == T_VERT ? p.kclo : p.klo;
-            tc::bulk_load(kdst, sh + int64_t(tile) * (kKHalf / 2), 2 * kKHalf, k_full + bk);
-            tc::bulk_load(kdst + 2 * kKHalf, sl + int64_t(tile) * (kKHalf / 2), 2 * kKHalf,
-                          k_full + bk);
+          // pre-swizzled tiles: hi (2 halves) and lo are one contiguous 16 KB run each
+          const __nv_bfloat16* sh = my.kind == T_VERT ? p.kchi : p.khi;
+          const __nv_bfloat16* sl = my.kind == T_VERT ? p.kclo : p.klo;
+          tc::bulk_load(kdst, sh + int64_t(tile) * (kKHalf / 2), 2 * kKHalf, k_full + bk);
+          tc::bulk_load(kdst + 2 * kKHalf, sl + int64_t(tile) * (kKHalf / 2), 2 * kKHalf,
+                        k_full + bk);
 #else
-            const CUtensorMap* mh = kinds[j] == T_VERT ? &map_kc_hi : &map_k_hi;
-            const CUtensorMap* ml = kinds[j] == T_VERT ? &map_kc_lo : &map_k_lo;
-            tc::tma_load_3d(kdst + 0 * kKHalf, mh, k_full + bk, 0, 0, tile);
-            tc::tma_load_3d(kdst + 1 * kKHalf, mh, k_full + bk, 0, 0, tile + 1);
-            tc::tma_load_3d(kdst + 2 * kKHalf, ml, k_full + bk, 0, 0, tile);
-            tc::tma_load_3d(kdst + 3 * kKHalf, ml, k_full + bk, 0, 0, tile + 1);
+          const CUtensorMap* mh = my.kind == T_VERT ? &map_kc_hi : &map_k_hi;
+          const CUtensorMap* ml = my.kind == T_VERT ? &map_kc_lo : &map_k_lo;
+          tc::tma_load_3d(kdst + 0 * kKHalf, mh, k_full + bk, 0, 0, tile);
+          tc::tma_load_3d(kdst + 1 * kKHalf, mh, k_full + bk, 0, 0, tile + 1);
+          tc::tma_load_3d(kdst + 2 * kKHalf, ml, k_full + bk, 0, 0, tile);
+          tc::tma_load_3d(kdst + 3 * kKHalf, ml, k_full + bk, 0, 0, tile + 1);
 #endif
 #if !defined(LCX_TC_TRACE_PV) && !defined(LCX_TC_TRACE_SM)
-            trace_mark(p, T, 1);
+          trace_mark(p, Tj, 1);
 #endif
-          }
-          __syncwarp();
-          ++T;
         }
+        __syncwarp();
+        M += nb;
+        T += nb;
       }
     }
-    {
-      TileMeta& mt = next_slot();
-      if (lane == 0) mt.kind = T_END;
-      publish();
-    }
+    slot_wait(M);
+    if (lane == 0) metas[M % kMetaSlots].kind = T_END;
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(m_full + int(M % kMetaSlots));
+    ++M;
     if (lane == 0 && p.tile_count)
       atomicAdd(reinterpret_cast<unsigned long long*>(p.tile_count), (unsigned long long)T);
+#ifdef LCX_TC_WAITPROF
+    wacc[7] = clock64() - t_start;
+#endif
+    WAITP_FLUSH(0);
   } else if (warp == kWarpMma) {
     // ==================================================== QK issuer ====
     uint32_t T = 0, E = 0, M = 0;
@@ -576,7 +573,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     const uint64_t dk0 = tc::sdesc_sw128(tc::smem_u32(smem + OFF_K));
     for (;;) {
       const int slot = M % kMetaSlots;
-      tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1);
+      WAITP(0, tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1));
       const int kind = metas[slot].kind;
       const int flags = metas[slot].flags;
       __syncwarp();
@@ -585,18 +582,21 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       if (kind == T_END) break;
       if (kind == T_EMPTY) continue;
       if (flags & F_EPOCH) {
-        tc::mbar_wait(q_ready, E & 1);
+        WAITP(1, tc::mbar_wait(q_ready, E & 1));
         ++E;
       }
       const int bk = T % NK, bs = T % NS;
-      tc::mbar_wait(k_full + bk, (T / NK) & 1);
-      tc::mbar_wait(s_free + bs, ((T / NS) & 1) ^ 1);  // PV(T - NS) released S/P buffer
+      WAITP(2, tc::mbar_wait(k_full + bk, (T / NK) & 1));
+      WAITP(3, tc::mbar_wait(s_free + bs, ((T / NS) & 1) ^ 1));  // PV(T - NS) released S/P
       tc::tc_fence_after();
 #ifndef LCX_TC_TRACE_PV
       if (lane == 0) trace_mark(p, T, 7);
 #endif
       const uint64_t dk = dk0 + ((bk * kKStage) >> 4);
       const uint32_t dS = tmem + bs * BN;
+#ifdef LCX_TC_WAITPROF
+      const long long t_iss = clock64();
+#endif
 #pragma unroll
 #ifdef LCX_TC_ONE_TERM  // timing experiment only: hi.hi product alone
       for (int combo = 0; combo < 1; ++combo) {
@@ -615,17 +615,24 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       }
       tc::mma_commit_warp(k_empty + bk);
       tc::mma_commit_warp(s_full + bs);
+#ifdef LCX_TC_WAITPROF
+      wacc[4] += clock64() - t_iss;
+#endif
 #ifndef LCX_TC_TRACE_PV
       if (lane == 0) trace_mark(p, T, 3);
 #endif
       ++T;
     }
+#ifdef LCX_TC_WAITPROF
+    wacc[7] = clock64() - t_start;
+#endif
+    WAITP_FLUSH(1);
   } else if (warp == kWarpV) {
     // ===================================================== V TMA loads ====
     uint32_t T = 0, M = 0;
     for (;;) {
       const int slot = M % kMetaSlots;
-      tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1);
+      WAITP(0, tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1));
       const int kind = metas[slot].kind;
       const int h = metas[slot].h;
       const int key0 = int(metas[slot].key0);
@@ -636,7 +643,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       if (kind == T_EMPTY) continue;
       if (lane == 0) {
         const int bv = T % NV;
-        tc::mbar_wait(v_empty + bv, ((T / NV) & 1) ^ 1);
+        WAITP(1, tc::mbar_wait(v_empty + bv, ((T / NV) & 1) ^ 1));
         tc::mbar_expect_tx(v_full + bv, kVStage);
         const uint32_t vdst = smem_base + OFF_V + bv * kVStage;
         const int64_t vtile = kind == T_VERT ? int64_t(h) * (p.capp / 64) + key0 / 64
@@ -657,13 +664,17 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       __syncwarp();
       ++T;
     }
+#ifdef LCX_TC_WAITPROF
+    wacc[7] = clock64() - t_start;
+#endif
+    WAITP_FLUSH(2);
   } else if (warp == kWarpPv) {
     // ============================================== PV issuer (O += P V) ====
     uint32_t T = 0, M = 0;
     const uint64_t dv0 = tc::sdesc_sw128(tc::smem_u32(smem + OFF_V));
     for (;;) {
       const int slot = M % kMetaSlots;
-      tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1);
+      WAITP(0, tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1));
 #ifdef LCX_TC_TRACE_PV
       if (lane == 0) trace_mark(p, T, 0);
 #endif
@@ -675,11 +686,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       if (kind == T_END) break;
       if (kind == T_EMPTY) continue;
       const int bs = T % NS, bv = T % NV;
-      tc::mbar_wait(p_full + bs, (T / NS) & 1);
+      WAITP(1, tc::mbar_wait(p_full + bs, (T / NS) & 1));
 #ifdef LCX_TC_TRACE_PV  // columns 0 / 1 / 2: PV issuer passed the meta / P / V waits
       if (lane == 0) trace_mark(p, T, 1);
 #endif
-      tc::mbar_wait(v_full + bv, (T / NV) & 1);
+      WAITP(2, tc::mbar_wait(v_full + bv, (T / NV) & 1));
 #ifdef LCX_TC_TRACE_PV
       if (lane == 0) trace_mark(p, T, 2);
 #endif
@@ -695,6 +706,10 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       if (lane == 0) trace_mark(p, T, 4);
       ++T;
     }
+#ifdef LCX_TC_WAITPROF
+    wacc[7] = clock64() - t_start;
+#endif
+    WAITP_FLUSH(3);
   } else {
     // ============================= softmax / correction / epilogue ====
     // Two warp groups take alternate tiles of the stream (group g: tiles T with
@@ -728,12 +743,12 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     };
     for (;;) {
       const int slot = M % kMetaSlots;
-      tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1);
+      WAITP(0, tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1));
       const TileMeta& mt = metas[slot];
       const int kind = mt.kind, flags = mt.flags;
       if (kind == T_END) {
         if ((T & 1) == uint32_t(grp))  // match the last tile's hand-off (or the initial one)
-          asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
+          WAITP(2, asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory"));
         break;
       }
       const int64_t i0 = mt.i0, rend = mt.rend;
@@ -785,7 +800,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       if (flags & F_FIRST) {
         // the other group's epilogue of the previous item (its last tile, T - 1) has read
         // O and S(T - 1) is consumed, so O / Q of this CTA's TMEM are free
-        asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
+        WAITP(2, asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory"));
         tc::tc_fence_after();
         m_init = -INFINITY;
         if (p.init) {
@@ -817,7 +832,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       const int b = T % NS;
       const uint32_t ph = (T / NS) & 1;
       float sv[64];
-      tc::mbar_wait(s_full + b, ph);
+      WAITP(1, tc::mbar_wait(s_full + b, ph));
       tc::tc_fence_after();
       tc::tmem_ld32(tmem + lane_base + b * BN, sv);
       tc::tmem_ld32(tmem + lane_base + b * BN + 32, sv + 32);
@@ -826,6 +841,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       if (wq == 0 && lane == 0) trace_mark(p, T, 5);
 #else
       if (threadIdx.x == 0) trace_mark(p, T, 5);
+#endif
+#ifdef LCX_TC_WAITPROF
+      const long long t_sg = clock64();
 #endif
       if (flags & F_EPOCH_AFTER) rotate_row(next_pattern);  // the old pattern's QKs are done
 #ifdef LCX_TC_FAKE_SOFTMAX  // timing experiment only: no softmax math
@@ -847,6 +865,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #pragma unroll
         for (int u = 0; u < 4; ++u) t4[u] = fmaxf(t4[u], fmaxf(sv[cc + u], sv[cc + 4 + u]));
       const float tmax = fmaxf(fmaxf(t4[0], t4[1]), fmaxf(t4[2], t4[3]));
+#ifdef LCX_TC_WAITPROF
+      wacc[5] += clock64() - t_sg;
+#endif
       // ---- running max: previous tile's (other group) unless the item starts here
       if (!(flags & F_FIRST)) asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
       const float m_prev = (flags & F_FIRST) ? m_init : mbuf[((T - 1) & 1) * 128 + r];
@@ -864,10 +885,13 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #endif
       // an item's last tile hands over only after its epilogue (next item's O / Q)
       if (!(flags & F_LAST)) asm volatile("bar.arrive %0, 64;" ::"r"(bar_out) : "memory");
+#ifdef LCX_TC_WAITPROF
+      const long long t_ex = clock64();
+#endif
       if (__any_sync(0xffffffffu, need && m_prev != -INFINITY)) {
         // O holds PV up to tile T - 1 at max m_prev: complete it, then rescale
         const uint32_t Tp = T - 1;
-        tc::mbar_wait(s_free + (Tp % NS), (Tp / NS) & 1);
+        WAITP(3, tc::mbar_wait(s_free + (Tp % NS), (Tp / NS) & 1));
         tc::tc_fence_after();
         const float f = (need && m_prev != -INFINITY) ? ex2(m_prev - m) : 1.f;
 #pragma unroll 1
@@ -910,6 +934,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(p_full + b);
+#ifdef LCX_TC_WAITPROF
+      wacc[6] += clock64() - t_ex;
+#endif
 #ifdef LCX_TC_TRACE_SM
       if (wq == 0 && lane == 0) trace_mark(p, T, 6);
 #else
@@ -921,11 +948,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         float lt = l;
         if (!(flags & F_FIRST)) {
           const uint32_t To = T - 1;  // the other group's last tile of this item
-          tc::mbar_wait(p_full + (To % NS), (To / NS) & 1);
+          WAITP(4, tc::mbar_wait(p_full + (To % NS), (To / NS) & 1));
           const float2 lo = lbuf[(((To >> 1) & 1) * 2 + (grp ^ 1)) * 128 + r];
           if (lo.x > 0.f) lt += lo.x * ex2(lo.y - m);
         }
-        tc::mbar_wait(s_free + b, ph);  // this item's last PV is complete
+        WAITP(4, tc::mbar_wait(s_free + b, ph));  // this item's last PV is complete
         tc::tc_fence_after();
         const float inv = lt > 0.f ? 1.f / lt : 0.f;
         float4* o = reinterpret_cast<float4*>(p.out + (i * p.hq + h) * int64_t(HD));
@@ -949,6 +976,10 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       }
       ++T;
     }
+#ifdef LCX_TC_WAITPROF
+    wacc[7] = clock64() - t_start;
+#endif
+    if (wq == 0) WAITP_FLUSH(4);
   }
   tc::tc_fence_before();
   __syncthreads();

@@ -562,7 +562,7 @@ int lcx_set_profiling(lcx_context* ctx, int enabled) {
 }
 
 int lcx_debug_trace(lcx_context* ctx, int enable, long long* host_out) {
-  const size_t bytes = 512 * 8 * sizeof(long long);
+  const size_t bytes = (512 * 8 + 64) * sizeof(long long);  // per-tile marks + wait profile
   if (enable && !ctx->trace) {
     LCX_CHECK_CUDA(cudaMalloc(&ctx->trace, bytes));
     LCX_CHECK_CUDA(cudaMemset(ctx->trace, 0, bytes));
