@@ -748,7 +748,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       const int kind = mt.kind, flags = mt.flags;
       if (kind == T_END) {
         if ((T & 1) == uint32_t(grp))  // match the last tile's hand-off (or the initial one)
-          WAITP(2, asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory"));
+          asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
         break;
       }
       const int64_t i0 = mt.i0, rend = mt.rend;
@@ -800,7 +800,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       if (flags & F_FIRST) {
         // the other group's epilogue of the previous item (its last tile, T - 1) has read
         // O and S(T - 1) is consumed, so O / Q of this CTA's TMEM are free
-        WAITP(2, asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory"));
+        asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
         tc::tc_fence_after();
         m_init = -INFINITY;
         if (p.init) {
@@ -827,7 +827,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           }
           tc::tmem_wait_st();
         }
-        rotate_row(pattern);
+        WAITP(2, rotate_row(pattern));
       }
       const int b = T % NS;
       const uint32_t ph = (T / NS) & 1;
@@ -845,7 +845,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #ifdef LCX_TC_WAITPROF
       const long long t_sg = clock64();
 #endif
-      if (flags & F_EPOCH_AFTER) rotate_row(next_pattern);  // the old pattern's QKs are done
+      if (flags & F_EPOCH_AFTER) WAITP(2, rotate_row(next_pattern));  // old pattern's QKs done
 #ifdef LCX_TC_FAKE_SOFTMAX  // timing experiment only: no softmax math
       for (int cc = 0; cc < 64; ++cc) sv[cc] = -INFINITY;
       mask = ~0ull;
