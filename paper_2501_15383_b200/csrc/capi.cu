@@ -97,6 +97,11 @@ __global__ void shard_lists_kernel(const int32_t* __restrict__ v, const int32_t*
 }
 
 // far[0] += slashes with d >= far_d, far[1] += all slashes (over heads)
+__global__ void store_ints_kernel(const int* __restrict__ src, int* dst, int count) {
+  if (int(threadIdx.x) < count) dst[threadIdx.x] = src[threadIdx.x];
+  __threadfence_system();
+}
+
 __global__ void far_count_kernel(const int32_t* __restrict__ sl, const int32_t* __restrict__ ns,
                                  int64_t cap_s, int64_t far_d, int* far) {
   const int h = blockIdx.x;  // one block per head
@@ -531,7 +536,8 @@ int lcx_context_create(int device, lcx_context** out) {
   ctx->sm_count = prop.multiProcessorCount;
   LCX_CHECK_CUDA(cudaMalloc(&ctx->tile_counter, 2 * sizeof(int64_t)));
   LCX_CHECK_CUDA(cudaMalloc(&ctx->far_dev, 2 * sizeof(int)));
-  LCX_CHECK_CUDA(cudaMallocHost(&ctx->far_host, 4 * sizeof(int)));
+  LCX_CHECK_CUDA(cudaHostAlloc(&ctx->far_host, 4 * sizeof(int), cudaHostAllocMapped));
+  LCX_CHECK_CUDA(cudaHostGetDevicePointer(&ctx->far_host_dev, ctx->far_host, 0));
   for (auto& e : ctx->far_ev) LCX_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   LCX_CHECK_CUDA(cudaMemset(ctx->tile_counter, 0, 2 * sizeof(int64_t)));
   *out = ctx;
@@ -1088,8 +1094,10 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
         LCX_CHECK_CUDA(cudaMemsetAsync(ctx->far_dev, 0, 2 * sizeof(int), st));
         far_count_kernel<<<hq, 256, 0, st>>>(slist, scnt, cap_s, kTcSegment, ctx->far_dev);
         LCX_CHECK_LAUNCH();
-        LCX_CHECK_CUDA(cudaMemcpyAsync(ctx->far_host + 2 * (ci & 1), ctx->far_dev, 2 * sizeof(int),
-                                       cudaMemcpyDeviceToHost, st));
+        // stored into mapped host memory by a kernel, not a D2H copy: on the host entry the
+        // copy engine is busy with the output rows and a copy on this stream would wait
+        store_ints_kernel<<<1, 32, 0, st>>>(ctx->far_dev, ctx->far_host_dev + 2 * (ci & 1), 2);
+        LCX_CHECK_LAUNCH();
         LCX_CHECK_CUDA(cudaEventRecord(ctx->far_ev[ci & 1], st));
       }
     }

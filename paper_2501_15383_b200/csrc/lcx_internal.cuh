@@ -127,7 +127,9 @@ struct lcx_context {
   cudaStream_t h2d = nullptr, d2h = nullptr;
   // key-window decision of chunked prefill: far-slash counts of the last two chunks
   int* far_dev = nullptr;        // device [2]
-  int* far_host = nullptr;       // pinned [2][2]
+  int* far_host = nullptr;       // pinned, mapped [2][2]
+  int* far_host_dev = nullptr;   // device alias of far_host (written by a kernel: no copy
+                                 // engine, so it never queues behind the host entry's D2H)
   cudaEvent_t far_ev[2] = {nullptr, nullptr};
 };
 
