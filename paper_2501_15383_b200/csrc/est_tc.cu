@@ -270,15 +270,12 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
             float acc = 0.f;
             const float* col = Tb + ch * 64 * 65 + c;
             if (p.block == 64) {
-              float a2 = 0.f, a3 = 0.f, a4 = 0.f;  // fixed trip count: unrolled, 4 chains
-#pragma unroll 16
-              for (int q = 0; q < 64; q += 4) {
-                acc += col[q * 65];
-                a2 += col[(q + 1) * 65];
-                a3 += col[(q + 2) * 65];
-                a4 += col[(q + 3) * 65];
-              }
-              acc = (acc + a2) + (a3 + a4);
+              float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 chains, all loads up front
+#pragma unroll
+              for (int q = 0; q < 64; q += 8)
+#pragma unroll
+                for (int u = 0; u < 8; ++u) a[u] += col[(q + u) * 65];
+              acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
             } else {
               for (int q = 0; q < p.block; ++q) acc += col[q * 65];
             }
@@ -290,22 +287,23 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
           const int dh = et >> 7, e = et & 127;
           const int hd = g * p.group + (it.pair % p.pairs_per_group) * 2 + dh;
           if ((it.pair % p.pairs_per_group) * 2 + dh < p.group && e < 127) {
-            float acc = 0.f;
             const int q0 = e > 63 ? e - 63 : 0;
             const int q1 = min(p.block - 1, e);
             // diagonal e walks T with stride 66 (= row 65 + column 1); zeros past the
-            // estimator rows make the fixed-count form exact
+            // estimator rows make the fixed-count form exact.  Fixed trip count with
+            // predicated adds (8 independent chains, every load in flight at once); reads
+            // past the diagonal stay inside the Q staging area and are discarded.
             const float* dg = Tb + (dh * 64 + q0) * 65 + (q0 - e + 63);
             const int cnt = q1 - q0 + 1;
-            float a2 = 0.f;
-            int q = 0;
-#pragma unroll 4
-            for (; q + 1 < cnt; q += 2) {
-              acc += dg[q * 66];
-              a2 += dg[(q + 1) * 66];
-            }
-            if (q < cnt) acc += dg[q * 66];
-            acc += a2;
+            float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int q = 0; q < 64; q += 8)
+#pragma unroll
+              for (int u = 0; u < 8; ++u) {
+                const float x = dg[(q + u) * 66];
+                a[u] += (q + u < cnt) ? x : 0.f;
+              }
+            const float acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
             p.diag_part[(int64_t(hd) * p.ntiles + it.t0 + t) * 128 + e] = acc;
           }
         }

@@ -22,6 +22,7 @@ ap.add_argument("--s", type=int, default=131072)
 ap.add_argument("--c", type=int, default=262144)
 ap.add_argument("--path", default="auto")
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--tc-min", type=int, nargs="+", default=[0], help="tc_min_entries sweep (0 = default)")
 a = ap.parse_args()
 budgets = a.budget or [[1000, 6096]]
 ctx = context(0)
@@ -31,6 +32,7 @@ for n in a.n:
         dca = (a.s, a.c, min(a.s, a.c - a.s))
         temp = yarn_temperature(n / a.c)
         for bv, bs in budgets:
+          for tcm in a.tc_min:
             for rep in range(a.reps):
                 ctx.set_profiling(True)
                 torch.cuda.synchronize()
@@ -38,7 +40,7 @@ for n in a.n:
                 r = D.chunked_prefill(q, k, v, chunk_len=a.chunk, last_q=64, budget=(bv, bs),
                                       position_mode="dca_continuous", dca=dca, temperature=temp,
                                       rope_base=1e7, kernel_path=a.path, return_admitted=True,
-                                      return_selections=True)
+                                      return_selections=True, tc_min_entries=tcm)
                 torch.cuda.synchronize()
                 wall = time.time() - t
                 st = ctx.stats()
@@ -47,7 +49,7 @@ for n in a.n:
                 sl = r["slashes"]
                 # slash spread: fraction of selected offsets < 8192
                 near = float((sl[..., :] < 8192).float().mean().item())
-                out = dict(n=n, kind=kind, budget=[bv, bs], wall_s=round(wall, 3),
+                out = dict(n=n, kind=kind, budget=[bv, bs], tc_min=tcm, wall_s=round(wall, 3),
                            E=E, tok_s=round(n / wall), simt_entries=st["simt_entries"],
                            tc_tiles=st["tc_tiles"], launches=st["launches"],
                            ms=dict(est=round(st["ms_estimate"], 2), sel=round(st["ms_select"], 2),
