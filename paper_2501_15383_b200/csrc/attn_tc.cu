@@ -51,7 +51,9 @@ constexpr int BM = 128, BN = 64, HD = 128;
 constexpr int kThreads = 384;
 constexpr int kSoftmaxWarps = 8;
 constexpr int kWarpProducer = 8, kWarpMma = 9, kWarpPv = 10, kWarpV = 11;
-constexpr int NK = 4, NV = 4, NS = 4;                // K / V smem stages, S (+P) TMEM buffers
+// two S buffers suffice (NS = 2, 3, 4 measure the same); the TMEM they free holds a
+// second rotated Q, so the Q of the next DCA pattern is in place before its first QK
+constexpr int NK = 4, NV = 4, NS = 2;                // K / V smem stages, S (+P) TMEM buffers
 constexpr uint32_t kKHalf = BN * 64 * 2;             // 8 KB
 constexpr uint32_t kKStage = 4 * kKHalf;             // hi0 hi1 lo0 lo1 = 32 KB
 constexpr uint32_t kVStage = HD * BN * 2;            // 16 KB
@@ -64,13 +66,14 @@ constexpr int kMetaSlots = 16;                      // tile metadata ring (448 B
 // (l, m) [2 slot][2 warp group][128]
 constexpr uint32_t OFF_RED = OFF_META + kMetaSlots * 448;
 constexpr uint32_t kSmemBytes = OFF_RED + 2 * 128 * 4 + 2 * 2 * 128 * 8 + 1024;  // + align slack
-// TMEM (512 columns x 128 lanes): S/P buffers [0, 256), O [256, 384), rotated
-// Q hi [384, 448) and lo [448, 512) as the A operand of every QK MMA (bf16 pairs
-// per 32-bit column), so all MMAs read only B from shared memory.
+// TMEM (512 columns x 128 lanes): S/P buffers [0, 128), O [128, 256), two rotated Q
+// buffers [256, 384) and [384, 512) (hi, then lo; bf16 pairs per 32-bit column) as
+// the A operand of every QK MMA, so all MMAs read only B from shared memory.  DCA
+// pattern group x of an item uses Q buffer x & 1.
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t COL_O = NS * BN;
-constexpr uint32_t COL_QHI = COL_O + HD;
-constexpr uint32_t COL_QLO = COL_QHI + HD / 2;
+constexpr uint32_t COL_Q = COL_O + HD;  // Q buffer b: hi at COL_Q + 128 b, lo at + 64
+constexpr uint32_t QBUF = HD;
 constexpr float kRescaleThresh = 8.f;
 
 constexpr uint32_t IDESC_QK = tc::idesc_f16(BM, BN, 1, 1);   // bf16 x bf16
@@ -236,7 +239,7 @@ __device__ __forceinline__ int64_t qpos_of(const TcParams& p, int pattern, int64
 // Rotate this thread's query row (its 64-dim half) by its pattern position and
 // store the bf16 hi / lo split into TMEM (row = lane, dim pair = column).
 __device__ __forceinline__ void rotate_q(const TcParams& p, const Item& it, int pattern, int r,
-                                         int part, uint32_t tmem_row) {
+                                         int part, uint32_t tmem_row, int qbuf) {
   const int64_t i = it.i0 + r;
   const bool ok = i < it.rend;
   const uint4* src = reinterpret_cast<const uint4*>(p.q + (i * p.hq + it.h) * int64_t(HD));
@@ -262,8 +265,9 @@ __device__ __forceinline__ void rotate_q(const TcParams& p, const Item& it, int 
       lo[c8 * 4 + k] = *reinterpret_cast<const uint32_t*>(&l2);
     }
   }
-  tc::tmem_st32(tmem_row + COL_QHI + part * 32, reinterpret_cast<const float*>(hi));
-  tc::tmem_st32(tmem_row + COL_QLO + part * 32, reinterpret_cast<const float*>(lo));
+  const uint32_t qc = tmem_row + COL_Q + qbuf * QBUF;
+  tc::tmem_st32(qc + part * 32, reinterpret_cast<const float*>(hi));
+  tc::tmem_st32(qc + HD / 2 + part * 32, reinterpret_cast<const float*>(lo));
   tc::tmem_wait_st();
 }
 
@@ -273,7 +277,8 @@ enum { T_EMPTY = 3, T_END = 4 };
 enum { F_FIRST = 1, F_LAST = 2, F_EPOCH = 4, F_EPOCH_AFTER = 8 };
 struct TileMeta {
   int32_t kind, flags, pattern, next_pattern;
-  int32_t h, count, nfar, pad;
+  int32_t h, count, nfar, grp;  // grp: the tile's pattern group within its item
+  int32_t gpat[3], ng;          // the item's group patterns and group count
   int64_t i0, rend, key0, sbase;
   uint64_t vmask;
   uint32_t sw[8];
@@ -359,12 +364,12 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
   const tc::SBar s_full = v_empty + NV;        // [NS] QK commit -> softmax
   const tc::SBar s_free = s_full + NS;         // [NS] PV commit (S/P buffer, O updated)
   const tc::SBar p_full = s_free + NS;         // [NS] softmax wrote P -> PV issuer
-  const tc::SBar q_ready = p_full + NS;        // softmax rotated Q -> QK issuer
-  const tc::SBar m_full = q_ready + 1;         // [kMetaSlots]
+  const tc::SBar q_ready = p_full + NS;        // [2] softmax rotated Q buffer b -> QK issuer
+  const tc::SBar m_full = q_ready + 2;         // [kMetaSlots]
   const tc::SBar m_empty = m_full + kMetaSlots;  // [kMetaSlots]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR) +
-                        2 * (2 * NK + 2 * NV + 3 * NS + 1 + 2 * kMetaSlots);
-  static_assert((2 * NK + 2 * NV + 3 * NS + 1 + 2 * kMetaSlots + 1) * 8 <= 512,
+                        2 * (2 * NK + 2 * NV + 3 * NS + 2 + 2 * kMetaSlots);
+  static_assert((2 * NK + 2 * NV + 3 * NS + 2 + 2 * kMetaSlots + 1) * 8 <= 512,
                 "barrier area overflow");
   TileMeta* metas = reinterpret_cast<TileMeta*>(smem + OFF_META);
 
@@ -388,6 +393,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       tc::mbar_init(p_full + b, kSoftmaxWarps / 2);  // the tile's warp group
     }
     tc::mbar_init(q_ready, kSoftmaxWarps / 2);
+    tc::mbar_init(q_ready + 1, kSoftmaxWarps / 2);
     for (int b = 0; b < kMetaSlots; ++b) {
       tc::mbar_init(m_full + b, 1);
       tc::mbar_init(m_empty + b, kSoftmaxWarps + 3);  // softmax + QK + PV + V warps
@@ -488,6 +494,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           mt.flags = flags;
           mt.pattern = pattern;
           mt.next_pattern = next_pattern;
+          mt.grp = my.grp;
+          mt.gpat[0] = it.grp[0].pattern;
+          mt.gpat[1] = it.grp[1].pattern;
+          mt.gpat[2] = it.grp[2].pattern;
+          mt.ng = it.ng;
           mt.h = it.h;
           mt.count = my.count;
           mt.i0 = it.i0;
@@ -576,14 +587,15 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       WAITP(0, tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1));
       const int kind = metas[slot].kind;
       const int flags = metas[slot].flags;
+      const int qb = metas[slot].grp & 1;  // Q buffer of the tile's pattern group
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(m_empty + slot);
       ++M;
       if (kind == T_END) break;
       if (kind == T_EMPTY) continue;
-      if (flags & F_EPOCH) {
-        WAITP(1, tc::mbar_wait(q_ready, E & 1));
-        ++E;
+      if (flags & F_EPOCH) {  // first tile of a group: its Q buffer is (or will be) filled
+        WAITP(1, tc::mbar_wait(q_ready + qb, (E >> (qb * 16)) & 1));
+        E += 1u << (qb * 16);  // per-buffer use counts (low / high half)
       }
       const int bk = T % NK, bs = T % NS;
       WAITP(2, tc::mbar_wait(k_full + bk, (T / NK) & 1));
@@ -603,7 +615,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #else
       for (int combo = 0; combo < 3; ++combo) {
 #endif
-        const uint32_t qa = tmem + (combo == 2 ? COL_QLO : COL_QHI);  // hi.hi, hi.lo, lo.hi
+        const uint32_t qa = tmem + COL_Q + qb * QBUF + (combo == 2 ? HD / 2 : 0);  // hh, hl, lh
         const uint64_t ka = dk + (combo == 1 ? ((2 * kKHalf) >> 4) : 0);
 #pragma unroll
         for (int half = 0; half < 2; ++half)
@@ -734,16 +746,19 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     float m_init = -INFINITY;           // running max at the item start (key-window passes)
     Item qi{};  // only i0 / rend / h used by rotate_q
     if (grp == 1) asm volatile("bar.arrive %0, 64;" ::"r"(bar_out) : "memory");  // T = 0 is g0's
-    auto rotate_row = [&](int pattern) {
-      rotate_q(p, qi, pattern, r, 0, tmem + lane_base);
-      rotate_q(p, qi, pattern, r, 1, tmem + lane_base);
+    auto rotate_row = [&](int pattern, int qbuf) {
+      rotate_q(p, qi, pattern, r, 0, tmem + lane_base, qbuf);
+      rotate_q(p, qi, pattern, r, 1, tmem + lane_base, qbuf);
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(q_ready);
+      if (lane == 0) tc::mbar_arrive(q_ready + qbuf);
     };
     for (;;) {
       const int slot = M % kMetaSlots;
       WAITP(0, tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1));
+#ifdef LCX_TC_WAITPROF
+      const long long t_meta = clock64();
+#endif
       const TileMeta& mt = metas[slot];
       const int kind = mt.kind, flags = mt.flags;
       if (kind == T_END) {
@@ -774,9 +789,13 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           mask = lim >= 63 ? ~0ull : (lim < 0 ? 0ull : ((2ull << lim) - 1));
         }
       }
-      const int pattern = mt.pattern, next_pattern = mt.next_pattern;
+      const int pattern = mt.pattern, tgrp = mt.grp, ng = mt.ng;
+      const int gpat1 = mt.gpat[1], gpat2 = mt.gpat[2];
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(m_empty + slot);
+#ifdef LCX_TC_WAITPROF
+      wacc[3] += clock64() - t_meta;
+#endif
       ++M;
       if (kind == T_EMPTY) {
         if (grp == 0 && row_ok && !p.init) {  // init passes keep the running state
@@ -827,16 +846,17 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           }
           tc::tmem_wait_st();
         }
-        WAITP(2, rotate_row(pattern));
+        // group 0's Q, and group 1's into the other buffer ahead of its first QK
+        WAITP(2, rotate_row(pattern, tgrp & 1));
+        if (tgrp + 1 < ng) WAITP(2, rotate_row(gpat1, (tgrp + 1) & 1));
       }
       const int b = T % NS;
       const uint32_t ph = (T / NS) & 1;
       float sv[64];
       WAITP(1, tc::mbar_wait(s_full + b, ph));
       tc::tc_fence_after();
-      tc::tmem_ld32(tmem + lane_base + b * BN, sv);
-      tc::tmem_ld32(tmem + lane_base + b * BN + 32, sv + 32);
-      tc::tmem_wait_ld();
+      WAITP(4, tc::tmem_ld32(tmem + lane_base + b * BN, sv);
+            tc::tmem_ld32(tmem + lane_base + b * BN + 32, sv + 32); tc::tmem_wait_ld());
 #ifdef LCX_TC_TRACE_SM  // owner group's quadrant-0 warp: 5 S got, 0 m handed over, 6 P put
       if (wq == 0 && lane == 0) trace_mark(p, T, 5);
 #else
@@ -845,7 +865,8 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #ifdef LCX_TC_WAITPROF
       const long long t_sg = clock64();
 #endif
-      if (flags & F_EPOCH_AFTER) WAITP(2, rotate_row(next_pattern));  // old pattern's QKs done
+      // the group's QKs are complete: its Q buffer takes the group after next
+      if ((flags & F_EPOCH_AFTER) && tgrp + 2 < ng) WAITP(2, rotate_row(gpat2, tgrp & 1));
 #ifdef LCX_TC_FAKE_SOFTMAX  // timing experiment only: no softmax math
       for (int cc = 0; cc < 64; ++cc) sv[cc] = -INFINITY;
       mask = ~0ull;
@@ -891,7 +912,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       if (__any_sync(0xffffffffu, need && m_prev != -INFINITY)) {
         // O holds PV up to tile T - 1 at max m_prev: complete it, then rescale
         const uint32_t Tp = T - 1;
-        WAITP(3, tc::mbar_wait(s_free + (Tp % NS), (Tp / NS) & 1));
+        tc::mbar_wait(s_free + (Tp % NS), (Tp / NS) & 1);
         tc::tc_fence_after();
         const float f = (need && m_prev != -INFINITY) ? ex2(m_prev - m) : 1.f;
 #pragma unroll 1
@@ -948,11 +969,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         float lt = l;
         if (!(flags & F_FIRST)) {
           const uint32_t To = T - 1;  // the other group's last tile of this item
-          WAITP(4, tc::mbar_wait(p_full + (To % NS), (To / NS) & 1));
+          tc::mbar_wait(p_full + (To % NS), (To / NS) & 1);
           const float2 lo = lbuf[(((To >> 1) & 1) * 2 + (grp ^ 1)) * 128 + r];
           if (lo.x > 0.f) lt += lo.x * ex2(lo.y - m);
         }
-        WAITP(4, tc::mbar_wait(s_free + b, ph));  // this item's last PV is complete
+        tc::mbar_wait(s_free + b, ph);  // this item's last PV is complete
         tc::tc_fence_after();
         const float inv = lt > 0.f ? 1.f / lt : 0.f;
         float4* o = reinterpret_cast<float4*>(p.out + (i * p.hq + h) * int64_t(HD));
