@@ -16,6 +16,9 @@
 //   ChunkSelection, PrefillState, PrefillResult, chunked_prefill .. sparse.hpp:17-129
 //   RecallReport, attention_recall, RecallAggregate, RecallMeasurement,
 //   measure_budget_recall ....................................... refine.hpp:15-40
+//   SparsityPlan, CriticalSet::to_json / from_json ............... sparse.hpp:27-58
+//   CalibrationSample, CalibrationSet, RefineConfig, HeadRefineRecord, RefineReport,
+//   refine_plan, offline_search ................................. refine.hpp:42-92
 //
 // A program written against the reference recompiles against this header and links
 // liblongctx_b200.so instead of longctx_core.  Inputs are fp64 host matrices as in
@@ -24,14 +27,17 @@
 // Every compute entry runs on the GPU: there is no CPU fallback (without a usable
 // sm_100 device the call throws Error("cuda", ...)).
 //
-// Not on the prefill path and therefore not provided: rope_apply /
-// stable_softmax_rows (test helpers of the reference), SparsityPlan and the JSON
-// (de)serialisers, refine_plan / offline_search.
+// JSON: the reference exchanges nlohmann::json values; this header exchanges their
+// text (to_json returns what nlohmann's dump(2) prints for the same value, from_json
+// parses it), so a caller writes / reads the same files without the nlohmann
+// dependency.  Not provided: rope_apply / stable_softmax_rows (test helpers of the
+// reference).
 #pragma once
 
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <map>
 #include <optional>
 #include <span>
 #include <stdexcept>
@@ -99,6 +105,8 @@ inline constexpr const char* domain = "domain";
 inline constexpr const char* causality = "causality";
 inline constexpr const char* empty_row = "empty_row";
 inline constexpr const char* empty_calibration = "empty_calibration";
+inline constexpr const char* parse = "parse_error";
+inline constexpr const char* schema = "schema_violation";
 inline constexpr const char* cuda = "cuda";          // B200 build: device / launch failure
 inline constexpr const char* internal = "internal";
 }  // namespace errkind
@@ -164,6 +172,15 @@ struct HeadBudget {
   bool operator==(const HeadBudget&) const = default;
 };
 
+// Per (layer, head) budgets; JSON object {"layer.head": {"slash": S, "vertical": V}}.
+struct SparsityPlan {
+  std::map<std::pair<std::size_t, std::size_t>, HeadBudget> budgets;
+  HeadBudget& at(std::size_t layer, std::size_t head);
+  const HeadBudget& at(std::size_t layer, std::size_t head) const;  // Error("config") if absent
+  std::string to_json() const;
+  static SparsityPlan from_json(const std::string& text);
+};
+
 struct CriticalSet {
   std::vector<std::size_t> verticals;  // sorted unique column indices
   std::vector<std::size_t> slashes;    // sorted unique diagonal offsets
@@ -171,6 +188,9 @@ struct CriticalSet {
   bool admits(std::size_t i, std::size_t j) const;
   std::vector<std::size_t> admitted_row(std::size_t i) const;
   std::size_t admitted_count() const;
+  // {"contextLength": n, "slashes": [...], "verticals": [...]}
+  std::string to_json() const;
+  static CriticalSet from_json(const std::string& text);
   bool operator==(const CriticalSet&) const = default;
 };
 
@@ -241,6 +261,49 @@ struct RecallMeasurement {
 
 double measure_budget_recall(const AttentionInput& input, HeadBudget budget,
                              const RecallMeasurement& measure);
+
+struct CalibrationSample {
+  std::size_t layer = 0;
+  std::size_t head = 0;
+  AttentionInput input;
+};
+using CalibrationSet = std::vector<CalibrationSample>;
+
+struct RefineConfig {
+  double threshold = 0.9;
+  std::size_t vertical_increment = 4;
+  std::size_t slash_increment = 4;
+  std::size_t max_rounds = 8;
+  HeadBudget budget_cap{64, 64};
+  RecallMeasurement measure{};
+  void validate() const;
+};
+
+struct HeadRefineRecord {
+  std::size_t layer = 0;
+  std::size_t head = 0;
+  std::size_t rounds = 0;
+  HeadBudget initial_budget;
+  HeadBudget final_budget;
+  double initial_recall = 0.0;
+  double final_recall = 0.0;
+};
+
+struct RefineReport {
+  std::vector<HeadRefineRecord> heads;
+};
+
+// Grows each sampled head's budget by the increments while its recall over the
+// calibration samples stays below the threshold (refine.cpp:98-138).  On the device
+// the dense LSE and the estimator matrix of every calibration input are computed once
+// per call and reused by every budget tried (they do not depend on the budget).
+std::pair<SparsityPlan, RefineReport> refine_plan(const CalibrationSet& calib,
+                                                  const SparsityPlan& plan,
+                                                  const RefineConfig& cfg);
+// Per head, the first grid point (sorted by total budget) whose recall reaches the
+// threshold, else the last (refine.cpp:140-164).
+SparsityPlan offline_search(const CalibrationSet& calib, const std::vector<HeadBudget>& grid,
+                            double threshold, const RecallMeasurement& measure = {});
 
 // ------------------------------------------------- B200-specific controls --
 namespace b200 {
