@@ -141,3 +141,52 @@ def test_config3_recall_monotone_in_budget(D):
             assert bool((rec >= prev - 4e-3).all())
         prev = rec
     assert float(prev.min()) >= 1.0 - 4e-3  # full budget == dense
+
+
+def test_bench_config_1m_planted_sampled(D, port):
+    """The benchmarked workload itself (bench.py defaults: 1M tokens, 7B heads, DCA
+    s = 131072 / c = 262144, YaRN t(4), rope base 1e7, budget (1000, 6096), planted
+    inputs): for two heads and the first, a middle and the last chunk, the index contract
+    on the device's own scores and sampled rows against the row-list oracle; every
+    selection sorted, unique and in range; lse finite."""
+    import torch
+    from oracle import Critical
+    from paper_2501_15383_b200.synth import make_qkv, yarn_temperature
+    n, hq, hkv, L, lq, bud = 1 << 20, 28, 4, 32768, 64, (1000, 6096)
+    s, c = 131072, 262144
+    t = yarn_temperature(n / c)
+    q, k, v = make_qkv(n, hq, hkv, kind="planted", seed=1)
+    kw = dict(chunk_len=L, last_q=lq, budget=bud, position_mode="dca_continuous",
+              dca=(s, c, s), temperature=t, rope_base=1e7)
+    r = D.chunked_prefill(q, k, v, **kw)
+    assert torch.isfinite(r["lse"]).all() and torch.isfinite(r["out"]).all()
+    nch = n // L
+    for ci in range(nch):  # structural properties of every selection
+        t1 = (ci + 1) * L
+        for h in range(hq):
+            vv = r["verticals"][ci, h, :int(r["nv"][ci, h])]
+            ss = r["slashes"][ci, h, :int(r["ns"][ci, h])]
+            assert bool((vv[1:] > vv[:-1]).all()) and bool((ss[1:] > ss[:-1]).all())
+            assert int(vv.min()) >= 0 and int(vv.max()) < t1 and int(ss.max()) < t1
+    rng = np.random.default_rng(3)
+    for h in (5, 22):
+        g = h // 7
+        qh, kh, vh = _host(q, h), _host(k, g), _host(v, g)
+        for ci in (0, nch // 2, nch - 1):
+            t0, t1 = ci * L, (ci + 1) * L
+            gv = r["verticals"][ci, h, :int(r["nv"][ci, h])].tolist()
+            gs = r["slashes"][ci, h, :int(r["ns"][ci, h])].tolist()
+            col, sl = D.line_scores(q, k, q_row0=t0, nq=L, nk=t1, last_q=lq,
+                                    position_mode="dca_continuous", dca=(s, c, s),
+                                    rope_base=1e7)
+            crit = port.select_from_scores(col[h].double().cpu().numpy(),
+                                           sl[h].double().cpu().numpy(), t1, lq, bud)
+            assert gv == crit.verticals and gs == crit.slashes, (h, ci)
+            rows = sorted({t0, t1 - 1, *rng.integers(t0, t1, 3).tolist()})
+            o_ref, l_ref = port.attention_rows(qh[:t1], kh[:t1], vh[:t1], rows,
+                                               Critical(gv, gs, t1), rope_base=1e7,
+                                               temperature=t, dca=(s, c, s))
+            o = r["out"][rows, h].double().cpu().numpy()
+            lse = r["lse"][h, rows].double().cpu().numpy()
+            assert row_rel_err(o, o_ref) <= TOL["bf16"], (h, ci)
+            assert lse_rel_err(lse, l_ref) <= TOL["bf16"], (h, ci)
