@@ -214,20 +214,6 @@ __device__ __forceinline__ int grp_pattern(const Item& it, int g) {
   return g == 0 ? it.grp[0].pattern : (g == 1 ? it.grp[1].pattern : it.grp[2].pattern);
 }
 
-// bits [lo, lo + 64) of a bitmap (zeros outside [0, 32 * words))
-__device__ __forceinline__ uint64_t bits64(const uint32_t* bits, int64_t words, int64_t lo) {
-  if (lo <= -64) return 0;
-  const int64_t base = lo < 0 ? 0 : lo;
-  const int64_t w = base >> 5;
-  const int sh = int(base & 31);
-  auto word = [&](int64_t k) -> uint64_t { return k < words ? bits[k] : 0u; };
-  const uint64_t a = word(w) | (word(w + 1) << 32);
-  const uint64_t b = word(w + 2);
-  uint64_t r = sh ? ((a >> sh) | (b << (64 - sh))) : a;
-  if (lo < 0) r <<= (-lo);
-  return r;
-}
-
 __device__ __forceinline__ int64_t qpos_of(const TcParams& p, int pattern, int64_t i) {
   if (p.rel_mode == 0) return p.pos_q ? p.pos_q[i] : i;
   const int64_t im = i % p.s;
@@ -284,14 +270,10 @@ struct TileMeta {
   uint32_t sw[8];
   int32_t keys[64];
 };
-#ifndef LCX_TC_PREFETCH
-#define LCX_TC_PREFETCH 0
-#endif
-constexpr int kPrefetchLead = LCX_TC_PREFETCH;  // tiles (0 = off)
 #ifndef LCX_TC_BULK
 #define LCX_TC_BULK 1  // 1-D bulk copies of the pre-swizzled tiles (else 3-D tensor TMA)
 #endif
-constexpr int kTraceTiles = 512;
+[[maybe_unused]] constexpr int kTraceTiles = 512;
 // trace columns: 0 meta ready (producer), 1 K TMA issued, 2 V TMA issued,
 // 3 QK issued (MMA), 4 PV issued, 5 softmax got S, 6 softmax P written, 7 kind
 // pipeline trace (tools/trace_tc.py): compiled in only with -DLCX_TC_TRACE -- the
@@ -916,14 +898,14 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         tc::tc_fence_after();
         const float f = (need && m_prev != -INFINITY) ? ex2(m_prev - m) : 1.f;
 #pragma unroll 1
-        for (int q4 = 0; q4 < 4; ++q4) {
-          float ov[32];
-          const uint32_t ta = tmem + lane_base + COL_O + q4 * 32;
-          tc::tmem_ld32(ta, ov);
+        for (int q8 = 0; q8 < 8; ++q8) {  // 16 columns at a time: S is still live here
+          float ov[16];
+          const uint32_t ta = tmem + lane_base + COL_O + q8 * 16;
+          tc::tmem_ld16(ta, ov);
           tc::tmem_wait_ld();
 #pragma unroll
-          for (int x = 0; x < 32; ++x) ov[x] *= f;
-          tc::tmem_st32(ta, ov);
+          for (int x = 0; x < 16; ++x) ov[x] *= f;
+          tc::tmem_st16f(ta, ov);
         }
         tc::tmem_wait_st();
       }
@@ -937,17 +919,20 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       const float mm = m == -INFINITY ? 0.f : m;
       const float2 nm2 = make_float2(-mm, -mm);
       float2 rs2 = make_float2(0.f, 0.f);
-      uint32_t pw[32];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const float2 x = __fadd2_rn(make_float2(sv[2 * k], sv[2 * k + 1]), nm2);
-        const float2 pp = make_float2(ex2(x.x), ex2(x.y));
-        rs2 = __fadd2_rn(rs2, pp);
-        const __half2 h2 = __floats2half2_rn(pp.x, pp.y);
-        pw[k] = *reinterpret_cast<const uint32_t*>(&h2);
+      for (int hf = 0; hf < 2; ++hf) {  // two 32-key halves: fewer live registers
+        uint32_t pw[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int c = hf * 32 + 2 * k;
+          const float2 x = __fadd2_rn(make_float2(sv[c], sv[c + 1]), nm2);
+          const float2 pp = make_float2(ex2(x.x), ex2(x.y));
+          rs2 = __fadd2_rn(rs2, pp);
+          const __half2 h2 = __floats2half2_rn(pp.x, pp.y);
+          pw[k] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+        tc::tmem_st16(tmem + lane_base + b * BN + hf * 16, pw);
       }
-      tc::tmem_st16(tmem + lane_base + b * BN, pw);
-      tc::tmem_st16(tmem + lane_base + b * BN + 16, pw + 16);
       tc::tmem_wait_st();
       l += rs2.x + rs2.y;
       // partial (l, m) for the item's epilogue (ordered before the P release below)
