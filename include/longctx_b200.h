@@ -172,6 +172,11 @@ const char* lcx_version(void);
 int lcx_device_ok(int device);
 /* Enables per-stage CUDA-event timing inside lcx_chunked_prefill (synchronizing). */
 int lcx_set_profiling(lcx_context* ctx, int enabled);
+/* Per-chunk device time (ms, estimator through attention) of the last chunked prefill
+ * run with profiling on: *count = number of chunks; up to cap values copied to out (may
+ * be NULL).  The measured costs a DCPP chunk schedule is fitted to (engine_sim.cpp:117-166,
+ * longctx::b200::measure_chunk_costs). */
+int lcx_get_chunk_ms(lcx_context* ctx, float* out, int64_t cap, int64_t* count);
 int lcx_get_stats(lcx_context* ctx, lcx_prefill_stats* out);
 /* Debug: record CTA-0 per-tile clock64 timestamps of the tcgen05 attention
  * pipeline (512 tiles x 8 columns) and copy them to host_out (may be NULL). */

@@ -19,6 +19,8 @@
 //   SparsityPlan, CriticalSet::to_json / from_json ............... sparse.hpp:27-58
 //   CalibrationSample, CalibrationSet, RefineConfig, HeadRefineRecord, RefineReport,
 //   refine_plan, offline_search ................................. refine.hpp:42-92
+//   CostModel, chunk_cost, ChunkSchedule, fixed_schedule, dcpp_schedule
+//   ................................................... engine_sim.hpp:10-43
 //
 // A program written against the reference recompiles against this header and links
 // liblongctx_b200.so instead of longctx_core.  Inputs are fp64 host matrices as in
@@ -305,8 +307,51 @@ std::pair<SparsityPlan, RefineReport> refine_plan(const CalibrationSet& calib,
 SparsityPlan offline_search(const CalibrationSet& calib, const std::vector<HeadBudget>& grid,
                             double threshold, const RecallMeasurement& measure = {});
 
+// -------------------------------------------------------- engine_sim.hpp --
+// Prefill chunk cost attn_coeff * n * h + self_coeff * n^2 / 2 + lin_coeff * n +
+// fixed_cost for n tokens after h cached ones (engine_sim.hpp:10-21).
+struct CostModel {
+  double attn_coeff = 0.0;
+  double self_coeff = 0.0;
+  double lin_coeff = 0.0;
+  double fixed_cost = 0.0;
+  void validate() const;
+};
+
+double chunk_cost(const CostModel& model, std::size_t n, std::size_t h);
+
+// Chunk boundaries as exclusive end indices (engine_sim.hpp:23-35).
+struct ChunkSchedule {
+  std::vector<std::size_t> boundaries;
+  std::size_t total_tokens() const { return boundaries.empty() ? 0 : boundaries.back(); }
+  std::size_t chunk_count() const { return boundaries.size(); }
+  std::vector<std::size_t> sizes() const;
+  std::pair<std::size_t, std::size_t> chunk(std::size_t idx) const;
+  void validate() const;
+};
+
+ChunkSchedule fixed_schedule(std::size_t tokens, std::size_t chunks);
+// DCPP: per-chunk costs as equal as the token grid allows (engine_sim.cpp:117-166).
+ChunkSchedule dcpp_schedule(std::size_t tokens, std::size_t chunks, const CostModel& model);
+
 // ------------------------------------------------- B200-specific controls --
 namespace b200 {
+// One measured prefill chunk: n tokens after h cached ones took `ms` on the device.
+struct ChunkCostSample {
+  std::size_t n = 0;
+  std::size_t h = 0;
+  double ms = 0.0;
+};
+// Runs chunked_prefill (same arguments) on the device with per-chunk CUDA events and
+// returns every chunk's (n, h, ms) -- the measured costs a DCPP schedule is fed with.
+std::vector<ChunkCostSample> measure_chunk_costs(
+    const AttentionInput& input, std::size_t chunk_len, std::size_t last_q, HeadBudget budget,
+    PrefillMode mode, PositionMode pos_mode, const std::optional<ChunkConfig>& cfg,
+    const SelectionOptions& opts = {});
+// Non-negative least-squares fit of the four CostModel coefficients to measured chunk
+// costs (Error("config") when fewer than one sample).
+CostModel fit_cost_model(const std::vector<ChunkCostSample>& samples);
+
 enum class Precision { F32, BF16 };
 // Device storage type of q / k / v for the calls made by this thread (default F32:
 // the 1e-5 parity path; BF16: the tcgen05 path, 2e-3).

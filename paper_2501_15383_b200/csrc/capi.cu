@@ -589,6 +589,14 @@ int lcx_get_stats(lcx_context* ctx, lcx_prefill_stats* out) {
   return LCX_OK;
 }
 
+int lcx_get_chunk_ms(lcx_context* ctx, float* out, int64_t cap, int64_t* count) {
+  if (!count) return fail(LCX_ERR_DIMENSION, "null count");
+  *count = int64_t(ctx->chunk_ms.size());
+  if (out)
+    for (int64_t i = 0; i < std::min<int64_t>(cap, *count); ++i) out[i] = ctx->chunk_ms[size_t(i)];
+  return LCX_OK;
+}
+
 int lcx_estimate_block(lcx_context* ctx, const lcx_attention_input* in, int64_t q_row0,
                        int64_t nq, int64_t nk, int64_t last_q, int32_t pos_mode,
                        const lcx_chunk_config* cfg, float* est_out, void* stream) {
@@ -1151,9 +1159,11 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
   if (prof) {
     LCX_CHECK_CUDA(cudaEventSynchronize(ev[6 * (nchunks - 1) + 3]));
     double ms_est = 0, ms_sel = 0, ms_att = 0, ms_tc = 0;
+    ctx->chunk_ms.assign(size_t(nchunks), 0.f);
     for (int64_t ci = 0; ci < nchunks; ++ci) {
       cudaEvent_t* e = &ev[6 * ci];
       float t = 0;
+      cudaEventElapsedTime(&ctx->chunk_ms[size_t(ci)], e[0], e[3]);
       if (sparse) {
         cudaEventElapsedTime(&t, e[0], e[1]);
         ms_est += t;

@@ -1,6 +1,8 @@
 // Internal declarations shared by the CUDA translation units of liblongctx_b200.
 #pragma once
 
+#include <vector>
+
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -121,6 +123,7 @@ struct lcx_context {
   int64_t* tile_counter = nullptr;  // device: [0] executed tcgen05 tiles, [1] CUDA-core entries
   long long* trace = nullptr;        // device: optional tcgen05 pipeline trace (debug)
   lcx_prefill_stats stats{};
+  std::vector<float> chunk_ms;  // per-chunk device time of the last profiled prefill
   // host-buffer entry: device staging + copy streams (created lazily)
   char* stage = nullptr;
   size_t stage_bytes = 0;

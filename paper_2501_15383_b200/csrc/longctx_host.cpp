@@ -581,6 +581,34 @@ double measure_budget_recall(const AttentionInput& input, HeadBudget budget,
 
 // ---------------------------------------------------------------- b200:: --
 namespace b200 {
+std::vector<ChunkCostSample> measure_chunk_costs(const AttentionInput& input,
+                                                 std::size_t chunk_len, std::size_t last_q,
+                                                 HeadBudget budget, PrefillMode mode,
+                                                 PositionMode pos_mode,
+                                                 const std::optional<ChunkConfig>& cfg,
+                                                 const SelectionOptions& opts) {
+  lcx_context* ctx = context();
+  check(lcx_set_profiling(ctx, 1));
+  try {
+    (void)chunked_prefill(input, chunk_len, last_q, budget, mode, pos_mode, cfg, opts);
+  } catch (...) {
+    lcx_set_profiling(ctx, 0);
+    throw;
+  }
+  int64_t count = 0;
+  check(lcx_get_chunk_ms(ctx, nullptr, 0, &count));
+  std::vector<float> ms(static_cast<size_t>(count));
+  check(lcx_get_chunk_ms(ctx, ms.data(), count, &count));
+  check(lcx_set_profiling(ctx, 0));
+  std::vector<ChunkCostSample> out;
+  const std::size_t n = input.seq_len();
+  for (int64_t c = 0; c < count; ++c) {
+    const std::size_t b = std::size_t(c) * chunk_len, e = std::min(n, b + chunk_len);
+    out.push_back(ChunkCostSample{e - b, b, double(ms[size_t(c)])});
+  }
+  return out;
+}
+
 void set_precision(Precision p) { g_precision = p; }
 Precision precision() { return g_precision; }
 void set_device(int device) { g_device = device; }

@@ -9,6 +9,8 @@
 // empty); the reader is a small recursive-descent parser for the JSON grammar.
 #include <algorithm>
 #include <cctype>
+#include <cmath>
+#include <cstddef>
 #include <cstdlib>
 #include <map>
 #include <string>
@@ -418,5 +420,193 @@ SparsityPlan offline_search(const CalibrationSet& calib, const std::vector<HeadB
   }
   return plan;
 }
+
+}  // namespace longctx
+
+// ------------------------------------------------------- DCPP chunk sizing --
+// engine_sim.cpp:33-166 restated: cost model, fixed and cost-balanced schedules.
+namespace longctx {
+
+void CostModel::validate() const {
+  if (attn_coeff < 0 || self_coeff < 0 || lin_coeff < 0 || fixed_cost < 0)
+    fail(errkind::config, "cost coefficients must be non-negative");
+}
+
+double chunk_cost(const CostModel& m, std::size_t n, std::size_t h) {
+  if (n == 0) fail(errkind::domain, "chunk must contain at least one token");
+  const double x = double(n);
+  return m.attn_coeff * x * double(h) + m.self_coeff * x * x / 2.0 + m.lin_coeff * x +
+         m.fixed_cost;
+}
+
+std::vector<std::size_t> ChunkSchedule::sizes() const {
+  std::vector<std::size_t> out;
+  out.reserve(boundaries.size());
+  std::size_t prev = 0;
+  for (std::size_t b : boundaries) {
+    out.push_back(b - prev);
+    prev = b;
+  }
+  return out;
+}
+
+std::pair<std::size_t, std::size_t> ChunkSchedule::chunk(std::size_t idx) const {
+  return {idx == 0 ? 0 : boundaries[idx - 1], boundaries[idx]};
+}
+
+void ChunkSchedule::validate() const {
+  if (boundaries.empty()) fail(errkind::config, "schedule has no chunks");
+  std::size_t prev = 0;
+  for (std::size_t b : boundaries) {
+    if (b <= prev) fail(errkind::config, "chunk boundaries must be strictly increasing");
+    prev = b;
+  }
+}
+
+ChunkSchedule fixed_schedule(std::size_t tokens, std::size_t chunks) {
+  if (chunks == 0 || chunks > tokens) fail(errkind::config, "chunk count must lie in [1, tokens]");
+  ChunkSchedule s;
+  const std::size_t base = tokens / chunks, extra = tokens % chunks;  // remainder to the left
+  std::size_t pos = 0;
+  for (std::size_t c = 0; c < chunks; ++c) s.boundaries.push_back(pos += base + (c < extra));
+  return s;
+}
+
+namespace {
+// Feasibility of a per-chunk cost bound tau: walk left to right, each chunk taking
+// tokens while its cost stays within tau (leaving one token per remaining chunk), the
+// last chunk taking the rest.  Empty result = infeasible.
+std::vector<std::size_t> walk_under(double tau, std::size_t tokens, std::size_t chunks,
+                                    const CostModel& m) {
+  std::vector<std::size_t> ends;
+  std::size_t pos = 0;
+  for (std::size_t c = 0; c < chunks && pos < tokens; ++c) {
+    std::size_t take = c + 1 == chunks ? tokens - pos : 1;
+    if (chunk_cost(m, take, pos) > tau) return {};
+    if (c + 1 < chunks) {
+      const std::size_t cap = tokens - pos - (chunks - c - 1);
+      while (take < cap && chunk_cost(m, take + 1, pos) <= tau) ++take;
+    }
+    pos += take;
+    ends.push_back(pos);
+  }
+  if (pos != tokens) return {};
+  return ends;
+}
+}  // namespace
+
+ChunkSchedule dcpp_schedule(std::size_t tokens, std::size_t chunks, const CostModel& m) {
+  m.validate();
+  if (chunks == 0 || chunks > tokens) fail(errkind::config, "chunk count must lie in [1, tokens]");
+  if (chunks == 1) return ChunkSchedule{{tokens}};
+  // bisection on the largest admissible chunk cost (the whole prompt as one chunk
+  // bounds it from above)
+  const double t = double(tokens);
+  double lo = 0.0;
+  double hi = m.attn_coeff * t * t + m.self_coeff * t * t / 2.0 + m.lin_coeff * t +
+              m.fixed_cost + 1.0;
+  for (int it = 0; it < 200 && hi > lo; ++it) {
+    const double mid = lo + (hi - lo) / 2.0;
+    if (!(mid > lo && mid < hi)) break;
+    if (walk_under(mid, tokens, chunks, m).empty()) lo = mid;
+    else hi = mid;
+  }
+  ChunkSchedule s{walk_under(hi, tokens, chunks, m)};
+  if (s.boundaries.empty()) fail(errkind::domain, "chunk cost search failed to converge");
+  // the walk may need fewer chunks: halve the costliest splittable chunk until the count
+  // is met (splitting never raises a chunk's cost)
+  while (s.chunk_count() < chunks) {
+    std::size_t best = s.chunk_count();
+    double best_cost = -1.0;
+    for (std::size_t c = 0; c < s.chunk_count(); ++c) {
+      const auto [b, e] = s.chunk(c);
+      if (e - b < 2) continue;
+      const double cost = chunk_cost(m, e - b, b);
+      if (cost > best_cost) {
+        best_cost = cost;
+        best = c;
+      }
+    }
+    const auto [b, e] = s.chunk(best);
+    s.boundaries.insert(s.boundaries.begin() + std::ptrdiff_t(best), b + (e - b) / 2);
+  }
+  s.validate();
+  return s;
+}
+
+namespace b200 {
+CostModel fit_cost_model(const std::vector<ChunkCostSample>& samples) {
+  if (samples.empty()) fail(errkind::config, "cost fit needs at least one measured chunk");
+  // features of a chunk: n*h, n^2/2, n, 1.  Least squares on the active set by
+  // Householder QR in long double (the features are nearly collinear over a narrow
+  // range of chunk sizes, which squares badly in the normal equations); the most
+  // negative coefficient leaves the set until all are >= 0 (4 unknowns: <= 4 passes).
+  using LD = long double;
+  auto feat = [](const ChunkCostSample& x, int k) -> LD {
+    const LD n = LD(x.n), h = LD(x.h);
+    return k == 0 ? n * h : k == 1 ? n * n / 2 : k == 2 ? n : LD(1);
+  };
+  const std::size_t m = samples.size();
+  bool active[4] = {true, true, true, true};
+  double coef[4] = {0, 0, 0, 0};
+  for (int pass = 0; pass < 4; ++pass) {
+    int idx[4], na = 0;
+    for (int k = 0; k < 4; ++k)
+      if (active[k]) idx[na++] = k;
+    std::vector<LD> A(m * std::size_t(na)), y(m);
+    std::vector<LD> scale(std::size_t(na), 0);
+    for (int a = 0; a < na; ++a) {
+      for (std::size_t i = 0; i < m; ++i) scale[a] += feat(samples[i], idx[a]) * feat(samples[i], idx[a]);
+      scale[a] = scale[a] > 0 ? 1 / std::sqrt(scale[a]) : 0;  // unit-norm columns
+      for (std::size_t i = 0; i < m; ++i) A[i * na + a] = feat(samples[i], idx[a]) * scale[a];
+    }
+    for (std::size_t i = 0; i < m; ++i) y[i] = samples[i].ms;
+    // Householder QR: A = Q R, then R c = Q^T y
+    const int kc = int(std::min<std::size_t>(std::size_t(na), m));
+    for (int j = 0; j < kc; ++j) {
+      LD norm = 0;
+      for (std::size_t i = std::size_t(j); i < m; ++i) norm += A[i * na + j] * A[i * na + j];
+      norm = std::sqrt(norm);
+      if (norm == 0) continue;
+      const LD alpha = A[std::size_t(j) * na + j] > 0 ? -norm : norm;
+      std::vector<LD> v(m, 0);
+      for (std::size_t i = std::size_t(j); i < m; ++i) v[i] = A[i * na + j];
+      v[std::size_t(j)] -= alpha;
+      LD vv = 0;
+      for (std::size_t i = std::size_t(j); i < m; ++i) vv += v[i] * v[i];
+      if (vv == 0) continue;
+      for (int c = j; c < na; ++c) {
+        LD d = 0;
+        for (std::size_t i = std::size_t(j); i < m; ++i) d += v[i] * A[i * na + c];
+        d = 2 * d / vv;
+        for (std::size_t i = std::size_t(j); i < m; ++i) A[i * na + c] -= d * v[i];
+      }
+      LD d = 0;
+      for (std::size_t i = std::size_t(j); i < m; ++i) d += v[i] * y[i];
+      d = 2 * d / vv;
+      for (std::size_t i = std::size_t(j); i < m; ++i) y[i] -= d * v[i];
+    }
+    LD c[4] = {0, 0, 0, 0};
+    for (int j = kc - 1; j >= 0; --j) {  // back substitution; rank-deficient columns -> 0
+      const LD r = A[std::size_t(j) * na + j];
+      if (std::fabs(double(r)) < 1e-13) continue;
+      LD acc = y[std::size_t(j)];
+      for (int k = j + 1; k < kc; ++k) acc -= A[std::size_t(j) * na + k] * c[k];
+      c[j] = acc / r;
+    }
+    for (int k = 0; k < 4; ++k) coef[k] = 0.0;
+    int worst = -1;
+    for (int a = 0; a < na; ++a) {
+      coef[idx[a]] = double(c[a] * scale[a]);
+      if (coef[idx[a]] < 0 && (worst < 0 || coef[idx[a]] < coef[worst])) worst = idx[a];
+    }
+    if (worst < 0) break;
+    active[worst] = false;
+    coef[worst] = 0.0;
+  }
+  return CostModel{std::max(0.0, coef[0]), std::max(0.0, coef[1]), std::max(0.0, coef[2]),
+                   std::max(0.0, coef[3])};
+}
+}  // namespace b200
 
 }  // namespace longctx

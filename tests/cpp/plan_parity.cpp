@@ -7,6 +7,11 @@
 //       CPU: our JSON text equals the text the reference CLI wrote (minus the two
 //       bookkeeping keys its harness adds), round trips, and the error kinds of malformed
 //       plans (schema_violation / parse_error / config).
+//   plan_parity --dcpp <dcpp_golden.txt>
+//       CPU: fixed / DCPP chunk schedules identical to the reference's
+//       (engine_sim.cpp:77-166) and the non-negative cost-model fit.
+//   plan_parity --measure
+//       GPU: measured per-chunk costs of the device prefill, fitted, scheduled.
 //   plan_parity --refine <refine_golden.txt>
 //       GPU: every refine_plan / offline_search case reproduces the reference's budgets,
 //       rounds and plan text exactly and its recalls within 1e-4 (fp32 device path vs the
@@ -272,11 +277,96 @@ static int refine_mode(const std::string& path) {
   return failures == 0 && ncase > 0 ? 0 : 1;
 }
 
+// ---------------------------------------------------------------- DCPP --
+static int dcpp_mode(const std::string& path) {
+  std::ifstream f(path);
+  Reader r{f};
+  int ncase = 0;
+  for (;;) {
+    const std::string tag = r.get<std::string>();
+    if (tag == "end") break;
+    const auto tokens = r.get<std::size_t>(), chunks = r.get<std::size_t>();
+    CostModel m;
+    m.attn_coeff = r.get<double>();
+    m.self_coeff = r.get<double>();
+    m.lin_coeff = r.get<double>();
+    m.fixed_cost = r.get<double>();
+    std::vector<std::size_t> exp_fixed(r.get<std::size_t>()), exp_dcpp;
+    for (auto& b : exp_fixed) b = r.get<std::size_t>();
+    exp_dcpp.resize(r.get<std::size_t>());
+    for (auto& b : exp_dcpp) b = r.get<std::size_t>();
+    CHECK(fixed_schedule(tokens, chunks).boundaries == exp_fixed);
+    const ChunkSchedule d = dcpp_schedule(tokens, chunks, m);
+    CHECK(d.boundaries == exp_dcpp);
+    if (d.boundaries != exp_dcpp) std::fprintf(stderr, "dcpp mismatch tokens %zu chunks %zu\n", tokens, chunks);
+    ++ncase;
+  }
+  // worked example (test_engine_sim.cpp:61-73) and error kinds
+  CHECK((dcpp_schedule(100, 2, CostModel{1, 1, 0, 0}).sizes() == std::vector<std::size_t>{71, 29}));
+  CHECK(kind_of([] { dcpp_schedule(3, 4, CostModel{1, 1, 0, 0}); }) == "config");
+  CHECK(kind_of([] { fixed_schedule(3, 0); }) == "config");
+  CHECK(kind_of([] { CostModel{-1, 0, 0, 0}.validate(); }) == "config");
+  CHECK(kind_of([] { chunk_cost(CostModel{}, 0, 0); }) == "domain");
+  // the cost fit recovers a model from exact samples of it
+  const CostModel truth{2e-6, 5e-7, 3e-3, 0.4};
+  std::vector<b200::ChunkCostSample> samples;
+  for (std::size_t c = 0; c < 32; ++c) {
+    const std::size_t n = 1000 + (c * 7919) % 1500, h = c * 4096;  // n, h independent
+    samples.push_back({n, h, chunk_cost(truth, n, h)});
+  }
+  const CostModel fit = b200::fit_cost_model(samples);
+  auto rel = [](double a, double b) { return std::fabs(a - b) / std::max(std::fabs(b), 1e-30); };
+  CHECK(rel(fit.attn_coeff, truth.attn_coeff) < 1e-6 && rel(fit.self_coeff, truth.self_coeff) < 1e-5);
+  CHECK(rel(fit.lin_coeff, truth.lin_coeff) < 1e-4 && rel(fit.fixed_cost, truth.fixed_cost) < 1e-3);
+  // negative least-squares components are clamped out (non-negative fit)
+  std::vector<b200::ChunkCostSample> lin;
+  for (std::size_t n = 1; n <= 20; ++n) lin.push_back({n, 0, 3.0 * double(n) - 1.0});
+  const CostModel lf = b200::fit_cost_model(lin);
+  CHECK(lf.attn_coeff >= 0 && lf.self_coeff >= 0 && lf.lin_coeff >= 0 && lf.fixed_cost >= 0);
+  CHECK(kind_of([] { b200::fit_cost_model({}); }) == "config");
+  std::printf("dcpp cases: %d, failures %d\n", ncase, failures);
+  return failures == 0 && ncase > 0 ? 0 : 1;
+}
+
+// measured chunk costs of the device prefill -> fitted model -> DCPP schedule (GPU)
+static int measure_mode() {
+  const std::size_t n = 8192, dim = 128, L = 1024;
+  AttentionInput in;
+  std::uint64_t st = 12345;
+  auto u = [&]() {
+    st = st * 6364136223846793005ull + 1442695040888963407ull;
+    return double(int64_t(st >> 11) % 2000001 - 1000000) * 1e-6;
+  };
+  for (Matrix* m : {&in.q, &in.k, &in.v}) {
+    *m = Matrix(n, dim);
+    for (auto& x : m->values) x = u();
+  }
+  in.positions_q.resize(n);
+  in.positions_k.resize(n);
+  for (std::size_t i = 0; i < n; ++i) in.positions_q[i] = in.positions_k[i] = std::int64_t(i);
+  b200::set_precision(b200::Precision::BF16);
+  const auto samples = b200::measure_chunk_costs(in, L, 64, HeadBudget{64, 128}, PrefillMode::Sparse,
+                                                 PositionMode::Standard, std::nullopt);
+  CHECK(samples.size() == n / L);
+  for (std::size_t c = 0; c < samples.size(); ++c) {
+    CHECK(samples[c].n == L && samples[c].h == c * L && samples[c].ms > 0.0);
+    std::printf("chunk %zu: n %zu h %zu %.3f ms\n", c, samples[c].n, samples[c].h, samples[c].ms);
+  }
+  const CostModel m = b200::fit_cost_model(samples);
+  const ChunkSchedule s = dcpp_schedule(n, n / L, m);
+  CHECK(s.total_tokens() == n && s.chunk_count() == n / L);
+  std::printf("fit: attn %.3g self %.3g lin %.3g fixed %.3g; failures %d\n", m.attn_coeff,
+              m.self_coeff, m.lin_coeff, m.fixed_cost, failures);
+  return failures == 0 ? 0 : 1;
+}
+
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "";
   try {
     if (mode == "--json" && argc == 4) return json_mode(argv[2], argv[3]);
     if (mode == "--refine" && argc == 3) return refine_mode(argv[2]);
+    if (mode == "--dcpp" && argc == 3) return dcpp_mode(argv[2]);
+    if (mode == "--measure" && argc == 2) return measure_mode();
   } catch (const Error& e) {
     std::fprintf(stderr, "Error(%s): %s\n", e.kind().c_str(), e.what());
     return 2;

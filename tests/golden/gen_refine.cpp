@@ -25,6 +25,7 @@
 #include <string>
 #include <vector>
 
+#include "longctx/engine_sim.hpp"
 #include "longctx/planted.hpp"
 #include "longctx/refine.hpp"
 #include "longctx/sparse.hpp"
@@ -136,7 +137,41 @@ static void offline_case(std::ostream& o, const CalibrationSet& calib,
   put_str(o, offline_search(calib, grid, threshold, m).to_json().dump(2));
 }
 
-int main() {
+// DCPP chunk sizing (engine_sim.cpp:117-166): "dcpp tokens chunks a s l f" then the
+// fixed and the DCPP boundaries, one line each ("count b0 b1 ...")
+static int dcpp_main() {
+  std::ostream& o = std::cout;
+  char buf[128];
+  auto emit = [&](std::size_t tokens, std::size_t chunks, const CostModel& m) {
+    std::snprintf(buf, sizeof buf, "%.17g %.17g %.17g %.17g", m.attn_coeff, m.self_coeff,
+                  m.lin_coeff, m.fixed_cost);
+    o << "dcpp " << tokens << " " << chunks << " " << buf << "\n";
+    for (const ChunkSchedule& s : {fixed_schedule(tokens, chunks), dcpp_schedule(tokens, chunks, m)}) {
+      o << s.boundaries.size();
+      for (auto b : s.boundaries) o << " " << b;
+      o << "\n";
+    }
+  };
+  emit(100, 2, CostModel{1.0, 1.0, 0.0, 0.0});  // test_engine_sim.cpp:61-73
+  emit(57, 1, CostModel{1.0, 1.0, 0.5, 2.0});
+  emit(57, 57, CostModel{1.0, 1.0, 0.5, 2.0});
+  emit(1 << 20, 32, CostModel{1.0, 0.0, 0.0, 0.0});  // pure cross-chunk attention
+  emit(1 << 20, 8, CostModel{2e-9, 1e-9, 3e-4, 5.0});
+  std::mt19937_64 rng(21);
+  std::uniform_real_distribution<double> coeff(0.0, 3.0);
+  std::uniform_int_distribution<std::size_t> tokens_pick(10, 4000);
+  for (int trial = 0; trial < 24; ++trial) {
+    const std::size_t tokens = tokens_pick(rng);
+    std::uniform_int_distribution<std::size_t> k_pick(1, std::min<std::size_t>(tokens, 40));
+    const std::size_t k = k_pick(rng);
+    emit(tokens, k, CostModel{coeff(rng), coeff(rng), coeff(rng), coeff(rng)});
+  }
+  o << "end\n";
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "dcpp") return dcpp_main();
   std::ostream& o = std::cout;
   const SelectionOptions kNoForced{false, false, true};
   {  // a planted column needs growth (test_refine.cpp:102-124)

@@ -35,6 +35,9 @@ def main():
     out = subprocess.run([exe], check=True, capture_output=True, text=True).stdout
     with open(os.path.join(HERE, "refine_golden.txt"), "w") as f:
         f.write(out)
+    dc = subprocess.run([exe, "dcpp"], check=True, capture_output=True, text=True).stdout
+    with open(os.path.join(HERE, "dcpp_golden.txt"), "w") as f:
+        f.write(dc)
     shutil.copy(REF + "/out/sparsity/critical_set.json", os.path.join(HERE, "ref_critical_set.json"))
     shutil.copy(REF + "/out/refine/plan_refined.json", os.path.join(HERE, "ref_plan_refined.json"))
     print("wrote refine_golden.txt,", len(out), "bytes")

@@ -1,6 +1,6 @@
 """Sparsity plans, their JSON, and budget refinement through
 the C++ drop-in (tests/cpp/plan_parity.cpp), against fixtures the reference produced
-(tests/golden/make_refine_golden.py):
+(tests/golden/make_refine_golden.py), plus DCPP chunk sizing (§8(f) row 4):
 
   * CPU: CriticalSet / SparsityPlan JSON text equals what the reference CLI wrote
     (proj/out/sparsity/critical_set.json, proj/out/refine/plan_refined.json), round trips,
@@ -37,6 +37,19 @@ def test_plan_json_matches_reference_text():
     r = subprocess.run([build_binary(), "--json", os.path.join(GOLD, "ref_critical_set.json"),
                         os.path.join(GOLD, "ref_plan_refined.json")],
                        capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_dcpp_schedules_match_reference():
+    r = subprocess.run([build_binary(), "--dcpp", os.path.join(GOLD, "dcpp_golden.txt")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+def test_measured_chunk_costs_feed_dcpp():
+    r = subprocess.run([build_binary(), "--measure"], capture_output=True, text=True,
+                       timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
 
 
