@@ -798,6 +798,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         ++T;
         continue;
       }
+#ifdef LCX_TC_WAITPROF
+      const long long t_first = clock64();
+#endif
       if (flags & F_FIRST) {
         // the other group's epilogue of the previous item (its last tile, T - 1) has read
         // O and S(T - 1) is consumed, so O / Q of this CTA's TMEM are free
@@ -829,16 +832,20 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           tc::tmem_wait_st();
         }
         // group 0's Q, and group 1's into the other buffer ahead of its first QK
-        WAITP(2, rotate_row(pattern, tgrp & 1));
-        if (tgrp + 1 < ng) WAITP(2, rotate_row(gpat1, (tgrp + 1) & 1));
+        rotate_row(pattern, tgrp & 1);
+        if (tgrp + 1 < ng) rotate_row(gpat1, (tgrp + 1) & 1);
       }
+#ifdef LCX_TC_WAITPROF
+      wacc[2] += clock64() - t_first;  // item start: hand-over wait, O restore, Q rotations
+#endif
       const int b = T % NS;
       const uint32_t ph = (T / NS) & 1;
       float sv[64];
       WAITP(1, tc::mbar_wait(s_full + b, ph));
       tc::tc_fence_after();
-      WAITP(4, tc::tmem_ld32(tmem + lane_base + b * BN, sv);
-            tc::tmem_ld32(tmem + lane_base + b * BN + 32, sv + 32); tc::tmem_wait_ld());
+      tc::tmem_ld32(tmem + lane_base + b * BN, sv);
+      tc::tmem_ld32(tmem + lane_base + b * BN + 32, sv + 32);
+      tc::tmem_wait_ld();
 #ifdef LCX_TC_TRACE_SM  // owner group's quadrant-0 warp: 5 S got, 0 m handed over, 6 P put
       if (wq == 0 && lane == 0) trace_mark(p, T, 5);
 #else
@@ -848,7 +855,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       const long long t_sg = clock64();
 #endif
       // the group's QKs are complete: its Q buffer takes the group after next
-      if ((flags & F_EPOCH_AFTER) && tgrp + 2 < ng) WAITP(2, rotate_row(gpat2, tgrp & 1));
+      if ((flags & F_EPOCH_AFTER) && tgrp + 2 < ng) rotate_row(gpat2, tgrp & 1);
 #ifdef LCX_TC_FAKE_SOFTMAX  // timing experiment only: no softmax math
       for (int cc = 0; cc < 64; ++cc) sv[cc] = -INFINITY;
       mask = ~0ull;
@@ -872,7 +879,13 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       wacc[5] += clock64() - t_sg;
 #endif
       // ---- running max: previous tile's (other group) unless the item starts here
+#ifdef LCX_TC_WAITPROF
+      const long long t_hand = clock64();
+#endif
       if (!(flags & F_FIRST)) asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
+#ifdef LCX_TC_WAITPROF
+      wacc[4] += clock64() - t_hand;  // the previous tile's running max (other group)
+#endif
       const float m_prev = (flags & F_FIRST) ? m_init : mbuf[((T - 1) & 1) * 128 + r];
       // lazy rescale: the max moves only past a threshold (P <= 2^8 in fp16)
       const bool need = tmax > m_prev + kRescaleThresh;
@@ -979,6 +992,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
               lt > 0.f ? (m + log2f(lt)) * 0.69314718055994530942f : -INFINITY;
         tc::tc_fence_before();
         asm volatile("bar.arrive %0, 64;" ::"r"(bar_out) : "memory");
+
       }
       ++T;
     }
