@@ -161,17 +161,21 @@ __global__ void __launch_bounds__(kCT)
 select_cluster_kernel(const float* __restrict__ scores, int64_t n, int64_t k,
                       int64_t prefix_len, int32_t* __restrict__ out,
                       int32_t* __restrict__ count, int64_t cap) {
-  __shared__ int hist[256];
+  constexpr int kW = kCT / 32;         // warps per CTA
+  __shared__ int whist[kW][256];       // per-warp digit histograms (no atomic contention)
+  __shared__ int hist[256];            // this CTA's histogram, read by the cluster via DSMEM
   __shared__ int warp_sums[32];
   __shared__ int total;
   __shared__ uint32_t sh_prefix;
   __shared__ long long sh_remaining;
-  __shared__ long long sh_cnt[2];  // [0] emitted by this CTA, [1] its equal count
+  __shared__ long long sh_cnt[2];      // [0] emitted by this CTA, [1] its equal count
+  __shared__ int w_gt[kW], w_eq[kW], w_eqp[kW];  // per-warp counts of the emission
+  __shared__ long long w_base[kW], w_take[kW];
   const int rank = cluster_rank();
   const int h = blockIdx.x / kCl;
   const float* sc = scores + int64_t(h) * n;
   int32_t* o = out + int64_t(h) * cap;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t lo = n * rank / kCl, hi = n * (rank + 1) / kCl;
   // (the k >= n and k <= 0 cases are handled by the single-CTA kernel)
   if (rank == 0)
@@ -179,87 +183,107 @@ select_cluster_kernel(const float* __restrict__ scores, int64_t n, int64_t k,
   uint32_t prefix = 0, mask = 0;
   long long remaining = k;
   for (int shift = 24; shift >= 0; shift -= 8) {
-    for (int b = tid; b < 256; b += kCT) hist[b] = 0;
+    for (int b = tid; b < kW * 256; b += kCT) (&whist[0][0])[b] = 0;
     __syncthreads();
     for (int64_t i = lo + tid; i < hi; i += kCT) {
       const uint32_t u = float_to_ordered(sc[i]);
-      if ((u & mask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1);
+      if ((u & mask) == prefix) atomicAdd(&whist[wid][(u >> shift) & 255u], 1);
+    }
+    __syncthreads();
+    if (tid < 256) {
+      int c = 0;
+#pragma unroll
+      for (int w = 0; w < kW; ++w) c += whist[w][tid];
+      hist[tid] = c;
     }
     cluster_sync();  // all eighths histogrammed
-    if (tid == 0) {
-      long long cum = 0;
-      int chosen = 0;
-      for (int dgt = 255; dgt >= 0; --dgt) {
-        long long c = 0;
-        for (int r = 0; r < kCl; ++r) c += ld_dsmem_i32(dsmem(&hist[dgt], r));
-        if (cum + c >= remaining) {
-          chosen = dgt;
-          break;
-        }
-        cum += c;
-      }
-      sh_remaining = remaining - cum;
-      sh_prefix = prefix | (uint32_t(chosen) << shift);
+    // digit d = 255 - t for thread t: the cluster-wide count, then the count of all larger
+    // digits (exclusive scan in descending digit order); exactly one digit straddles k
+    int c = 0;
+    if (tid < 256)
+      for (int r = 0; r < kCl; ++r) c += ld_dsmem_i32(dsmem(&hist[255 - tid], r));
+    const int before = block_excl_scan(c, warp_sums, &total);
+    if (tid < 256 && before < remaining && before + c >= remaining) {
+      sh_remaining = remaining - before;
+      sh_prefix = prefix | (uint32_t(255 - tid) << shift);
     }
-    cluster_sync();  // every CTA read every histogram before the next pass clears its own
+    cluster_sync();  // the choice is published; every CTA read every histogram
     prefix = sh_prefix;
     remaining = sh_remaining;
     mask |= 255u << shift;
   }
   const uint32_t T = prefix;
   const long long need_eq = remaining;
-  // phase 1: this eighth's equal count and its emitted greater-than count
-  int gt_c = 0, eq_c = 0;
-  for (int64_t i = lo + tid; i < hi; i += kCT) {
-    const uint32_t u = float_to_ordered(sc[i]);
-    gt_c += (u > T) && (i >= prefix_len);
-    eq_c += (u == T);
+  // ---- emission: warp w of the CTA owns a contiguous slice of the CTA's eighth, so the
+  // output (ascending indices) needs only per-warp offsets -- no block barrier per element
+  const int64_t span = hi - lo;
+  const int64_t wlo = lo + span * wid / kW, whi = lo + span * (wid + 1) / kW;
+  {  // pass A: per-warp counts
+    int gt = 0, eq = 0, eqp = 0;
+    for (int64_t i = wlo + lane; i < whi; i += 32) {
+      const uint32_t u = float_to_ordered(sc[i]);
+      gt += (u > T) && (i >= prefix_len);
+      eq += (u == T);
+      eqp += (u == T) && (i < prefix_len);
+    }
+    gt = __reduce_add_sync(0xffffffffu, gt);
+    eq = __reduce_add_sync(0xffffffffu, eq);
+    eqp = __reduce_add_sync(0xffffffffu, eqp);
+    if (lane == 0) {
+      w_gt[wid] = gt;
+      w_eq[wid] = eq;
+      w_eqp[wid] = eqp;
+    }
   }
-  block_excl_scan(gt_c, warp_sums, &total);
-  gt_c = total;
-  block_excl_scan(eq_c, warp_sums, &total);
-  eq_c = total;
-  if (tid == 0) sh_cnt[1] = eq_c;
-  cluster_sync();
-  // ties go to the lowest indices: this eighth takes the equals ranked
-  // [eq_before, eq_before + take) in index order
-  long long eq_before = 0;
-  for (int r = 0; r < rank; ++r) eq_before += ld_dsmem_i64(dsmem(&sh_cnt[1], r));
-  long long take = need_eq - eq_before;
-  take = take < 0 ? 0 : (take > eq_c ? eq_c : take);
+  __syncthreads();
   if (tid == 0) {
-    // taken equals inside the forced prefix are already written
-    long long pref = 0, seen = 0;
-    const int64_t pe = hi < prefix_len ? hi : prefix_len;
-    for (int64_t i = lo; i < pe && seen < take; ++i)
-      if (float_to_ordered(sc[i]) == T) {
-        ++seen;
-        ++pref;
-      }
-    sh_cnt[0] = gt_c + take - pref;  // emitted by this eighth
+    long long e = 0;
+    for (int w = 0; w < kW; ++w) e += w_eq[w];
+    sh_cnt[1] = e;
+  }
+  cluster_sync();
+  if (tid == 0) {
+    // ties go to the lowest indices: this eighth takes the equals ranked
+    // [eq_before, eq_before + take) in index order, warp by warp
+    long long eq_before = 0;
+    for (int r = 0; r < rank; ++r) eq_before += ld_dsmem_i64(dsmem(&sh_cnt[1], r));
+    long long take = need_eq - eq_before;
+    take = take < 0 ? 0 : (take > sh_cnt[1] ? sh_cnt[1] : take);
+    long long emitted = 0;
+    for (int w = 0; w < kW; ++w) {
+      const long long tw = take < w_eq[w] ? take : w_eq[w];
+      take -= tw;
+      w_take[w] = tw;
+      // the warp's taken equals are its first tw in index order; those inside the forced
+      // prefix are written already (prefix indices come first within the slice)
+      w_base[w] = emitted;
+      emitted += w_gt[w] + tw - (tw < w_eqp[w] ? tw : w_eqp[w]);
+    }
+    sh_cnt[0] = emitted;
   }
   cluster_sync();
   long long base = prefix_len;
   for (int r = 0; r < rank; ++r) base += ld_dsmem_i64(dsmem(&sh_cnt[0], r));
-  // phase 2: emit in ascending index order
-  long long eq_seen = 0, out_seen = 0;
-  for (int64_t b0 = lo; b0 < hi; b0 += kCT) {
-    const int64_t i = b0 + tid;
-    uint32_t u = 0;
-    if (i < hi) u = float_to_ordered(sc[i]);
-    const int g = (i < hi) && (u > T);
-    const int e = (i < hi) && (u == T);
-    const int e_rank = block_excl_scan(e, warp_sums, &total);
-    const int e_total = total;
-    const int sel = g || (e && (eq_seen + e_rank) < take);
-    const int emit = sel && (i >= prefix_len);
-    const int pos = block_excl_scan(emit, warp_sums, &total);
-    const int emit_total = total;
-    if (emit) o[base + out_seen + pos] = int32_t(i);
-    eq_seen += e_total;
-    out_seen += emit_total;
+  {  // pass B: emit the warp's slice in ascending index order
+    const long long wb = base + w_base[wid], tw = w_take[wid];
+    long long eq_seen = 0, out_seen = 0;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t b0 = wlo; b0 < whi; b0 += 32) {
+      const int64_t i = b0 + lane;
+      uint32_t u = 0;
+      if (i < whi) u = float_to_ordered(sc[i]);
+      const bool g = (i < whi) && (u > T);
+      const bool e = (i < whi) && (u == T);
+      const unsigned em = __ballot_sync(0xffffffffu, e);
+      const bool sel = g || (e && eq_seen + __popc(em & lt) < tw);
+      const bool emit = sel && (i >= prefix_len);
+      const unsigned om = __ballot_sync(0xffffffffu, emit);
+      if (emit) o[wb + out_seen + __popc(om & lt)] = int32_t(i);
+      eq_seen += __popc(em);
+      out_seen += __popc(om);
+    }
   }
-  if (rank == kCl - 1 && tid == 0) count[h] = int32_t(base + out_seen);
+  if (rank == kCl - 1 && tid == 0) count[h] = int32_t(base + sh_cnt[0]);
   cluster_sync();  // keep every CTA's shared memory alive until all DSMEM reads are done
 }
 
