@@ -735,6 +735,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(q_ready + qbuf);
     };
+#ifdef LCX_TC_WAITPROF
+    long long t_own = 0;  // start of the last own tile
+#endif
     for (;;) {
       const int slot = M % kMetaSlots;
       WAITP(0, tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1));
@@ -800,6 +803,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       }
 #ifdef LCX_TC_WAITPROF
       const long long t_first = clock64();
+      t_own = t_first;
 #endif
       if (flags & F_FIRST) {
         // the other group's epilogue of the previous item (its last tile, T - 1) has read
@@ -879,13 +883,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       wacc[5] += clock64() - t_sg;
 #endif
       // ---- running max: previous tile's (other group) unless the item starts here
-#ifdef LCX_TC_WAITPROF
-      const long long t_hand = clock64();
-#endif
       if (!(flags & F_FIRST)) asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
-#ifdef LCX_TC_WAITPROF
-      wacc[4] += clock64() - t_hand;  // the previous tile's running max (other group)
-#endif
       const float m_prev = (flags & F_FIRST) ? m_init : mbuf[((T - 1) & 1) * 128 + r];
       // lazy rescale: the max moves only past a threshold (P <= 2^8 in fp16)
       const bool need = tmax > m_prev + kRescaleThresh;
@@ -994,6 +992,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         asm volatile("bar.arrive %0, 64;" ::"r"(bar_out) : "memory");
 
       }
+#ifdef LCX_TC_WAITPROF
+      wacc[4] += clock64() - t_own;  // whole own tile, item start to P release / epilogue
+#endif
       ++T;
     }
 #ifdef LCX_TC_WAITPROF

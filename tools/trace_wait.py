@@ -24,7 +24,7 @@ names = {0: ("producer", ["m_empty", "k_empty"]),
          1: ("QK", ["m_full", "q_ready", "k_full", "s_free", "issue"]),
          2: ("V", ["m_full", "v_empty"]),
          3: ("PV", ["m_full", "p_full", "v_full"]),
-         4: ("softmax", ["m_full", "s_full", "item start", "meta+mask", "max handoff", "max phase",
+         4: ("softmax", ["m_full", "s_full", "item start", "meta+mask", "own tile (all)", "max phase",
                          "exp phase"])}
 for role, (nm, sites) in names.items():
     tot = w[role, 7]
