@@ -439,11 +439,12 @@ void est_tc_plan(const EstTcArgs& a, EstTcPlan& pl) {
     pl.near_begin = near_key <= 0 ? 0 : std::min<int64_t>(pl.ntiles, (near_key + 63) / 64);
     if (pl.near_begin < pl.far_end) pl.near_begin = pl.far_end;
   }
-  // pieces of 1/32 of the chunk's tensor-core tiles (>= 4 tiles): a function of the key
+  // pieces of 1/37 of the chunk's tensor-core tiles (>= 4 tiles): a function of the key
   // range only, so a head's row statistics (combined over pieces in a fixed order) are
-  // bitwise the same whichever heads a call covers; <= 2 x 33 stats slots
+  // bitwise the same whichever heads a call covers; <= 2 x 38 stats slots.  37 pieces x
+  // 16 head pairs (7B: 4 KV heads x 4 pairs) = 592 CTAs = exactly 4 waves on 148 SMs
   const int64_t tc_tiles = pl.far_end + (pl.ntiles - pl.near_begin);
-  pl.per = int(std::max<int64_t>(4, (tc_tiles + 31) / 32));
+  pl.per = int(std::max<int64_t>(4, (tc_tiles + 36) / 37));
   const int nf = int((pl.far_end + pl.per - 1) / pl.per);
   const int nn = int((pl.ntiles - pl.near_begin + pl.per - 1) / pl.per);
   pl.tc_splits = nf + nn;
