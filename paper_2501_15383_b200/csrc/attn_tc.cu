@@ -408,7 +408,21 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     auto slot_wait = [&](uint32_t mm) {
       WAITP(0, tc::mbar_wait(m_empty + int(mm % kMetaSlots), ((mm / kMetaSlots) & 1) ^ 1));
     };
-    for (int item = blockIdx.x; item < p.nitems; item += gridDim.x) {
+    // items come from a global queue (ascending, so neighbouring CTAs still work on
+    // neighbouring row blocks of a head and share their K / V tiles in L2) -- CTAs that
+    // drew cheap items take more, instead of a fixed round-robin share
+    int static_item = int(blockIdx.x);
+    auto next_item = [&]() -> int {
+      if (!p.item_counter) {
+        const int x = static_item;
+        static_item += int(gridDim.x);
+        return x;
+      }
+      int v = 0;
+      if (lane == 0) v = atomicAdd(p.item_counter, 1);
+      return __shfl_sync(0xffffffffu, v, 0);
+    };
+    for (int item = next_item(); item < p.nitems; item = next_item()) {
       const Item it = plans[item];
       if (it.ntiles == 0) {
         slot_wait(M);
@@ -1010,6 +1024,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 
 __global__ void plan_items_kernel(const TcParams p, Item* __restrict__ plans) {
   const int item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item == 0 && p.item_counter) *p.item_counter = 0;  // the launch that follows draws from 0
   if (item >= p.nitems) return;
   Item it;
   setup_item(p, item, it);

@@ -37,6 +37,7 @@ struct TcParams {
   int64_t key_lo, key_hi;
   int vert_pass, init;
   const int* win_flags; int win;  // optional: skip the pass when win_flags[win] == 0
+  int* item_counter;  // optional: dynamic item queue (reset by plan_items_kernel)
   // pre-swizzled tiled operands (TcBuffers), loaded with 1-D bulk copies
   const __nv_bfloat16 *khi, *klo, *kchi, *kclo;
   const __half *vt, *vct;

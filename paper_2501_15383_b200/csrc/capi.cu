@@ -409,6 +409,7 @@ int attention_chunk(lcx_context* ctx, const lcx_attention_input* in, AttnWS& w, 
   p.lse = lse;
   p.lse_stride = lse_stride;
   p.tile_count = ctx->profiling ? ctx->tile_counter : nullptr;
+  p.item_counter = ctx->item_counter;
   p.trace = ctx->trace;
   p.plans = w.plans;
   if (ev_tc0) LCX_CHECK_CUDA(cudaEventRecord(ev_tc0, st));
@@ -535,6 +536,7 @@ int lcx_context_create(int device, lcx_context** out) {
   ctx->device = device;
   ctx->sm_count = prop.multiProcessorCount;
   LCX_CHECK_CUDA(cudaMalloc(&ctx->tile_counter, 2 * sizeof(int64_t)));
+  LCX_CHECK_CUDA(cudaMalloc(&ctx->item_counter, sizeof(int)));
   LCX_CHECK_CUDA(cudaMalloc(&ctx->far_dev, 2 * sizeof(int)));
   LCX_CHECK_CUDA(cudaHostAlloc(&ctx->far_host, 4 * sizeof(int), cudaHostAllocMapped));
   LCX_CHECK_CUDA(cudaHostGetDevicePointer(&ctx->far_host_dev, ctx->far_host, 0));
@@ -550,6 +552,7 @@ int lcx_context_destroy(lcx_context* ctx) {
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->rope) cudaFree(ctx->rope);
   if (ctx->tile_counter) cudaFree(ctx->tile_counter);
+  if (ctx->item_counter) cudaFree(ctx->item_counter);
   if (ctx->trace) cudaFree(ctx->trace);
   if (ctx->far_dev) cudaFree(ctx->far_dev);
   if (ctx->far_host) cudaFreeHost(ctx->far_host);

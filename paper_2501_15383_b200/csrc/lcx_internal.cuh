@@ -121,6 +121,7 @@ struct lcx_context {
   // persistent device scratch (counters)
   int profiling = 0;
   int64_t* tile_counter = nullptr;  // device: [0] executed tcgen05 tiles, [1] CUDA-core entries
+  int* item_counter = nullptr;      // device: dynamic item queue of the tcgen05 attention
   long long* trace = nullptr;        // device: optional tcgen05 pipeline trace (debug)
   lcx_prefill_stats stats{};
   std::vector<float> chunk_ms;  // per-chunk device time of the last profiled prefill
