@@ -48,9 +48,18 @@ constexpr int BM = 128, BN = 64, HD = 128;
 // warps 0-7 softmax (TMEM lane quadrant = warp % 4, column half = warp / 4),
 // warp 8 producer (tile metadata + K TMA), warp 9 QK issuer + TMEM allocator,
 // warp 10 PV issuer, warp 11 V TMA
-constexpr int kThreads = 384;
-constexpr int kSoftmaxWarps = 8;
-constexpr int kWarpProducer = 8, kWarpMma = 9, kWarpPv = 10, kWarpV = 11;
+#ifndef LCX_TC_GROUPS
+#define LCX_TC_GROUPS 2
+#endif
+constexpr int kGroups = LCX_TC_GROUPS;          // softmax warp groups (tile T: T % kGroups)
+constexpr int kSoftmaxWarps = 4 * kGroups;
+constexpr int kThreads = 32 * (kSoftmaxWarps + 4);
+constexpr int kWarpProducer = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1,
+              kWarpPv = kSoftmaxWarps + 2, kWarpV = kSoftmaxWarps + 3;
+// registers: with more than two groups the launch grants 65536 / kThreads per thread;
+// the control warp group gives some up (setmaxnreg) for the softmax groups
+constexpr int kRegCtl = 72;
+constexpr int kRegSoftmax = ((65536 - 128 * kRegCtl) / (32 * kSoftmaxWarps)) / 8 * 8;
 // two S buffers suffice (NS = 2, 3, 4 measure the same); the TMEM they free holds a
 // second rotated Q, so the Q of the next DCA pattern is in place before its first QK
 constexpr int NK = 4, NV = 4, NS = 2;                // K / V smem stages, S (+P) TMEM buffers
@@ -60,12 +69,15 @@ constexpr uint32_t kVStage = HD * BN * 2;            // 16 KB
 constexpr uint32_t OFF_K = 0;
 constexpr uint32_t OFF_V = OFF_K + NK * kKStage;     // 128 KB
 constexpr uint32_t OFF_BAR = OFF_V + NV * kVStage;   // 192 KB
-constexpr uint32_t OFF_META = OFF_BAR + 512;
+constexpr uint32_t OFF_META = OFF_BAR + 1024;
 constexpr int kMetaSlots = 16;                      // tile metadata ring (448 B slots)
 // softmax hand-off area: running max per tile parity [2][128], partial sums
 // (l, m) [2 slot][2 warp group][128]
 constexpr uint32_t OFF_RED = OFF_META + kMetaSlots * 448;
-constexpr uint32_t kSmemBytes = OFF_RED + 2 * 128 * 4 + 2 * 2 * 128 * 8 + 1024;  // + align slack
+// softmax exchange: running max per group [kGroups][128], partial sums (l, m)
+// [2 slot][kGroups][128]
+constexpr uint32_t kSmemBytes =
+    OFF_RED + kGroups * 128 * 4 + 2 * kGroups * 128 * 8 + 1024;  // + align slack
 // TMEM (512 columns x 128 lanes): S/P buffers [0, 128), O [128, 256), two rotated Q
 // buffers [256, 384) and [384, 512) (hi, then lo; bf16 pairs per 32-bit column) as
 // the A operand of every QK MMA, so all MMAs read only B from shared memory.  DCA
@@ -349,9 +361,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
   const tc::SBar q_ready = p_full + NS;        // [2] softmax rotated Q buffer b -> QK issuer
   const tc::SBar m_full = q_ready + 2;         // [kMetaSlots]
   const tc::SBar m_empty = m_full + kMetaSlots;  // [kMetaSlots]
+  const tc::SBar hand = m_empty + kMetaSlots;    // [kGroups][4] running max of a tile ready
+  const tc::SBar lpub = hand + 4 * kGroups;      // [kGroups] partial sums of a tile written
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR) +
-                        2 * (2 * NK + 2 * NV + 3 * NS + 2 + 2 * kMetaSlots);
-  static_assert((2 * NK + 2 * NV + 3 * NS + 2 + 2 * kMetaSlots + 1) * 8 <= 512,
+                        2 * (2 * NK + 2 * NV + 3 * NS + 2 + 2 * kMetaSlots + 5 * kGroups);
+  static_assert((2 * NK + 2 * NV + 3 * NS + 2 + 2 * kMetaSlots + 5 * kGroups + 1) * 8 <= 1024,
                 "barrier area overflow");
   TileMeta* metas = reinterpret_cast<TileMeta*>(smem + OFF_META);
 
@@ -372,10 +386,12 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     for (int b = 0; b < NS; ++b) {
       tc::mbar_init(s_full + b, 1);
       tc::mbar_init(s_free + b, 1);
-      tc::mbar_init(p_full + b, kSoftmaxWarps / 2);  // the tile's warp group
+      tc::mbar_init(p_full + b, 4);  // the tile's warp group
     }
-    tc::mbar_init(q_ready, kSoftmaxWarps / 2);
-    tc::mbar_init(q_ready + 1, kSoftmaxWarps / 2);
+    tc::mbar_init(q_ready, 4);
+    tc::mbar_init(q_ready + 1, 4);
+    for (int b = 0; b < 4 * kGroups; ++b) tc::mbar_init(hand + b, 1);
+    for (int b = 0; b < kGroups; ++b) tc::mbar_init(lpub + b, 4);
     for (int b = 0; b < kMetaSlots; ++b) {
       tc::mbar_init(m_full + b, 1);
       tc::mbar_init(m_empty + b, kSoftmaxWarps + 3);  // softmax + QK + PV + V warps
@@ -396,6 +412,12 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if constexpr (kGroups > 2) {  // rebalance the register file towards the softmax groups
+    if (warp >= kSoftmaxWarps)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtl));
+    else
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
+  }
 
   if (warp == kWarpProducer) {
     // ============================ producer: tile stream + metadata + K loads ====
@@ -720,28 +742,27 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     WAITP_FLUSH(3);
   } else {
     // ============================= softmax / correction / epilogue ====
-    // Two warp groups take alternate tiles of the stream (group g: tiles T with
-    // T % 2 == g); within a group, warp = TMEM lane quadrant and thread = query row
-    // with all 64 columns of the tile.  The groups run out of phase -- one computes
-    // a tile's max while the other exponentiates the previous tile -- and hand the
-    // row's running max over per tile through shared memory with named barriers
-    // (quadrant q: id 1 + q for group 0 -> 1, id 5 + q for 1 -> 0; strictly
-    // alternating arrive / sync).  Each group keeps its own partial row sum l
-    // expressed at the max it last used; the owner of an item's last tile combines
-    // both (the other group's (l, m) published before its P release) in the epilogue.
+    // kGroups warp groups take the tiles of the stream in turn (group g: tiles T with
+    // T % kGroups == g); within a group, warp = TMEM lane quadrant and thread = query
+    // row with all 64 columns of the tile.  The groups run out of phase -- one computes
+    // a tile's max while the others exponentiate earlier tiles -- and pass the row's
+    // running max on per tile through shared memory, signalled on an mbarrier per
+    // (group, quadrant).  Each group keeps its own partial row sum l expressed at the max
+    // it last used; the owner of an item's last tile combines all of them (each published
+    // before the group's P release) in the epilogue.
     const int wq = warp & 3;       // TMEM lane quadrant
-    const int grp = warp >> 2;     // warp group: tiles of this parity
+    const int grp = warp >> 2;     // warp group
     const int r = wq * 32 + lane;
     const uint32_t lane_base = uint32_t(wq * 32) << 16;
-    float* mbuf = reinterpret_cast<float*>(smem + OFF_RED);        // [2][128] m after tile T
-    float2* lbuf = reinterpret_cast<float2*>(smem + OFF_RED + 1024);  // [2][2][128] (l, m)
-    const uint32_t bar_in = grp == 0 ? 5 + wq : 1 + wq;   // other group -> this group
-    const uint32_t bar_out = grp == 0 ? 1 + wq : 5 + wq;  // this group -> other group
-    uint32_t T = 0, M = 0;
+    float* mbuf = reinterpret_cast<float*>(smem + OFF_RED);  // [kGroups][128] m after tile
+    float2* lbuf = reinterpret_cast<float2*>(smem + OFF_RED + kGroups * 128 * 4);
+    const tc::SBar h_in = hand + (((grp + kGroups - 1) % kGroups) * 4 + wq);  // predecessor
+    const tc::SBar h_out = hand + (grp * 4 + wq);
+    uint32_t T = 0, M = 0, T_first = 0;
     float l = 0.f, m_used = -INFINITY;  // this group's partial sum, at max m_used
     float m_init = -INFINITY;           // running max at the item start (key-window passes)
     Item qi{};  // only i0 / rend / h used by rotate_q
-    if (grp == 1) asm volatile("bar.arrive %0, 64;" ::"r"(bar_out) : "memory");  // T = 0 is g0's
+    if (grp == kGroups - 1 && lane == 0) tc::mbar_arrive(h_out);  // tile 0: no predecessor
     auto rotate_row = [&](int pattern, int qbuf) {
       rotate_q(p, qi, pattern, r, 0, tmem + lane_base, qbuf);
       rotate_q(p, qi, pattern, r, 1, tmem + lane_base, qbuf);
@@ -760,16 +781,12 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #endif
       const TileMeta& mt = metas[slot];
       const int kind = mt.kind, flags = mt.flags;
-      if (kind == T_END) {
-        if ((T & 1) == uint32_t(grp))  // match the last tile's hand-off (or the initial one)
-          asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
-        break;
-      }
+      if (kind == T_END) break;
       const int64_t i0 = mt.i0, rend = mt.rend;
       const int h = mt.h;
       const int64_t i = i0 + r;
       const bool row_ok = i < rend;
-      const bool mine = kind != T_EMPTY && (T & 1) == uint32_t(grp);
+      const bool mine = kind != T_EMPTY && T % kGroups == uint32_t(grp);
       uint64_t mask = 0;
       if (mine && row_ok) {
         if (kind == T_VERT) {
@@ -804,9 +821,10 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         }
         continue;
       }
-      if (flags & F_FIRST) {  // both groups start the item (partial sums, Q rotation rows)
+      if (flags & F_FIRST) {  // every group starts the item (partial sums, Q rotation rows)
         l = 0.f;
         m_used = -INFINITY;
+        T_first = T;
         qi.i0 = i0;
         qi.rend = rend;
         qi.h = h;
@@ -819,10 +837,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       const long long t_first = clock64();
       t_own = t_first;
 #endif
+      const uint32_t k = T / kGroups;  // this group's tile index (hand-off phase)
       if (flags & F_FIRST) {
-        // the other group's epilogue of the previous item (its last tile, T - 1) has read
-        // O and S(T - 1) is consumed, so O / Q of this CTA's TMEM are free
-        asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
+        // the previous item's last tile (T - 1, another group) finished its epilogue: O is
+        // read and S(T - 1) consumed, so O / Q of this CTA's TMEM are free
+        tc::mbar_wait(h_in, k & 1);
         tc::tc_fence_after();
         m_init = -INFINITY;
         if (p.init) {
@@ -897,12 +916,13 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       wacc[5] += clock64() - t_sg;
 #endif
       // ---- running max: previous tile's (other group) unless the item starts here
-      if (!(flags & F_FIRST)) asm volatile("bar.sync %0, 64;" ::"r"(bar_in) : "memory");
-      const float m_prev = (flags & F_FIRST) ? m_init : mbuf[((T - 1) & 1) * 128 + r];
+      if (!(flags & F_FIRST)) tc::mbar_wait(h_in, k & 1);
+      const float m_prev =
+          (flags & F_FIRST) ? m_init : mbuf[((T + kGroups - 1) % kGroups) * 128 + r];
       // lazy rescale: the max moves only past a threshold (P <= 2^8 in fp16)
       const bool need = tmax > m_prev + kRescaleThresh;
       const float m = need ? tmax : m_prev;
-      mbuf[(T & 1) * 128 + r] = m;
+      mbuf[grp * 128 + r] = m;
 #ifdef LCX_TC_TRACE_SM  // column 1: flags | kind << 8 | rescale << 12 (a value, not a time)
       if (wq == 0 && lane == 0) {
         trace_mark(p, T, 0);
@@ -912,7 +932,10 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       }
 #endif
       // an item's last tile hands over only after its epilogue (next item's O / Q)
-      if (!(flags & F_LAST)) asm volatile("bar.arrive %0, 64;" ::"r"(bar_out) : "memory");
+      if (!(flags & F_LAST)) {
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(h_out);
+      }
 #ifdef LCX_TC_WAITPROF
       const long long t_ex = clock64();
 #endif
@@ -961,10 +984,13 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       tc::tmem_wait_st();
       l += rs2.x + rs2.y;
       // partial (l, m) for the item's epilogue (ordered before the P release below)
-      lbuf[(((T >> 1) & 1) * 2 + grp) * 128 + r] = make_float2(l, m_used);
+      lbuf[((k & 1) * kGroups + grp) * 128 + r] = make_float2(l, m_used);
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(p_full + b);
+      if (lane == 0) {
+        tc::mbar_arrive(p_full + b);
+        tc::mbar_arrive(lpub + grp);
+      }
 #ifdef LCX_TC_WAITPROF
       wacc[6] += clock64() - t_ex;
 #endif
@@ -977,10 +1003,12 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         // ---- epilogue: add the other group's partial sum, wait for the last PV,
         // normalize, store ----
         float lt = l;
-        if (!(flags & F_FIRST)) {
-          const uint32_t To = T - 1;  // the other group's last tile of this item
-          tc::mbar_wait(p_full + (To % NS), (To / NS) & 1);
-          const float2 lo = lbuf[(((To >> 1) & 1) * 2 + (grp ^ 1)) * 128 + r];
+#pragma unroll
+        for (uint32_t d = 1; d < uint32_t(kGroups); ++d) {  // the other groups' last tiles
+          if (T < T_first + d) break;
+          const uint32_t To = T - d, go = To % kGroups, ko = To / kGroups;
+          tc::mbar_wait(lpub + int(go), ko & 1);
+          const float2 lo = lbuf[((ko & 1) * kGroups + go) * 128 + r];
           if (lo.x > 0.f) lt += lo.x * ex2(lo.y - m);
         }
         tc::mbar_wait(s_free + b, ph);  // this item's last PV is complete
@@ -1003,7 +1031,8 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           p.lse[int64_t(h) * p.lse_stride + i] =
               lt > 0.f ? (m + log2f(lt)) * 0.69314718055994530942f : -INFINITY;
         tc::tc_fence_before();
-        asm volatile("bar.arrive %0, 64;" ::"r"(bar_out) : "memory");
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(h_out);
 
       }
 #ifdef LCX_TC_WAITPROF
