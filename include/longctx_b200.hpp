@@ -351,6 +351,10 @@ std::vector<ChunkCostSample> measure_chunk_costs(
 // Non-negative least-squares fit of the four CostModel coefficients to measured chunk
 // costs (Error("config") when fewer than one sample).
 CostModel fit_cost_model(const std::vector<ChunkCostSample>& samples);
+// The per-chunk selection log of a chunked prefill as the reference CLI writes it
+// (prefill_selections.json, harness.cpp:430-438, without its configHash / version keys).
+std::string prefill_selections_json(const PrefillState& state);
+std::vector<ChunkSelection> prefill_selections_from_json(const std::string& text);
 
 enum class Precision { F32, BF16 };
 // Device storage type of q / k / v for the calls made by this thread (default F32:

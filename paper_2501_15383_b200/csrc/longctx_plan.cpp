@@ -330,12 +330,68 @@ SparsityPlan SparsityPlan::from_json(const std::string& text) {  // sparse.cpp:5
 }
 
 // ------------------------------------------------------------ CriticalSet --
-std::string CriticalSet::to_json() const {  // sparse.cpp:121-125
-  return json_object({{"contextLength", std::to_string(context_length)},
-                      {"slashes", json_array(slashes, 2)},
-                      {"verticals", json_array(verticals, 2)}},
-                     0);
+namespace {
+std::string crit_json(const CriticalSet& c, int ind) {  // sparse.cpp:121-125
+  return json_object({{"contextLength", std::to_string(c.context_length)},
+                      {"slashes", json_array(c.slashes, ind + 2)},
+                      {"verticals", json_array(c.verticals, ind + 2)}},
+                     ind);
 }
+}  // namespace
+
+std::string CriticalSet::to_json() const { return crit_json(*this, 0); }
+
+namespace b200 {
+std::string prefill_selections_json(const PrefillState& state) {  // harness.cpp:430-438
+  std::string arr;
+  if (state.selections.empty()) {
+    arr = "[]";
+  } else {
+    arr = "[\n";
+    for (std::size_t x = 0; x < state.selections.size(); ++x) {
+      const ChunkSelection& cs = state.selections[x];
+      arr += indent(4) + json_object({{"begin", std::to_string(cs.begin)},
+                                      {"chunk", std::to_string(cs.chunk_index)},
+                                      {"critical", crit_json(cs.critical, 6)},
+                                      {"end", std::to_string(cs.end)}},
+                                     4);
+      arr += x + 1 < state.selections.size() ? ",\n" : "\n";
+    }
+    arr += indent(2) + "]";
+  }
+  return json_object({{"selections", arr}}, 0);
+}
+
+std::vector<ChunkSelection> prefill_selections_from_json(const std::string& text) {
+  const JVal j = Parser(text).parse();
+  const JVal* sel = j.kind == JVal::Obj ? j.find("selections") : nullptr;
+  if (!sel || sel->kind != JVal::Arr) fail(errkind::schema, "prefill selections need a \"selections\" array");
+  std::vector<ChunkSelection> out;
+  for (const JVal& e : sel->arr) {
+    const JVal* b = e.kind == JVal::Obj ? e.find("begin") : nullptr;
+    const JVal* c = e.kind == JVal::Obj ? e.find("chunk") : nullptr;
+    const JVal* en = e.kind == JVal::Obj ? e.find("end") : nullptr;
+    const JVal* cr = e.kind == JVal::Obj ? e.find("critical") : nullptr;
+    if (!b || !c || !en || !cr || cr->kind != JVal::Obj)
+      fail(errkind::schema, "a selection needs begin, chunk, end and critical");
+    ChunkSelection cs;
+    cs.begin = as_size(*b, "begin");
+    cs.chunk_index = as_size(*c, "chunk");
+    cs.end = as_size(*en, "end");
+    const JVal* n = cr->find("contextLength");
+    const JVal* v = cr->find("verticals");
+    const JVal* sl = cr->find("slashes");
+    if (!n || !v || !sl) fail(errkind::schema, "critical set needs contextLength, verticals and slashes");
+    cs.critical.context_length = as_size(*n, "contextLength");
+    cs.critical.verticals = as_size_array(*v, "verticals");
+    cs.critical.slashes = as_size_array(*sl, "slashes");
+    sort_unique(cs.critical.verticals);
+    sort_unique(cs.critical.slashes);
+    out.push_back(std::move(cs));
+  }
+  return out;
+}
+}  // namespace b200
 
 CriticalSet CriticalSet::from_json(const std::string& text) {  // sparse.cpp:127-135
   const JVal j = Parser(text).parse();

@@ -3,7 +3,7 @@
 // code and checked against fixtures the REFERENCE produced (tests/golden/
 // make_refine_golden.py).
 //
-//   plan_parity --json <ref_critical_set.json> <ref_plan_refined.json>
+//   plan_parity --json <ref_critical_set.json> <ref_plan_refined.json> <ref_prefill_selections.json>
 //       CPU: our JSON text equals the text the reference CLI wrote (minus the two
 //       bookkeeping keys its harness adds), round trips, and the error kinds of malformed
 //       plans (schema_violation / parse_error / config).
@@ -66,6 +66,24 @@ static std::string kind_of(F&& f) {
     return e.kind();
   }
   return "none";
+}
+
+static int selections_check(const std::string& path) {
+  // prefill_selections.json of the reference CLI (harness.cpp:430-438): parse, re-emit,
+  // compare the text; the example config's four chunk selections
+  const std::string text = slurp(path);
+  PrefillState st;
+  st.selections = b200::prefill_selections_from_json(text);
+  CHECK(st.selections.size() == 4);
+  if (st.selections.size() == 4) {
+    CHECK((st.selections[0].critical.verticals == std::vector<std::size_t>{0, 64, 171}));
+    CHECK(st.selections[3].begin == 768 && st.selections[3].end == 1024);
+  }
+  CHECK(b200::prefill_selections_json(st) == strip_harness_keys(text));
+  CHECK(b200::prefill_selections_json(PrefillState{}) == "{\n  \"selections\": []\n}");
+  CHECK(kind_of([] { b200::prefill_selections_from_json("{\"selections\": [{}]}"); }) ==
+        "schema_violation");
+  return 0;
 }
 
 static int json_mode(const std::string& crit_path, const std::string& plan_path) {
@@ -363,7 +381,10 @@ static int measure_mode() {
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "";
   try {
-    if (mode == "--json" && argc == 4) return json_mode(argv[2], argv[3]);
+    if (mode == "--json" && argc == 5) {
+      selections_check(argv[4]);
+      return json_mode(argv[2], argv[3]);
+    }
     if (mode == "--refine" && argc == 3) return refine_mode(argv[2]);
     if (mode == "--dcpp" && argc == 3) return dcpp_mode(argv[2]);
     if (mode == "--measure" && argc == 2) return measure_mode();

@@ -9,7 +9,8 @@ library compiled in place (oracle/_ref/liblongctx_ref.so), runs it, and writes i
 output (calibration inputs, configs, and the reference's refine_plan / offline_search
 results and CriticalSet / SparsityPlan JSON) to refine_golden.txt.  It also copies the
 reference's own committed JSON outputs proj/out/sparsity/critical_set.json and
-proj/out/refine/plan_refined.json (files the reference CLI wrote) as ref_*.json: their
+proj/out/refine/plan_refined.json, proj/out/sparsity/prefill_selections.json (files
+the reference CLI wrote) as ref_*.json: their
 text pins the JSON formatting (the nlohmann bundled here prints arrays inline, the
 reference's build one element per line).  The GPU box only reads the committed files.
 """
@@ -40,6 +41,8 @@ def main():
         f.write(dc)
     shutil.copy(REF + "/out/sparsity/critical_set.json", os.path.join(HERE, "ref_critical_set.json"))
     shutil.copy(REF + "/out/refine/plan_refined.json", os.path.join(HERE, "ref_plan_refined.json"))
+    shutil.copy(REF + "/out/sparsity/prefill_selections.json",
+                os.path.join(HERE, "ref_prefill_selections.json"))
     print("wrote refine_golden.txt,", len(out), "bytes")
 
 

@@ -2,8 +2,9 @@
 the C++ drop-in (tests/cpp/plan_parity.cpp), against fixtures the reference produced
 (tests/golden/make_refine_golden.py), plus DCPP chunk sizing (§8(f) row 4):
 
-  * CPU: CriticalSet / SparsityPlan JSON text equals what the reference CLI wrote
-    (proj/out/sparsity/critical_set.json, proj/out/refine/plan_refined.json), round trips,
+  * CPU: CriticalSet / SparsityPlan / prefill-selection JSON text equals what the
+    reference CLI wrote (proj/out/sparsity/critical_set.json, prefill_selections.json,
+    proj/out/refine/plan_refined.json), round trips,
     and malformed plans / configs raise the reference's error kinds;
   * GPU: refine_plan and offline_search reproduce the reference's budgets, rounds and
     plans exactly and its recalls within 1e-4, on the reference's refinement scenarios
@@ -35,7 +36,8 @@ def build_binary():
 
 def test_plan_json_matches_reference_text():
     r = subprocess.run([build_binary(), "--json", os.path.join(GOLD, "ref_critical_set.json"),
-                        os.path.join(GOLD, "ref_plan_refined.json")],
+                        os.path.join(GOLD, "ref_plan_refined.json"),
+                        os.path.join(GOLD, "ref_prefill_selections.json")],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
 
