@@ -56,10 +56,10 @@ constexpr int kSoftmaxWarps = 4 * kGroups;
 constexpr int kThreads = 32 * (kSoftmaxWarps + 4);
 constexpr int kWarpProducer = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1,
               kWarpPv = kSoftmaxWarps + 2, kWarpV = kSoftmaxWarps + 3;
-// registers: with more than two groups the launch grants 65536 / kThreads per thread;
-// the control warp group gives some up (setmaxnreg) for the softmax groups
-constexpr int kRegCtl = 72;
-constexpr int kRegSoftmax = ((65536 - 128 * kRegCtl) / (32 * kSoftmaxWarps)) / 8 * 8;
+// The softmax code is written for any number of groups, but a third group needs more
+// registers than 65536 / 512 per thread: compiled at 128 it spills ~2.6 KB and ran 3.4x
+// slower (setmaxnreg does not help: ptxas still allocates for the launch-time limit).
+static_assert(kGroups == 2, "the register file holds two softmax groups of 168-register warps");
 // two S buffers suffice (NS = 2, 3, 4 measure the same); the TMEM they free holds a
 // second rotated Q, so the Q of the next DCA pattern is in place before its first QK
 constexpr int NK = 4, NV = 4, NS = 2;                // K / V smem stages, S (+P) TMEM buffers
@@ -412,12 +412,6 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if constexpr (kGroups > 2) {  // rebalance the register file towards the softmax groups
-    if (warp >= kSoftmaxWarps)
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegCtl));
-    else
-      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegSoftmax));
-  }
 
   if (warp == kWarpProducer) {
     // ============================ producer: tile stream + metadata + K loads ====
