@@ -62,7 +62,12 @@ constexpr int kWarpProducer = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1,
 static_assert(kGroups == 2, "the register file holds two softmax groups of 168-register warps");
 // two S buffers suffice (NS = 2, 3, 4 measure the same); the TMEM they free holds a
 // second rotated Q, so the Q of the next DCA pattern is in place before its first QK
-constexpr int NK = 4, NV = 4, NS = 2;                // K / V smem stages, S (+P) TMEM buffers
+#ifndef LCX_TC_QBUFS
+#define LCX_TC_QBUFS 2
+#endif
+// two rotated-Q buffers with two S buffers, or one Q buffer with four S buffers
+constexpr int kQBufs = LCX_TC_QBUFS;
+constexpr int NK = 4, NV = 4, NS = kQBufs == 2 ? 2 : 4;  // K / V smem stages, S (+P) TMEM
 constexpr uint32_t kKHalf = BN * 64 * 2;             // 8 KB
 constexpr uint32_t kKStage = 4 * kKHalf;             // hi0 hi1 lo0 lo1 = 32 KB
 constexpr uint32_t kVStage = HD * BN * 2;            // 16 KB
@@ -599,7 +604,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       WAITP(0, tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1));
       const int kind = metas[slot].kind;
       const int flags = metas[slot].flags;
-      const int qb = metas[slot].grp & 1;  // Q buffer of the tile's pattern group
+      const int qb = kQBufs == 2 ? (metas[slot].grp & 1) : 0;  // Q buffer of the tile's group
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(m_empty + slot);
       ++M;
@@ -799,7 +804,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           mask = lim >= 63 ? ~0ull : (lim < 0 ? 0ull : ((2ull << lim) - 1));
         }
       }
-      const int pattern = mt.pattern, tgrp = mt.grp, ng = mt.ng;
+      const int pattern = mt.pattern, tgrp = mt.grp, ng = mt.ng, next_pattern = mt.next_pattern;
       const int gpat1 = mt.gpat[1], gpat2 = mt.gpat[2];
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(m_empty + slot);
@@ -863,8 +868,12 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           tc::tmem_wait_st();
         }
         // group 0's Q, and group 1's into the other buffer ahead of its first QK
-        rotate_row(pattern, tgrp & 1);
-        if (tgrp + 1 < ng) rotate_row(gpat1, (tgrp + 1) & 1);
+        if constexpr (kQBufs == 2) {
+          rotate_row(pattern, tgrp & 1);
+          if (tgrp + 1 < ng) rotate_row(gpat1, (tgrp + 1) & 1);
+        } else {
+          rotate_row(pattern, 0);
+        }
       }
 #ifdef LCX_TC_WAITPROF
       wacc[2] += clock64() - t_first;  // item start: hand-over wait, O restore, Q rotations
@@ -886,7 +895,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       const long long t_sg = clock64();
 #endif
       // the group's QKs are complete: its Q buffer takes the group after next
-      if ((flags & F_EPOCH_AFTER) && tgrp + 2 < ng) rotate_row(gpat2, tgrp & 1);
+      if constexpr (kQBufs == 2) {
+        if ((flags & F_EPOCH_AFTER) && tgrp + 2 < ng) rotate_row(gpat2, tgrp & 1);
+      } else {
+        if (flags & F_EPOCH_AFTER) rotate_row(next_pattern, 0);  // old pattern's QKs done
+      }
 #ifdef LCX_TC_FAKE_SOFTMAX  // timing experiment only: no softmax math
       for (int cc = 0; cc < 64; ++cc) sv[cc] = -INFINITY;
       mask = ~0ull;
