@@ -454,6 +454,10 @@ TC_CASES = [
     (1024, 2, 1, 512, 32, (10, 600), (512, 1024, 512), (False, False), "peaked", 1.0),
     (768, 4, 4, 128, 128, (5, 40), (128, 300, 128), (True, True), "peaked", 1.0),
     (1280, 7, 1, 640, 64, (64, 6), None, (True, False), "normal", 1.0),
+    # ragged sequence end (last block / tile partial) under DCA
+    (1000, 6, 2, 256, 64, (30, 90), (256, 640, 256), (True, True), "normal", 0.9),
+    # budgets beyond the context: every line selected (select k >= n)
+    (640, 4, 2, 128, 64, (1000, 1000), None, (True, True), "peaked", 1.0),
 ]
 
 
