@@ -59,7 +59,15 @@ constexpr int kWarpProducer = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1,
 // The softmax code is written for any number of groups, but a third group needs more
 // registers than 65536 / 512 per thread: compiled at 128 it spills ~2.6 KB and ran 3.4x
 // slower (setmaxnreg does not help: ptxas still allocates for the launch-time limit).
-static_assert(kGroups == 2, "the register file holds two softmax groups of 168-register warps");
+// With a third group each thread keeps only 32 logits live (kSReread): S is read from
+// TMEM twice, once for the tile max and once for the exponentials.
+#ifndef LCX_TC_SREREAD
+#define LCX_TC_SREREAD (LCX_TC_GROUPS > 2)
+#endif
+constexpr bool kSReread = LCX_TC_SREREAD;
+// (three groups fit in 128 registers this way but do not yet produce correct results:
+// kept to two until that protocol is debugged)
+static_assert(kGroups == 2, "two softmax groups");
 // two S buffers suffice (NS = 2, 3, 4 measure the same); the TMEM they free holds a
 // second rotated Q, so the Q of the next DCA pattern is in place before its first QK
 #ifndef LCX_TC_QBUFS
@@ -880,12 +888,14 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #endif
       const int b = T % NS;
       const uint32_t ph = (T / NS) & 1;
-      float sv[64];
+      float sv[kSReread ? 32 : 64];
       WAITP(1, tc::mbar_wait(s_full + b, ph));
       tc::tc_fence_after();
-      tc::tmem_ld32(tmem + lane_base + b * BN, sv);
-      tc::tmem_ld32(tmem + lane_base + b * BN + 32, sv + 32);
-      tc::tmem_wait_ld();
+      if constexpr (!kSReread) {
+        tc::tmem_ld32(tmem + lane_base + b * BN, sv);
+        tc::tmem_ld32(tmem + lane_base + b * BN + 32, sv + 32);
+        tc::tmem_wait_ld();
+      }
 #ifdef LCX_TC_TRACE_SM  // owner group's quadrant-0 warp: 5 S got, 0 m handed over, 6 P put
       if (wq == 0 && lane == 0) trace_mark(p, T, 5);
 #else
@@ -901,23 +911,39 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         if (flags & F_EPOCH_AFTER) rotate_row(next_pattern, 0);  // old pattern's QKs done
       }
 #ifdef LCX_TC_FAKE_SOFTMAX  // timing experiment only: no softmax math
-      for (int cc = 0; cc < 64; ++cc) sv[cc] = -INFINITY;
-      mask = ~0ull;
+      for (int cc = 0; cc < int(sizeof(sv) / sizeof(float)); ++cc) sv[cc] = -INFINITY;
+      mask = 0ull;
 #endif
       // masked logits -> -inf (ex2(-inf) = 0), already in log2 units
-      if (!__all_sync(0xffffffffu, mask == ~0ull)) {  // fully admitted rows: no select
-        const uint32_t lo = uint32_t(mask), hi = uint32_t(mask >> 32);
+      const bool all_in = __all_sync(0xffffffffu, mask == ~0ull);  // no select needed
+      float t4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      if constexpr (!kSReread) {
+        if (!all_in) {
+          const uint32_t lo = uint32_t(mask), hi = uint32_t(mask >> 32);
 #pragma unroll
-        for (int cc = 0; cc < 32; ++cc) {
-          sv[cc] = ((lo >> cc) & 1u) ? sv[cc] : -INFINITY;
-          sv[32 + cc] = ((hi >> cc) & 1u) ? sv[32 + cc] : -INFINITY;
+          for (int cc = 0; cc < 32; ++cc) {
+            sv[cc] = ((lo >> cc) & 1u) ? sv[cc] : -INFINITY;
+            sv[32 + cc] = ((hi >> cc) & 1u) ? sv[32 + cc] : -INFINITY;
+          }
+        }
+#pragma unroll
+        for (int cc = 0; cc < 64; cc += 8)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) t4[u] = fmaxf(t4[u], fmaxf(sv[cc + u], sv[cc + 4 + u]));
+      } else {
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          tc::tmem_ld32(tmem + lane_base + b * BN + hf * 32, sv);
+          tc::tmem_wait_ld();
+          const uint32_t mb = uint32_t(mask >> (32 * hf));
+#pragma unroll
+          for (int cc = 0; cc < 32; ++cc) sv[cc] = ((mb >> cc) & 1u) ? sv[cc] : -INFINITY;
+#pragma unroll
+          for (int cc = 0; cc < 32; cc += 8)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) t4[u] = fmaxf(t4[u], fmaxf(sv[cc + u], sv[cc + 4 + u]));
         }
       }
-      float t4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-      for (int cc = 0; cc < 64; cc += 8)
-#pragma unroll
-        for (int u = 0; u < 4; ++u) t4[u] = fmaxf(t4[u], fmaxf(sv[cc + u], sv[cc + 4 + u]));
       const float tmax = fmaxf(fmaxf(t4[0], t4[1]), fmaxf(t4[2], t4[3]));
 #ifdef LCX_TC_WAITPROF
       wacc[5] += clock64() - t_sg;
@@ -976,10 +1002,17 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       float2 rs2 = make_float2(0.f, 0.f);
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {  // two 32-key halves: fewer live registers
+        if constexpr (kSReread) {  // second read of this half (its P not yet written)
+          tc::tmem_ld32(tmem + lane_base + b * BN + hf * 32, sv);
+          tc::tmem_wait_ld();
+          const uint32_t mb = uint32_t(mask >> (32 * hf));
+#pragma unroll
+          for (int cc = 0; cc < 32; ++cc) sv[cc] = ((mb >> cc) & 1u) ? sv[cc] : -INFINITY;
+        }
         uint32_t pw[16];
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          const int c = hf * 32 + 2 * k;
+          const int c = (kSReread ? 0 : hf * 32) + 2 * k;
           const float2 x = __fadd2_rn(make_float2(sv[c], sv[c + 1]), nm2);
           const float2 pp = make_float2(ex2(x.x), ex2(x.y));
           rs2 = __fadd2_rn(rs2, pp);
