@@ -67,7 +67,9 @@ constexpr int kWarpProducer = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1,
 constexpr bool kSReread = LCX_TC_SREREAD;
 // (three groups fit in 128 registers this way but do not yet produce correct results:
 // kept to two until that protocol is debugged)
+#ifndef LCX_TC_ALLOW_GROUPS3
 static_assert(kGroups == 2, "two softmax groups");
+#endif
 // two S buffers suffice (NS = 2, 3, 4 measure the same); the TMEM they free holds a
 // second rotated Q, so the Q of the next DCA pattern is in place before its first QK
 #ifndef LCX_TC_QBUFS
