@@ -76,8 +76,19 @@ static_assert(kGroups == 2, "two softmax groups");
 #define LCX_TC_QBUFS 2
 #endif
 // two rotated-Q buffers with two S buffers, or one Q buffer with four S buffers
-constexpr int kQBufs = LCX_TC_QBUFS;
-constexpr int NK = 4, NV = 4, NS = kQBufs == 2 ? 2 : 4;  // K / V smem stages, S (+P) TMEM
+// Split O (LCX_TC_SPLIT_O): each softmax group accumulates its own tiles into its own O
+// in TMEM, at its own running max, and the two are merged in the item's epilogue -- the
+// groups no longer hand the running max to each other tile by tile.  TMEM then holds
+// two S buffers, two O and one rotated-Q buffer.
+#ifndef LCX_TC_SPLIT_O
+#define LCX_TC_SPLIT_O 0
+#endif
+constexpr bool kSplitO = LCX_TC_SPLIT_O;
+constexpr int kQBufs = kSplitO ? 1 : LCX_TC_QBUFS;
+constexpr int kOBufs = kSplitO ? kGroups : 1;
+constexpr int NK = 4, NV = 4;  // K / V smem stages
+constexpr int NS = (kSplitO || kQBufs == 2) ? 2 : 4;  // S (+P) TMEM buffers
+static_assert(!kSplitO || NS == kGroups, "split O: S(T) full implies PV(T - kGroups) done");
 constexpr uint32_t kKHalf = BN * 64 * 2;             // 8 KB
 constexpr uint32_t kKStage = 4 * kKHalf;             // hi0 hi1 lo0 lo1 = 32 KB
 constexpr uint32_t kVStage = HD * BN * 2;            // 16 KB
@@ -99,7 +110,8 @@ constexpr uint32_t kSmemBytes =
 // pattern group x of an item uses Q buffer x & 1.
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t COL_O = NS * BN;
-constexpr uint32_t COL_Q = COL_O + HD;  // Q buffer b: hi at COL_Q + 128 b, lo at + 64
+constexpr uint32_t COL_Q = COL_O + kOBufs * HD;  // Q buffer b: hi at COL_Q + 128 b, lo at + 64
+static_assert(COL_Q + kQBufs * HD <= 512, "TMEM columns");
 constexpr uint32_t QBUF = HD;
 constexpr float kRescaleThresh = 8.f;
 
@@ -378,9 +390,10 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
   const tc::SBar m_empty = m_full + kMetaSlots;  // [kMetaSlots]
   const tc::SBar hand = m_empty + kMetaSlots;    // [kGroups][4] running max of a tile ready
   const tc::SBar lpub = hand + 4 * kGroups;      // [kGroups] partial sums of a tile written
+  const tc::SBar edone = lpub + kGroups;         // split O: an item's epilogue read both O
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR) +
-                        2 * (2 * NK + 2 * NV + 3 * NS + 2 + 2 * kMetaSlots + 5 * kGroups);
-  static_assert((2 * NK + 2 * NV + 3 * NS + 2 + 2 * kMetaSlots + 5 * kGroups + 1) * 8 <= 1024,
+                        2 * (2 * NK + 2 * NV + 3 * NS + 2 + 2 * kMetaSlots + 5 * kGroups + 1);
+  static_assert((2 * NK + 2 * NV + 3 * NS + 2 + 2 * kMetaSlots + 5 * kGroups + 2) * 8 <= 1024,
                 "barrier area overflow");
   TileMeta* metas = reinterpret_cast<TileMeta*>(smem + OFF_META);
 
@@ -407,6 +420,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     tc::mbar_init(q_ready + 1, 4);
     for (int b = 0; b < 4 * kGroups; ++b) tc::mbar_init(hand + b, 1);
     for (int b = 0; b < kGroups; ++b) tc::mbar_init(lpub + b, 4);
+    tc::mbar_init(edone, 4);
     for (int b = 0; b < kMetaSlots; ++b) {
       tc::mbar_init(m_full + b, 1);
       tc::mbar_init(m_empty + b, kSoftmaxWarps + 3);  // softmax + QK + PV + V warps
@@ -709,7 +723,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     WAITP_FLUSH(2);
   } else if (warp == kWarpPv) {
     // ============================================== PV issuer (O += P V) ====
-    uint32_t T = 0, M = 0;
+    uint32_t T = 0, M = 0, T_first = 0;
     const uint64_t dv0 = tc::sdesc_sw128(tc::smem_u32(smem + OFF_V));
     for (;;) {
       const int slot = M % kMetaSlots;
@@ -735,11 +749,16 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #endif
       tc::tc_fence_after();
       const uint64_t dv = dv0 + ((bv * kVStage) >> 4);
-      const bool first = (flags & F_FIRST) != 0;
+      if (flags & F_FIRST) T_first = T;
+      // the first PV into an O of the item overwrites it (a key-window pass > 0 restored
+      // the running O into the first tile's O)
+      const bool first = kSplitO ? (T - T_first < uint32_t(kGroups) && !(p.init && T == T_first))
+                                 : ((flags & F_FIRST) && !p.init);
+      const uint32_t dO = tmem + COL_O + (kSplitO ? (T % kGroups) * HD : 0);
 #pragma unroll
       for (int kk = 0; kk < BN / 16; ++kk)  // P (fp16, 2 per column) aliases S buffer bs
-        tc::mma_f16_ts_warp(tmem + COL_O, tmem + bs * BN + kk * 8, dv + ((kk * 32) >> 4),
-                            IDESC_PV, (first && !p.init && kk == 0) ? 0u : 1u);
+        tc::mma_f16_ts_warp(dO, tmem + bs * BN + kk * 8, dv + ((kk * 32) >> 4),
+                            IDESC_PV, (first && kk == 0) ? 0u : 1u);
       tc::mma_commit_warp(v_empty + bv);
       tc::mma_commit_warp(s_free + bs);
       if (lane == 0) trace_mark(p, T, 4);
@@ -763,6 +782,8 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     const int grp = warp >> 2;     // warp group
     const int r = wq * 32 + lane;
     const uint32_t lane_base = uint32_t(wq * 32) << 16;
+    const uint32_t col_o = COL_O + (kSplitO ? uint32_t(grp) * HD : 0u);  // this group's O
+    uint32_t J = 0, J_cur = 0;  // split O: items started, index of the current one
     float* mbuf = reinterpret_cast<float*>(smem + OFF_RED);  // [kGroups][128] m after tile
     float2* lbuf = reinterpret_cast<float2*>(smem + OFF_RED + kGroups * 128 * 4);
     const tc::SBar h_in = hand + (((grp + kGroups - 1) % kGroups) * 4 + wq);  // predecessor
@@ -771,7 +792,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     float l = 0.f, m_used = -INFINITY;  // this group's partial sum, at max m_used
     float m_init = -INFINITY;           // running max at the item start (key-window passes)
     Item qi{};  // only i0 / rend / h used by rotate_q
-    if (grp == kGroups - 1 && lane == 0) tc::mbar_arrive(h_out);  // tile 0: no predecessor
+    if (!kSplitO && grp == kGroups - 1 && lane == 0) tc::mbar_arrive(h_out);  // tile 0
     auto rotate_row = [&](int pattern, int qbuf) {
       rotate_q(p, qi, pattern, r, 0, tmem + lane_base, qbuf);
       rotate_q(p, qi, pattern, r, 1, tmem + lane_base, qbuf);
@@ -834,6 +855,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         l = 0.f;
         m_used = -INFINITY;
         T_first = T;
+        J_cur = J++;
         qi.i0 = i0;
         qi.rend = rend;
         qi.h = h;
@@ -847,11 +869,19 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       t_own = t_first;
 #endif
       const uint32_t k = T / kGroups;  // this group's tile index (hand-off phase)
+      if (kSplitO && T - T_first < uint32_t(kGroups) && J_cur > 0) {
+        // this group's first tile of the item: the previous item's epilogue has read both
+        // O (this group's next PV overwrites its O) and its QKs are done (Q is free)
+        tc::mbar_wait(edone, (J_cur - 1) & 1);
+        tc::tc_fence_after();
+      }
       if (flags & F_FIRST) {
         // the previous item's last tile (T - 1, another group) finished its epilogue: O is
         // read and S(T - 1) consumed, so O / Q of this CTA's TMEM are free
-        tc::mbar_wait(h_in, k & 1);
-        tc::tc_fence_after();
+        if constexpr (!kSplitO) {
+          tc::mbar_wait(h_in, k & 1);
+          tc::tc_fence_after();
+        }
         m_init = -INFINITY;
         if (p.init) {
           // key-window pass > 0: continue from the row's running (o, lse) -- O goes back
@@ -873,7 +903,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
               ov[4 * x + 2] = v.z;
               ov[4 * x + 3] = v.w;
             }
-            tc::tmem_st32(tmem + lane_base + COL_O + q4 * 32, ov);
+            tc::tmem_st32(tmem + lane_base + col_o + q4 * 32, ov);
           }
           tc::tmem_wait_st();
         }
@@ -895,8 +925,8 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       tc::tc_fence_after();
       if constexpr (!kSReread) {
         tc::tmem_ld32(tmem + lane_base + b * BN, sv);
-        tc::tmem_ld32(tmem + lane_base + b * BN + 32, sv + 32);
-        tc::tmem_wait_ld();
+        tc::tmem_ld32_wait(tmem + lane_base + b * BN + 32, sv + 32);
+        tc::tmem_wait_ld_dep32(sv);
       }
 #ifdef LCX_TC_TRACE_SM  // owner group's quadrant-0 warp: 5 S got, 0 m handed over, 6 P put
       if (wq == 0 && lane == 0) trace_mark(p, T, 5);
@@ -935,8 +965,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       } else {
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
-          tc::tmem_ld32(tmem + lane_base + b * BN + hf * 32, sv);
-          tc::tmem_wait_ld();
+          tc::tmem_ld32_wait(tmem + lane_base + b * BN + hf * 32, sv);
           const uint32_t mb = uint32_t(mask >> (32 * hf));
 #pragma unroll
           for (int cc = 0; cc < 32; ++cc) sv[cc] = ((mb >> cc) & 1u) ? sv[cc] : -INFINITY;
@@ -951,13 +980,14 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       wacc[5] += clock64() - t_sg;
 #endif
       // ---- running max: previous tile's (other group) unless the item starts here
-      if (!(flags & F_FIRST)) tc::mbar_wait(h_in, k & 1);
-      const float m_prev =
-          (flags & F_FIRST) ? m_init : mbuf[((T + kGroups - 1) % kGroups) * 128 + r];
+      if (!kSplitO && !(flags & F_FIRST)) tc::mbar_wait(h_in, k & 1);
+      const float m_prev = kSplitO ? m_used
+                           : (flags & F_FIRST) ? m_init
+                                               : mbuf[((T + kGroups - 1) % kGroups) * 128 + r];
       // lazy rescale: the max moves only past a threshold (P <= 2^8 in fp16)
       const bool need = tmax > m_prev + kRescaleThresh;
       const float m = need ? tmax : m_prev;
-      mbuf[grp * 128 + r] = m;
+      if constexpr (!kSplitO) mbuf[grp * 128 + r] = m;
 #ifdef LCX_TC_TRACE_SM  // column 1: flags | kind << 8 | rescale << 12 (a value, not a time)
       if (wq == 0 && lane == 0) {
         trace_mark(p, T, 0);
@@ -967,7 +997,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       }
 #endif
       // an item's last tile hands over only after its epilogue (next item's O / Q)
-      if (!(flags & F_LAST)) {
+      if (!kSplitO && !(flags & F_LAST)) {
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(h_out);
       }
@@ -976,16 +1006,19 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #endif
       if (__any_sync(0xffffffffu, need && m_prev != -INFINITY)) {
         // O holds PV up to tile T - 1 at max m_prev: complete it, then rescale
-        const uint32_t Tp = T - 1;
-        tc::mbar_wait(s_free + (Tp % NS), (Tp / NS) & 1);
-        tc::tc_fence_after();
+        // (split O: this group's last PV, T - kGroups, completed before QK(T) took its S
+        // buffer)
+        if constexpr (!kSplitO) {
+          const uint32_t Tp = T - 1;
+          tc::mbar_wait(s_free + (Tp % NS), (Tp / NS) & 1);
+          tc::tc_fence_after();
+        }
         const float f = (need && m_prev != -INFINITY) ? ex2(m_prev - m) : 1.f;
 #pragma unroll 1
         for (int q8 = 0; q8 < 8; ++q8) {  // 16 columns at a time: S is still live here
           float ov[16];
-          const uint32_t ta = tmem + lane_base + COL_O + q8 * 16;
-          tc::tmem_ld16(ta, ov);
-          tc::tmem_wait_ld();
+          const uint32_t ta = tmem + lane_base + col_o + q8 * 16;
+          tc::tmem_ld16_wait(ta, ov);
 #pragma unroll
           for (int x = 0; x < 16; ++x) ov[x] *= f;
           tc::tmem_st16f(ta, ov);
@@ -1005,8 +1038,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {  // two 32-key halves: fewer live registers
         if constexpr (kSReread) {  // second read of this half (its P not yet written)
-          tc::tmem_ld32(tmem + lane_base + b * BN + hf * 32, sv);
-          tc::tmem_wait_ld();
+          tc::tmem_ld32_wait(tmem + lane_base + b * BN + hf * 32, sv);
           const uint32_t mb = uint32_t(mask >> (32 * hf));
 #pragma unroll
           for (int cc = 0; cc < 32; ++cc) sv[cc] = ((mb >> cc) & 1u) ? sv[cc] : -INFINITY;
@@ -1041,7 +1073,59 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #else
       if (threadIdx.x == 0) trace_mark(p, T, 6);
 #endif
-      if (flags & F_LAST) {
+      if (kSplitO && (flags & F_LAST)) {
+        // ---- epilogue (split O): merge the other group's O (its last tile T - 1) into
+        // this group's, normalize, store; then release both O for the next item ----
+        float sx = l > 0.f ? 1.f : 0.f, sy = 0.f, ly = 0.f, mt = m_used;
+        const bool other = T > T_first;
+        if (other) {
+          const uint32_t To = T - 1, go = To % kGroups, ko = To / kGroups;
+          tc::mbar_wait(lpub + int(go), ko & 1);
+          const float2 lo = lbuf[((ko & 1) * kGroups + go) * 128 + r];
+          ly = lo.x;
+          if (lo.x > 0.f) {
+            if (l > 0.f) {
+              mt = fmaxf(m_used, lo.y);
+              sx = ex2(m_used - mt);
+              sy = ex2(lo.y - mt);
+            } else {
+              mt = lo.y;
+              sy = 1.f;
+            }
+          }
+        }
+        const float lt = l * sx + ly * sy;
+        tc::mbar_wait(s_free + b, ph);  // PV(T) complete, and every PV before it
+        tc::tc_fence_after();
+        const float inv = lt > 0.f ? 1.f / lt : 0.f;
+        const float ax = sx * inv, ay = sy * inv;
+        const uint32_t col_y = COL_O + uint32_t((grp + 1) % kGroups) * HD;
+        float4* o = reinterpret_cast<float4*>(p.out + (i * p.hq + h) * int64_t(HD));
+#pragma unroll 1
+        for (int q8 = 0; q8 < 8; ++q8) {
+          float ov[16], oy[16];
+          tc::tmem_ld16_wait(tmem + lane_base + col_o + q8 * 16, ov);
+          if (other) tc::tmem_ld16_wait(tmem + lane_base + col_y + q8 * 16, oy);
+          if (!other) {
+#pragma unroll
+            for (int x = 0; x < 16; ++x) oy[x] = 0.f;
+          }
+          if (row_ok) {
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+              o[q8 * 4 + x] = make_float4(ov[4 * x] * ax + oy[4 * x] * ay,
+                                          ov[4 * x + 1] * ax + oy[4 * x + 1] * ay,
+                                          ov[4 * x + 2] * ax + oy[4 * x + 2] * ay,
+                                          ov[4 * x + 3] * ax + oy[4 * x + 3] * ay);
+          }
+        }
+        if (row_ok)
+          p.lse[int64_t(h) * p.lse_stride + i] =
+              lt > 0.f ? (mt + log2f(lt)) * 0.69314718055994530942f : -INFINITY;
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(edone);
+      } else if (flags & F_LAST) {
         // ---- epilogue: add the other group's partial sum, wait for the last PV,
         // normalize, store ----
         float lt = l;
@@ -1060,8 +1144,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #pragma unroll 1
         for (int q4 = 0; q4 < 4; ++q4) {
           float ov[32];
-          tc::tmem_ld32(tmem + lane_base + COL_O + q4 * 32, ov);
-          tc::tmem_wait_ld();
+          tc::tmem_ld32_wait(tmem + lane_base + COL_O + q4 * 32, ov);
           if (row_ok) {
 #pragma unroll
             for (int x = 0; x < 8; ++x)

@@ -228,8 +228,7 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
       tc::mbar_wait(s_full + sb, (t / NSB) & 1);
       tc::tc_fence_after();
       float v[32];
-      tc::tmem_ld32(tmem + lane_base + sb * BN + part * 32, v);
-      tc::tmem_wait_ld();
+      tc::tmem_ld32_wait(tmem + lane_base + sb * BN + part * 32, v);
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(s_empty + sb);
