@@ -84,6 +84,12 @@ static_assert(kGroups == 2, "two softmax groups");
 #define LCX_TC_SPLIT_O 0
 #endif
 constexpr bool kSplitO = LCX_TC_SPLIT_O;
+// split O: exponentiate at the group's running max before the tile max is known (correct,
+// measured 2 % slower than max-first: 376 vs 369 ms per layer on one box)
+#ifndef LCX_TC_SPEC_EXP
+#define LCX_TC_SPEC_EXP 0
+#endif
+constexpr bool kSpecExp = LCX_TC_SPEC_EXP;
 constexpr int kQBufs = kSplitO ? 1 : LCX_TC_QBUFS;
 constexpr int kOBufs = kSplitO ? kGroups : 1;
 constexpr int NK = 4, NV = 4;  // K / V smem stages
@@ -948,7 +954,6 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #endif
       // masked logits -> -inf (ex2(-inf) = 0), already in log2 units
       const bool all_in = __all_sync(0xffffffffu, mask == ~0ull);  // no select needed
-      float t4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
       if constexpr (!kSReread) {
         if (!all_in) {
           const uint32_t lo = uint32_t(mask), hi = uint32_t(mask >> 32);
@@ -958,24 +963,93 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
             sv[32 + cc] = ((hi >> cc) & 1u) ? sv[32 + cc] : -INFINITY;
           }
         }
+      }
+      // ---- P = exp2(x - m) in fp16, written over the tile's S columns in TMEM:
+      // key c -> column c / 2 (two fp16 per 32-bit column).  Packed f32x2 subtract /
+      // accumulate (FADD2): half the FP32 instructions per key.  Returns the row sum.
+      auto exps_store = [&](float m) -> float {
+        const float mm = m == -INFINITY ? 0.f : m;
+        const float2 nm2 = make_float2(-mm, -mm);
+        float2 rs2 = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int cc = 0; cc < 64; cc += 8)
+        for (int hf = 0; hf < 2; ++hf) {  // two 32-key halves: fewer live registers
+          if constexpr (kSReread) {  // second read of this half (its P not yet written)
+            tc::tmem_ld32_wait(tmem + lane_base + b * BN + hf * 32, sv);
+            const uint32_t mb = uint32_t(mask >> (32 * hf));
 #pragma unroll
-          for (int u = 0; u < 4; ++u) t4[u] = fmaxf(t4[u], fmaxf(sv[cc + u], sv[cc + 4 + u]));
-      } else {
+            for (int cc = 0; cc < 32; ++cc) sv[cc] = ((mb >> cc) & 1u) ? sv[cc] : -INFINITY;
+          }
+          uint32_t pw[16];
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-          tc::tmem_ld32_wait(tmem + lane_base + b * BN + hf * 32, sv);
-          const uint32_t mb = uint32_t(mask >> (32 * hf));
+          for (int k = 0; k < 16; ++k) {
+            const int c = (kSReread ? 0 : hf * 32) + 2 * k;
+            const float2 x = __fadd2_rn(make_float2(sv[c], sv[c + 1]), nm2);
+            const float2 pp = make_float2(ex2(x.x), ex2(x.y));
+            rs2 = __fadd2_rn(rs2, pp);
+            const __half2 h2 = __floats2half2_rn(pp.x, pp.y);
+            pw[k] = *reinterpret_cast<const uint32_t*>(&h2);
+          }
+          tc::tmem_st16(tmem + lane_base + b * BN + hf * 16, pw);
+        }
+        return rs2.x + rs2.y;
+      };
+      auto tile_max = [&]() -> float {
+        float t4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        if constexpr (!kSReread) {
 #pragma unroll
-          for (int cc = 0; cc < 32; ++cc) sv[cc] = ((mb >> cc) & 1u) ? sv[cc] : -INFINITY;
-#pragma unroll
-          for (int cc = 0; cc < 32; cc += 8)
+          for (int cc = 0; cc < 64; cc += 8)
 #pragma unroll
             for (int u = 0; u < 4; ++u) t4[u] = fmaxf(t4[u], fmaxf(sv[cc + u], sv[cc + 4 + u]));
+        } else {
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            tc::tmem_ld32_wait(tmem + lane_base + b * BN + hf * 32, sv);
+            const uint32_t mb = uint32_t(mask >> (32 * hf));
+#pragma unroll
+            for (int cc = 0; cc < 32; ++cc) sv[cc] = ((mb >> cc) & 1u) ? sv[cc] : -INFINITY;
+#pragma unroll
+            for (int cc = 0; cc < 32; cc += 8)
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                t4[u] = fmaxf(t4[u], fmaxf(sv[cc + u], sv[cc + 4 + u]));
+          }
         }
-      }
-      const float tmax = fmaxf(fmaxf(t4[0], t4[1]), fmaxf(t4[2], t4[3]));
+        return fmaxf(fmaxf(t4[0], t4[1]), fmaxf(t4[2], t4[3]));
+      };
+      auto rescale_o = [&](float f) {
+#pragma unroll 1
+        for (int q8 = 0; q8 < 8; ++q8) {  // 16 columns at a time: S is still live here
+          float ov[16];
+          const uint32_t ta = tmem + lane_base + col_o + q8 * 16;
+          tc::tmem_ld16_wait(ta, ov);
+#pragma unroll
+          for (int x = 0; x < 16; ++x) ov[x] *= f;
+          tc::tmem_st16f(ta, ov);
+        }
+        tc::tmem_wait_st();
+      };
+      float rs;
+      if (kSplitO && kSpecExp && __all_sync(0xffffffffu, m_used != -INFINITY)) {
+        // split O: the group's own running max is known before the tile -- exponentiate
+        // at it straight away, independent of the tile max; only when some row's max
+        // moved past the threshold (rare after an item's first tiles) rescale and redo.
+        // The P written is the same as max-first would write.
+        rs = exps_store(m_used);
+        const float tmax = tile_max();
+        const bool need = tmax > m_used + kRescaleThresh;
+        if (__any_sync(0xffffffffu, need)) {
+          const float m = need ? tmax : m_used;
+          rescale_o(need ? ex2(m_used - m) : 1.f);  // own last PV done (S(T) is full)
+          if (need) l *= ex2(m_used - m);
+          m_used = m;
+          tc::tmem_wait_st();  // the speculative P stores land before their rewrite
+          rs = exps_store(m);
+        }
+#ifdef LCX_TC_WAITPROF
+        wacc[5] += clock64() - t_sg;
+#endif
+      } else {
+      const float tmax = tile_max();
 #ifdef LCX_TC_WAITPROF
       wacc[5] += clock64() - t_sg;
 #endif
@@ -1001,9 +1075,6 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(h_out);
       }
-#ifdef LCX_TC_WAITPROF
-      const long long t_ex = clock64();
-#endif
       if (__any_sync(0xffffffffu, need && m_prev != -INFINITY)) {
         // O holds PV up to tile T - 1 at max m_prev: complete it, then rescale
         // (split O: this group's last PV, T - kGroups, completed before QK(T) took its S
@@ -1013,50 +1084,19 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           tc::mbar_wait(s_free + (Tp % NS), (Tp / NS) & 1);
           tc::tc_fence_after();
         }
-        const float f = (need && m_prev != -INFINITY) ? ex2(m_prev - m) : 1.f;
-#pragma unroll 1
-        for (int q8 = 0; q8 < 8; ++q8) {  // 16 columns at a time: S is still live here
-          float ov[16];
-          const uint32_t ta = tmem + lane_base + col_o + q8 * 16;
-          tc::tmem_ld16_wait(ta, ov);
-#pragma unroll
-          for (int x = 0; x < 16; ++x) ov[x] *= f;
-          tc::tmem_st16f(ta, ov);
-        }
-        tc::tmem_wait_st();
+        rescale_o((need && m_prev != -INFINITY) ? ex2(m_prev - m) : 1.f);
       }
       if (m != m_used) {  // this group's partial sum follows the row max
         if (m_used != -INFINITY) l *= ex2(m_used - m);
         m_used = m;
       }
-      // ---- P = exp2(x - m) in fp16, written over the tile's S columns in TMEM:
-      // key c -> column c / 2 (two fp16 per 32-bit column).  Packed f32x2 subtract /
-      // accumulate (FADD2): half the FP32 instructions per key.
-      const float mm = m == -INFINITY ? 0.f : m;
-      const float2 nm2 = make_float2(-mm, -mm);
-      float2 rs2 = make_float2(0.f, 0.f);
-#pragma unroll
-      for (int hf = 0; hf < 2; ++hf) {  // two 32-key halves: fewer live registers
-        if constexpr (kSReread) {  // second read of this half (its P not yet written)
-          tc::tmem_ld32_wait(tmem + lane_base + b * BN + hf * 32, sv);
-          const uint32_t mb = uint32_t(mask >> (32 * hf));
-#pragma unroll
-          for (int cc = 0; cc < 32; ++cc) sv[cc] = ((mb >> cc) & 1u) ? sv[cc] : -INFINITY;
-        }
-        uint32_t pw[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const int c = (kSReread ? 0 : hf * 32) + 2 * k;
-          const float2 x = __fadd2_rn(make_float2(sv[c], sv[c + 1]), nm2);
-          const float2 pp = make_float2(ex2(x.x), ex2(x.y));
-          rs2 = __fadd2_rn(rs2, pp);
-          const __half2 h2 = __floats2half2_rn(pp.x, pp.y);
-          pw[k] = *reinterpret_cast<const uint32_t*>(&h2);
-        }
-        tc::tmem_st16(tmem + lane_base + b * BN + hf * 16, pw);
+      rs = exps_store(m);
       }
+#ifdef LCX_TC_WAITPROF
+      const long long t_ex = clock64();
+#endif
       tc::tmem_wait_st();
-      l += rs2.x + rs2.y;
+      l += rs;
       // partial (l, m) for the item's epilogue (ordered before the P release below)
       lbuf[((k & 1) * kGroups + grp) * 128 + r] = make_float2(l, m_used);
       tc::tc_fence_before();
@@ -1135,7 +1175,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           const uint32_t To = T - d, go = To % kGroups, ko = To / kGroups;
           tc::mbar_wait(lpub + int(go), ko & 1);
           const float2 lo = lbuf[((ko & 1) * kGroups + go) * 128 + r];
-          if (lo.x > 0.f) lt += lo.x * ex2(lo.y - m);
+          if (lo.x > 0.f) lt += lo.x * ex2(lo.y - m_used);
         }
         tc::mbar_wait(s_free + b, ph);  // this item's last PV is complete
         tc::tc_fence_after();
@@ -1154,7 +1194,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         }
         if (row_ok)
           p.lse[int64_t(h) * p.lse_stride + i] =
-              lt > 0.f ? (m + log2f(lt)) * 0.69314718055994530942f : -INFINITY;
+              lt > 0.f ? (m_used + log2f(lt)) * 0.69314718055994530942f : -INFINITY;
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(h_out);
