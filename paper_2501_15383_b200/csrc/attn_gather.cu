@@ -17,9 +17,13 @@
 //       logit = rope(q_i, qpos(i, pattern)) . rope(k_j, kpos(j)) * scale
 //             == rope(q_i, dca_relative(i, j)) . k_j * scale          (dca.cpp:62-80)
 //     with no per-entry trigonometry or table reads;
-//   * 8 lanes per query row, 16 dims each (four 16-byte loads of K, two of V), two
+//   * 16 lanes per query row, 8 dims each (two 16-byte loads of K, one of V), two
 //     entries in flight per row, and one online-softmax update per pair of entries;
-//   * the 8 lanes scan 8 diagonals of the row's sorted segment list at once (ballot);
+//     80 registers, 3 CTAs (24 warps) per SM.  Measured at 1M (planted, per layer):
+//     8 lanes x 16 dims at 2 CTAs 78 ms, 16 x 8 at 3 CTAs 68-72 ms, at 4 CTAs (spills)
+//     68 ms, 16 x 8 with 3 or 4 entries in flight 80-89 ms;
+//   * the lanes of a row scan as many diagonals of its sorted segment list at once
+//     (ballot);
 //     segments (d, first row, last row) come pre-split per 64-row half of the block.
 // The tensor-core partial (o_tc, lse_tc) of the row is the initial state; rows with no
 // entry in this pass keep their state untouched.  Entries on a vertical column belong to
@@ -30,10 +34,22 @@
 namespace lcx {
 namespace {
 
-constexpr int kRows = 32;    // rows per CTA
-constexpr int kLanes = 8;    // lanes per row
-constexpr int kDims = 16;    // dims per lane
+#ifndef LCX_GATHER_LANES
+#define LCX_GATHER_LANES 16
+#endif
+constexpr int kLanes = LCX_GATHER_LANES;  // lanes per row (8 or 16)
+constexpr int kDims = 128 / kLanes;       // dims per lane
+constexpr int kRows = 256 / kLanes;       // rows per CTA
 constexpr int kThreads = kRows * kLanes;
+#ifndef LCX_GATHER_MINB
+#define LCX_GATHER_MINB (LCX_GATHER_LANES == 16 ? 3 : 2)
+#endif
+constexpr int kMinBlocks = LCX_GATHER_MINB;  // resident CTAs per SM
+#ifndef LCX_GATHER_INFLIGHT
+#define LCX_GATHER_INFLIGHT 2
+#endif
+constexpr int kInflight = LCX_GATHER_INFLIGHT;  // entries of a row loaded at once
+static_assert(kLanes == 8 || kLanes == 16, "8 or 16 lanes per row");
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
   const uint32_t w[4] = {u.x, u.y, u.z, u.w};
@@ -45,8 +61,8 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
 }
 
 struct KVRow {
-  float4 k[4];
-  uint4 v[2];
+  float4 k[kDims / 4];
+  uint4 v[kDims / 8];
 };
 
 __device__ __forceinline__ void load_row(const float* kf, const __nv_bfloat16* vb, int64_t j,
@@ -54,9 +70,9 @@ __device__ __forceinline__ void load_row(const float* kf, const __nv_bfloat16* v
   const float4* kp = reinterpret_cast<const float4*>(kf + j * stride);
   const uint4* vp = reinterpret_cast<const uint4*>(vb + j * stride);
 #pragma unroll
-  for (int t = 0; t < 4; ++t) r.k[t] = __ldg(kp + t);
-  r.v[0] = __ldg(vp);
-  r.v[1] = __ldg(vp + 1);
+  for (int t = 0; t < kDims / 4; ++t) r.k[t] = __ldg(kp + t);
+#pragma unroll
+  for (int t = 0; t < kDims / 8; ++t) r.v[t] = __ldg(vp + t);
 }
 
 __device__ __forceinline__ int64_t qpos_of(const GatherArgs& a, int pattern, int64_t i,
@@ -67,7 +83,7 @@ __device__ __forceinline__ int64_t qpos_of(const GatherArgs& a, int pattern, int
   return a.c - 1;
 }
 
-__global__ void __launch_bounds__(kThreads, 2) attn_gather_kernel(const GatherArgs a) {
+__global__ void __launch_bounds__(kThreads, kMinBlocks) attn_gather_kernel(const GatherArgs a) {
   // a window with no segment (and before the chunk's rows: no self-fallback rows) is empty
   if (a.win_flags && !a.win_flags[a.win] && a.key_hi <= a.row_begin) return;
   const int lane = threadIdx.x & (kLanes - 1);
@@ -75,7 +91,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_gather_kernel(const GatherAr
   const int64_t i = a.row_begin + int64_t(blockIdx.x) * kRows + rw;
   const int h = blockIdx.y;
   const int g = h / a.group;
-  const unsigned gmask = 0xffu << (threadIdx.x & 24);
+  constexpr unsigned kRowMask = (1u << kLanes) - 1u;
+  const int lane0 = threadIdx.x & (32 - kLanes);  // first lane of this row in the warp
+  const unsigned gmask = kRowMask << lane0;
   if (i >= a.row_end) return;
 
   const int r = int((i - a.row_begin) & 127);
@@ -104,8 +122,8 @@ __global__ void __launch_bounds__(kThreads, 2) attn_gather_kernel(const GatherAr
   float qraw[kDims];
   {
     const uint4* qp = reinterpret_cast<const uint4*>(a.q + (i * a.hq + h) * 128 + lane * kDims);
-    bf16x8_to_f32(__ldg(qp), qraw);
-    bf16x8_to_f32(__ldg(qp + 1), qraw + 8);
+#pragma unroll
+    for (int t = 0; t < kDims / 8; ++t) bf16x8_to_f32(__ldg(qp + t), qraw + 8 * t);
   }
   // running state = the partial so far (tensor-core tiles + earlier passes)
   float o[kDims], m = -INFINITY, l = 0.f;
@@ -157,7 +175,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_gather_kernel(const GatherAr
   auto dot_of = [&](const KVRow& kv) {
     float d0 = 0.f, d1 = 0.f;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int t = 0; t < kDims / 4; ++t) {
       d0 = fmaf(qr[4 * t], kv.k[t].x, d0);
       d1 = fmaf(qr[4 * t + 1], kv.k[t].y, d1);
       d0 = fmaf(qr[4 * t + 2], kv.k[t].z, d0);
@@ -167,12 +185,13 @@ __global__ void __launch_bounds__(kThreads, 2) attn_gather_kernel(const GatherAr
     d += __shfl_xor_sync(gmask, d, 1);
     d += __shfl_xor_sync(gmask, d, 2);
     d += __shfl_xor_sync(gmask, d, 4);
+    if constexpr (kLanes == 16) d += __shfl_xor_sync(gmask, d, 8);
     return d * a.scale_log2;
   };
   auto accumulate = [&](float p, const KVRow& kv) {
     float vf[kDims];
-    bf16x8_to_f32(kv.v[0], vf);
-    bf16x8_to_f32(kv.v[1], vf + 8);
+#pragma unroll
+    for (int t = 0; t < kDims / 8; ++t) bf16x8_to_f32(kv.v[t], vf + 8 * t);
 #pragma unroll
     for (int t = 0; t < kDims; ++t) o[t] = fmaf(p, vf[t], o[t]);
   };
@@ -203,38 +222,47 @@ __global__ void __launch_bounds__(kThreads, 2) attn_gather_kernel(const GatherAr
         ok = !((vb[jj >> 5] >> (jj & 31)) & 1u);
       }
     }
-    unsigned okm = __ballot_sync(gmask, ok) >> (threadIdx.x & 24);
-    const unsigned stopm = __ballot_sync(gmask, stop) >> (threadIdx.x & 24);
+    unsigned okm = (__ballot_sync(gmask, ok) >> lane0) & kRowMask;
+    const unsigned stopm = (__ballot_sync(gmask, stop) >> lane0) & kRowMask;
     while (okm) {
-      const int src0 = __ffs(okm) - 1;
-      okm &= okm - 1;
-      const int64_t j0 = __shfl_sync(gmask, (long long)jj, src0, kLanes);
-      int64_t j1 = -1;
-      if (okm) {
-        const int src1 = __ffs(okm) - 1;
-        okm &= okm - 1;
-        j1 = __shfl_sync(gmask, (long long)jj, src1, kLanes);
+      // up to kInflight entries of this row at once: loads first, then the math
+      int64_t jv[kInflight];
+      int cnt = 0;
+#pragma unroll
+      for (int f = 0; f < kInflight; ++f) {
+        jv[f] = -1;
+        if (okm) {
+          const int src = __ffs(okm) - 1;
+          okm &= okm - 1;
+          jv[f] = __shfl_sync(gmask, (long long)jj, src, kLanes);
+          ++cnt;
+        }
       }
-      KVRow r0, r1;
-      load_row(kf, vbase, j0, stride, r0);
-      if (j1 >= 0) load_row(kf, vbase, j1, stride, r1);
-      ensure_pattern(j0);
-      const float s0 = dot_of(r0);
-      float s1 = -INFINITY;
-      if (j1 >= 0) {
-        ensure_pattern(j1);
-        s1 = dot_of(r1);
+      KVRow rv[kInflight];
+#pragma unroll
+      for (int f = 0; f < kInflight; ++f)
+        if (jv[f] >= 0) load_row(kf, vbase, jv[f], stride, rv[f]);
+      float sv[kInflight];
+      float smax = -INFINITY;
+#pragma unroll
+      for (int f = 0; f < kInflight; ++f) {
+        sv[f] = -INFINITY;
+        if (jv[f] >= 0) {
+          ensure_pattern(jv[f]);
+          sv[f] = dot_of(rv[f]);
+        }
+        smax = fmaxf(smax, sv[f]);
       }
-      raise_max(s0, s1);
-      const float p0 = exp2f(s0 - m);
-      l += p0;
-      accumulate(p0, r0);
-      if (j1 >= 0) {
-        const float p1 = exp2f(s1 - m);
-        l += p1;
-        accumulate(p1, r1);
+      raise_max(smax, -INFINITY);
+#pragma unroll
+      for (int f = 0; f < kInflight; ++f) {
+        if (jv[f] >= 0) {
+          const float pf = exp2f(sv[f] - m);
+          l += pf;
+          accumulate(pf, rv[f]);
+        }
       }
-      entries += j1 >= 0 ? 2 : 1;
+      entries += cnt;
     }
     if (stopm) break;
   }
