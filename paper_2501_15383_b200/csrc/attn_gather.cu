@@ -21,7 +21,7 @@
 //     entries in flight per row, and one online-softmax update per pair of entries;
 //     80 registers, 3 CTAs (24 warps) per SM.  Measured at 1M (planted, per layer):
 //     8 lanes x 16 dims at 2 CTAs 78 ms, 16 x 8 at 3 CTAs 68-72 ms, at 4 CTAs (spills)
-//     68 ms, 16 x 8 with 3 or 4 entries in flight 80-89 ms;
+//     68 ms, 16 x 8 with 3 or 4 entries in flight 80-89 ms, 32 x 4 at 4 CTAs 78 ms;
 //   * the lanes of a row scan as many diagonals of its sorted segment list at once
 //     (ballot);
 //     segments (d, first row, last row) come pre-split per 64-row half of the block.
@@ -49,7 +49,8 @@ constexpr int kMinBlocks = LCX_GATHER_MINB;  // resident CTAs per SM
 #define LCX_GATHER_INFLIGHT 2
 #endif
 constexpr int kInflight = LCX_GATHER_INFLIGHT;  // entries of a row loaded at once
-static_assert(kLanes == 8 || kLanes == 16, "8 or 16 lanes per row");
+static_assert(kLanes == 8 || kLanes == 16 || kLanes == 32, "8, 16 or 32 lanes per row");
+constexpr int kVVec = kDims >= 8 ? kDims / 8 : 1;  // 16-byte (or one 8-byte) V loads per lane
 
 __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
   const uint32_t w[4] = {u.x, u.y, u.z, u.w};
@@ -62,8 +63,23 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
 
 struct KVRow {
   float4 k[kDims / 4];
-  uint4 v[kDims / 8];
+  uint4 v[kVVec];  // kDims == 4: only .x / .y used
 };
+
+// kDims bf16 values at p (16-byte aligned for kDims >= 8, 8-byte for 4) -> fp32
+__device__ __forceinline__ void load_bf16(const __nv_bfloat16* p, float* f) {
+  if constexpr (kDims >= 8) {
+#pragma unroll
+    for (int t = 0; t < kDims / 8; ++t)
+      bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(p) + t), f + 8 * t);
+  } else {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+    f[0] = __uint_as_float(u.x << 16);
+    f[1] = __uint_as_float(u.x & 0xffff0000u);
+    f[2] = __uint_as_float(u.y << 16);
+    f[3] = __uint_as_float(u.y & 0xffff0000u);
+  }
+}
 
 __device__ __forceinline__ void load_row(const float* kf, const __nv_bfloat16* vb, int64_t j,
                                          int64_t stride, KVRow& r) {
@@ -71,8 +87,13 @@ __device__ __forceinline__ void load_row(const float* kf, const __nv_bfloat16* v
   const uint4* vp = reinterpret_cast<const uint4*>(vb + j * stride);
 #pragma unroll
   for (int t = 0; t < kDims / 4; ++t) r.k[t] = __ldg(kp + t);
+  if constexpr (kDims >= 8) {
 #pragma unroll
-  for (int t = 0; t < kDims / 8; ++t) r.v[t] = __ldg(vp + t);
+    for (int t = 0; t < kDims / 8; ++t) r.v[t] = __ldg(vp + t);
+  } else {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(vp));
+    r.v[0] = make_uint4(u.x, u.y, 0u, 0u);
+  }
 }
 
 __device__ __forceinline__ int64_t qpos_of(const GatherArgs& a, int pattern, int64_t i,
@@ -91,7 +112,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) attn_gather_kernel(const
   const int64_t i = a.row_begin + int64_t(blockIdx.x) * kRows + rw;
   const int h = blockIdx.y;
   const int g = h / a.group;
-  constexpr unsigned kRowMask = (1u << kLanes) - 1u;
+  constexpr unsigned kRowMask = kLanes == 32 ? 0xffffffffu : (1u << (kLanes & 31)) - 1u;
   const int lane0 = threadIdx.x & (32 - kLanes);  // first lane of this row in the warp
   const unsigned gmask = kRowMask << lane0;
   if (i >= a.row_end) return;
@@ -122,8 +143,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) attn_gather_kernel(const
   float qraw[kDims];
   {
     const uint4* qp = reinterpret_cast<const uint4*>(a.q + (i * a.hq + h) * 128 + lane * kDims);
-#pragma unroll
-    for (int t = 0; t < kDims / 8; ++t) bf16x8_to_f32(__ldg(qp + t), qraw + 8 * t);
+    load_bf16(reinterpret_cast<const __nv_bfloat16*>(qp), qraw);
   }
   // running state = the partial so far (tensor-core tiles + earlier passes)
   float o[kDims], m = -INFINITY, l = 0.f;
@@ -185,13 +205,21 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) attn_gather_kernel(const
     d += __shfl_xor_sync(gmask, d, 1);
     d += __shfl_xor_sync(gmask, d, 2);
     d += __shfl_xor_sync(gmask, d, 4);
-    if constexpr (kLanes == 16) d += __shfl_xor_sync(gmask, d, 8);
+    if constexpr (kLanes >= 16) d += __shfl_xor_sync(gmask, d, 8);
+    if constexpr (kLanes >= 32) d += __shfl_xor_sync(gmask, d, 16);
     return d * a.scale_log2;
   };
   auto accumulate = [&](float p, const KVRow& kv) {
     float vf[kDims];
+    if constexpr (kDims >= 8) {
 #pragma unroll
-    for (int t = 0; t < kDims / 8; ++t) bf16x8_to_f32(kv.v[t], vf + 8 * t);
+      for (int t = 0; t < kDims / 8; ++t) bf16x8_to_f32(kv.v[t], vf + 8 * t);
+    } else {
+      vf[0] = __uint_as_float(kv.v[0].x << 16);
+      vf[1] = __uint_as_float(kv.v[0].x & 0xffff0000u);
+      vf[2] = __uint_as_float(kv.v[0].y << 16);
+      vf[3] = __uint_as_float(kv.v[0].y & 0xffff0000u);
+    }
 #pragma unroll
     for (int t = 0; t < kDims; ++t) o[t] = fmaf(p, vf[t], o[t]);
   };
