@@ -65,8 +65,9 @@ constexpr int kWarpProducer = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1,
 #define LCX_TC_SREREAD (LCX_TC_GROUPS > 2)
 #endif
 constexpr bool kSReread = LCX_TC_SREREAD;
-// (three groups fit in 128 registers this way but do not yet produce correct results:
-// kept to two until that protocol is debugged)
+// Three groups fit in 128 registers this way and are correct (with NS = 3, below), but
+// measure slower than two: 397 vs 364 ms per 1M layer on one box (one Q buffer, S read
+// twice, spills) -- kept behind LCX_TC_ALLOW_GROUPS3.
 #ifndef LCX_TC_ALLOW_GROUPS3
 static_assert(kGroups == 2, "two softmax groups");
 #endif
@@ -90,10 +91,14 @@ constexpr bool kSplitO = LCX_TC_SPLIT_O;
 #define LCX_TC_SPEC_EXP 0
 #endif
 constexpr bool kSpecExp = LCX_TC_SPEC_EXP;
-constexpr int kQBufs = kSplitO ? 1 : LCX_TC_QBUFS;
+// A softmax group waits for S(T) on buffer T % NS with a phase parity; that is only
+// sound if the group itself observed the buffer's previous phase (tile T - NS), i.e. if
+// NS is a multiple of the group count -- three groups take three S buffers and one Q.
+constexpr int kQBufs = (kSplitO || kGroups == 3) ? 1 : LCX_TC_QBUFS;
 constexpr int kOBufs = kSplitO ? kGroups : 1;
 constexpr int NK = 4, NV = 4;  // K / V smem stages
-constexpr int NS = (kSplitO || kQBufs == 2) ? 2 : 4;  // S (+P) TMEM buffers
+constexpr int NS = kGroups == 3 ? 3 : ((kSplitO || kQBufs == 2) ? 2 : 4);  // S (+P) TMEM
+static_assert(NS % kGroups == 0, "each group must see every phase of its S buffers");
 static_assert(!kSplitO || NS == kGroups, "split O: S(T) full implies PV(T - kGroups) done");
 constexpr uint32_t kKHalf = BN * 64 * 2;             // 8 KB
 constexpr uint32_t kKStage = 4 * kKHalf;             // hi0 hi1 lo0 lo1 = 32 KB
