@@ -20,18 +20,20 @@
 //          vertical (the vertical path owns entries on both);
 //   DENSE  full causal attention (PrefillMode::Full / full_attention).
 // Slash entries in the remaining relative tiles go to the CUDA-core gather path
-// (attn_simt.cu) as (d, first row, last row) segments and are merged in place.
+// (attn_gather.cu) as (d, first row, last row) segments and are merged in place.
 //
 // Precision (bf16 storage, 2e-3 contract): q and k are rotated in fp32 and split
 // into bf16 hi + lo; S = q_hi k_hi + q_hi k_lo + q_lo k_hi (3 MMAs, fp32 TMEM
 // accumulate); P is fp16 (<= 2^8 under a lazy-rescale threshold of 8 in log2
 // units); V is fp16.  Executed MMA work per tile = 4 units vs 2 algorithmic.
 //
-// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer (one lane), w2 TMEM
-// allocator, w4..w7 softmax / correction / epilogue (thread = query row, TMEM
-// lane quadrant = warp % 4).  Pipelines: K (hi+lo) and V^T double-buffered,
-// S double-buffered in TMEM (2 x 64 columns), O in TMEM (128 columns), P
-// double-buffered in smem.
+// Warp roles (384 threads): warps 0-7 softmax / correction / epilogue in two groups
+// of four that take alternate tiles (thread = query row, TMEM lane quadrant =
+// warp % 4), warp 8 producer (tile metadata ring + K loads), warp 9 QK issuer + TMEM
+// owner, warp 10 PV issuer, warp 11 V loads.  Pipelines: K (hi+lo) and V^T in four
+// shared-memory stages, S double-buffered in TMEM (2 x 64 columns) with P (fp16)
+// written over it, O in TMEM (128 columns), rotated Q hi/lo in TMEM (two buffers, one
+// per DCA pattern group parity) as the A operand of every QK MMA.
 #include <cuda.h>
 
 #include "lcx_internal.cuh"
@@ -45,7 +47,7 @@ namespace lcx {
 namespace {
 
 constexpr int BM = 128, BN = 64, HD = 128;
-// warps 0-7 softmax (TMEM lane quadrant = warp % 4, column half = warp / 4),
+// warps 0-7 softmax (TMEM lane quadrant = warp % 4, group = warp / 4),
 // warp 8 producer (tile metadata + K TMA), warp 9 QK issuer + TMEM allocator,
 // warp 10 PV issuer, warp 11 V TMA
 #ifndef LCX_TC_GROUPS
