@@ -127,6 +127,18 @@ constexpr uint32_t COL_Q = COL_O + kOBufs * HD;  // Q buffer b: hi at COL_Q + 12
 static_assert(COL_Q + kQBufs * HD <= 512, "TMEM columns");
 constexpr uint32_t QBUF = HD;
 constexpr float kRescaleThresh = 8.f;
+// producer / V-load warps: sleepy polling (ns between polls) instead of suspended
+// try_wait, 0 = off.  A suspended waiter is woken by other barriers' traffic and
+// re-polls: ncu counts ~700 warp instructions per tile in wait loops, taken from the
+// softmax warps' sub-partitions.  Same-box A/B (attn_tc ms per 1M layer): off 363 /
+// 360, 30 ns 361-363, 100 ns 359-361, 300 ns 357-358, 1000 ns 357-360, 3000 ns 374;
+// the PV issuer's wait for P (critical path) at 40 ns: 363.
+#ifndef LCX_TC_SLEEPY
+#define LCX_TC_SLEEPY 300
+#endif
+#ifndef LCX_TC_SLEEPY_PV  // the PV issuer's wait for P (on the critical path)
+#define LCX_TC_SLEEPY_PV 0
+#endif
 
 constexpr uint32_t IDESC_QK = tc::idesc_f16(BM, BN, 1, 1);   // bf16 x bf16
 constexpr uint32_t IDESC_PV = tc::idesc_f16(BM, HD, 0, 0);   // f16 x f16
@@ -464,7 +476,12 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     uint32_t T = 0, M = 0;
     const Item* plans = reinterpret_cast<const Item*>(p.plans);
     auto slot_wait = [&](uint32_t mm) {
+#if LCX_TC_SLEEPY
+      WAITP(0, tc::mbar_wait_sleepy(m_empty + int(mm % kMetaSlots), ((mm / kMetaSlots) & 1) ^ 1,
+                                    LCX_TC_SLEEPY));
+#else
       WAITP(0, tc::mbar_wait(m_empty + int(mm % kMetaSlots), ((mm / kMetaSlots) & 1) ^ 1));
+#endif
     };
     // items come from a global queue (ascending, so neighbouring CTAs still work on
     // neighbouring row blocks of a head and share their K / V tiles in L2) -- CTAs that
@@ -588,7 +605,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           trace_mark(p, Tj, 0);
 #endif
           const int bk = Tj % NK;
+#if LCX_TC_SLEEPY
+          WAITP(1, tc::mbar_wait_sleepy(k_empty + bk, ((Tj / NK) & 1) ^ 1, LCX_TC_SLEEPY));
+#else
           WAITP(1, tc::mbar_wait(k_empty + bk, ((Tj / NK) & 1) ^ 1));
+#endif
           tc::mbar_expect_tx(k_full + bk, kKStage);
           const uint32_t kdst = smem_base + OFF_K + bk * kKStage;
           int tile = my.kind == T_VERT ? int((int64_t(it.h) * (p.capp / 64) + my.key0 / 64) * 2)
@@ -709,7 +730,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       if (kind == T_EMPTY) continue;
       if (lane == 0) {
         const int bv = T % NV;
+#if LCX_TC_SLEEPY
+        WAITP(1, tc::mbar_wait_sleepy(v_empty + bv, ((T / NV) & 1) ^ 1, LCX_TC_SLEEPY));
+#else
         WAITP(1, tc::mbar_wait(v_empty + bv, ((T / NV) & 1) ^ 1));
+#endif
         tc::mbar_expect_tx(v_full + bv, kVStage);
         const uint32_t vdst = smem_base + OFF_V + bv * kVStage;
         const int64_t vtile = kind == T_VERT ? int64_t(h) * (p.capp / 64) + key0 / 64
@@ -752,7 +777,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       if (kind == T_END) break;
       if (kind == T_EMPTY) continue;
       const int bs = T % NS, bv = T % NV;
+#if LCX_TC_SLEEPY_PV
+      WAITP(1, tc::mbar_wait_sleepy(p_full + bs, (T / NS) & 1, LCX_TC_SLEEPY_PV));
+#else
       WAITP(1, tc::mbar_wait(p_full + bs, (T / NS) & 1));
+#endif
 #ifdef LCX_TC_TRACE_PV  // columns 0 / 1 / 2: PV issuer passed the meta / P / V waits
       if (lane == 0) trace_mark(p, T, 1);
 #endif

@@ -66,6 +66,23 @@ __device__ __forceinline__ void mbar_wait(SBar bar, uint32_t parity) {
       : "memory");
 #endif
 }
+// Wait for warps off the critical path: poll with test_wait and sleep between polls, so
+// the waiting warp does not take issue slots (a suspended try_wait is woken by other
+// barriers' traffic and re-polls) from the softmax warps sharing its SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleepy(SBar bar, uint32_t parity, uint32_t ns) {
+  for (;;) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar.a), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(ns);
+  }
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   mbar_wait(sbar(bar), parity);
 }
