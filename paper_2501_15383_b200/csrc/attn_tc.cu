@@ -136,6 +136,10 @@ constexpr float kRescaleThresh = 8.f;
 #ifndef LCX_TC_SLEEPY
 #define LCX_TC_SLEEPY 300
 #endif
+// QK / PV MMAs issued eight / four per asm block (one elect, offsets added in PTX)
+#ifndef LCX_TC_MMA_X8
+#define LCX_TC_MMA_X8 0
+#endif
 #ifndef LCX_TC_SLEEPY_PV  // the PV issuer's wait for P (on the critical path)
 #define LCX_TC_SLEEPY_PV 0
 #endif
@@ -692,6 +696,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #endif
         const uint32_t qa = tmem + COL_Q + qb * QBUF + (combo == 2 ? HD / 2 : 0);  // hh, hl, lh
         const uint64_t ka = dk + (combo == 1 ? ((2 * kKHalf) >> 4) : 0);
+#if LCX_TC_MMA_X8
+        tc::mma_f16_ts_x8_warp(dS, qa, ka, kKHalf >> 4, IDESC_QK, combo ? 1u : 0u);
+#else
 #pragma unroll
         for (int half = 0; half < 2; ++half)
 #pragma unroll
@@ -699,6 +706,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
             tc::mma_f16_ts_warp(dS, qa + half * 32 + kk * 8,
                                 ka + ((half * kKHalf + kk * 32) >> 4), IDESC_QK,
                                 (combo | half | kk) ? 1u : 0u);
+#endif
       }
       tc::mma_commit_warp(k_empty + bk);
       tc::mma_commit_warp(s_full + bs);
@@ -797,10 +805,15 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       const bool first = kSplitO ? (T - T_first < uint32_t(kGroups) && !(p.init && T == T_first))
                                  : ((flags & F_FIRST) && !p.init);
       const uint32_t dO = tmem + COL_O + (kSplitO ? (T % kGroups) * HD : 0);
+#if LCX_TC_MMA_X8
+      static_assert(BN / 16 == 4, "four PV MMAs per tile");
+      tc::mma_f16_ts_x4_warp(dO, tmem + bs * BN, dv, IDESC_PV, first ? 0u : 1u);
+#else
 #pragma unroll
       for (int kk = 0; kk < BN / 16; ++kk)  // P (fp16, 2 per column) aliases S buffer bs
         tc::mma_f16_ts_warp(dO, tmem + bs * BN + kk * 8, dv + ((kk * 32) >> 4),
                             IDESC_PV, (first && kk == 0) ? 0u : 1u);
+#endif
       tc::mma_commit_warp(v_empty + bv);
       tc::mma_commit_warp(s_free + bs);
       if (lane == 0) trace_mark(p, T, 4);

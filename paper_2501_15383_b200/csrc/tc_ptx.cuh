@@ -174,6 +174,57 @@ __device__ __forceinline__ void mma_f16_ss_warp(uint32_t d_tmem, uint64_t adesc,
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Eight TS MMAs of one K = 128 product in one asm block (one elect, one predicate):
+// MMA x covers A columns a_tmem + a_off[x] and B descriptor bdesc + b_off[x]
+// (half = x / 4, kk = x % 4: A + 32 half + 8 kk, B + bhalf half + 2 kk in 16-byte units);
+// the first accumulates iff `accumulate`, the rest always.
+__device__ __forceinline__ void mma_f16_ts_x8_warp(uint32_t d_tmem, uint32_t a_tmem,
+                                                   uint64_t bdesc, uint32_t bhalf,
+                                                   uint32_t idesc, uint32_t accumulate) {
+  const uint64_t b1 = bdesc + bhalf;
+  asm volatile(
+      "{\n\t.reg .pred p, t, e;\n\t"
+      ".reg .b32 a1, a2, a3, a4, a5, a6, a7;\n\t"
+      ".reg .b64 c1, c2, c3, c5, c6, c7;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "setp.eq.b32 t, %5, %5;\n\t"
+      "add.u32 a1, %1, 8;\n\t add.u32 a2, %1, 16;\n\t add.u32 a3, %1, 24;\n\t"
+      "add.u32 a4, %1, 32;\n\t add.u32 a5, %1, 40;\n\t add.u32 a6, %1, 48;\n\t"
+      "add.u32 a7, %1, 56;\n\t"
+      "add.u64 c1, %2, 2;\n\t add.u64 c2, %2, 4;\n\t add.u64 c3, %2, 6;\n\t"
+      "add.u64 c5, %3, 2;\n\t add.u64 c6, %3, 4;\n\t add.u64 c7, %3, 6;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %4, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], c1, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], c2, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], c3, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a4], %3, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a5], c5, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a6], c6, %4, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a7], c7, %4, t;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "l"(b1), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Four TS MMAs (A + 8 kk, B + 2 kk), the first accumulating iff `accumulate`.
+__device__ __forceinline__ void mma_f16_ts_x4_warp(uint32_t d_tmem, uint32_t a_tmem,
+                                                   uint64_t bdesc, uint32_t idesc,
+                                                   uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, t, e;\n\t"
+      ".reg .b32 a1, a2, a3;\n\t"
+      ".reg .b64 c1, c2, c3;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "setp.eq.b32 t, %4, %4;\n\t"
+      "add.u32 a1, %1, 8;\n\t add.u32 a2, %1, 16;\n\t add.u32 a3, %1, 24;\n\t"
+      "add.u64 c1, %2, 2;\n\t add.u64 c2, %2, 4;\n\t add.u64 c3, %2, 6;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], c1, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], c2, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], c3, %3, t;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void mma_f16_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
                                                 uint32_t idesc, uint32_t accumulate) {
   asm volatile(
