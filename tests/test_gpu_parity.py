@@ -458,6 +458,10 @@ TC_CASES = [
     (1000, 6, 2, 256, 64, (30, 90), (256, 640, 256), (True, True), "normal", 0.9),
     # budgets beyond the context: every line selected (select k >= n)
     (640, 4, 2, 128, 64, (1000, 1000), None, (True, True), "peaked", 1.0),
+    # tiny sequences: one row; a second chunk of two rows; DCA shorter than one chunk pair
+    (1, 2, 1, 128, 64, (4, 4), None, (True, True), "normal", 1.0),
+    (130, 4, 2, 128, 64, (8, 16), None, (True, True), "normal", 1.0),
+    (200, 4, 2, 128, 64, (3, 5), (128, 256, 128), (False, True), "peaked", 0.9),
 ]
 
 
