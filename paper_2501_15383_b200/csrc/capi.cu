@@ -857,6 +857,10 @@ int lcx_chunked_prefill_host(lcx_context* ctx, const lcx_attention_input* hin,
   }
   Arena ar{ctx->stage, ctx->stage_bytes, 0};
   plan(ar, &dq, &dk, &dv, &dpq, &dpk, &dout, &dlse, &dsv, &dsnv, &dss, &dsns, &dadm);
+  if (sel) {  // list padding past each count reads as 0, as the device entry leaves it
+    LCX_CHECK_CUDA(cudaMemsetAsync(dsv, 0, sizeof(int32_t) * size_t(nch) * hq * cap_v, st));
+    LCX_CHECK_CUDA(cudaMemsetAsync(dss, 0, sizeof(int32_t) * size_t(nch) * hq * cap_s, st));
+  }
   if (!ctx->h2d) LCX_CHECK_CUDA(cudaStreamCreateWithFlags(&ctx->h2d, cudaStreamNonBlocking));
   if (!ctx->d2h) LCX_CHECK_CUDA(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking));
   // positions are validated before the chunk loop: upload them first

@@ -552,12 +552,13 @@ def test_tc_sparse_attention_custom_positions(D, port):
 
 # ------------------------------------------------------------ host entry --
 @pytest.mark.parametrize("precision,dca", [("bf16", (256, 768, 256)), ("fp32", None)])
-def test_host_entry_equals_device_entry(D, port, precision, dca):
+@pytest.mark.parametrize("n", [1280, 1000, 3])
+def test_host_entry_equals_device_entry(D, port, precision, dca, n):
     """lcx_chunked_prefill_host (host buffers, chunk-pipelined copies) computes exactly
     what the device entry computes: same kernels, bitwise-equal outputs and selections;
-    and the oracle agrees."""
+    and the oracle agrees (full, ragged and tiny sequences)."""
     import torch
-    n, hq, hkv = 1280, 4, 2
+    hq, hkv = 4, 2
     q, k, v = _mh_inputs(n, hq, hkv, 128, precision, 21)
     dt = torch.float32 if precision == "fp32" else torch.bfloat16
     H = lambda x: torch.tensor(x).to(dt).contiguous().pin_memory()  # noqa: E731
