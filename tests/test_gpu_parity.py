@@ -579,13 +579,14 @@ def test_host_entry_equals_device_entry(D, port, precision, dca, n):
 @pytest.mark.parametrize("shards", [2, 3])
 @pytest.mark.parametrize("path,precision,dca", [("tc", "bf16", (256, 768, 256)),
                                                 ("simt", "fp32", None)])
-def test_line_sharded_prefill_merges_to_unsharded(D, port, shards, path, precision, dca):
+@pytest.mark.parametrize("n", [1024, 200])
+def test_line_sharded_prefill_merges_to_unsharded(D, port, shards, path, precision, dca, n):
     """North star (e): every shard attends over its part of the selected lines; the LSE
     merge of the partials (on-device merge of stacked partials, and the collective path's
     per-shard scaling + sum) equals the unsharded operator and the oracle; admitted
     counts add up (rank 0 reports the exact count, sparse.cpp:115-119)."""
     import torch
-    n, hq, hkv = 1024, 4, 2
+    hq, hkv = 4, 2
     q, k, v = _mh_inputs(n, hq, hkv, 128, precision, 31, "peaked")
     dt = torch.float32 if precision == "fp32" else torch.bfloat16
     T = lambda x: torch.tensor(x).to(dt).cuda().contiguous()  # noqa: E731
