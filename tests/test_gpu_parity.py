@@ -517,9 +517,10 @@ def test_tc_prefill_matches_oracle(D, port, case):
 
 
 @pytest.mark.parametrize("dca", [None, (256, 640, 256)])
-def test_tc_full_attention(D, port, dca):
+@pytest.mark.parametrize("n", [1024, 1, 333])
+def test_tc_full_attention(D, port, dca, n):
     import torch
-    n, hq, hkv = 1024, 2, 1
+    hq, hkv = 2, 1
     q, k, v = _mh_inputs(n, hq, hkv, 128, "bf16", 3, "peaked")
     T = lambda x: torch.tensor(x).to(torch.bfloat16).cuda().contiguous()  # noqa: E731
     out, lse = D.full_attention(T(q), T(k), T(v), dca=dca, kernel_path="tc", temperature=0.9)
