@@ -1001,6 +1001,9 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
                  cap_s < std::min<int64_t>(cfg->budget_slash, n) + block_max))
     return fail(LCX_ERR_DIMENSION, "selection capacity below budget + forced lines");
   const int tc_min = cfg->tc_min_entries > 0 ? cfg->tc_min_entries : kDefaultTcMin;
+  // recall check scratch rows: the last B rows of a chunk, from a 128-aligned row on the
+  // tensor-core path
+  const int64_t kRecRows = block_max + (tc ? 127 : 0);
 
   // workspace plan (largest chunk = the last one: nk = n)
   EstimateArgs e_max = base_est(in, ctx, n - std::min(L, n), std::min(L, n), n, cfg->last_q,
@@ -1038,9 +1041,9 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
         *ins = A.template take<int32_t>(size_t(hq));
       }
       if (est_tc) k3 = A.template take<uint8_t>(est_tc_k3_bytes(n, in->hkv));
-      if (out->recall) {  // dense rows of the recall check: [128][hq][dim] O + [hq][128] lse
-        rec_o = A.template take<float>(size_t(128) * hq * in->dim);
-        rec_l = A.template take<float>(size_t(hq) * 128);
+      if (out->recall) {  // dense rows of the recall check: [rows][hq][dim] O + [hq][rows] lse
+        rec_o = A.template take<float>(size_t(kRecRows) * hq * in->dim);
+        rec_l = A.template take<float>(size_t(hq) * kRecRows);
       }
       if (shards > 1) {  // this shard's lines
         ov = A.template take<int32_t>(size_t(hq) * cap_v);
@@ -1145,15 +1148,17 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
                             out->admitted ? out->admitted + ci * hq : nullptr, st,
                             (prof && tc) ? e[4] : nullptr, (prof && tc) ? e[5] : nullptr, shards > 1 ? &full : nullptr));
     if (sparse && out->recall) {
-      // dense LSE of the chunk's last rows (the TC path needs a 128-aligned row block)
+      // dense LSE of the chunk's last rows; the TC path starts them at a 128-aligned row
+      // (its chunks are 128-aligned), so at most B + 127 rows
       const int64_t b = std::min(cfg->last_q, t1 - t0);
-      const int64_t r0 = tc ? std::max<int64_t>(t0, t1 - 128) : t1 - b;
+      const int64_t r0 = tc ? std::max<int64_t>(t0, (t1 - b) / 128 * 128) : t1 - b;
+      if (t1 - r0 > kRecRows) return fail(LCX_ERR_INTERNAL, "recall scratch too small");
       float* o_base = rec_o - r0 * hq * in->dim;  // rows [r0, t1) -> scratch rows
-      float* l_base = rec_l - r0;                 // lse[h * 128 + i - r0]
+      float* l_base = rec_l - r0;                 // lse[h * kRecRows + i - r0]
       LCX_TRY(attention_chunk(ctx, in, w, r0, t1, false, nullptr, nullptr, 0, nullptr, nullptr,
-                              0, dca, s, dca ? c : 1, tc_min, o_base, l_base, 128, nullptr,
-                              st));
-      LCX_TRY(chunk_recall_launch(out->lse, n, rec_l, 128, r0, t1 - b, t1, hq,
+                              0, dca, s, dca ? c : 1, tc_min, o_base, l_base, kRecRows,
+                              nullptr, st));
+      LCX_TRY(chunk_recall_launch(out->lse, n, rec_l, kRecRows, r0, t1 - b, t1, hq,
                                   out->recall + ci * hq, st));
     }
     if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[3], st));

@@ -627,12 +627,13 @@ def test_line_sharded_prefill_merges_to_unsharded(D, port, shards, path, precisi
 # ------------------------------------------------------------- recall check --
 @pytest.mark.parametrize("precision,dca", [("bf16", (256, 768, 256)), ("fp32", None),
                                            ("bf16", None)])
-def test_prefill_recall_check(D, port, precision, dca):
+@pytest.mark.parametrize("n,lq", [(1024, 64), (1000, 64), (40, 64), (700, 200)])
+def test_prefill_recall_check(D, port, precision, dca, n, lq):
     """North star (d): the operator's recall check (dense LSE of each chunk's last lastQ
     rows vs the sparse LSE) equals the reference's attention_recall on the oracle's
     sparse and dense LSE of the same rows (refine.cpp:51-72); full budget -> recall 1."""
     import torch
-    n, hq, hkv, chunk, lq = 1024, 2, 1, 256, 64
+    hq, hkv, chunk = 2, 1, 256
     q, k, v = _mh_inputs(n, hq, hkv, 128, precision, 41, "peaked")
     dt = torch.float32 if precision == "fp32" else torch.bfloat16
     T = lambda x: torch.tensor(x).to(dt).cuda().contiguous()  # noqa: E731
@@ -646,8 +647,9 @@ def test_prefill_recall_check(D, port, precision, dca):
                                            "sparse", 1 if dca else 0, dca, temperature=0.9)
         o_f, l_f, _ = port.chunked_prefill(q[:, h], k[:, 0], v[:, 0], chunk, lq, (8, 16),
                                            "full", 1 if dca else 0, dca, temperature=0.9)
-        for ci in range(n // chunk):
-            rows = slice((ci + 1) * chunk - lq, (ci + 1) * chunk)
+        for ci in range(-(-n // chunk)):  # the last B = min(lastQ, rows) rows of each chunk
+            t1 = min(n, (ci + 1) * chunk)
+            rows = slice(t1 - min(lq, t1 - ci * chunk), t1)
             per, agg = port.attention_recall(l_s[rows], l_f[rows], slack=1e-9)
             assert abs(rec[ci, h] - agg) <= tol, (ci, h, rec[ci, h], agg)
     full = D.chunked_prefill(T(q), T(k), T(v), budget=(n, n), return_recall=True, **kw)
