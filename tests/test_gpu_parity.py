@@ -462,6 +462,9 @@ TC_CASES = [
     (1, 2, 1, 128, 64, (4, 4), None, (True, True), "normal", 1.0),
     (130, 4, 2, 128, 64, (8, 16), None, (True, True), "normal", 1.0),
     (200, 4, 2, 128, 64, (3, 5), (128, 256, 128), (False, True), "peaked", 0.9),
+    # zero budgets: only forced lines, or nothing at all (every row falls back to itself)
+    (512, 4, 2, 256, 64, (0, 0), None, (False, False), "normal", 1.0),
+    (512, 4, 2, 256, 64, (0, 0), (256, 384, 128), (True, True), "normal", 1.0),
 ]
 
 
