@@ -391,11 +391,12 @@ def test_measure_budget_recall(L, ref):
 
 # ---------------------------------------------------------- multi-head batch --
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
-def test_multihead_gqa_prefill(D, port, precision):
+@pytest.mark.parametrize("n", [640, 300, 1])
+def test_multihead_gqa_prefill(D, port, precision, n):
     """Batched [n, H, D] entry with GQA (hq=7*hkv): every head equals the single-head
     oracle run on its (q head, kv head) pair."""
     import torch
-    n, hq, hkv, dim = 640, 14, 2, 128
+    hq, hkv, dim = 14, 2, 128
     rng = np.random.default_rng(1)
     q = rounded(rng.standard_normal((n, hq, dim)), precision)
     k = rounded(rng.standard_normal((n, hkv, dim)), precision)
