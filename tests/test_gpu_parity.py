@@ -158,8 +158,9 @@ def test_select_critical_one_row_trick(L, ref):
 
 # ----------------------------------------------------------------- attention --
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
-def test_sparse_attention_standard(L, port, precision):
-    n, dim = 512, 128
+@pytest.mark.parametrize("n", [512, 129, 1])
+def test_sparse_attention_standard(L, port, precision, n):
+    dim = 128
     q, k, v = rin(port, 11, n, dim, precision)
     crit = port.select_critical(port.estimate_block(q, k, 64), (20, 30), n)
     ref = port.sparse_attention(q, k, v, crit)
@@ -197,8 +198,9 @@ def test_sparse_attention_custom_positions(L, port):
 
 
 @pytest.mark.parametrize("dca", [None, (48, 128, 48)])
-def test_full_attention(L, port, dca):
-    n, dim = 300, 64
+@pytest.mark.parametrize("n", [300, 1])
+def test_full_attention(L, port, dca, n):
+    dim = 64
     q, k, v = rin(port, 14, n, dim, "fp32")
     ref = port.full_attention(q, k, v, dca=dca)
     got = L.full_attention(L.AttentionInput(q, k, v), L.ChunkConfig(*dca) if dca else None)
