@@ -39,7 +39,12 @@ namespace {
 #endif
 constexpr int kLanes = LCX_GATHER_LANES;  // lanes per row (8 or 16)
 constexpr int kDims = 128 / kLanes;       // dims per lane
-constexpr int kRows = 256 / kLanes;       // rows per CTA
+// 128-thread CTAs at 6 per SM: the gather itself 72 -> 68 ms, but the attention kernel
+// running beside it loses as much (363 vs 359 ms): step time equal, kept at 256
+#ifndef LCX_GATHER_THREADS
+#define LCX_GATHER_THREADS 256
+#endif
+constexpr int kRows = LCX_GATHER_THREADS / kLanes;  // rows per CTA
 constexpr int kThreads = kRows * kLanes;
 #ifndef LCX_GATHER_MINB
 #define LCX_GATHER_MINB (LCX_GATHER_LANES == 16 ? 3 : 2)
