@@ -532,6 +532,8 @@ int lcx_context_create(int device, lcx_context** out) {
   if (prop.major != 10)
     return fail(LCX_ERR_CUDA, std::string("device ") + prop.name +
                                   " is not sm_100-class; kernels are built for sm_100a only");
+  DeviceScope on(device);  // the context's buffers live on `device`
+  if (on.err != cudaSuccess) return fail(LCX_ERR_CUDA, "cudaSetDevice failed");
   auto* ctx = new lcx_context();
   ctx->device = device;
   ctx->sm_count = prop.multiProcessorCount;
@@ -548,6 +550,7 @@ int lcx_context_create(int device, lcx_context** out) {
 
 int lcx_context_destroy(lcx_context* ctx) {
   if (!ctx) return LCX_OK;
+  DeviceScope on(ctx->device);
   cudaDeviceSynchronize();
   if (ctx->ws) cudaFree(ctx->ws);
   if (ctx->rope) cudaFree(ctx->rope);
@@ -566,11 +569,13 @@ int lcx_context_destroy(lcx_context* ctx) {
 }
 
 int lcx_set_profiling(lcx_context* ctx, int enabled) {
+  LCX_ON_DEVICE(ctx);
   ctx->profiling = enabled;
   return LCX_OK;
 }
 
 int lcx_debug_trace(lcx_context* ctx, int enable, long long* host_out) {
+  LCX_ON_DEVICE(ctx);
   const size_t bytes = (512 * 8 + 64) * sizeof(long long);  // per-tile marks + wait profile
   if (enable && !ctx->trace) {
     LCX_CHECK_CUDA(cudaMalloc(&ctx->trace, bytes));
@@ -593,6 +598,7 @@ int lcx_get_stats(lcx_context* ctx, lcx_prefill_stats* out) {
 }
 
 int lcx_get_chunk_ms(lcx_context* ctx, float* out, int64_t cap, int64_t* count) {
+  LCX_ON_DEVICE(ctx);
   if (!count) return fail(LCX_ERR_DIMENSION, "null count");
   *count = int64_t(ctx->chunk_ms.size());
   if (out)
@@ -603,6 +609,7 @@ int lcx_get_chunk_ms(lcx_context* ctx, float* out, int64_t cap, int64_t* count) 
 int lcx_estimate_block(lcx_context* ctx, const lcx_attention_input* in, int64_t q_row0,
                        int64_t nq, int64_t nk, int64_t last_q, int32_t pos_mode,
                        const lcx_chunk_config* cfg, float* est_out, void* stream) {
+  LCX_ON_DEVICE(ctx);
   LCX_TRY(validate_input(in));
   if (last_q <= 0) return fail(LCX_ERR_CONFIG, "lastQ must be positive");
   if (nq <= 0 || nk <= 0) return fail(LCX_ERR_DIMENSION, "empty query or key matrix");
@@ -628,6 +635,7 @@ int lcx_estimate_block(lcx_context* ctx, const lcx_attention_input* in, int64_t 
 int lcx_line_scores(lcx_context* ctx, const lcx_attention_input* in, int64_t q_row0, int64_t nq,
                     int64_t nk, int64_t last_q, int32_t pos_mode, const lcx_chunk_config* cfg,
                     int32_t slash_mean, float* col_score, float* slash_score, void* stream) {
+  LCX_ON_DEVICE(ctx);
   LCX_TRY(validate_input(in));
   if (last_q <= 0) return fail(LCX_ERR_CONFIG, "lastQ must be positive");
   if (nq <= 0 || nk <= 0 || nq > nk || q_row0 + nq != nk || nk > in->n)
@@ -665,6 +673,7 @@ int lcx_select_from_scores(lcx_context* ctx, const float* col_score, const float
                            int64_t budget_slash, const lcx_selection_options* opts,
                            int32_t* verticals, int32_t* nv, int64_t cap_v, int32_t* slashes,
                            int32_t* ns, int64_t cap_s, void* stream) {
+  LCX_ON_DEVICE(ctx);
   (void)ctx;
   if (n <= 0 || block <= 0 || block > n)
     return fail(LCX_ERR_DIMENSION, "estimation block row count out of range");
@@ -682,6 +691,7 @@ int lcx_select_critical(lcx_context* ctx, const float* est, int32_t heads, int64
                         const lcx_selection_options* opts, int32_t* verticals, int32_t* nv,
                         int64_t cap_v, int32_t* slashes, int32_t* ns, int64_t cap_s,
                         void* stream) {
+  LCX_ON_DEVICE(ctx);
   if (n <= 0 || block <= 0 || block > n)
     return fail(LCX_ERR_DIMENSION, "estimation block row count out of range");
   lcx_selection_options o = opts ? *opts : lcx_selection_options{1, 1, 1};
@@ -703,6 +713,7 @@ int lcx_sparse_attention(lcx_context* ctx, const lcx_attention_input* in,
                          const int32_t* slashes, const int32_t* ns, int64_t cap_s,
                          int32_t use_dca, const lcx_chunk_config* dca, int32_t kernel_path,
                          float* out, float* lse, void* stream) {
+  LCX_ON_DEVICE(ctx);
   LCX_TRY(validate_input(in));
   if (use_dca) LCX_TRY(validate_chunk(dca));
   cudaStream_t st = S(stream);
@@ -732,6 +743,7 @@ int lcx_attention_rel(lcx_context* ctx, const lcx_attention_input* in, const int
                       const int32_t* nv, int64_t cap_v, const int32_t* slashes,
                       const int32_t* ns, int64_t cap_s, const int64_t* rel, float* out,
                       float* lse, void* stream) {
+  LCX_ON_DEVICE(ctx);
   LCX_TRY(validate_input(in));
   if (!rel) return fail(LCX_ERR_DIMENSION, "relative-position override must be n x n");
   const bool sparse = verticals != nullptr;
@@ -772,6 +784,13 @@ int lcx_attention_rel(lcx_context* ctx, const lcx_attention_input* in, const int
   a.cap_s = cap_s;
   a.vbits = w.vbits;
   a.bit_words = w.words;
+  // unsharded: the full selection is this call's selection, and rows with no admitted
+  // line attend to themselves (sparse.cpp:111)
+  a.fverts = verticals;
+  a.fnv = nv;
+  a.fslashes = slashes;
+  a.fns = ns;
+  a.do_fallback = 1;
   a.out = out;
   a.lse = lse;
   a.lse_stride = n;
@@ -781,6 +800,7 @@ int lcx_attention_rel(lcx_context* ctx, const lcx_attention_input* in, const int
 int lcx_full_attention(lcx_context* ctx, const lcx_attention_input* in, int32_t use_dca,
                        const lcx_chunk_config* dca, int32_t kernel_path, float* out, float* lse,
                        void* stream) {
+  LCX_ON_DEVICE(ctx);
   LCX_TRY(validate_input(in));
   if (use_dca) LCX_TRY(validate_chunk(dca));
   cudaStream_t st = S(stream);
@@ -808,6 +828,7 @@ int lcx_full_attention(lcx_context* ctx, const lcx_attention_input* in, int32_t 
 
 int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
                         const lcx_prefill_config* cfg, lcx_prefill_output* out, void* stream) {
+  LCX_ON_DEVICE(ctx);
   return prefill_impl(ctx, in, cfg, out, S(stream), nullptr, nullptr);
 }
 
@@ -815,6 +836,7 @@ int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
 int lcx_chunked_prefill_host(lcx_context* ctx, const lcx_attention_input* hin,
                              const lcx_prefill_config* cfg, lcx_prefill_output* hout,
                              void* stream) {
+  LCX_ON_DEVICE(ctx);
   LCX_TRY(validate_input(hin));
   if (!cfg || !hout || !hout->out || !hout->lse)
     return fail(LCX_ERR_DIMENSION, "null config/output");
@@ -1214,14 +1236,15 @@ extern "C" {
 int lcx_attention_recall(lcx_context* ctx, const float* lse_sparse, const float* lse_full,
                          int64_t n, double slack, float* per_query, double* aggregate,
                          void* stream) {
+  LCX_ON_DEVICE(ctx);
   if (n <= 0) return fail(LCX_ERR_DIMENSION, "recall needs at least one query");
   cudaStream_t st = S(stream);
   Sizer sz;
-  sz.take<double>(1);
+  sz.take<double>(1025);
   sz.take<int>(1);
   LCX_TRY(ensure_workspace(ctx, sz.off));
   Arena ar{ctx->ws, ctx->ws_bytes, 0};
-  double* dsum = ar.take<double>(1);
+  double* dsum = ar.take<double>(1025);  // total + per-block partials (fixed-order sum)
   int* dbad = ar.take<int>(1);
   LCX_TRY(recall_kernel_launch(lse_sparse, lse_full, n, slack, per_query, dsum, dbad, st));
   double hsum = 0;
@@ -1237,6 +1260,7 @@ int lcx_attention_recall(lcx_context* ctx, const float* lse_sparse, const float*
 int lcx_lse_scale_partial(lcx_context* ctx, float* o, const float* lse_own, const float* lse_all,
                           int32_t parts, int64_t n, int32_t hq, int32_t dim, float* lse_out,
                           void* stream) {
+  LCX_ON_DEVICE(ctx);
   (void)ctx;
   if (parts <= 0 || n <= 0 || hq <= 0 || dim <= 0)
     return fail(LCX_ERR_DIMENSION, "merge needs at least one part, row, head and dim");
@@ -1245,6 +1269,7 @@ int lcx_lse_scale_partial(lcx_context* ctx, float* o, const float* lse_own, cons
 
 int lcx_lse_merge(lcx_context* ctx, const float* o_parts, const float* lse_parts, int32_t parts,
                   int64_t rows, int32_t dim, float* out, float* lse_out, void* stream) {
+  LCX_ON_DEVICE(ctx);
   (void)ctx;
   if (parts <= 0) return fail(LCX_ERR_DIMENSION, "merge needs at least one part");
   return lse_merge_launch(o_parts, lse_parts, parts, rows, dim, out, lse_out, S(stream));

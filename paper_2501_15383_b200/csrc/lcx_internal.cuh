@@ -52,6 +52,25 @@ inline int fail(int code, const std::string& msg) {
   return code;
 }
 
+// Every C-ABI entry runs on its context's device, whatever device the caller has current,
+// and restores the caller's device on return.
+struct DeviceScope {
+  int prev = -1, dev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceScope(int d) : dev(d) {
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceScope() {
+    if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+  }
+};
+#define LCX_ON_DEVICE(ctx)                                                          \
+  if (!(ctx)) return ::lcx::fail(LCX_ERR_INTERNAL, "null context");                \
+  ::lcx::DeviceScope _lcx_dev((ctx)->device);                                       \
+  if (_lcx_dev.err != cudaSuccess)                                                  \
+  return ::lcx::fail(LCX_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(_lcx_dev.err))
+
 // -------------------------------------------------------- device helpers --
 __host__ __device__ __forceinline__ int64_t lcx_min64(int64_t a, int64_t b) { return a < b ? a : b; }
 __host__ __device__ __forceinline__ int64_t lcx_max64(int64_t a, int64_t b) { return a > b ? a : b; }

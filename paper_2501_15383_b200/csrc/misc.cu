@@ -28,9 +28,14 @@ __global__ void bitmap_kernel(const int32_t* __restrict__ lists, const int32_t* 
 }
 
 // refine.cpp:51-72: r = exp(lse_s - lse_f); > 1 + slack is an error; clamp to 1.
+// The aggregate is deterministic: each block writes its partial sum (fixed grid-stride
+// order, fixed shuffle tree, fixed cross-warp order) and recall_final_kernel adds the
+// block partials in index order.
+constexpr int kRecallBlocks = 1024;
 __global__ void recall_kernel(const float* __restrict__ ls, const float* __restrict__ lf,
                               int64_t n, double slack, float* __restrict__ per,
-                              double* __restrict__ sum, int* __restrict__ bad) {
+                              double* __restrict__ partial, int* __restrict__ bad) {
+  __shared__ double warp_sum[8];
   double local = 0.0;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
@@ -41,7 +46,20 @@ __global__ void recall_kernel(const float* __restrict__ ls, const float* __restr
     local += r;
   }
   for (int o = 16; o >= 1; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd(sum, local);
+  if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = local;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) t += warp_sum[w];
+    partial[blockIdx.x] = t;
+  }
+}
+
+__global__ void recall_final_kernel(const double* __restrict__ partial, int blocks,
+                                    double* __restrict__ sum) {
+  double t = 0.0;
+  for (int b = 0; b < blocks; ++b) t += partial[b];
+  *sum = t;
 }
 
 // out = sum_g exp(lse_g - lse) o_g, lse = logsumexp_g lse_g (empty shards: -inf)
@@ -151,13 +169,15 @@ int build_bitmaps(const int32_t* lists, const int32_t* counts, int64_t cap, int 
   return LCX_OK;
 }
 
+// sum_dev: kRecallBlocks + 1 doubles (block partials, then the total)
 int recall_kernel_launch(const float* ls, const float* lf, int64_t n, double slack, float* per,
                          double* sum_dev, int* bad_dev, cudaStream_t st) {
-  LCX_CHECK_CUDA(cudaMemsetAsync(sum_dev, 0, sizeof(double), st));
   LCX_CHECK_CUDA(cudaMemsetAsync(bad_dev, 0, sizeof(int), st));
-  const int64_t blocks = std::min<int64_t>(1024, (n + 255) / 256);
-  recall_kernel<<<unsigned(std::max<int64_t>(1, blocks)), 256, 0, st>>>(ls, lf, n, slack, per,
-                                                                        sum_dev, bad_dev);
+  const int blocks =
+      int(std::max<int64_t>(1, std::min<int64_t>(kRecallBlocks, (n + 255) / 256)));
+  recall_kernel<<<unsigned(blocks), 256, 0, st>>>(ls, lf, n, slack, per, sum_dev + 1, bad_dev);
+  LCX_CHECK_LAUNCH();
+  recall_final_kernel<<<1, 1, 0, st>>>(sum_dev + 1, blocks, sum_dev);
   LCX_CHECK_LAUNCH();
   return LCX_OK;
 }

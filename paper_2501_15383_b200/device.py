@@ -38,8 +38,11 @@ def _ptr(t):
     return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p()
 
 
-def _stream(stream=None):
-    s = stream if stream is not None else torch.cuda.current_stream()
+def _stream(stream=None, ctx=None):
+    """The caller's stream, else torch's current stream ON THE CONTEXT'S DEVICE (the C-ABI
+    runs every entry on its context's device, whatever device is current)."""
+    s = stream if stream is not None else torch.cuda.current_stream(
+        ctx.device if ctx is not None else None)
     return C.c_void_p(s.cuda_stream)
 
 
@@ -132,7 +135,7 @@ def chunked_prefill(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
                        recall.data_ptr() if recall is not None else None)
     ctx = ctx or context(dev.index)
     check(lib().lcx_chunked_prefill(ctx.ptr, C.byref(inp), C.byref(cfg), C.byref(o),
-                                    _stream(stream)))
+                                    _stream(stream, ctx)))
     res = dict(out=out, lse=lse, **sel)
     if admitted is not None:
         res["admitted"] = admitted
@@ -153,7 +156,7 @@ def estimate_block(q, k, *, q_row0, nq, nk, last_q, position_mode="standard", dc
     ctx = ctx or context(q.device.index)
     check(lib().lcx_estimate_block(ctx.ptr, C.byref(inp), int(q_row0), int(nq), int(nk),
                                    int(last_q), pm, C.byref(d) if d else None, _ptr(est),
-                                   _stream(stream)))
+                                   _stream(stream, ctx)))
     return est
 
 
@@ -168,7 +171,7 @@ def line_scores(q, k, *, q_row0, nq, nk, last_q, position_mode="standard", dca=N
     check(lib().lcx_line_scores(ctx.ptr, C.byref(inp), int(q_row0), int(nq), int(nk),
                                 int(last_q), POSITION_MODES[position_mode],
                                 C.byref(d) if d else None, int(slash_mean), _ptr(col), _ptr(sl),
-                                _stream(stream)))
+                                _stream(stream, ctx)))
     return col, sl
 
 
@@ -187,7 +190,7 @@ def select_from_scores(col, slash, *, block, budget, opts: Options | None = None
     ctx = ctx or context(dev.index)
     check(lib().lcx_select_from_scores(ctx.ptr, _ptr(col), _ptr(slash), heads, n, int(block), bv,
                                        bs, C.byref(o), _ptr(v), _ptr(nv), cap_v, _ptr(s),
-                                       _ptr(ns), cap_s, _stream(stream)))
+                                       _ptr(ns), cap_s, _stream(stream, ctx)))
     return v, nv, s, ns
 
 
@@ -207,7 +210,7 @@ def select_critical(est, *, n, budget, opts: Options | None = None, stream=None,
     ctx = ctx or context(dev.index)
     check(lib().lcx_select_critical(ctx.ptr, _ptr(est), heads, block, n, bv, bs, C.byref(o),
                                     _ptr(v), _ptr(nv), cap_v, _ptr(s), _ptr(ns), cap_s,
-                                    _stream(stream)))
+                                    _stream(stream, ctx)))
     return v, nv, s, ns
 
 
@@ -224,7 +227,7 @@ def sparse_attention(q, k, v, verticals, nv, slashes, ns, *, dca=None, positions
                                      verticals.shape[-1], _ptr(slashes), _ptr(ns),
                                      slashes.shape[-1], int(d is not None),
                                      C.byref(d) if d else None, KERNEL_PATHS[kernel_path],
-                                     _ptr(out), _ptr(lse), _stream(stream)))
+                                     _ptr(out), _ptr(lse), _stream(stream, ctx)))
     return out, lse
 
 
@@ -238,7 +241,7 @@ def full_attention(q, k, v, *, dca=None, positions_q=None, positions_k=None, rop
     ctx = ctx or context(q.device.index)
     check(lib().lcx_full_attention(ctx.ptr, C.byref(inp), int(d is not None),
                                    C.byref(d) if d else None, KERNEL_PATHS[kernel_path],
-                                   _ptr(out), _ptr(lse), _stream(stream)))
+                                   _ptr(out), _ptr(lse), _stream(stream, ctx)))
     return out, lse
 
 
@@ -253,7 +256,7 @@ def attention_recall(lse_sparse, lse_full, *, slack=1e-5, stream=None, ctx=None)
     agg = C.c_double()
     ctx = ctx or context(lse_sparse.device.index)
     check(lib().lcx_attention_recall(ctx.ptr, _ptr(lse_sparse), _ptr(lse_full), n, float(slack),
-                                     _ptr(per), C.byref(agg), _stream(stream)))
+                                     _ptr(per), C.byref(agg), _stream(stream, ctx)))
     return per, agg.value
 
 
@@ -270,7 +273,7 @@ def lse_scale_partial(o, lse_own, lse_all, *, stream=None, ctx=None):
     tot = torch.empty((hq, n), dtype=torch.float32, device=o.device)
     ctx = ctx or context(o.device.index)
     check(lib().lcx_lse_scale_partial(ctx.ptr, _ptr(o), _ptr(lse_own), _ptr(lse_all), g, n, hq,
-                                      dim, _ptr(tot), _stream(stream)))
+                                      dim, _ptr(tot), _stream(stream, ctx)))
     return tot
 
 
@@ -283,7 +286,7 @@ def lse_merge(o_parts, lse_parts, *, stream=None, ctx=None):
     lse = torch.empty((rows,), dtype=torch.float32, device=o_parts.device)
     ctx = ctx or context(o_parts.device.index)
     check(lib().lcx_lse_merge(ctx.ptr, _ptr(o_parts), _ptr(lse_parts), g, rows, dim, _ptr(out),
-                              _ptr(lse), _stream(stream)))
+                              _ptr(lse), _stream(stream, ctx)))
     return out, lse
 
 
@@ -331,5 +334,5 @@ def chunked_prefill_host(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
     ctx = ctx or context(device)
     with torch.cuda.device(device):
         check(lib().lcx_chunked_prefill_host(ctx.ptr, C.byref(inp), C.byref(cfg), C.byref(o),
-                                             _stream(stream)))
+                                             _stream(stream, ctx)))
     return dict(out=out, lse=lse, **sel)

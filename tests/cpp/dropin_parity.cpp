@@ -190,6 +190,16 @@ int main(int argc, char** argv) {
   const RelPositionMatrix rel = dca_position_matrix(n, cfg);
   const AttentionResult ra = full_attention(t, &rel);
   put(o, ra.output.values);
+  // 3b. sparse attention under the explicit override (harness.cpp:399, DCA sparsity check),
+  //     once with the selection above and once with lines that leave the first rows empty
+  //     (self fallback, sparse.cpp:111)
+  const AttentionResult rs = sparse_attention(t, crit, &rel);
+  put(o, rs.output.values);
+  put(o, rs.lse);
+  const CriticalSet late{{5}, {3}, n};
+  const AttentionResult rf = sparse_attention(t, late, &rel);
+  put(o, rf.output.values);
+  put(o, rf.lse);
   // 4. recall
   put(o, {measure_budget_recall(in, budget, RecallMeasurement{})});
   o.close();

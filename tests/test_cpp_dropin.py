@@ -14,6 +14,8 @@ import subprocess
 import numpy as np
 import pytest
 
+from oracle import Critical
+
 from helpers import TOL, lse_rel_err, rounded, row_rel_err
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -101,6 +103,12 @@ def test_dropin_matches_oracle(port, tmp_path, precision):
     assert row_rel_err(o_dca, o_ref) <= tol and lse_rel_err(lse, l_ref) <= tol
     o_rel = next(rec).reshape(n, dim)
     assert row_rel_err(o_rel, o_ref) <= 1e-5
+    # 3b. sparse attention under the RelPositionMatrix override (CUDA-core path)
+    t_yarn = port.yarn_temperature(2.0)
+    for c in (crit, Critical([5], [3], n)):
+        o_ref, l_ref = port.sparse_attention(q, k, v, c, temperature=t_yarn, dca=cfg)
+        o, lse = next(rec).reshape(n, dim), next(rec)
+        assert row_rel_err(o, o_ref) <= TOL["fp32"] and lse_rel_err(lse, l_ref) <= TOL["fp32"]
     # 4. measure_budget_recall
     got = next(rec)[0]
     assert 0.0 < got <= 1.0
