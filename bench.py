@@ -278,12 +278,45 @@ def approx_admitted(a):
     return tot * a.hq
 
 
+COUNTS = os.path.join(ROOT, "profiles", "workload_counts.json")
+
+
+def counts_key(a):
+    s, c = a.dca
+    return (f"n={a.n} hq={a.hq} hkv={a.hkv} chunk={a.chunk} last_q={a.last_q} "
+            f"budget={a.budget[0]},{a.budget[1]} dca={s},{c} rope_base={a.rope_base:g} "
+            f"kind={a.kind} seed={a.seed}")
+
+
+def load_counts(a):
+    try:
+        return json.load(open(COUNTS)).get(counts_key(a))
+    except Exception:
+        return None
+
+
+def save_counts(a, admitted):
+    """The exact admitted-entry count of this workload's selection (the GPU run's), kept in
+    a committed file so that the reference arm -- which runs first, on a fresh box -- can
+    project the reference CPU path onto the same exact count."""
+    try:
+        d = json.load(open(COUNTS)) if os.path.exists(COUNTS) else {}
+        d[counts_key(a)] = {"admitted_entries": int(admitted),
+                            "estimator_entries": int(exact_estimator_entries(a))}
+        os.makedirs(os.path.dirname(COUNTS), exist_ok=True)
+        with open(COUNTS, "w") as f:
+            json.dump(d, f, indent=1, sort_keys=True)
+    except Exception:
+        pass
+
+
 # ------------------------------------------------------------ reference arm --
 def run_reference(a, rank):
     if rank != 0:
         return
     est_full = exact_estimator_entries(a)
-    e_full = approx_admitted(a)
+    known = load_counts(a)
+    e_full = known["admitted_entries"] if known else approx_admitted(a)
     steps = []
     for w in range(a.warmup + a.steps):
         r = cpu_reference(a, est_full, e_full, reps=1)
@@ -302,13 +335,42 @@ def run_reference(a, rank):
                          "rates_us_per_entry_wall": last["rates_us_per_entry_wall"]},
         "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "note": "admitted entries projected as min(i+1, V+1+S+lastQ) per row (upper bound); "
-                "the main arm's cpu_baseline uses the exact count of its GPU run",
+        "projected": True,
+        "note": ("PROJECTED, not a full run: the reference CPU path needs hours per 1M-token "
+                 "layer, so each step times the reference's own chunked_prefill / "
+                 "estimate_block on a bounded sample (cpu_baseline.sample) and projects its "
+                 "per-entry rates onto this workload's exact estimator entries and "
+                 + ("the exact admitted-entry count of the GPU run's selection "
+                    "(profiles/workload_counts.json)" if known else
+                    "an UPPER-BOUND admitted count min(i+1, V+1+S+lastQ) per row (no GPU "
+                    "count recorded for this config)")),
+        "admitted_entries": e_full,
+        "admitted_entries_exact": bool(known),
     }
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------- ours --
+def relaunch(a):
+    """`bench.py --gpus N` (N > 1) outside torchrun: start N NCCL ranks on this node
+    (one process per GPU), the same launch the driver uses.  Fails loudly when the node
+    has fewer than N GPUs -- never a silent single-GPU run."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        sys.stderr.write(f"bench.py: --gpus {a.gpus} but this node has {have} CUDA device(s)\n")
+        sys.exit(2)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     a = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -317,6 +379,11 @@ def main():
     if a.impl == "reference":
         run_reference(a, rank)
         return
+    if "WORLD_SIZE" not in os.environ and a.gpus > 1:
+        relaunch(a)
+    if world != a.gpus:
+        sys.stderr.write(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(2)
 
     import torch
     import torch.distributed as dist
@@ -395,6 +462,8 @@ def main():
         dist.all_reduce(t_all[1:], op=dist.ReduceOp.SUM)
         ms = float(mx[0])
     E_total = int(t_all[1].item())
+    if rank == 0:
+        save_counts(a, E_total)
     ms_step = ms / a.steps
     value = a.n / (ms_step / 1e3)
 

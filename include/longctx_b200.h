@@ -123,7 +123,24 @@ typedef struct {
    * only.  0 / 1 = unsharded. */
   int32_t shard_rank;
   int32_t shard_count;
+  /* Phases of a sharded layer (multi-GPU, paper_2501_15383_b200/shard.py):
+   *   LCX_PHASE_ALL     estimator + selection + attention per chunk (the operator);
+   *   LCX_PHASE_SELECT  estimator + selection of every chunk only, into the selection
+   *                     log (out->sel_*, required), for query heads
+   *                     [est_head_begin, est_head_end) -- the other heads' slots are left
+   *                     untouched (the shards' slots are combined across GPUs);
+   *   LCX_PHASE_ATTEND  attention of every chunk only, over the selection log given in
+   *                     out->sel_* (required).
+   * A head's selection depends only on its own rows and the keys, so splitting the
+   * estimator by heads gives every shard bitwise the unsharded lists. */
+  int32_t phase;
+  int32_t est_head_begin, est_head_end;  /* 0 / 0 = every head */
+  /* != 0: record a context-owned CUDA event once chunk c's out / lse rows are final
+   * (see lcx_stream_wait_chunk) */
+  int32_t record_chunk_events;
 } lcx_prefill_config;
+
+enum { LCX_PHASE_ALL = 0, LCX_PHASE_SELECT = 1, LCX_PHASE_ATTEND = 2 };
 
 typedef struct {
   float* out;              /* [n][hq][dim] */
@@ -256,6 +273,12 @@ int lcx_chunked_prefill(lcx_context* ctx, const lcx_attention_input* in,
 int lcx_chunked_prefill_host(lcx_context* ctx, const lcx_attention_input* in,
                              const lcx_prefill_config* cfg, lcx_prefill_output* out,
                              void* stream);
+
+/* Makes `stream` wait until chunk `chunk` of the last lcx_chunked_prefill on this context
+ * (run with record_chunk_events) has its out / lse rows final: per-chunk work on another
+ * stream -- e.g. the log-sum-exp merge of KV-line shards over NCCL -- overlaps the
+ * attention of the chunks after it. */
+int lcx_stream_wait_chunk(lcx_context* ctx, int64_t chunk, void* stream);
 
 /* ---- recall (part d) ----------------------------------------------------- */
 /* per_query[i] = min(1, exp(lse_s - lse_f)); LCX_ERR_DOMAIN if any value

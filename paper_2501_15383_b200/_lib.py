@@ -53,7 +53,9 @@ class PrefillConfigC(C.Structure):
                 ("mode", C.c_int32), ("position_mode", C.c_int32), ("dca", ChunkConfigC),
                 ("opts", SelectionOptionsC), ("kernel_path", C.c_int32),
                 ("tc_min_entries", C.c_int32), ("shard_rank", C.c_int32),
-                ("shard_count", C.c_int32)]
+                ("shard_count", C.c_int32), ("phase", C.c_int32),
+                ("est_head_begin", C.c_int32), ("est_head_end", C.c_int32),
+                ("record_chunk_events", C.c_int32)]
 
 
 class PrefillOutputC(C.Structure):
@@ -76,6 +78,7 @@ EXPORTS = [
     "lcx_line_scores", "lcx_select_from_scores", "lcx_select_critical", "lcx_sparse_attention",
     "lcx_full_attention", "lcx_chunked_prefill", "lcx_chunked_prefill_host",
     "lcx_attention_recall", "lcx_lse_merge", "lcx_lse_scale_partial", "lcx_attention_rel",
+    "lcx_stream_wait_chunk",
 ]
 
 _lib = None
@@ -118,6 +121,7 @@ def lib() -> C.CDLL:
                                                    P(PrefillOutputC), vp]
             L.lcx_attention_recall.argtypes = [vp, vp, vp, i64, dbl, vp, P(dbl), vp]
             L.lcx_lse_merge.argtypes = [vp, vp, vp, i32, i64, i32, vp, vp, vp]
+            L.lcx_stream_wait_chunk.argtypes = [vp, i64, vp]
             L.lcx_lse_scale_partial.argtypes = [vp, vp, vp, vp, i32, i64, i32, i32, vp, vp]
             L.lcx_attention_rel.argtypes = [vp, P(AttentionInputC), vp, vp, i64, vp, vp, i64, vp,
                                             vp, vp, vp]

@@ -561,6 +561,7 @@ int lcx_context_destroy(lcx_context* ctx) {
   if (ctx->far_host) cudaFreeHost(ctx->far_host);
   for (auto& e : ctx->far_ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : ctx->chunk_done) cudaEventDestroy(e);
   if (ctx->stage) cudaFree(ctx->stage);
   if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
   if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
@@ -987,10 +988,24 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
                  lcx_prefill_output* out, cudaStream_t st, const cudaEvent_t* ready,
                  const cudaEvent_t* done, const std::function<int(int64_t)>* on_chunk) {
   LCX_TRY(validate_input(in));
-  if (!cfg || !out || !out->out || !out->lse) return fail(LCX_ERR_DIMENSION, "null config/output");
+  if (!cfg || !out) return fail(LCX_ERR_DIMENSION, "null config/output");
+  const int phase = cfg->phase;
+  if (phase != LCX_PHASE_ALL && phase != LCX_PHASE_SELECT && phase != LCX_PHASE_ATTEND)
+    return fail(LCX_ERR_CONFIG, "unknown prefill phase");
+  const bool do_select = phase != LCX_PHASE_ATTEND, do_attend = phase != LCX_PHASE_SELECT;
+  if (do_attend && (!out->out || !out->lse)) return fail(LCX_ERR_DIMENSION, "null output");
   if (cfg->chunk_len <= 0) return fail(LCX_ERR_CONFIG, "chunkLen must be positive");
   if (cfg->last_q <= 0) return fail(LCX_ERR_CONFIG, "lastQ must be positive");
   const bool sparse = cfg->mode == LCX_PREFILL_SPARSE;
+  if (phase != LCX_PHASE_ALL &&
+      (!sparse || !out->sel_verticals || !out->sel_nv || !out->sel_slashes || !out->sel_ns))
+    return fail(LCX_ERR_CONFIG, "select / attend phases need sparse mode and a selection log");
+  const int eh0 = cfg->est_head_end > 0 ? cfg->est_head_begin : 0;
+  const int eh1 = cfg->est_head_end > 0 ? cfg->est_head_end : in->hq;
+  if (eh0 < 0 || eh1 > in->hq || eh0 >= eh1)
+    return fail(LCX_ERR_CONFIG, "estimator head range out of range");
+  if (phase == LCX_PHASE_ALL && (eh0 != 0 || eh1 != in->hq))
+    return fail(LCX_ERR_CONFIG, "an estimator head range needs the select phase");
   if (sparse && cfg->chunk_len < cfg->last_q)
     return fail(LCX_ERR_CONFIG, "sparse prefill requires chunkLen >= lastQ");
   const bool dca = cfg->position_mode == LCX_POS_DCA_CONTINUOUS;
@@ -1043,7 +1058,7 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
   }
   int32_t *ov = nullptr, *onv = nullptr, *os = nullptr, *ons = nullptr;
   float *rec_o = nullptr, *rec_l = nullptr;
-  if (out->recall && shards > 1)
+  if (out->recall && (shards > 1 || phase != LCX_PHASE_ALL))
     return fail(LCX_ERR_CONFIG, "the recall check needs the merged (unsharded) lse");
   auto layout = [&](auto& A, AttnWS& w, float** col, float** sl, int32_t** iv, int32_t** inv,
                     int32_t** is, int32_t** ins, size_t* est_off) {
@@ -1092,6 +1107,14 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
   const bool prof = ctx->profiling != 0;
   const long long launches0 = g_launches;
   std::vector<cudaEvent_t> ev;
+  if (cfg->record_chunk_events) {
+    while (int64_t(ctx->chunk_done.size()) < nchunks) {
+      cudaEvent_t e;
+      LCX_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ctx->chunk_done.push_back(e);
+    }
+  }
+  ctx->chunk_events = cfg->record_chunk_events ? nchunks : 0;
   if (prof) {
     LCX_CHECK_CUDA(cudaMemsetAsync(ctx->tile_counter, 0, 2 * sizeof(int64_t), st));
     ev.resize(size_t(6 * nchunks + 1));
@@ -1110,10 +1133,10 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
     if (ready) LCX_CHECK_CUDA(cudaStreamWaitEvent(st, ready[ci], 0));
     if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[0], st));
     // rotated K / V^T of this chunk's new key rows (chunks only ever append keys)
-    if (tc)
+    if (tc && do_attend)
       LCX_TRY(tc_prepare_rows(in->k, in->v, n, t0, t1, in->hkv, in->positions_k, dca ? 1 : 0, s,
                               ctx->rope, w.B, st));
-    if (sparse) {
+    if (sparse && do_select) {
       if (est_tc)
         LCX_TRY(est_tc_prepare_keys(in->k, t0, t1, in->hkv, k3_tiles, ctx->rope, k3, st));
       EstimateArgs es = base_est(in, ctx, t0, t1 - t0, t1, cfg->last_q, dca ? 1 : 0, c);
@@ -1122,14 +1145,33 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
       es.col = col;
       es.slash = sl;
       es.slash_mean = cfg->opts.slash_mean;
+      es.h0 = eh0;
+      es.h1 = eh1;
       Arena a2 = est_ar;
       LCX_TRY(estimate_simt(ctx, es, a2, st));
       if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[1], st));
-      LCX_TRY(select_lines(col, hq, t1, cfg->budget_vertical, cfg->opts.force_sink_column, 1,
-                           vlist, vcnt, cap_v, st));
-      LCX_TRY(select_lines(sl, hq, t1, cfg->budget_slash, cfg->opts.force_local_band, block,
-                           slist, scnt, cap_s, st));
+      const int neh = eh1 - eh0;
+      LCX_TRY(select_lines(col + int64_t(eh0) * t1, neh, t1, cfg->budget_vertical,
+                           cfg->opts.force_sink_column, 1, vlist + eh0 * cap_v, vcnt + eh0,
+                           cap_v, st));
+      LCX_TRY(select_lines(sl + int64_t(eh0) * t1, neh, t1, cfg->budget_slash,
+                           cfg->opts.force_local_band, block, slist + eh0 * cap_s, scnt + eh0,
+                           cap_s, st));
       if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[2], st));
+    }
+    if (!do_attend) {
+      if (prof) {
+        LCX_CHECK_CUDA(cudaEventRecord(e[3], st));
+        LCX_CHECK_CUDA(cudaEventRecord(e[4], st));
+        LCX_CHECK_CUDA(cudaEventRecord(e[5], st));
+      }
+      continue;
+    }
+    if (sparse) {
+      if (prof && !do_select) {
+        LCX_CHECK_CUDA(cudaEventRecord(e[1], st));
+        LCX_CHECK_CUDA(cudaEventRecord(e[2], st));
+      }
       if (tc) {  // how many selected slashes reach beyond one key window (see below)
         LCX_CHECK_CUDA(cudaMemsetAsync(ctx->far_dev, 0, 2 * sizeof(int), st));
         far_count_kernel<<<hq, 256, 0, st>>>(slist, scnt, cap_s, kTcSegment, ctx->far_dev);
@@ -1185,6 +1227,7 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
     }
     if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[3], st));
     if (done) LCX_CHECK_CUDA(cudaEventRecord(done[ci], st));
+    if (cfg->record_chunk_events) LCX_CHECK_CUDA(cudaEventRecord(ctx->chunk_done[size_t(ci)], st));
     if (on_chunk) LCX_TRY((*on_chunk)(ci));  // e.g. enqueue this chunk's D2H now
   }
   ctx->stats = lcx_prefill_stats{};
@@ -1254,6 +1297,14 @@ int lcx_attention_recall(lcx_context* ctx, const float* lse_sparse, const float*
   LCX_CHECK_CUDA(cudaStreamSynchronize(st));
   if (hbad) return fail(LCX_ERR_DOMAIN, "recall above 1: sparse lse exceeds full lse");
   if (aggregate) *aggregate = hsum / double(n);
+  return LCX_OK;
+}
+
+int lcx_stream_wait_chunk(lcx_context* ctx, int64_t chunk, void* stream) {
+  LCX_ON_DEVICE(ctx);
+  if (chunk < 0 || chunk >= ctx->chunk_events)
+    return fail(LCX_ERR_DIMENSION, "no completion event recorded for this chunk");
+  LCX_CHECK_CUDA(cudaStreamWaitEvent(S(stream), ctx->chunk_done[size_t(chunk)], 0));
   return LCX_OK;
 }
 

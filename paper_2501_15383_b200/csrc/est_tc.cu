@@ -33,6 +33,10 @@ namespace lcx {
 namespace {
 
 constexpr int BN = 64;             // keys per tile
+#ifndef LCX_EST_PIECES
+#define LCX_EST_PIECES 296
+#endif
+constexpr int kEstPieces = LCX_EST_PIECES;  // tensor-core pieces per head pair (see est_tc_plan)
 constexpr int kQBox = 128 * 64 * 2;   // one [128 rows][64 dims] bf16 box = 16 KB
 constexpr int kKBox = 64 * 64 * 2;    // one [64 keys][64 dims] box = 8 KB
 constexpr int kQBytes = 6 * kQBox;    // 3 terms x 2 halves = 96 KB
@@ -63,8 +67,9 @@ __device__ __forceinline__ Item decode_item(const EstTcParams& p, int idx) {
   const int nf = int((p.far_end + p.per - 1) / p.per);
   const int nn = int((p.ntiles - p.near_begin + p.per - 1) / p.per);
   Item it;
-  it.pair = idx / (nf + nn);
-  const int k = idx - it.pair * (nf + nn);
+  const int pl = idx / (nf + nn);
+  it.pair = p.pair0 + pl;
+  const int k = idx - pl * (nf + nn);
   it.split = k;
   if (k < nf) {
     it.far = 1;
@@ -290,8 +295,9 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
             const int q1 = min(p.block - 1, e);
             // diagonal e walks T with stride 66 (= row 65 + column 1); zeros past the
             // estimator rows make the fixed-count form exact.  Fixed trip count with
-            // predicated adds (8 independent chains, every load in flight at once); reads
-            // past the diagonal stay inside the Q staging area and are discarded.
+            // predicated loads and adds (8 independent chains, every load in flight at
+            // once); nothing past the diagonal is read (it may be the other buffer, which
+            // the next tile's threads are writing).
             const float* dg = Tb + (dh * 64 + q0) * 65 + (q0 - e + 63);
             const int cnt = q1 - q0 + 1;
             float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -299,8 +305,8 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
             for (int q = 0; q < 64; q += 8)
 #pragma unroll
               for (int u = 0; u < 8; ++u) {
-                const float x = dg[(q + u) * 66];
-                a[u] += (q + u < cnt) ? x : 0.f;
+                const float x = (q + u < cnt) ? dg[(q + u) * 66] : 0.f;
+                a[u] += x;
               }
             const float acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
             p.diag_part[(int64_t(hd) * p.ntiles + it.t0 + t) * 128 + e] = acc;
@@ -362,11 +368,11 @@ __global__ void est_k3_kernel(const __nv_bfloat16* __restrict__ k, int64_t r0, i
 
 // Q3 [far 0/1][npairs][3 terms][2 halves][128 rows][64 dims]: row = 64 * (head in pair) + r
 __global__ void est_q3_kernel(const __nv_bfloat16* __restrict__ q, int hq, int group,
-                              int pairs_per_group, int npairs, int64_t nk, int64_t block,
-                              int far_too, int64_t c, const float2* __restrict__ rope,
-                              __nv_bfloat16* __restrict__ q3) {
+                              int pairs_per_group, int npairs, int pair0, int64_t nk,
+                              int64_t block, int far_too, int64_t c,
+                              const float2* __restrict__ rope, __nv_bfloat16* __restrict__ q3) {
   const int row = blockIdx.x;        // 0..127
-  const int pair = blockIdx.y;
+  const int pair = pair0 + int(blockIdx.y);
   const int far = blockIdx.z;
   if (far && !far_too) return;
   const int pr = threadIdx.x;        // 0..63
@@ -423,9 +429,16 @@ void est_tc_size(int hq, int hkv, Sizer& sz) {
   sz.take<uint8_t>(size_t(2) * npairs * 6 * kQBox);  // q3
 }
 
+int est_tc_max_splits() { return 2 * (kEstPieces + 2); }
+
 void est_tc_plan(const EstTcArgs& a, EstTcPlan& pl) {
   const int group = a.hq / a.hkv, ppg = (group + 1) / 2;
   pl.npairs = a.hkv * ppg;
+  // head pairs meeting the call's heads [h0, h1): pair of head h = (h / group) * ppg +
+  // (h % group) / 2
+  auto pair_of = [&](int h) { return (h / group) * ppg + (h % group) / 2; };
+  pl.pair0 = a.h1 > a.h0 ? pair_of(a.h0) : 0;
+  pl.pair1 = a.h1 > a.h0 ? pair_of(a.h1 - 1) + 1 : 0;
   pl.ntiles = (a.nk + 63) / 64;
   pl.far_end = 0;
   pl.near_begin = 0;
@@ -438,16 +451,18 @@ void est_tc_plan(const EstTcArgs& a, EstTcPlan& pl) {
     pl.near_begin = near_key <= 0 ? 0 : std::min<int64_t>(pl.ntiles, (near_key + 63) / 64);
     if (pl.near_begin < pl.far_end) pl.near_begin = pl.far_end;
   }
-  // pieces of 1/37 of the chunk's tensor-core tiles (>= 4 tiles): a function of the key
-  // range only, so a head's row statistics (combined over pieces in a fixed order) are
-  // bitwise the same whichever heads a call covers; <= 2 x 38 stats slots.  37 pieces x
-  // 16 head pairs (7B: 4 KV heads x 4 pairs) = 592 CTAs = exactly 4 waves on 148 SMs
+  // pieces of 1/kEstPieces of the chunk's tensor-core tiles (>= 4 tiles): a function of
+  // the key range only, so a head's row statistics (combined over pieces in a fixed
+  // order) are bitwise the same whichever heads a call covers -- the estimator shards
+  // over GPUs by head pairs with no exchange.  kEstPieces = 37 x 8: 16 head pairs (7B)
+  // = 4736 CTAs on one GPU, and still 592 (4 full waves on 148 SMs) for the two pairs of
+  // one rank of eight.
   const int64_t tc_tiles = pl.far_end + (pl.ntiles - pl.near_begin);
-  pl.per = int(std::max<int64_t>(4, (tc_tiles + 36) / 37));
+  pl.per = int(std::max<int64_t>(4, (tc_tiles + kEstPieces - 1) / kEstPieces));
   const int nf = int((pl.far_end + pl.per - 1) / pl.per);
   const int nn = int((pl.ntiles - pl.near_begin + pl.per - 1) / pl.per);
   pl.tc_splits = nf + nn;
-  pl.items = pl.npairs * (nf + nn);
+  pl.items = (pl.pair1 - pl.pair0) * (nf + nn);
 }
 
 // One pass of the estimator for one chunk on the tensor cores over the far and near
@@ -467,10 +482,10 @@ int est_tc_run(const EstTcArgs& a, const EstTcPlan& pl, Arena& ar, cudaStream_t 
   if (pl.items == 0) return LCX_OK;
   const bool dca = a.pos_mode == 1;
   if (a.pass == 1) {  // operands: rotated, 3-term split query rows (near and far)
-    dim3 grid(128, unsigned(npairs), 2);
+    dim3 grid(128, unsigned(pl.pair1 - pl.pair0), 2);
     est_q3_kernel<<<grid, 64, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(a.q), a.hq, group,
-                                       ppg, npairs, a.nk, a.block, dca ? 1 : 0, a.c, a.rope,
-                                       reinterpret_cast<__nv_bfloat16*>(q3));
+                                       ppg, npairs, pl.pair0, a.nk, a.block, dca ? 1 : 0, a.c,
+                                       a.rope, reinterpret_cast<__nv_bfloat16*>(q3));
     LCX_CHECK_LAUNCH();
   }
   CUtensorMap mq, mk3, mkr;
@@ -484,6 +499,7 @@ int est_tc_run(const EstTcArgs& a, const EstTcPlan& pl, Arena& ar, cudaStream_t 
   p.group = group;
   p.pairs_per_group = ppg;
   p.npairs = npairs;
+  p.pair0 = pl.pair0;
   p.nk = a.nk;
   p.block = int(a.block);
   p.ntiles_k = a.k3_tiles;

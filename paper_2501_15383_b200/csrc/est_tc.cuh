@@ -7,6 +7,7 @@ namespace lcx {
 
 struct EstTcParams {
   int group, pairs_per_group, npairs;
+  int pair0;                 // first head pair of this call (items cover pairs [pair0, ...))
   int64_t nk;
   int block;
   int64_t ntiles_k;          // 64-key tiles of the K3 buffer (its row stride)
@@ -30,13 +31,15 @@ struct EstTcArgs {
   const float2* rope;
   const void* k3; int64_t k3_tiles;  // rotated 3-term keys (est_tc_prepare_keys)
   int sm_count;
+  int h0, h1;                    // query heads of the call: pairs meeting [h0, h1)
   int pass;                      // 1 or 2
   int nsplit;                    // total stats slots (TC pieces + CUDA-core mixed splits)
   float2* stats; const float2* rowstat; float* col_part; float* diag_part;
 };
 
 struct EstTcPlan {
-  int npairs;
+  int npairs;          // all head pairs (q3 layout)
+  int pair0, pair1;    // pairs of this call
   int64_t ntiles, far_end, near_begin;
   int per, tc_splits, items;
 };
@@ -47,6 +50,7 @@ int est_tc_prepare_keys(const void* k, int64_t r0, int64_t r1, int hkv, int64_t 
                         const float2* rope, void* k3, cudaStream_t st);
 void est_tc_size(int hq, int hkv, Sizer& sz);
 void est_tc_plan(const EstTcArgs& a, EstTcPlan& pl);
+int est_tc_max_splits();  // upper bound of EstTcPlan::tc_splits (stats slots)
 int est_tc_run(const EstTcArgs& a, const EstTcPlan& pl, Arena& ar, cudaStream_t st);
 
 }  // namespace lcx

@@ -46,13 +46,14 @@ struct EstDev {
   int nrt;           // row tiles
   int64_t tile0, tile_end;  // key tiles this launch covers
   int split0, nsplit_total; // stats slot of split 0, slots per head
+  int h0;                    // first query head of this call (grid y = heads of the call)
 };
 
 // ---- prep: rotate the estimator query rows and the keys ------------------
 template <typename T>
 __global__ void est_prep_q(EstDev a) {
   const int64_t r = blockIdx.x;
-  const int h = blockIdx.y;
+  const int h = a.h0 + int(blockIdx.y);
   const int64_t gi = a.gbase + r;
   const int P = a.dim / 2;
   const T* qrow = reinterpret_cast<const T*>(a.q) + (gi * a.hq + h) * a.dim;
@@ -101,7 +102,7 @@ est_tile_kernel(EstDev a, float2* __restrict__ stats, const float2* __restrict__
   float* Kf = Kn + kKeys * DP;            // [64][DP]
   float* Ps = Kf + kKeys * DP;            // [64][65]
 
-  const int split = blockIdx.x, h = blockIdx.y, rt = blockIdx.z;
+  const int split = blockIdx.x, h = a.h0 + int(blockIdx.y), rt = blockIdx.z;
   const int g = h / a.group;
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
   const int64_t row0 = int64_t(rt) * kRows;
@@ -266,12 +267,13 @@ est_tile_kernel(EstDev a, float2* __restrict__ stats, const float2* __restrict__
   }
 }
 
-__global__ void est_combine_stats(const float2* __restrict__ stats, int hq, int nsplit,
+__global__ void est_combine_stats(const float2* __restrict__ stats, int h0, int nh, int nsplit,
                                   int64_t block, float2* __restrict__ rowstat) {
-  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= int64_t(hq) * block) return;
-  const int h = int(idx / block);
-  const int64_t r = idx % block;
+  const int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= int64_t(nh) * block) return;
+  const int h = h0 + int(x / block);
+  const int64_t r = x % block;
+  const int64_t idx = int64_t(h) * block + r;
   float m = -INFINITY;
   for (int s = 0; s < nsplit; ++s) m = fmaxf(m, stats[(int64_t(h) * nsplit + s) * block + r].x);
   float sum = 0.f;
@@ -285,14 +287,15 @@ __global__ void est_combine_stats(const float2* __restrict__ stats, int hq, int 
 // col_score[h][j] = sum over row tiles ascending; slash_score[h][d] = sum over the
 // (row tile, key tile) partials that contain d, ascending, then mean / sum.
 __global__ void est_combine_lines(const float* __restrict__ col_part,
-                                  const float* __restrict__ diag_part, int hq, int nrt,
-                                  int64_t nk, int64_t block, int64_t gbase, int64_t ntiles,
-                                  int slash_mean, float* __restrict__ col,
+                                  const float* __restrict__ diag_part, int hq, int h0, int nh,
+                                  int nrt, int64_t nk, int64_t block, int64_t gbase,
+                                  int64_t ntiles, int slash_mean, float* __restrict__ col,
                                   float* __restrict__ slash) {
-  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= int64_t(hq) * nk) return;
-  const int h = int(idx / nk);
-  const int64_t x = idx % nk;
+  const int64_t y = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (y >= int64_t(nh) * nk) return;
+  const int h = h0 + int(y / nk);
+  const int64_t x = y % nk;
+  const int64_t idx = int64_t(h) * nk + x;
   if (col) {
     float s = 0.f;
     for (int rt = 0; rt < nrt; ++rt) s += col_part[(int64_t(rt) * hq + h) * nk + x];
@@ -346,6 +349,8 @@ EstTcArgs tc_args(const EstimateArgs& a, int sm_count) {
   t.k3 = a.k3;
   t.k3_tiles = a.k3_tiles;
   t.sm_count = sm_count;
+  t.h0 = a.h1 > 0 ? a.h0 : 0;
+  t.h1 = a.h1 > 0 ? a.h1 : a.hq;
   return t;
 }
 
@@ -378,7 +383,7 @@ void estimate_simt_size(const EstimateArgs& a, Sizer& sz, int sm_count) {
   // tensor-core estimator's <= 2 x 66 pieces plus the mixed tiles' splits)
   int nsplit_all, tps_all, nrt_all;
   plan(a, sm_count, ntiles, nsplit_all, tps_all, nrt_all);
-  const int nst = std::max(nsplit_all, nsplit + 136) + 1;
+  const int nst = std::max(nsplit_all, nsplit + est_tc_max_splits()) + 1;
   sz.take<float>(size_t(a.hq) * a.block * a.dim);                       // qn
   if (a.pos_mode == 1) sz.take<float>(size_t(a.hq) * a.block * a.dim);  // qf
   sz.take<float>(size_t(a.nk) * a.hkv * a.dim);                         // kn
@@ -422,6 +427,8 @@ int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream
   d.tile_end = s1;
   d.split0 = tc_splits;
   d.nsplit_total = nst;
+  const int h0 = a.h1 > 0 ? a.h0 : 0, nh = (a.h1 > 0 ? a.h1 : a.hq) - h0;
+  d.h0 = h0;
   float* qn = ar.take<float>(size_t(a.hq) * a.block * a.dim);
   float* qf = a.pos_mode == 1 ? ar.take<float>(size_t(a.hq) * a.block * a.dim) : nullptr;
   float* kn = ar.take<float>(size_t(a.nk) * a.hkv * a.dim);
@@ -451,7 +458,7 @@ int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream
   const bool bf = a.dtype == LCX_BF16;
   const bool simt = nsplit > 0;
   if (simt) {
-    dim3 grid(unsigned(a.block), unsigned(a.hq));
+    dim3 grid(unsigned(a.block), unsigned(nh));
     if (bf) est_prep_q<__nv_bfloat16><<<grid, 64, 0, st>>>(d);
     else est_prep_q<float><<<grid, 64, 0, st>>>(d);
     LCX_CHECK_LAUNCH();
@@ -480,7 +487,7 @@ int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream
     }
     return LCX_OK;
   };
-  dim3 grid(unsigned(std::max(nsplit, 1)), unsigned(a.hq), unsigned(nrt));
+  dim3 grid(unsigned(std::max(nsplit, 1)), unsigned(nh), unsigned(nrt));
   // ---- pass 1: row max / sum-exp ----
   if (tc) {
     Arena ta_ar = tc_ar;
@@ -502,8 +509,8 @@ int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream
     LCX_CHECK_LAUNCH();
   }
   {
-    const int64_t rows = int64_t(a.hq) * a.block;
-    est_combine_stats<<<unsigned((rows + 255) / 256), 256, 0, st>>>(stats, a.hq, nst, a.block,
+    const int64_t rows = int64_t(nh) * a.block;
+    est_combine_stats<<<unsigned((rows + 255) / 256), 256, 0, st>>>(stats, h0, nh, nst, a.block,
                                                                     rowstat);
     LCX_CHECK_LAUNCH();
   }
@@ -523,10 +530,10 @@ int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream
     LCX_CHECK_LAUNCH();
   }
   if (a.col || a.slash) {
-    const int64_t total = int64_t(a.hq) * a.nk;
+    const int64_t total = int64_t(nh) * a.nk;
     est_combine_lines<<<unsigned((total + 255) / 256), 256, 0, st>>>(
-        col_part, diag_part, a.hq, nrt, a.nk, a.block, a.nk - a.block, ntiles, a.slash_mean,
-        a.col, a.slash);
+        col_part, diag_part, a.hq, h0, nh, nrt, a.nk, a.block, a.nk - a.block, ntiles,
+        a.slash_mean, a.col, a.slash);
     LCX_CHECK_LAUNCH();
   }
   return LCX_OK;

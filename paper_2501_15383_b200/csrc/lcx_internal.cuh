@@ -154,6 +154,9 @@ struct lcx_context {
   int* far_host_dev = nullptr;   // device alias of far_host (written by a kernel: no copy
                                  // engine, so it never queues behind the host entry's D2H)
   cudaEvent_t far_ev[2] = {nullptr, nullptr};
+  // per-chunk completion events of the last prefill run with record_chunk_events
+  std::vector<cudaEvent_t> chunk_done;
+  int64_t chunk_events = 0;
 };
 
 namespace lcx {
@@ -183,6 +186,10 @@ struct EstimateArgs {
   // (est_tc_prepare_keys); nullptr = CUDA-core estimator for every tile
   const void* k3;
   int64_t k3_tiles;
+  // query heads [h0, h1) only (sharded estimator); h1 == 0: all heads.  Each head's
+  // scores are a function of its own rows and the keys only (bitwise the same whatever
+  // range a call covers).
+  int h0, h1;
 };
 int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream_t st);
 void estimate_simt_size(const EstimateArgs& a, Sizer& sz, int sm_count);

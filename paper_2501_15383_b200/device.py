@@ -91,13 +91,18 @@ def chunked_prefill(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
                     positions_q=None, positions_k=None, rope_base=1e4, temperature=1.0,
                     kernel_path="auto", return_selections=True, return_admitted=False,
                     tc_min_entries=0, out=None, lse=None, stream=None, ctx=None, shard=None,
-                    return_recall=False):
+                    return_recall=False, phase="all", est_heads=None, selections=None,
+                    record_chunk_events=False):
     """longctx::chunked_prefill (sparse.hpp:125-129) over all heads of one layer.
 
     shard=(rank, count): KV-line sharding -- out / lse are this shard's partials
     (see lse_scale_partial and paper_2501_15383_b200/shard.py).
     return_recall: the recall check (north star (d)) -- recall [chunks, hq] = mean over
-    each chunk's last min(last_q, rows) rows of min(1, exp(lse_sparse - lse_full))."""
+    each chunk's last min(last_q, rows) rows of min(1, exp(lse_sparse - lse_full)).
+    phase "select" / "attend" (sharded layers, shard.py): estimator + selection only (for
+    query heads est_heads = (h0, h1)), or attention only over the given ``selections``
+    (dict verticals / nv / slashes / ns, as returned).  record_chunk_events: per-chunk
+    completion events (see stream_wait_chunk)."""
     inp = make_input(q, k, v, positions_q, positions_k, rope_base, temperature)
     opts = opts or Options()
     n, hq, dim = q.shape
@@ -106,13 +111,24 @@ def chunked_prefill(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
     nchunks = max(1, -(-n // max(int(chunk_len), 1)))
     block = min(int(last_q), int(chunk_len))
     cap_v, cap_s = bv + 2, bs + block + 1
+    if selections is not None:
+        cap_v, cap_s = selections["verticals"].shape[2], selections["slashes"].shape[2]
+    if phase == "select":  # no attention: no outputs
+        out = lse = torch.empty(0, dtype=torch.float32, device=dev)
     if out is None:
         out = torch.empty((n, hq, dim), dtype=torch.float32, device=dev)
     if lse is None:
         lse = torch.empty((hq, n), dtype=torch.float32, device=dev)
     sel = {}
     sparse = mode == "sparse"
-    if return_selections and sparse:
+    phases = {"all": 0, "select": 1, "attend": 2}
+    if phase not in phases:
+        raise Error("config", f"unknown phase {phase}")
+    if selections is not None:
+        sel = dict(selections)
+    elif phase != "all" and not sparse:
+        raise Error("config", "select / attend phases apply to sparse prefill")
+    elif (return_selections or phase != "all") and sparse:
         sel["verticals"] = torch.zeros((nchunks, hq, cap_v), dtype=torch.int32, device=dev)
         sel["nv"] = torch.zeros((nchunks, hq), dtype=torch.int32, device=dev)
         sel["slashes"] = torch.zeros((nchunks, hq, cap_s), dtype=torch.int32, device=dev)
@@ -123,9 +139,11 @@ def chunked_prefill(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
         if return_recall else None
     pm = POSITION_MODES[position_mode] if isinstance(position_mode, str) else int(position_mode)
     sr, sc = shard if shard is not None else (0, 1)
+    eh0, eh1 = est_heads if est_heads is not None else (0, 0)
     cfg = PrefillConfigC(int(chunk_len), int(last_q), bv, bs, PREFILL_MODES[mode], pm,
                          _chunk(dca) or ChunkConfigC(0, 0, 0), opts.c(),
-                         KERNEL_PATHS[kernel_path], int(tc_min_entries), int(sr), int(sc))
+                         KERNEL_PATHS[kernel_path], int(tc_min_entries), int(sr), int(sc),
+                         phases[phase], int(eh0), int(eh1), int(bool(record_chunk_events)))
     o = PrefillOutputC(out.data_ptr(), lse.data_ptr(),
                        sel["verticals"].data_ptr() if sel else None,
                        sel["nv"].data_ptr() if sel else None,
@@ -142,6 +160,13 @@ def chunked_prefill(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
     if recall is not None:
         res["recall"] = recall
     return res
+
+
+def stream_wait_chunk(chunk, stream, *, device=None, ctx=None):
+    """``stream`` waits for chunk ``chunk`` of the last chunked_prefill on the context (run
+    with record_chunk_events=True) to have its out / lse rows final."""
+    ctx = ctx or context(device)
+    check(lib().lcx_stream_wait_chunk(ctx.ptr, int(chunk), C.c_void_p(stream.cuda_stream)))
 
 
 def estimate_block(q, k, *, q_row0, nq, nk, last_q, position_mode="standard", dca=None,

@@ -4,22 +4,32 @@ One process per GPU; torch.distributed (NCCL over NVLink / NVSwitch) is the plum
 Strategies (``plan``):
 
   single  G == 1.
-  head    Head sharding, no collective on the data path.  With
-          Hkv % G == 0 rank r owns whole KV heads and their query heads (KV-head
-          sharding); with G % Hkv == 0 each KV head's query heads are split across
-          G / Hkv ranks (e.g. 7B at G = 8: 4 + 3 of the 7 heads of one KV head), each
-          rank holding only its KV head.  Selection and attention are per query head
-          (D10), so every rank's result is exactly the single-GPU result for its heads.
-  seq     KV-line sharding with a log-sum-exp merge: every rank runs the estimator
-          and selection for all heads (bitwise-identical lists, no exchange), then
-          attends over its contiguous part of each head's sorted vertical / slash lists
-          (lcx_prefill_config.shard_rank / shard_count); the partials are merged with
-          all_gather(lse) + lcx_lse_scale_partial + reduce_scatter(sum of scaled O), so
-          rank r ends with the exact output rows [r n / G, (r+1) n / G).
+  head    KV-head sharding, no collective on the data path: with
+          Hkv % G == 0 rank r owns whole KV heads and their query heads.  Selection and
+          attention are per query head (D10), so every rank's result is exactly the
+          single-GPU result for its heads.
+  seq     KV sharding with a log-sum-exp merge (the "auto" choice when Hkv % G != 0, e.g.
+          Qwen2.5-7B's 4 KV heads on 8 GPUs):
+            1. sharded estimator: rank r runs the Vertical-Slash estimator + selection of
+               every chunk for its head pairs only (lcx phase SELECT, est_head_begin/end);
+               a head's lists depend only on its own rows and the keys, so they are
+               bitwise the unsharded lists.  One all_reduce (sum of int32 lists, every
+               head written by exactly one rank) gives every rank the full selection.
+            2. sharded attention: rank r attends, for every row, the KV entries of its
+               part of each head's selected lines -- the contiguous part
+               [r cnt / G, (r+1) cnt / G) of each sorted vertical and slash list (lcx phase
+               ATTEND, shard_rank / shard_count) -- which partitions every row's admitted
+               KV entries over the ranks (V∩S and self-fallback ownership follow the full
+               lists).
+            3. per-chunk merge, overlapped with the next chunks' attention on a side
+               stream: once chunk c's partial rows are final (lcx_stream_wait_chunk),
+               all_gather of their lse, lcx_lse_scale_partial (o <- o e^(lse_g - lse)),
+               reduce_scatter (sum) of the scaled O rows -- rank r ends with rows
+               [t0 + r L / G, t0 + (r+1) L / G) of every chunk.
 
-``merge_partials`` is written against torch.distributed only, so the collective
-orchestration is exercised by world-size-2 gloo tests on CPU (tests/test_shard.py) with
-the scaling step injected; on GPUs the scaling step is the CUDA kernel.
+The seq orchestration (``seq_prefill``) is written against torch.distributed with the
+device steps injectable, so it runs under world-size-2 gloo on CPU (tests/test_shard.py);
+on GPUs the steps are the lcx C-ABI entries.
 """
 from __future__ import annotations
 
@@ -51,12 +61,16 @@ class Plan:
         if self.kind == "head":
             return (f"head-sharded x{self.world} ({self.hq} Q / {self.hkv} KV heads on rank "
                     f"{self.rank}; no collective)")
-        return (f"KV-line sharded x{self.world} + LSE merge over NCCL (all_gather lse, "
-                f"reduce_scatter O)")
+        return (f"KV-sharded x{self.world}: estimator split by head pairs (selections "
+                f"all_reduced), each row's KV entries split by line, per-chunk LSE merge "
+                f"over NCCL (all_gather lse, reduce_scatter O) overlapped with attention")
 
 
-def head_partition(hq: int, hkv: int, world: int):
-    """[(h0, h1, g0, g1)] per rank, or None when heads cannot be split evenly by groups."""
+def head_partition(hq: int, hkv: int, world: int, split_groups: bool = False):
+    """[(h0, h1, g0, g1)] per rank, or None when heads cannot be split evenly by groups.
+    Whole KV heads per rank when Hkv % G == 0; with split_groups also G % Hkv == 0, each KV
+    head's query heads split over G / Hkv ranks (unbalanced when the group size is not a
+    multiple: 7B at G = 8 gives 4 + 3 -- the seq strategy balances that case instead)."""
     group = hq // hkv
     parts = []
     if hkv % world == 0:
@@ -65,7 +79,7 @@ def head_partition(hq: int, hkv: int, world: int):
             g0 = r * per
             parts.append((g0 * group, (g0 + per) * group, g0, g0 + per))
         return parts
-    if world % hkv == 0:
+    if split_groups and world % hkv == 0:
         split = world // hkv
         if split > group:
             return None
@@ -77,19 +91,42 @@ def head_partition(hq: int, hkv: int, world: int):
     return None
 
 
+def est_head_ranges(hq: int, hkv: int, world: int):
+    """Query-head range [h0, h1) of each rank's share of the estimator: the head PAIRS of
+    the tensor-core estimator (one M = 128 tile = two heads of one KV head) split
+    contiguously over the ranks (7B: 16 pairs -> 2 per rank at G = 8; 14B: 24 -> 3).
+    A rank with no pair gets (0, 0)."""
+    group = hq // hkv
+    ppg = (group + 1) // 2
+    npairs = hkv * ppg
+
+    def first(p):
+        return (p // ppg) * group + 2 * (p % ppg)
+
+    def last(p):
+        return min(first(p) + 2, (p // ppg) * group + group)
+
+    out = []
+    for r in range(world):
+        p0, p1 = r * npairs // world, (r + 1) * npairs // world
+        out.append((first(p0), last(p1 - 1)) if p1 > p0 else (0, 0))
+    return out
+
+
 def plan(n: int, hq: int, hkv: int, world: int, rank: int, mode: str = "auto") -> Plan:
     if world == 1:
         return Plan("single", 1, 0, n, hq, hkv, 0, 0, 0, n)
-    parts = head_partition(hq, hkv, world) if mode in ("auto", "head") else None
+    parts = head_partition(hq, hkv, world, split_groups=mode == "head") \
+        if mode in ("auto", "head") else None
     if parts is not None:
         h0, h1, g0, g1 = parts[rank]
         return Plan("head", world, rank, n, h1 - h0, g1 - g0, h0, g0, 0, n)
     if mode == "head":
         raise ValueError(f"cannot head-shard {hq}Q/{hkv}KV over {world} ranks")
-    if n % world:
-        raise ValueError("seq sharding needs n divisible by the world size")
     rows = n // world
-    return Plan("seq", world, rank, n, hq, hkv, 0, 0, rank * rows, rows)
+    eh = est_head_ranges(hq, hkv, world)[rank]
+    return Plan("seq", world, rank, n, hq, hkv, 0, 0, rank * rows, rows,
+                notes={"est_heads": eh})
 
 
 def take(p: Plan, q, k, v):
@@ -115,21 +152,127 @@ def merge_partials(out, lse, group=None, scale_fn=None):
     return rows, tot
 
 
+def chunk_bounds(n: int, chunk_len: int):
+    return [(t0, min(n, t0 + chunk_len)) for t0 in range(0, n, chunk_len)]
+
+
+def seq_prefill(world, rank, n, chunk_len, est_heads, run_select, run_attend, wait_chunk,
+                scale_fn, new_sel, new_out, comm_stream=None, group=None):
+    """The seq strategy's orchestration over torch.distributed (see the module doc).
+
+    run_select(h0, h1, sel): fills this rank's heads of the selection log sel (dict of
+      [chunks, hq, cap] / [chunks, hq] int32 tensors, zero elsewhere);
+    run_attend(sel, out, lse): this rank's partial attention of every chunk (out
+      [n, hq, dim] normalised within the shard, lse [hq, n]); enqueued asynchronously;
+    wait_chunk(c, stream): stream waits until chunk c's partial rows are final;
+    scale_fn(o, lse_own, lse_all) -> lse_tot: the per-shard scaling of the merge.
+    Returns (sel, rows [sum_c L_c / G, hq, dim] = this rank's merged rows of every chunk,
+    lse_tot [hq, n])."""
+    import torch.distributed as dist
+    sel = new_sel()
+    h0, h1 = est_heads
+    if h1 > h0:
+        run_select(h0, h1, sel)
+    for key in ("verticals", "nv", "slashes", "ns"):  # each head written by one rank
+        dist.all_reduce(sel[key], group=group)
+    out, lse = new_out()
+    run_attend(sel, out, lse)
+    hq, dim = out.shape[1], out.shape[2]
+    parts, lse_tot = [], torch.empty_like(lse)
+    ctx = torch.cuda.stream(comm_stream) if comm_stream is not None else _nullctx()
+    with ctx:
+        for c, (t0, t1) in enumerate(chunk_bounds(n, chunk_len)):
+            wait_chunk(c, comm_stream)
+            rows = t1 - t0
+            lse_c = lse[:, t0:t1].contiguous()
+            lse_all = torch.empty((world, hq, rows), dtype=lse.dtype, device=lse.device)
+            dist.all_gather_into_tensor(lse_all.view(-1), lse_c.view(-1), group=group)
+            o_c = out[t0:t1]
+            lse_tot[:, t0:t1] = scale_fn(o_c, lse_c, lse_all)
+            if rows % world == 0:
+                mine = torch.empty((rows // world, hq, dim), dtype=out.dtype, device=out.device)
+                dist.reduce_scatter_tensor(mine.view(-1), o_c.reshape(-1), group=group)
+            else:  # ragged last chunk: all_reduce, keep this rank's slice
+                dist.all_reduce(o_c, group=group)
+                a, b = rank * rows // world, (rank + 1) * rows // world
+                mine = o_c[a:b]
+            parts.append(mine)
+    if comm_stream is not None:
+        torch.cuda.current_stream().wait_stream(comm_stream)
+    return sel, torch.cat(parts, dim=0), lse_tot
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def seq_row_ranges(n: int, chunk_len: int, world: int, rank: int):
+    """The global rows [a, b) of each chunk that rank owns after the seq merge."""
+    out = []
+    for t0, t1 in chunk_bounds(n, chunk_len):
+        rows = t1 - t0
+        out.append((t0 + rank * rows // world, t0 + (rank + 1) * rows // world))
+    return out
+
+
 def prefill(p: Plan, q, k, v, **kw):
     if p.kind != "seq":
         return D.chunked_prefill(q, k, v, **kw)
-    r = D.chunked_prefill(q, k, v, shard=(p.rank, p.world), **kw)
-    rows, tot = merge_partials(r["out"], r["lse"])
-    r["rows"], r["lse"] = rows, tot
-    return r
+    kw = dict(kw)
+    kw.pop("return_selections", None)
+    return_admitted = kw.pop("return_admitted", False)
+    kw.pop("return_recall", None)
+    n, hq, dim = q.shape
+    L = int(kw["chunk_len"])
+    nch = -(-n // L)
+    block = min(int(kw["last_q"]), L)
+    bv, bs = kw["budget"]
+    cap_v, cap_s = int(bv) + 2, int(bs) + block + 1
+    dev = q.device
+    res = {}
+
+    def new_sel():
+        z = lambda *shape: torch.zeros(shape, dtype=torch.int32, device=dev)  # noqa: E731
+        return {"verticals": z(nch, hq, cap_v), "nv": z(nch, hq),
+                "slashes": z(nch, hq, cap_s), "ns": z(nch, hq)}
+
+    def new_out():
+        return (torch.empty((n, hq, dim), dtype=torch.float32, device=dev),
+                torch.empty((hq, n), dtype=torch.float32, device=dev))
+
+    def run_select(h0, h1, sel):
+        D.chunked_prefill(q, k, v, phase="select", est_heads=(h0, h1), selections=sel, **kw)
+
+    def run_attend(sel, out, lse):
+        r = D.chunked_prefill(q, k, v, phase="attend", selections=sel, shard=(p.rank, p.world),
+                              record_chunk_events=True, out=out, lse=lse,
+                              return_admitted=return_admitted, **kw)
+        if "admitted" in r:
+            res["admitted"] = r["admitted"]
+
+    def wait_chunk(c, stream):
+        D.stream_wait_chunk(c, stream, device=dev.index)
+
+    comm = p.notes.setdefault("comm_stream", torch.cuda.Stream(device=dev))
+    sel, rows, tot = seq_prefill(p.world, p.rank, n, L, p.notes["est_heads"], run_select,
+                                 run_attend, wait_chunk, D.lse_scale_partial, new_sel, new_out,
+                                 comm_stream=comm)
+    res.update(sel)
+    res["rows"], res["lse"] = rows, tot
+    return res
 
 
 def e2e(p: Plan, q, k, v, steps, barrier, world, dev, **kw):
     """Same operator through the host-buffer entry: pinned host Q/K/V in, host O / lse /
-    selections out, all copies inside the timed region (lcx_chunked_prefill_host).
-    Head-sharded and single-GPU plans only (the line-sharded merge runs on device)."""
+    selections out, all copies inside the timed region (lcx_chunked_prefill_host; for the
+    seq strategy: the rank's Q/K/V copied in, shard.prefill, its merged rows, lse and the
+    selection log copied out)."""
     if p.kind == "seq":
-        return {"value": None, "skipped": "e2e host entry covers single / head-sharded plans"}
+        return e2e_seq(p, q, k, v, steps, barrier, world, dev, **kw)
     try:
         import psutil
         need = (q.numel() + k.numel() + v.numel()) * q.element_size() \
@@ -174,3 +317,47 @@ def e2e(p: Plan, q, k, v, steps, barrier, world, dev, **kw):
             "d2h_bytes_per_step": oh.numel() * 4 + lh.numel() * 4 + sel_bytes,
             "host_wall_ms_per_step": wall / steps,
             "api": "lcx_chunked_prefill_host (pinned host buffers, chunk-pipelined copies)"}
+
+
+def e2e_seq(p: Plan, q, k, v, steps, barrier, world, dev, **kw):
+    import torch.distributed as dist
+    qh = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
+    kh = torch.empty(k.shape, dtype=k.dtype, pin_memory=True)
+    vh = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+    qh.copy_(q)
+    kh.copy_(k)
+    vh.copy_(v)
+    n, hq, dim = q.shape
+    qd, kd, vd = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+
+    def one():
+        for d, h in ((qd, qh), (kd, kh), (vd, vh)):
+            d.copy_(h, non_blocking=True)
+        r = prefill(p, qd, kd, vd, **kw)
+        outs = [r["rows"], r["lse"]] + [r[x] for x in ("verticals", "nv", "slashes", "ns")]
+        hs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in outs]
+        for h, t in zip(hs, outs):
+            h.copy_(t, non_blocking=True)
+        return hs
+
+    one()
+    barrier()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        hs = one()
+    e1.record(stream)
+    barrier()
+    wall = (time.perf_counter() - t0) * 1e3
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t[0])
+    return {"ms_per_step": ms / steps, "unit": "tokens/s",
+            "h2d_bytes_per_step": (qh.numel() + kh.numel() + vh.numel()) * qh.element_size(),
+            "d2h_bytes_per_step": sum(h.numel() * h.element_size() for h in hs),
+            "host_wall_ms_per_step": wall / steps,
+            "api": "shard.prefill (seq: sharded estimator, line-sharded attention, NCCL "
+                   "LSE merge) between pinned-host copies of this rank's inputs / outputs"}

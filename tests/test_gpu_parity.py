@@ -630,6 +630,83 @@ def test_line_sharded_prefill_merges_to_unsharded(D, port, shards, path, precisi
     assert row_rel_err(mo[:, 1], o_ref) <= tol
 
 
+@pytest.mark.parametrize("geom", [(28, 4), (40, 8)])
+@pytest.mark.parametrize("dca", [None, (1024, 3072, 1024)])
+def test_sharded_estimator_selections_bitwise_g_invariant(D, geom, dca):
+    """North star (e), sharded estimator: the select phase of each of G = 2 / 4 / 8 ranks
+    (its head pairs only, run one after the other on this GPU) writes exactly its heads'
+    slots, and the union of the G shards' lists is bitwise the unsharded selection (every
+    chunk, every head); the attend phase over the union equals the unsharded operator
+    bitwise (same lists, same kernels)."""
+    import torch
+    from paper_2501_15383_b200 import shard as SH
+    from paper_2501_15383_b200.synth import make_qkv
+    hq, hkv = geom
+    n = 4096
+    q, k, v = make_qkv(n, hq, hkv, kind="planted", seed=5, device="cuda", rope_base=1e6)
+    kw = dict(chunk_len=1024, last_q=64, budget=(48, 160), temperature=0.9, rope_base=1e6,
+              position_mode="dca_continuous" if dca else "standard", dca=dca)
+    full = D.chunked_prefill(q, k, v, **kw)
+    keys = ("verticals", "nv", "slashes", "ns")
+    for G in (2, 4, 8):
+        union = {x: torch.zeros_like(full[x]) for x in keys}
+        for r, (h0, h1) in enumerate(SH.est_head_ranges(hq, hkv, G)):
+            if h1 <= h0:
+                continue
+            sel = {x: torch.full_like(full[x], -7) for x in keys}
+            D.chunked_prefill(q, k, v, phase="select", est_heads=(h0, h1), selections=sel, **kw)
+            for x in keys:
+                assert (sel[x][:, :h0] == -7).all() and (sel[x][:, h1:] == -7).all()
+                union[x][:, h0:h1] = sel[x][:, h0:h1]
+        for x in keys:
+            assert torch.equal(union[x], full[x]), (G, x)
+    att = D.chunked_prefill(q, k, v, phase="attend", selections=union, **kw)
+    assert torch.equal(att["out"], full["out"]) and torch.equal(att["lse"], full["lse"])
+
+
+def test_seq_prefill_one_gpu_emulation(D):
+    """The seq strategy's merge on the device (lcx_stream_wait_chunk + lse_scale_partial)
+    for G = 2 shards emulated in one process: a trivial process group of size 1 cannot run
+    it, so each 'rank' here runs the attend phase of its line shard and the per-chunk
+    merge is formed as seq_prefill forms it (all_gather = stack, reduce_scatter = sum +
+    slice); the merged rows equal the unsharded operator within the bf16 tolerance."""
+    import torch
+    from paper_2501_15383_b200 import shard as SH
+    from paper_2501_15383_b200.synth import make_qkv
+    n, hq, hkv, G, L = 4096, 28, 4, 2, 1024
+    q, k, v = make_qkv(n, hq, hkv, kind="planted", seed=6, device="cuda", rope_base=1e6)
+    kw = dict(chunk_len=L, last_q=64, budget=(48, 160), temperature=0.9, rope_base=1e6,
+              position_mode="dca_continuous", dca=(2048, 4096, 2048))
+    full = D.chunked_prefill(q, k, v, **kw)
+    sel = {x: full[x] for x in ("verticals", "nv", "slashes", "ns")}
+    parts = []
+    for r in range(G):
+        out = torch.empty((n, hq, 128), device="cuda")
+        lse = torch.empty((hq, n), device="cuda")
+        D.chunked_prefill(q, k, v, phase="attend", selections=sel, shard=(r, G),
+                          record_chunk_events=True, out=out, lse=lse, **kw)
+        side = torch.cuda.Stream()
+        for c in range(n // L):  # every chunk's event is recorded and waitable
+            D.stream_wait_chunk(c, side)
+        torch.cuda.current_stream().wait_stream(side)
+        parts.append((out, lse))
+    for r in range(G):
+        rows = []
+        for c, (t0, t1) in enumerate(SH.chunk_bounds(n, L)):
+            lse_all = torch.stack([p[1][:, t0:t1] for p in parts]).contiguous()
+            acc = torch.zeros((t1 - t0, hq, 128), device="cuda")
+            for out, lse in parts:
+                o_c = out[t0:t1].clone()
+                D.lse_scale_partial(o_c, lse[:, t0:t1].contiguous(), lse_all)
+                acc += o_c
+            a, b = SH.seq_row_ranges(n, L, G, r)[c]
+            rows.append(acc[a - t0:b - t0])
+        got = torch.cat(rows).double().cpu().numpy()
+        ref = torch.cat([full["out"][a:b] for a, b in SH.seq_row_ranges(n, L, G, r)])
+        ref = ref.double().cpu().numpy()
+        assert row_rel_err(got.reshape(-1, 128), ref.reshape(-1, 128)) <= 2e-3
+
+
 # ------------------------------------------------------------- recall check --
 @pytest.mark.parametrize("precision,dca", [("bf16", (256, 768, 256)), ("fp32", None),
                                            ("bf16", None)])

@@ -16,7 +16,7 @@ from paper_2501_15383_b200 import shard as SH
 @pytest.mark.parametrize("hq,hkv", [(28, 4), (40, 8), (14, 2)])
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
 def test_head_partition_covers_every_head_once(hq, hkv, world):
-    parts = SH.head_partition(hq, hkv, world)
+    parts = SH.head_partition(hq, hkv, world, split_groups=True)
     if world == 1:
         assert parts == [(0, hq, 0, hkv)]
     if parts is None:
@@ -35,13 +35,38 @@ def test_head_partition_covers_every_head_once(hq, hkv, world):
 
 
 def test_plans():
+    # 7B (4 KV heads) on 8 GPUs: KV sharding with the sharded estimator (auto)
     p = SH.plan(1 << 20, 28, 4, 8, 3)
+    assert p.kind == "seq" and p.notes["est_heads"] == (11, 14)
+    # ... or the unbalanced 4 + 3 query-head split when asked for explicitly
+    p = SH.plan(1 << 20, 28, 4, 8, 3, mode="head")
     assert p.kind == "head" and p.hkv == 1 and p.hq in (3, 4)
+    # 14B (8 KV heads) on 8 GPUs: whole KV heads, no collective
+    p = SH.plan(1 << 20, 40, 8, 8, 3)
+    assert p.kind == "head" and p.hkv == 1 and p.hq == 5
     p = SH.plan(1 << 20, 28, 4, 8, 3, mode="seq")
     assert p.kind == "seq" and p.row0 == 3 * (1 << 17) and p.rows == 1 << 17
     assert SH.plan(1 << 20, 28, 4, 1, 0).kind == "single"
     with pytest.raises(ValueError):
         SH.plan(1 << 20, 28, 4, 3, 0, mode="head")
+
+
+@pytest.mark.parametrize("hq,hkv", [(28, 4), (40, 8), (14, 2), (4, 2)])
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_est_head_ranges_cover_every_head_once_by_pairs(hq, hkv, world):
+    """The sharded estimator's head ranges: contiguous, disjoint, covering all heads, and
+    cut only at head-pair boundaries of a KV group (one tensor-core estimator tile)."""
+    rs = SH.est_head_ranges(hq, hkv, world)
+    assert len(rs) == world
+    heads = [h for a, b in rs for h in range(a, b)]
+    assert heads == list(range(hq))
+    group = hq // hkv
+    for a, b in rs:
+        if b > a:
+            assert (a % group) % 2 == 0              # starts a pair
+            assert b % group == 0 or (b % group) % 2 == 0   # ends a pair or the group
+    if hq == 28 and world == 8:  # 16 pairs: 2 per rank (4 or 3 heads)
+        assert [b - a for a, b in rs] == [4, 3] * 4
 
 
 def _torch_scale(out, lse, lse_all):
@@ -101,3 +126,82 @@ def test_lse_merge_orchestration_gloo_world2():
     res = [q.get(timeout=10) for _ in procs]
     for rank, err_o, err_l in res:
         assert err_o < 1e-5 and err_l < 1e-5, (rank, err_o, err_l)
+
+
+def _seq_worker(rank, world, port, q):
+    """seq_prefill over gloo: a small synthetic problem whose per-rank selection and
+    partial attention are injected (the device steps on GPUs)."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        rng = np.random.default_rng(1)          # same problem on every rank
+        n, hq, hkv, dim, keys, L, cap = 96, 6, 2, 8, 40, 32, 5
+        nch = n // L
+        logits = rng.standard_normal((hq, n, keys)) * 3
+        vals = rng.standard_normal((keys, dim))
+        owner = rng.integers(0, world, (hq, n, keys))   # which shard attends each entry
+        owner[1, 7, :] = world - 1                      # rows with no entry on shard 0
+        owner[4, 40:44, :] = 0
+        full_l = torch.logsumexp(torch.tensor(logits), dim=-1)
+        full_o = torch.einsum("hnk,kd->nhd", torch.softmax(torch.tensor(logits), -1),
+                              torch.tensor(vals))
+        want = {"verticals": rng.integers(0, 1 << 20, (nch, hq, cap)),
+                "nv": rng.integers(0, cap, (nch, hq)),
+                "slashes": rng.integers(0, 1 << 20, (nch, hq, cap + 2)),
+                "ns": rng.integers(0, cap + 2, (nch, hq))}
+        seen = []
+
+        def new_sel():
+            return {k: torch.zeros(v.shape, dtype=torch.int32) for k, v in want.items()}
+
+        def run_select(h0, h1, sel):
+            seen.append((h0, h1))
+            for k in sel:
+                sel[k][:, h0:h1] = torch.tensor(want[k][:, h0:h1], dtype=torch.int32)
+
+        def new_out():
+            return torch.empty((n, hq, dim)), torch.empty((hq, n))
+
+        def run_attend(sel, out, lse):
+            for k in want:  # attention sees the complete selection on every rank
+                assert (sel[k].numpy() == want[k]).all()
+            mine = torch.tensor(np.where(owner == rank, logits, -np.inf))
+            lse.copy_(torch.logsumexp(mine, dim=-1).float())
+            p = torch.softmax(mine, dim=-1).nan_to_num(0.0)
+            out.copy_(torch.einsum("hnk,kd->nhd", p, torch.tensor(vals)).float())
+
+        eh = SH.est_head_ranges(hq, hkv, world)[rank]
+        sel, rows, tot = SH.seq_prefill(world, rank, n, L, eh, run_select, run_attend,
+                                        lambda c, s: None, _torch_scale, new_sel, new_out)
+        ranges = SH.seq_row_ranges(n, L, world, rank)
+        ref = torch.cat([full_o[a:b] for a, b in ranges], dim=0)
+        err_o = (rows.double() - ref).abs().max().item()
+        err_l = (tot.double() - full_l).abs().max().item()
+        sel_ok = all((sel[k].numpy() == want[k]).all() for k in want)
+        q.put((rank, err_o, err_l, sel_ok, seen, rows.shape[0]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_seq_prefill_orchestration_gloo_world2():
+    """Sharded estimator (each rank selects only its head pairs; one all_reduce gives
+    every rank the full selection) + per-chunk LSE merge (all_gather lse, scale,
+    reduce_scatter): the merged rows equal the unsharded attention."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_seq_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in procs)
+    for rank, err_o, err_l, sel_ok, seen, nrows in res:
+        assert sel_ok, rank
+        assert err_o < 1e-5 and err_l < 1e-5, (rank, err_o, err_l)
+        assert nrows == 96 // 2
+        assert seen == [SH.est_head_ranges(6, 2, 2)[rank]]

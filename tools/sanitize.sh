@@ -13,7 +13,7 @@ for tool in memcheck racecheck synccheck initcheck; do
     cmd=$SMOKE; [ $what = cases ] && cmd=$CASES
     extra=""
     [ $tool = racecheck ] && extra="--racecheck-report all"
-    [ $tool = initcheck ] && extra="--track-unused-memory no"
+    [ $tool = initcheck ] && extra=""
     echo "== $tool $what" | tee -a gpurun_out/sanitize_summary.txt
     timeout 900 bash -c "$CS --tool $tool $extra --target-processes all --print-limit 50 \
         --error-exitcode 99 $cmd" > gpurun_out/sanitize_${tool}_${what}.log 2>&1
