@@ -127,8 +127,9 @@ typedef struct {
    *   LCX_PHASE_ALL     estimator + selection + attention per chunk (the operator);
    *   LCX_PHASE_SELECT  estimator + selection of every chunk only, into the selection
    *                     log (out->sel_*, required), for query heads
-   *                     [est_head_begin, est_head_end) -- the other heads' slots are left
-   *                     untouched (the shards' slots are combined across GPUs);
+   *                     [est_head_begin, est_head_end) -- those heads' list slots are
+   *                     written whole (zero past the count), the other heads' slots are
+   *                     left untouched (the shards' slots are combined across GPUs);
    *   LCX_PHASE_ATTEND  attention of every chunk only, over the selection log given in
    *                     out->sel_* (required).
    * A head's selection depends only on its own rows and the keys, so splitting the

@@ -371,3 +371,62 @@ class Rng:
     def next_u64(self):
         self.o.lib.lco_mt64_next.restype = C.c_uint64
         return self.o.lib.lco_mt64_next(self.buf)
+
+
+# ---------------------------------------------------------------------------------------
+# Fast fp64 restatement of the estimator's line scores for the large parity cases
+# (t1 up to 1M keys, where the per-entry-RoPE loop of lco_estimate_block takes minutes per
+# head).  Same math as sparse.cpp:142-188 (estimate_block) + 196-218 (line sums), using
+# rope(q, gi - j) . k == rope(q, gi) . rope(k, j) (exact in real arithmetic; ~1e-15 apart
+# in fp64, pinned against lco_estimate_block in tests/test_oracle_pin.py) and, for the
+# DcaContinuous far region (gi - j > c - 1), rope(q, c - 1) . k_j.
+def rope_rows(x, pos, rope_base):
+    """x [m, dim] rotated by positions pos [m] (attention.cpp:14-33, fp64 angles)."""
+    x = np.asarray(x, np.float64)
+    dim = x.shape[1]
+    th = np.power(float(rope_base), -np.arange(0, dim, 2, dtype=np.float64) / dim)
+    ang = np.asarray(pos, np.float64)[:, None] * th[None, :]
+    c, s = np.cos(ang), np.sin(ang)
+    xe, xo = x[:, 0::2], x[:, 1::2]
+    out = np.empty_like(x)
+    out[:, 0::2] = xe * c - xo * s
+    out[:, 1::2] = xe * s + xo * c
+    return out
+
+
+def estimate_probs_fast(q_rows, k, pos_mode=0, c=0, rope_base=1e4):
+    """est [B, t1] of estimate_block for the chunk's last B query rows q_rows (global rows
+    t1 - B .. t1 - 1) against keys k [t1, dim]."""
+    q_rows, k = np.asarray(q_rows, np.float64), np.asarray(k, np.float64)
+    B, dim = q_rows.shape
+    t1 = k.shape[0]
+    gi = np.arange(t1 - B, t1)
+    j = np.arange(t1)
+    logits = rope_rows(q_rows, gi, rope_base) @ rope_rows(k, j, rope_base).T
+    if pos_mode == 1:
+        far = (gi[:, None] - j[None, :]) > c - 1
+        if far.any():
+            lf = rope_rows(q_rows, np.full(B, c - 1), rope_base) @ k.T
+            logits = np.where(far, lf, logits)
+    logits /= np.sqrt(dim)
+    logits[j[None, :] > gi[:, None]] = -np.inf
+    logits -= logits.max(axis=1, keepdims=True)
+    np.exp(logits, out=logits)
+    logits /= logits.sum(axis=1, keepdims=True)
+    return logits
+
+
+def line_scores_fast(est, slash_mean=True):
+    """(col_score, slash_score) of an est [B, t1] block exactly as select_critical forms
+    them (sparse.cpp:196-218): column sums; per diagonal d = gi - j the sum (or mean over
+    its entries), -inf for empty bins."""
+    B, t1 = est.shape
+    col = est.sum(axis=0)
+    ssum = np.zeros(t1)
+    for r in range(B):
+        g = t1 - B + r
+        ssum[:g + 1] += est[r, g::-1]
+    d = np.arange(t1)
+    cnt = np.minimum(B, t1 - d)
+    score = ssum / cnt if slash_mean else ssum
+    return col, score

@@ -47,26 +47,61 @@ namespace lcx {
 namespace {
 
 constexpr int BM = 128, BN = 64, HD = 128;
-// Unit of the pipeline: a DOUBLE TILE (DT) = up to two 64-key tiles of one item and one DCA
-// pattern group, sharing one 128-column S buffer, one softmax pass over 128 logits per
-// row and one K = 128 PV step.  Every per-tile control cost (metadata ring, mbarrier
-// hand-offs, running-max hand-off, TMEM load/store waits) is paid once per 128 keys.
-// The two halves are independent 64-key tiles (any kinds, any keys): the QK MMAs of half
-// j write S columns [64 j, 64 j + 64) of the buffer, its P (fp16 pairs) lands in columns
-// [64 j, 64 j + 32), and the PV MMAs of half j read those with half j's V^T stage.
-//
-// warps 0-7 softmax (TMEM lane quadrant = warp % 4, group = warp / 4; group g takes the
-// DTs T with T % 2 == g), warp 8 producer (DT metadata + K loads), warp 9 QK issuer +
-// TMEM allocator, warp 10 PV issuer, warp 11 V loads
-constexpr int kGroups = 2;
+// warps 0-7 softmax (TMEM lane quadrant = warp % 4, group = warp / 4),
+// warp 8 producer (tile metadata + K TMA), warp 9 QK issuer + TMEM allocator,
+// warp 10 PV issuer, warp 11 V TMA
+#ifndef LCX_TC_GROUPS
+#define LCX_TC_GROUPS 2
+#endif
+constexpr int kGroups = LCX_TC_GROUPS;          // softmax warp groups (tile T: T % kGroups)
 constexpr int kSoftmaxWarps = 4 * kGroups;
 constexpr int kThreads = 32 * (kSoftmaxWarps + 4);
 constexpr int kWarpProducer = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1,
               kWarpPv = kSoftmaxWarps + 2, kWarpV = kSoftmaxWarps + 3;
-constexpr int NK = 4, NV = 4;  // K / V shared-memory stages, one 64-key tile each
-constexpr int NS = 2;          // S (+P) TMEM buffers, one DT each
+// The softmax code is written for any number of groups, but a third group needs more
+// registers than 65536 / 512 per thread: compiled at 128 it spills ~2.6 KB and ran 3.4x
+// slower (setmaxnreg does not help: ptxas still allocates for the launch-time limit).
+// With a third group each thread keeps only 32 logits live (kSReread): S is read from
+// TMEM twice, once for the tile max and once for the exponentials.
+#ifndef LCX_TC_SREREAD
+#define LCX_TC_SREREAD (LCX_TC_GROUPS > 2)
+#endif
+constexpr bool kSReread = LCX_TC_SREREAD;
+// Three groups fit in 128 registers this way and are correct (with NS = 3, below), but
+// measure slower than two: 397 vs 364 ms per 1M layer on one box (one Q buffer, S read
+// twice, spills) -- kept behind LCX_TC_ALLOW_GROUPS3.
+#ifndef LCX_TC_ALLOW_GROUPS3
+static_assert(kGroups == 2, "two softmax groups");
+#endif
+// two S buffers suffice (NS = 2, 3, 4 measure the same); the TMEM they free holds a
+// second rotated Q, so the Q of the next DCA pattern is in place before its first QK
+#ifndef LCX_TC_QBUFS
+#define LCX_TC_QBUFS 2
+#endif
+// two rotated-Q buffers with two S buffers, or one Q buffer with four S buffers
+// Split O (LCX_TC_SPLIT_O): each softmax group accumulates its own tiles into its own O
+// in TMEM, at its own running max, and the two are merged in the item's epilogue -- the
+// groups no longer hand the running max to each other tile by tile.  TMEM then holds
+// two S buffers, two O and one rotated-Q buffer.
+#ifndef LCX_TC_SPLIT_O
+#define LCX_TC_SPLIT_O 0
+#endif
+constexpr bool kSplitO = LCX_TC_SPLIT_O;
+// split O: exponentiate at the group's running max before the tile max is known (correct,
+// measured 2 % slower than max-first: 376 vs 369 ms per layer on one box)
+#ifndef LCX_TC_SPEC_EXP
+#define LCX_TC_SPEC_EXP 0
+#endif
+constexpr bool kSpecExp = LCX_TC_SPEC_EXP;
+// A softmax group waits for S(T) on buffer T % NS with a phase parity; that is only
+// sound if the group itself observed the buffer's previous phase (tile T - NS), i.e. if
+// NS is a multiple of the group count -- three groups take three S buffers and one Q.
+constexpr int kQBufs = (kSplitO || kGroups == 3) ? 1 : LCX_TC_QBUFS;
+constexpr int kOBufs = kSplitO ? kGroups : 1;
+constexpr int NK = 4, NV = 4;  // K / V smem stages
+constexpr int NS = kGroups == 3 ? 3 : ((kSplitO || kQBufs == 2) ? 2 : 4);  // S (+P) TMEM
 static_assert(NS % kGroups == 0, "each group must see every phase of its S buffers");
-constexpr int DTN = 2 * BN;                          // keys per double tile
+static_assert(!kSplitO || NS == kGroups, "split O: S(T) full implies PV(T - kGroups) done");
 constexpr uint32_t kKHalf = BN * 64 * 2;             // 8 KB
 constexpr uint32_t kKStage = 4 * kKHalf;             // hi0 hi1 lo0 lo1 = 32 KB
 constexpr uint32_t kVStage = HD * BN * 2;            // 16 KB
@@ -74,30 +109,39 @@ constexpr uint32_t OFF_K = 0;
 constexpr uint32_t OFF_V = OFF_K + NK * kKStage;     // 128 KB
 constexpr uint32_t OFF_BAR = OFF_V + NV * kVStage;   // 192 KB
 constexpr uint32_t OFF_META = OFF_BAR + 1024;
-constexpr int kMetaSlots = 8;                        // DT metadata ring
-constexpr uint32_t kMetaBytes = 720;
+constexpr int kMetaSlots = 16;                      // tile metadata ring (448 B slots)
+// softmax hand-off area: running max per tile parity [2][128], partial sums
+// (l, m) [2 slot][2 warp group][128]
+constexpr uint32_t OFF_RED = OFF_META + kMetaSlots * 448;
 // softmax exchange: running max per group [kGroups][128], partial sums (l, m)
 // [2 slot][kGroups][128]
-constexpr uint32_t OFF_RED = OFF_META + kMetaSlots * kMetaBytes;
 constexpr uint32_t kSmemBytes =
     OFF_RED + kGroups * 128 * 4 + 2 * kGroups * 128 * 8 + 1024;  // + align slack
-static_assert(kSmemBytes <= 227 * 1024, "shared memory");
-// TMEM (512 columns x 128 lanes): S/P buffers [0, 256) (128 columns per DT), O [256, 384),
-// rotated Q [384, 512) (hi, then lo; bf16 pairs per 32-bit column) -- the A operand of
-// every QK MMA, so all MMAs read only B from shared memory.  One Q buffer: at a DCA
-// pattern change the owner of the old pattern's last DT re-rotates it once that DT's S
-// is full (all of the old pattern's QKs are complete).
+// TMEM (512 columns x 128 lanes): S/P buffers [0, 128), O [128, 256), two rotated Q
+// buffers [256, 384) and [384, 512) (hi, then lo; bf16 pairs per 32-bit column) as
+// the A operand of every QK MMA, so all MMAs read only B from shared memory.  DCA
+// pattern group x of an item uses Q buffer x & 1.
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t COL_S = 0;
-constexpr uint32_t COL_O = NS * DTN;
-constexpr uint32_t COL_Q = COL_O + HD;
-static_assert(COL_Q + HD <= 512, "TMEM columns");
+constexpr uint32_t COL_O = NS * BN;
+constexpr uint32_t COL_Q = COL_O + kOBufs * HD;  // Q buffer b: hi at COL_Q + 128 b, lo at + 64
+static_assert(COL_Q + kQBufs * HD <= 512, "TMEM columns");
+constexpr uint32_t QBUF = HD;
 constexpr float kRescaleThresh = 8.f;
-// producer / V-load warps poll with a sleep (ns) instead of a suspended try_wait: their
-// waits are off the critical path and would otherwise take issue slots from the softmax
-// warps sharing their sub-partitions (round 1: -1 to -1.5 % kernel time at 300 ns)
+// producer / V-load warps: sleepy polling (ns between polls) instead of suspended
+// try_wait, 0 = off.  A suspended waiter is woken by other barriers' traffic and
+// re-polls: ncu counts ~700 warp instructions per tile in wait loops, taken from the
+// softmax warps' sub-partitions.  Same-box A/B (attn_tc ms per 1M layer): off 363 /
+// 360, 30 ns 361-363, 100 ns 359-361, 300 ns 357-358, 1000 ns 357-360, 3000 ns 374;
+// the PV issuer's wait for P (critical path) at 40 ns: 363.
 #ifndef LCX_TC_SLEEPY
 #define LCX_TC_SLEEPY 300
+#endif
+// QK / PV MMAs issued eight / four per asm block (one elect, offsets added in PTX)
+#ifndef LCX_TC_MMA_X8
+#define LCX_TC_MMA_X8 0
+#endif
+#ifndef LCX_TC_SLEEPY_PV  // the PV issuer's wait for P (on the critical path)
+#define LCX_TC_SLEEPY_PV 0
 #endif
 
 constexpr uint32_t IDESC_QK = tc::idesc_f16(BM, BN, 1, 1);   // bf16 x bf16
@@ -120,7 +164,6 @@ struct Item {
   int ng;
   Group grp[3];
   int ntiles;
-  int ndt;  // double tiles: the tiles of each pattern group paired in order
 };
 
 struct Tile {
@@ -165,7 +208,6 @@ __device__ void setup_item(const TcParams& p, int item, Item& it) {
   const int64_t ib = it.i0 >> 6;
   it.ng = 0;
   it.ntiles = 0;
-  it.ndt = 0;
   for (int x = 0; x < ng; ++x) {
     Group G{};
     G.klo = lo[x];
@@ -202,7 +244,6 @@ __device__ void setup_item(const TcParams& p, int item, Item& it) {
     if (G.nvt + G.nst == 0) continue;
     it.grp[it.ng++] = G;
     it.ntiles += G.nvt + G.nst;
-    it.ndt += (G.nvt + G.nst + 1) >> 1;
   }
 }
 
@@ -252,7 +293,7 @@ __device__ __forceinline__ int64_t qpos_of(const TcParams& p, int pattern, int64
 // Rotate this thread's query row (its 64-dim half) by its pattern position and
 // store the bf16 hi / lo split into TMEM (row = lane, dim pair = column).
 __device__ __forceinline__ void rotate_q(const TcParams& p, const Item& it, int pattern, int r,
-                                         int part, uint32_t tmem_row) {
+                                         int part, uint32_t tmem_row, int qbuf) {
   const int64_t i = it.i0 + r;
   const bool ok = i < it.rend;
   const uint4* src = reinterpret_cast<const uint4*>(p.q + (i * p.hq + it.h) * int64_t(HD));
@@ -278,32 +319,43 @@ __device__ __forceinline__ void rotate_q(const TcParams& p, const Item& it, int 
       lo[c8 * 4 + k] = *reinterpret_cast<const uint32_t*>(&l2);
     }
   }
-  const uint32_t qc = tmem_row + COL_Q;
+  const uint32_t qc = tmem_row + COL_Q + qbuf * QBUF;
   tc::tmem_st32(qc + part * 32, reinterpret_cast<const float*>(hi));
   tc::tmem_st32(qc + HD / 2 + part * 32, reinterpret_cast<const float*>(lo));
   tc::tmem_wait_st();
 }
 
-// Per-DT control record, written by the producer warp into a shared-memory ring so
-// that the MMA and softmax warps never touch global memory for control.
-enum { T_TILES = 0, T_EMPTY = 3, T_END = 4 };
+// Per-tile control record, written by the producer warp into a 4-deep shared
+// ring so that the MMA and softmax warps never touch global memory for control.
+enum { T_EMPTY = 3, T_END = 4 };
 enum { F_FIRST = 1, F_LAST = 2, F_EPOCH = 4, F_EPOCH_AFTER = 8 };
-struct SubMeta {  // one 64-key half of a DT
-  int32_t kind, count, nfar, pad;
-  int64_t key0, sbase;
+struct TileMeta {
+  int32_t kind, flags, pattern, next_pattern;
+  int32_t h, count, nfar, grp;  // grp: the tile's pattern group within its item
+  int32_t gpat[3], ng;          // the item's group patterns and group count
+  int64_t i0, rend, key0, sbase;
   uint64_t vmask;
   uint32_t sw[8];
   int32_t keys[64];
 };
-struct DtMeta {
-  int32_t kind, flags, pattern, next_pattern;
-  int32_t h, nsub, pad0, pad1;
-  int64_t i0, rend;
-  SubMeta sub[2];
-};
-static_assert(sizeof(DtMeta) <= kMetaBytes, "DT metadata slot overflow");
-static_assert(kMetaBytes % 16 == 0, "DT metadata slot alignment");
-
+#ifndef LCX_TC_BULK
+#define LCX_TC_BULK 1  // 1-D bulk copies of the pre-swizzled tiles (else 3-D tensor TMA)
+#endif
+[[maybe_unused]] constexpr int kTraceTiles = 512;
+// trace columns: 0 meta ready (producer), 1 K TMA issued, 2 V TMA issued,
+// 3 QK issued (MMA), 4 PV issued, 5 softmax got S, 6 softmax P written, 7 kind
+// pipeline trace (tools/trace_tc.py): compiled in only with -DLCX_TC_TRACE -- the
+// per-tile checks cost ~3 % of the kernel's instructions
+__device__ __forceinline__ void trace_mark(const TcParams& p, uint32_t T, int col) {
+#ifdef LCX_TC_TRACE
+  if (p.trace && blockIdx.x == 0 && T < kTraceTiles) p.trace[T * 8 + col] = clock64();
+#else
+  (void)p;
+  (void)T;
+  (void)col;
+#endif
+}
+static_assert(sizeof(TileMeta) <= 448, "tile metadata slot overflow");
 // wait profile (LCX_TC_WAITPROF, tools/trace_wait.py): cycles each role spends per wait
 // site, summed over all CTAs into trace[4096 + role * 8 + site]
 #ifdef LCX_TC_WAITPROF
@@ -341,27 +393,13 @@ __device__ __forceinline__ uint64_t window64(const uint32_t* sw, int off) {
   return sh ? ((a >> sh) | (b << (64 - sh))) : a;
 }
 
-// admitted-entry mask of row i over the 64 keys of one half (bit c: key c of the tile)
-__device__ __forceinline__ uint64_t sub_mask(const SubMeta& sm, int64_t i) {
-  if (sm.kind == T_VERT) {
-    int cnt = sm.nfar;  // keys below the row block: admitted by every row
-    while (cnt < sm.count) {
-      const int32_t kk = sm.keys[cnt];
-      if (kk < 0 || int64_t(kk) > i) break;
-      ++cnt;
-    }
-    return cnt >= 64 ? ~0ull : ((1ull << cnt) - 1);
-  }
-  if (sm.kind == T_SLASH) {
-    const int off = int(i - sm.key0 - 63 - sm.sbase);
-    return __brevll(window64(sm.sw, off)) & ~sm.vmask;
-  }
-  const int64_t lim = i - sm.key0;  // dense: causal
-  return lim >= 63 ? ~0ull : (lim < 0 ? 0ull : ((2ull << lim) - 1));
-}
-
 __global__ void __launch_bounds__(kThreads, 1)
-attn_tc_kernel(const TcParams p) {
+attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
+               const __grid_constant__ CUtensorMap map_k_lo,
+               const __grid_constant__ CUtensorMap map_vt,
+               const __grid_constant__ CUtensorMap map_kc_hi,
+               const __grid_constant__ CUtensorMap map_kc_lo,
+               const __grid_constant__ CUtensorMap map_vct) {
   // key-window pass with no slash tile anywhere in it (and no vertical pass): nothing to do
   if (!p.vert_pass && p.win_flags && !p.win_flags[p.win]) return;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -372,19 +410,21 @@ attn_tc_kernel(const TcParams p) {
   const tc::SBar k_full{smem_base + OFF_BAR};  // [NK] TMA -> MMA
   const tc::SBar k_empty = k_full + NK;        // [NK] QK commit -> producer
   const tc::SBar v_full = k_empty + NK;        // [NV]
-  const tc::SBar v_empty = v_full + NV;        // [NV] PV commit -> V loader
+  const tc::SBar v_empty = v_full + NV;        // [NV] PV commit -> producer
   const tc::SBar s_full = v_empty + NV;        // [NS] QK commit -> softmax
   const tc::SBar s_free = s_full + NS;         // [NS] PV commit (S/P buffer, O updated)
   const tc::SBar p_full = s_free + NS;         // [NS] softmax wrote P -> PV issuer
-  const tc::SBar q_ready = p_full + NS;        // [1] softmax rotated Q -> QK issuer
-  const tc::SBar m_full = q_ready + 1;         // [kMetaSlots]
+  const tc::SBar q_ready = p_full + NS;        // [2] softmax rotated Q buffer b -> QK issuer
+  const tc::SBar m_full = q_ready + 2;         // [kMetaSlots]
   const tc::SBar m_empty = m_full + kMetaSlots;  // [kMetaSlots]
-  const tc::SBar hand = m_empty + kMetaSlots;    // [kGroups][4] running max of a DT ready
-  const tc::SBar lpub = hand + 4 * kGroups;      // [kGroups] partial sums of a DT written
-  constexpr int kBars = 2 * NK + 2 * NV + 3 * NS + 1 + 2 * kMetaSlots + 5 * kGroups;
-  static_assert((kBars + 1) * 8 <= 1024, "barrier area overflow");
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR) + 2 * kBars;
-  DtMeta* metas = reinterpret_cast<DtMeta*>(smem + OFF_META);
+  const tc::SBar hand = m_empty + kMetaSlots;    // [kGroups][4] running max of a tile ready
+  const tc::SBar lpub = hand + 4 * kGroups;      // [kGroups] partial sums of a tile written
+  const tc::SBar edone = lpub + kGroups;         // split O: an item's epilogue read both O
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR) +
+                        2 * (2 * NK + 2 * NV + 3 * NS + 2 + 2 * kMetaSlots + 5 * kGroups + 1);
+  static_assert((2 * NK + 2 * NV + 3 * NS + 2 + 2 * kMetaSlots + 5 * kGroups + 2) * 8 <= 1024,
+                "barrier area overflow");
+  TileMeta* metas = reinterpret_cast<TileMeta*>(smem + OFF_META);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef LCX_TC_WAITPROF
@@ -403,11 +443,13 @@ attn_tc_kernel(const TcParams p) {
     for (int b = 0; b < NS; ++b) {
       tc::mbar_init(s_full + b, 1);
       tc::mbar_init(s_free + b, 1);
-      tc::mbar_init(p_full + b, 4);  // the DT's warp group
+      tc::mbar_init(p_full + b, 4);  // the tile's warp group
     }
     tc::mbar_init(q_ready, 4);
+    tc::mbar_init(q_ready + 1, 4);
     for (int b = 0; b < 4 * kGroups; ++b) tc::mbar_init(hand + b, 1);
     for (int b = 0; b < kGroups; ++b) tc::mbar_init(lpub + b, 4);
+    tc::mbar_init(edone, 4);
     for (int b = 0; b < kMetaSlots; ++b) {
       tc::mbar_init(m_full + b, 1);
       tc::mbar_init(m_empty + b, kSoftmaxWarps + 3);  // softmax + QK + PV + V warps
@@ -416,161 +458,191 @@ attn_tc_kernel(const TcParams p) {
     tc::fence_proxy_async();
   }
   if (warp == kWarpMma) tc::tmem_alloc(tmem_slot, kTmemCols);
+  if (warp == kWarpProducer && lane == 0) {
+    tc::tma_prefetch(&map_k_hi);
+    tc::tma_prefetch(&map_k_lo);
+    tc::tma_prefetch(&map_vt);
+    tc::tma_prefetch(&map_kc_hi);
+    tc::tma_prefetch(&map_kc_lo);
+    tc::tma_prefetch(&map_vct);
+  }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == kWarpProducer) {
-    // ====================================== producer: DT stream + metadata + K loads ====
-    // Batches of two DTs (four 64-key halves), one lane per half: lane j resolves half
-    // j % 2 of DT db + j / 2 (tile list entry, bitmap window), writes its part of the DT's
-    // record into the metadata ring, and issues its K loads.
-    uint32_t U = 0, M = 0;  // halves issued, DT records written
+    // ============================ producer: tile stream + metadata + K loads ====
+    // Batches of 4 tiles, one lane per tile: lane j resolves tile j (tile-list entry,
+    // bitmap window), waits for nothing but its slot, writes the tile's record into the
+    // metadata ring, publishes it and issues its K loads -- the batch's global loads and
+    // its four ring slots are all in flight at once.
+    uint32_t T = 0, M = 0;
     const Item* plans = reinterpret_cast<const Item*>(p.plans);
     auto slot_wait = [&](uint32_t mm) {
-      WAITP(0, tc::mbar_wait_sleepy(m_empty + int(mm % kMetaSlots),
-                                    ((mm / kMetaSlots) & 1) ^ 1, LCX_TC_SLEEPY));
+#if LCX_TC_SLEEPY
+      WAITP(0, tc::mbar_wait_sleepy(m_empty + int(mm % kMetaSlots), ((mm / kMetaSlots) & 1) ^ 1,
+                                    LCX_TC_SLEEPY));
+#else
+      WAITP(0, tc::mbar_wait(m_empty + int(mm % kMetaSlots), ((mm / kMetaSlots) & 1) ^ 1));
+#endif
     };
-    // items come from a global queue (ascending, so neighbouring CTAs work on neighbouring
-    // row blocks of a head and share their K / V tiles in L2)
+    // items come from a global queue (ascending, so neighbouring CTAs still work on
+    // neighbouring row blocks of a head and share their K / V tiles in L2) -- CTAs that
+    // drew cheap items take more, instead of a fixed round-robin share
+    int static_item = int(blockIdx.x);
     auto next_item = [&]() -> int {
+      if (!p.item_counter) {
+        const int x = static_item;
+        static_item += int(gridDim.x);
+        return x;
+      }
       int v = 0;
       if (lane == 0) v = atomicAdd(p.item_counter, 1);
       return __shfl_sync(0xffffffffu, v, 0);
     };
     for (int item = next_item(); item < p.nitems; item = next_item()) {
       const Item it = plans[item];
-      if (it.ndt == 0) {
+      if (it.ntiles == 0) {
         slot_wait(M);
-        DtMeta& mt = metas[M % kMetaSlots];
+        TileMeta& mt = metas[M % kMetaSlots];
         if (lane == 0) {
           mt.kind = T_EMPTY;
           mt.flags = F_FIRST | F_LAST;
           mt.h = it.h;
           mt.i0 = it.i0;
           mt.rend = it.rend;
-          mt.nsub = 0;
         }
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(m_full + int(M % kMetaSlots));
         ++M;
         continue;
       }
-      for (int db = 0; db < it.ndt; db += 2) {
-        const int nd = min(2, it.ndt - db);
-        // A: lane j < 4 -> DT d = db + j / 2, half s = j % 2: its pattern group x, the
-        // group's first tile and DT indices, the DT's half count
-        const int d = db + (lane >> 1), s = lane & 1;
-        int x = 0, dl = d, tb = 0, ngt = 0;
-#pragma unroll
-        for (int y = 0; y < 3; ++y) {
-          if (y >= it.ng) break;
-          ngt = it.grp[y].nvt + it.grp[y].nst;
-          const int ndy = (ngt + 1) >> 1;
-          x = y;
-          if (dl < ndy) break;
-          dl -= ndy;
-          tb += ngt;
-        }
-        const int nsub = min(2, ngt - 2 * dl);
-        const bool live = lane < 2 * nd && d < it.ndt;
-        const bool valid = live && s < nsub;
+      int carry_grp = -1;
+      for (int tb = 0; tb < it.ntiles; tb += 4) {
+        const int nb = min(4, it.ntiles - tb);
+        // A: lane j <= nb resolves tile tb + j (lane nb: the next tile's group)
         Tile my{};
+        my.grp = -1;
         my.kind = -1;
-        if (valid) my = get_tile(p, it, tb + 2 * dl + s);
-        // B: the half's record (SLASH: the 256-bit diagonal window and vertical mask)
+        if (lane <= nb && tb + lane < it.ntiles) my = get_tile(p, it, tb + lane);
+        const int up_grp = __shfl_up_sync(0xffffffffu, my.grp, 1);
+        const int dn_grp = __shfl_down_sync(0xffffffffu, my.grp, 1);
+        const int prev_grp = lane == 0 ? carry_grp : up_grp;
+        carry_grp = __shfl_sync(0xffffffffu, my.grp, nb - 1);
+        // B: lane j < nb builds its tile's record (SLASH: the 256-bit diagonal window)
+        const int t = tb + lane;
+        int flags = 0, pattern = 0, next_pattern = 0;
         uint32_t swv[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         uint64_t vmask = 0;
         int64_t sbase = 0;
-        if (valid && my.kind == T_SLASH) {
-          const int64_t lo = it.i0 - my.key0 - 63;
-          const int64_t wbase = lo >= 0 ? (lo >> 5) : -((-lo + 31) >> 5);
-          sbase = wbase * 32;
-          const uint32_t* sb = p.sbits + int64_t(it.h) * p.words;
+        if (lane < nb) {
+          if (t == 0) flags |= F_FIRST;
+          if (my.grp != prev_grp) flags |= F_EPOCH;
+          if (t + 1 == it.ntiles) flags |= F_LAST;
+          else if (dn_grp != my.grp) flags |= F_EPOCH_AFTER;
+          pattern = grp_pattern(it, my.grp);
+          next_pattern = (flags & F_EPOCH_AFTER) ? grp_pattern(it, dn_grp) : 0;
+          if (my.kind == T_SLASH) {
+            const int64_t lo = it.i0 - my.key0 - 63;
+            const int64_t wbase = lo >= 0 ? (lo >> 5) : -((-lo + 31) >> 5);
+            sbase = wbase * 32;
+            const uint32_t* sb = p.sbits + int64_t(it.h) * p.words;
 #pragma unroll
-          for (int w = 0; w < 8; ++w) {
-            const int64_t wi = wbase + w;
-            swv[w] = (wi >= 0 && wi < p.words) ? sb[wi] : 0u;
-          }
-          const uint32_t* vb = p.vbits + int64_t(it.h) * p.words;
-          const int64_t kw = my.key0 >> 5;
-          const uint32_t v0 = kw < p.words ? vb[kw] : 0u;
-          const uint32_t v1 = kw + 1 < p.words ? vb[kw + 1] : 0u;
-          vmask = uint64_t(v0) | (uint64_t(v1) << 32);
-        }
-        // C: the batch's ring slots, then every lane writes its part
-        for (int j = 0; j < nd; ++j) slot_wait(M + j);
-        if (live) {
-          DtMeta& mt = metas[(M + (lane >> 1)) % kMetaSlots];
-          if (s == 0) {
-            int flags = 0;
-            if (d == 0) flags |= F_FIRST;
-            if (dl == 0) flags |= F_EPOCH;
-            const int ndx = (ngt + 1) >> 1;
-            if (d + 1 == it.ndt) flags |= F_LAST;
-            else if (dl + 1 == ndx) flags |= F_EPOCH_AFTER;
-            mt.kind = T_TILES;
-            mt.flags = flags;
-            mt.pattern = grp_pattern(it, x);
-            mt.next_pattern = (flags & F_EPOCH_AFTER) ? grp_pattern(it, x + 1) : 0;
-            mt.h = it.h;
-            mt.nsub = nsub;
-            mt.i0 = it.i0;
-            mt.rend = it.rend;
-          }
-          if (valid) {
-            SubMeta& sm = mt.sub[s];
-            sm.kind = my.kind;
-            sm.count = my.count;
-            sm.key0 = my.key0;
-            sm.sbase = sbase;
-            sm.vmask = vmask;
-            if (my.kind == T_SLASH) {
-#pragma unroll
-              for (int w = 0; w < 8; ++w) sm.sw[w] = swv[w];
+            for (int w = 0; w < 8; ++w) {
+              const int64_t wi = wbase + w;
+              swv[w] = (wi >= 0 && wi < p.words) ? sb[wi] : 0u;
             }
+            const uint32_t* vb = p.vbits + int64_t(it.h) * p.words;
+            const int64_t kw = my.key0 >> 5;
+            const uint32_t v0 = kw < p.words ? vb[kw] : 0u;
+            const uint32_t v1 = kw + 1 < p.words ? vb[kw + 1] : 0u;
+            vmask = uint64_t(v0) | (uint64_t(v1) << 32);
           }
         }
-        // vertical halves' key lists, warp-wide
-        for (int j = 0; j < 2 * nd; ++j) {
+        // C: the batch's ring slots, then every lane writes its record; vertical tiles'
+        // key lists are written warp-wide
+        for (int j = 0; j < nb; ++j) slot_wait(M + j);
+        if (lane < nb) {
+          TileMeta& mt = metas[(M + lane) % kMetaSlots];
+          mt.kind = my.kind;
+          mt.flags = flags;
+          mt.pattern = pattern;
+          mt.next_pattern = next_pattern;
+          mt.grp = my.grp;
+          mt.gpat[0] = it.grp[0].pattern;
+          mt.gpat[1] = it.grp[1].pattern;
+          mt.gpat[2] = it.grp[2].pattern;
+          mt.ng = it.ng;
+          mt.h = it.h;
+          mt.count = my.count;
+          mt.i0 = it.i0;
+          mt.rend = it.rend;
+          mt.key0 = my.key0;
+          mt.sbase = sbase;
+          mt.vmask = vmask;
+          if (my.kind == T_SLASH) {
+#pragma unroll
+            for (int w = 0; w < 8; ++w) mt.sw[w] = swv[w];
+          }
+        }
+        for (int j = 0; j < nb; ++j) {
           if (__shfl_sync(0xffffffffu, my.kind, j) != T_VERT) continue;
           const long long key0j = __shfl_sync(0xffffffffu, (long long)my.key0, j);
           const int countj = __shfl_sync(0xffffffffu, my.count, j);
           const int32_t* c = p.ckeys + int64_t(it.h) * p.capp + key0j;
           const int32_t k0 = lane < countj ? c[lane] : -1;
           const int32_t k1 = lane + 32 < countj ? c[lane + 32] : -1;
-          SubMeta& sm = metas[(M + (j >> 1)) % kMetaSlots].sub[j & 1];
-          sm.keys[lane] = k0;
-          sm.keys[lane + 32] = k1;
+          TileMeta& mt = metas[(M + j) % kMetaSlots];
+          mt.keys[lane] = k0;
+          mt.keys[lane + 32] = k1;
           const unsigned f0 = __ballot_sync(0xffffffffu, k0 >= 0 && int64_t(k0) < it.i0);
           const unsigned f1 = __ballot_sync(0xffffffffu, k1 >= 0 && int64_t(k1) < it.i0);
-          if (lane == 0) sm.nfar = __popc(f0) + __popc(f1);
+          if (lane == 0) mt.nfar = __popc(f0) + __popc(f1);
         }
-        // D: publish (lane 2 k: DT db + k), then each valid lane issues its half's K loads
-        // (halves in stream order: DT db's, then DT db + 1's)
+        // D: publish (lane j: slot of tile j), then lane j issues tile j's K loads
         __syncwarp();
-        if (live && s == 0) tc::mbar_arrive(m_full + int((M + (lane >> 1)) % kMetaSlots));
-        const int nsub0 = __shfl_sync(0xffffffffu, nsub, 0);
-        const int nsub1 = nd > 1 ? __shfl_sync(0xffffffffu, nsub, 2) : 0;
-        if (valid) {
-          const uint32_t Uj = U + ((lane >> 1) ? nsub0 : 0) + s;
-          const int bk = Uj % NK;
-          WAITP(1, tc::mbar_wait_sleepy(k_empty + bk, ((Uj / NK) & 1) ^ 1, LCX_TC_SLEEPY));
+        if (lane < nb) {
+          tc::mbar_arrive(m_full + int((M + lane) % kMetaSlots));
+          const uint32_t Tj = T + lane;
+#if !defined(LCX_TC_TRACE_PV) && !defined(LCX_TC_TRACE_SM)
+          trace_mark(p, Tj, 0);
+#endif
+          const int bk = Tj % NK;
+#if LCX_TC_SLEEPY
+          WAITP(1, tc::mbar_wait_sleepy(k_empty + bk, ((Tj / NK) & 1) ^ 1, LCX_TC_SLEEPY));
+#else
+          WAITP(1, tc::mbar_wait(k_empty + bk, ((Tj / NK) & 1) ^ 1));
+#endif
           tc::mbar_expect_tx(k_full + bk, kKStage);
           const uint32_t kdst = smem_base + OFF_K + bk * kKStage;
-          const int64_t tile = my.kind == T_VERT
-                                   ? (int64_t(it.h) * (p.capp / 64) + my.key0 / 64) * 2
-                                   : (int64_t(it.g) * p.ntiles_k + my.key0 / 64) * 2;
+          int tile = my.kind == T_VERT ? int((int64_t(it.h) * (p.capp / 64) + my.key0 / 64) * 2)
+                                       : int((int64_t(it.g) * p.ntiles_k + my.key0 / 64) * 2);
+#ifdef LCX_TC_FAKE_LOADS  // timing experiment only: every tile loads from a small L2-resident set
+          tile &= 62;
+#endif
+#if LCX_TC_BULK
           // pre-swizzled tiles: hi (2 halves) and lo are one contiguous 16 KB run each
           const __nv_bfloat16* sh = my.kind == T_VERT ? p.kchi : p.khi;
           const __nv_bfloat16* sl = my.kind == T_VERT ? p.kclo : p.klo;
-          tc::bulk_load(kdst, sh + tile * (kKHalf / 2), 2 * kKHalf, k_full + bk);
-          tc::bulk_load(kdst + 2 * kKHalf, sl + tile * (kKHalf / 2), 2 * kKHalf, k_full + bk);
+          tc::bulk_load(kdst, sh + int64_t(tile) * (kKHalf / 2), 2 * kKHalf, k_full + bk);
+          tc::bulk_load(kdst + 2 * kKHalf, sl + int64_t(tile) * (kKHalf / 2), 2 * kKHalf,
+                        k_full + bk);
+#else
+          const CUtensorMap* mh = my.kind == T_VERT ? &map_kc_hi : &map_k_hi;
+          const CUtensorMap* ml = my.kind == T_VERT ? &map_kc_lo : &map_k_lo;
+          tc::tma_load_3d(kdst + 0 * kKHalf, mh, k_full + bk, 0, 0, tile);
+          tc::tma_load_3d(kdst + 1 * kKHalf, mh, k_full + bk, 0, 0, tile + 1);
+          tc::tma_load_3d(kdst + 2 * kKHalf, ml, k_full + bk, 0, 0, tile);
+          tc::tma_load_3d(kdst + 3 * kKHalf, ml, k_full + bk, 0, 0, tile + 1);
+#endif
+#if !defined(LCX_TC_TRACE_PV) && !defined(LCX_TC_TRACE_SM)
+          trace_mark(p, Tj, 1);
+#endif
         }
         __syncwarp();
-        M += nd;
-        U += nsub0 + nsub1;
+        M += nb;
+        T += nb;
       }
     }
     slot_wait(M);
@@ -579,95 +651,117 @@ attn_tc_kernel(const TcParams p) {
     if (lane == 0) tc::mbar_arrive(m_full + int(M % kMetaSlots));
     ++M;
     if (lane == 0 && p.tile_count)
-      atomicAdd(reinterpret_cast<unsigned long long*>(p.tile_count), (unsigned long long)U);
+      atomicAdd(reinterpret_cast<unsigned long long*>(p.tile_count), (unsigned long long)T);
 #ifdef LCX_TC_WAITPROF
     wacc[7] = clock64() - t_start;
 #endif
     WAITP_FLUSH(0);
   } else if (warp == kWarpMma) {
     // ==================================================== QK issuer ====
-    uint32_t T = 0, U = 0, E = 0, M = 0;
-    // all 32 lanes run this loop (warp-uniform); one elected lane issues
+    uint32_t T = 0, E = 0, M = 0;
+    // QK issuer: all 32 lanes run this loop (warp-uniform); one elected lane issues
     const uint64_t dk0 = tc::sdesc_sw128(tc::smem_u32(smem + OFF_K));
     for (;;) {
       const int slot = M % kMetaSlots;
       WAITP(0, tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1));
       const int kind = metas[slot].kind;
       const int flags = metas[slot].flags;
-      const int nsub = metas[slot].nsub;
+      const int qb = kQBufs == 2 ? (metas[slot].grp & 1) : 0;  // Q buffer of the tile's group
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(m_empty + slot);
       ++M;
       if (kind == T_END) break;
       if (kind == T_EMPTY) continue;
-      if (flags & F_EPOCH) {  // first DT of a pattern group: its Q is (or will be) rotated
-        WAITP(1, tc::mbar_wait(q_ready, E & 1));
-        ++E;
+      if (flags & F_EPOCH) {  // first tile of a group: its Q buffer is (or will be) filled
+        WAITP(1, tc::mbar_wait(q_ready + qb, (E >> (qb * 16)) & 1));
+        E += 1u << (qb * 16);  // per-buffer use counts (low / high half)
       }
-      const int bs = T % NS;
+      const int bk = T % NK, bs = T % NS;
+      WAITP(2, tc::mbar_wait(k_full + bk, (T / NK) & 1));
       WAITP(3, tc::mbar_wait(s_free + bs, ((T / NS) & 1) ^ 1));  // PV(T - NS) released S/P
-      const uint32_t dS = tmem + COL_S + bs * DTN;
-      for (int j = 0; j < nsub; ++j) {
-        const uint32_t Uj = U + j;
-        const int bk = Uj % NK;
-        WAITP(2, tc::mbar_wait(k_full + bk, (Uj / NK) & 1));
-        tc::tc_fence_after();
-        const uint64_t dk = dk0 + ((bk * kKStage) >> 4);
+      tc::tc_fence_after();
+#ifndef LCX_TC_TRACE_PV
+      if (lane == 0) trace_mark(p, T, 7);
+#endif
+      const uint64_t dk = dk0 + ((bk * kKStage) >> 4);
+      const uint32_t dS = tmem + bs * BN;
+#ifdef LCX_TC_WAITPROF
+      const long long t_iss = clock64();
+#endif
 #pragma unroll
-        for (int combo = 0; combo < 3; ++combo) {  // hh, hl, lh
-          const uint32_t qa = tmem + COL_Q + (combo == 2 ? HD / 2 : 0);
-          const uint64_t ka = dk + (combo == 1 ? ((2 * kKHalf) >> 4) : 0);
+#ifdef LCX_TC_ONE_TERM  // timing experiment only: hi.hi product alone
+      for (int combo = 0; combo < 1; ++combo) {
+#else
+      for (int combo = 0; combo < 3; ++combo) {
+#endif
+        const uint32_t qa = tmem + COL_Q + qb * QBUF + (combo == 2 ? HD / 2 : 0);  // hh, hl, lh
+        const uint64_t ka = dk + (combo == 1 ? ((2 * kKHalf) >> 4) : 0);
+#if LCX_TC_MMA_X8
+        tc::mma_f16_ts_x8_warp(dS, qa, ka, kKHalf >> 4, IDESC_QK, combo ? 1u : 0u);
+#else
 #pragma unroll
-          for (int half = 0; half < 2; ++half)
+        for (int half = 0; half < 2; ++half)
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              tc::mma_f16_ts_warp(dS + j * BN, qa + half * 32 + kk * 8,
-                                  ka + ((half * kKHalf + kk * 32) >> 4), IDESC_QK,
-                                  (combo | half | kk) ? 1u : 0u);
-        }
-        tc::mma_commit_warp(k_empty + bk);
+          for (int kk = 0; kk < 4; ++kk)
+            tc::mma_f16_ts_warp(dS, qa + half * 32 + kk * 8,
+                                ka + ((half * kKHalf + kk * 32) >> 4), IDESC_QK,
+                                (combo | half | kk) ? 1u : 0u);
+#endif
       }
+      tc::mma_commit_warp(k_empty + bk);
       tc::mma_commit_warp(s_full + bs);
+#ifdef LCX_TC_WAITPROF
+      wacc[4] += clock64() - t_iss;
+#endif
+#ifndef LCX_TC_TRACE_PV
+      if (lane == 0) trace_mark(p, T, 3);
+#endif
       ++T;
-      U += nsub;
     }
 #ifdef LCX_TC_WAITPROF
     wacc[7] = clock64() - t_start;
 #endif
     WAITP_FLUSH(1);
   } else if (warp == kWarpV) {
-    // ===================================================== V loads ====
-    uint32_t U = 0, M = 0;
+    // ===================================================== V TMA loads ====
+    uint32_t T = 0, M = 0;
     for (;;) {
       const int slot = M % kMetaSlots;
       WAITP(0, tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1));
       const int kind = metas[slot].kind;
       const int h = metas[slot].h;
-      const int nsub = metas[slot].nsub;
-      const int k0 = metas[slot].sub[0].kind, k1 = metas[slot].sub[1].kind;
-      const int64_t key00 = metas[slot].sub[0].key0, key01 = metas[slot].sub[1].key0;
+      const int key0 = int(metas[slot].key0);
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(m_empty + slot);
       ++M;
       if (kind == T_END) break;
       if (kind == T_EMPTY) continue;
       if (lane == 0) {
-        for (int j = 0; j < nsub; ++j) {
-          const uint32_t Uj = U + j;
-          const int bv = Uj % NV;
-          const int kd = j ? k1 : k0;
-          const int64_t key0 = j ? key01 : key00;
-          WAITP(1, tc::mbar_wait_sleepy(v_empty + bv, ((Uj / NV) & 1) ^ 1, LCX_TC_SLEEPY));
-          tc::mbar_expect_tx(v_full + bv, kVStage);
-          const uint32_t vdst = smem_base + OFF_V + bv * kVStage;
-          const int64_t vtile = kd == T_VERT ? int64_t(h) * (p.capp / 64) + key0 / 64
+        const int bv = T % NV;
+#if LCX_TC_SLEEPY
+        WAITP(1, tc::mbar_wait_sleepy(v_empty + bv, ((T / NV) & 1) ^ 1, LCX_TC_SLEEPY));
+#else
+        WAITP(1, tc::mbar_wait(v_empty + bv, ((T / NV) & 1) ^ 1));
+#endif
+        tc::mbar_expect_tx(v_full + bv, kVStage);
+        const uint32_t vdst = smem_base + OFF_V + bv * kVStage;
+        const int64_t vtile = kind == T_VERT ? int64_t(h) * (p.capp / 64) + key0 / 64
                                              : int64_t(h / p.group) * p.ntiles_k + key0 / 64;
-          tc::bulk_load(vdst, (kd == T_VERT ? p.vct : p.vt) + vtile * (kVStage / 2), kVStage,
-                        v_full + bv);
-        }
+#ifdef LCX_TC_FAKE_LOADS
+        const_cast<int64_t&>(vtile) = (vtile & 31);
+#endif
+#if LCX_TC_BULK
+        tc::bulk_load(vdst, (kind == T_VERT ? p.vct : p.vt) + vtile * (kVStage / 2), kVStage,
+                      v_full + bv);
+#else
+        tc::tma_load_3d(vdst, kind == T_VERT ? &map_vct : &map_vt, v_full + bv, 0, 0, int(vtile));
+#endif
+#ifndef LCX_TC_TRACE_PV
+        trace_mark(p, T, 2);
+#endif
       }
       __syncwarp();
-      U += nsub;
+      ++T;
     }
 #ifdef LCX_TC_WAITPROF
     wacc[7] = clock64() - t_start;
@@ -675,41 +769,55 @@ attn_tc_kernel(const TcParams p) {
     WAITP_FLUSH(2);
   } else if (warp == kWarpPv) {
     // ============================================== PV issuer (O += P V) ====
-    uint32_t T = 0, U = 0, M = 0;
+    uint32_t T = 0, M = 0, T_first = 0;
     const uint64_t dv0 = tc::sdesc_sw128(tc::smem_u32(smem + OFF_V));
     for (;;) {
       const int slot = M % kMetaSlots;
       WAITP(0, tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1));
+#ifdef LCX_TC_TRACE_PV
+      if (lane == 0) trace_mark(p, T, 0);
+#endif
       const int kind = metas[slot].kind;
       const int flags = metas[slot].flags;
-      const int nsub = metas[slot].nsub;
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(m_empty + slot);
       ++M;
       if (kind == T_END) break;
       if (kind == T_EMPTY) continue;
-      const int bs = T % NS;
+      const int bs = T % NS, bv = T % NV;
+#if LCX_TC_SLEEPY_PV
+      WAITP(1, tc::mbar_wait_sleepy(p_full + bs, (T / NS) & 1, LCX_TC_SLEEPY_PV));
+#else
       WAITP(1, tc::mbar_wait(p_full + bs, (T / NS) & 1));
-      // the first PV of an item overwrites O (a key-window pass > 0 restored the running O
-      // into TMEM before the item's first P was released)
-      const bool first = (flags & F_FIRST) && !p.init;
-      const uint32_t dO = tmem + COL_O;
-      for (int j = 0; j < nsub; ++j) {
-        const uint32_t Uj = U + j;
-        const int bv = Uj % NV;
-        WAITP(2, tc::mbar_wait(v_full + bv, (Uj / NV) & 1));
-        tc::tc_fence_after();
-        const uint64_t dv = dv0 + ((bv * kVStage) >> 4);
+#endif
+#ifdef LCX_TC_TRACE_PV  // columns 0 / 1 / 2: PV issuer passed the meta / P / V waits
+      if (lane == 0) trace_mark(p, T, 1);
+#endif
+      WAITP(2, tc::mbar_wait(v_full + bv, (T / NV) & 1));
+#ifdef LCX_TC_TRACE_PV
+      if (lane == 0) trace_mark(p, T, 2);
+#endif
+      tc::tc_fence_after();
+      const uint64_t dv = dv0 + ((bv * kVStage) >> 4);
+      if (flags & F_FIRST) T_first = T;
+      // the first PV into an O of the item overwrites it (a key-window pass > 0 restored
+      // the running O into the first tile's O)
+      const bool first = kSplitO ? (T - T_first < uint32_t(kGroups) && !(p.init && T == T_first))
+                                 : ((flags & F_FIRST) && !p.init);
+      const uint32_t dO = tmem + COL_O + (kSplitO ? (T % kGroups) * HD : 0);
+#if LCX_TC_MMA_X8
+      static_assert(BN / 16 == 4, "four PV MMAs per tile");
+      tc::mma_f16_ts_x4_warp(dO, tmem + bs * BN, dv, IDESC_PV, first ? 0u : 1u);
+#else
 #pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk)  // P (fp16, 2 per column) aliases S half j
-          tc::mma_f16_ts_warp(dO, tmem + COL_S + bs * DTN + j * BN + kk * 8,
-                              dv + ((kk * 32) >> 4), IDESC_PV,
-                              (first && j == 0 && kk == 0) ? 0u : 1u);
-        tc::mma_commit_warp(v_empty + bv);
-      }
+      for (int kk = 0; kk < BN / 16; ++kk)  // P (fp16, 2 per column) aliases S buffer bs
+        tc::mma_f16_ts_warp(dO, tmem + bs * BN + kk * 8, dv + ((kk * 32) >> 4),
+                            IDESC_PV, (first && kk == 0) ? 0u : 1u);
+#endif
+      tc::mma_commit_warp(v_empty + bv);
       tc::mma_commit_warp(s_free + bs);
+      if (lane == 0) trace_mark(p, T, 4);
       ++T;
-      U += nsub;
     }
 #ifdef LCX_TC_WAITPROF
     wacc[7] = clock64() - t_start;
@@ -717,19 +825,21 @@ attn_tc_kernel(const TcParams p) {
     WAITP_FLUSH(3);
   } else {
     // ============================= softmax / correction / epilogue ====
-    // The two warp groups take the DTs of the stream in turn (group g: DTs T with
-    // T % 2 == g); within a group, warp = TMEM lane quadrant and thread = query row with
-    // all 128 columns of the DT.  The groups run out of phase -- one computes a DT's max
-    // while the other exponentiates the previous one -- and pass the row's running max on
-    // per DT through shared memory, signalled on an mbarrier per (group, quadrant).  Each
-    // group keeps its own partial row sum l expressed at the max it last used; the owner
-    // of an item's last DT combines both (each published before the group's P release) in
-    // the epilogue.
+    // kGroups warp groups take the tiles of the stream in turn (group g: tiles T with
+    // T % kGroups == g); within a group, warp = TMEM lane quadrant and thread = query
+    // row with all 64 columns of the tile.  The groups run out of phase -- one computes
+    // a tile's max while the others exponentiate earlier tiles -- and pass the row's
+    // running max on per tile through shared memory, signalled on an mbarrier per
+    // (group, quadrant).  Each group keeps its own partial row sum l expressed at the max
+    // it last used; the owner of an item's last tile combines all of them (each published
+    // before the group's P release) in the epilogue.
     const int wq = warp & 3;       // TMEM lane quadrant
     const int grp = warp >> 2;     // warp group
     const int r = wq * 32 + lane;
     const uint32_t lane_base = uint32_t(wq * 32) << 16;
-    float* mbuf = reinterpret_cast<float*>(smem + OFF_RED);  // [kGroups][128] m after DT
+    const uint32_t col_o = COL_O + (kSplitO ? uint32_t(grp) * HD : 0u);  // this group's O
+    uint32_t J = 0, J_cur = 0;  // split O: items started, index of the current one
+    float* mbuf = reinterpret_cast<float*>(smem + OFF_RED);  // [kGroups][128] m after tile
     float2* lbuf = reinterpret_cast<float2*>(smem + OFF_RED + kGroups * 128 * 4);
     const tc::SBar h_in = hand + (((grp + kGroups - 1) % kGroups) * 4 + wq);  // predecessor
     const tc::SBar h_out = hand + (grp * 4 + wq);
@@ -737,38 +847,56 @@ attn_tc_kernel(const TcParams p) {
     float l = 0.f, m_used = -INFINITY;  // this group's partial sum, at max m_used
     float m_init = -INFINITY;           // running max at the item start (key-window passes)
     Item qi{};  // only i0 / rend / h used by rotate_q
-    if (grp == kGroups - 1 && lane == 0) tc::mbar_arrive(h_out);  // DT 0 has no predecessor
-    auto rotate_row = [&](int pattern) {
-      rotate_q(p, qi, pattern, r, 0, tmem + lane_base);
-      rotate_q(p, qi, pattern, r, 1, tmem + lane_base);
+    if (!kSplitO && grp == kGroups - 1 && lane == 0) tc::mbar_arrive(h_out);  // tile 0
+    auto rotate_row = [&](int pattern, int qbuf) {
+      rotate_q(p, qi, pattern, r, 0, tmem + lane_base, qbuf);
+      rotate_q(p, qi, pattern, r, 1, tmem + lane_base, qbuf);
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(q_ready);
+      if (lane == 0) tc::mbar_arrive(q_ready + qbuf);
     };
+#ifdef LCX_TC_WAITPROF
+    long long t_own = 0;  // start of the last own tile
+#endif
     for (;;) {
       const int slot = M % kMetaSlots;
       WAITP(0, tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1));
-      const DtMeta& mt = metas[slot];
+#ifdef LCX_TC_WAITPROF
+      const long long t_meta = clock64();
+#endif
+      const TileMeta& mt = metas[slot];
       const int kind = mt.kind, flags = mt.flags;
-      if (kind == T_END) {
-        if (T > 0 && (T - 1) % kGroups != uint32_t(grp))
-          tc::mbar_wait(lpub + int((T - 1) % kGroups), ((T - 1) / kGroups) & 1);
-        break;
-      }
+      if (kind == T_END) break;
       const int64_t i0 = mt.i0, rend = mt.rend;
       const int h = mt.h;
       const int64_t i = i0 + r;
       const bool row_ok = i < rend;
       const bool mine = kind != T_EMPTY && T % kGroups == uint32_t(grp);
-      const int nsub = mt.nsub;
-      uint64_t mask0 = 0, mask1 = 0;
+      uint64_t mask = 0;
       if (mine && row_ok) {
-        mask0 = sub_mask(mt.sub[0], i);
-        if (nsub > 1) mask1 = sub_mask(mt.sub[1], i);
+        if (kind == T_VERT) {
+          int cnt = mt.nfar;
+          while (cnt < mt.count) {
+            const int32_t kk = mt.keys[cnt];
+            if (kk < 0 || int64_t(kk) > i) break;
+            ++cnt;
+          }
+          mask = cnt >= 64 ? ~0ull : ((1ull << cnt) - 1);
+        } else if (kind == T_SLASH) {
+          const int off = int(i - mt.key0 - 63 - mt.sbase);
+          mask = __brevll(window64(mt.sw, off)) & ~mt.vmask;
+        } else {
+          const int64_t lim = i - mt.key0;
+          mask = lim >= 63 ? ~0ull : (lim < 0 ? 0ull : ((2ull << lim) - 1));
+        }
       }
-      const int pattern = mt.pattern, next_pattern = mt.next_pattern;
+      const int pattern = mt.pattern, tgrp = mt.grp, ng = mt.ng, next_pattern = mt.next_pattern;
+      const int gpat1 = mt.gpat[1], gpat2 = mt.gpat[2];
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(m_empty + slot);
+#ifdef LCX_TC_WAITPROF
+      wacc[3] += clock64() - t_meta;
+#endif
       ++M;
       if (kind == T_EMPTY) {
         if (grp == 0 && row_ok && !p.init) {  // init passes keep the running state
@@ -782,6 +910,7 @@ attn_tc_kernel(const TcParams p) {
         l = 0.f;
         m_used = -INFINITY;
         T_first = T;
+        J_cur = J++;
         qi.i0 = i0;
         qi.rend = rend;
         qi.h = h;
@@ -790,20 +919,32 @@ attn_tc_kernel(const TcParams p) {
         ++T;
         continue;
       }
-      const uint32_t k = T / kGroups;  // this group's DT index (hand-off phase)
-      if (flags & F_FIRST) {
-        // the previous item's last DT (T - 1, the other group) finished its epilogue: O is
-        // read and S(T - 1) consumed, so O / Q of this CTA's TMEM are free
-        WAITP(2, tc::mbar_wait(h_in, k & 1));
+#ifdef LCX_TC_WAITPROF
+      const long long t_first = clock64();
+      t_own = t_first;
+#endif
+      const uint32_t k = T / kGroups;  // this group's tile index (hand-off phase)
+      if (kSplitO && T - T_first < uint32_t(kGroups) && J_cur > 0) {
+        // this group's first tile of the item: the previous item's epilogue has read both
+        // O (this group's next PV overwrites its O) and its QKs are done (Q is free)
+        tc::mbar_wait(edone, (J_cur - 1) & 1);
         tc::tc_fence_after();
+      }
+      if (flags & F_FIRST) {
+        // the previous item's last tile (T - 1, another group) finished its epilogue: O is
+        // read and S(T - 1) consumed, so O / Q of this CTA's TMEM are free
+        if constexpr (!kSplitO) {
+          tc::mbar_wait(h_in, k & 1);
+          tc::tc_fence_after();
+        }
         m_init = -INFINITY;
         if (p.init) {
           // key-window pass > 0: continue from the row's running (o, lse) -- O goes back
           // into TMEM (the previous item's last PV completed before its epilogue read O)
           const float lp = row_ok ? p.lse[int64_t(h) * p.lse_stride + i] : -INFINITY;
-          const bool alive = lp != -INFINITY;
-          m_init = alive ? lp * 1.4426950408889634f : -INFINITY;
-          l = alive ? 1.f : 0.f;
+          const bool live = lp != -INFINITY;
+          m_init = live ? lp * 1.4426950408889634f : -INFINITY;
+          l = live ? 1.f : 0.f;
           m_used = m_init;
           const float4* o = reinterpret_cast<const float4*>(p.out + (i * p.hq + h) * int64_t(HD));
 #pragma unroll 1
@@ -811,76 +952,124 @@ attn_tc_kernel(const TcParams p) {
             float ov[32];
 #pragma unroll
             for (int x = 0; x < 8; ++x) {
-              const float4 v = alive ? o[q4 * 8 + x] : make_float4(0.f, 0.f, 0.f, 0.f);
+              const float4 v = live ? o[q4 * 8 + x] : make_float4(0.f, 0.f, 0.f, 0.f);
               ov[4 * x] = v.x;
               ov[4 * x + 1] = v.y;
               ov[4 * x + 2] = v.z;
               ov[4 * x + 3] = v.w;
             }
-            tc::tmem_st32(tmem + lane_base + COL_O + q4 * 32, ov);
+            tc::tmem_st32(tmem + lane_base + col_o + q4 * 32, ov);
           }
           tc::tmem_wait_st();
         }
-        rotate_row(pattern);
+        // group 0's Q, and group 1's into the other buffer ahead of its first QK
+        if constexpr (kQBufs == 2) {
+          rotate_row(pattern, tgrp & 1);
+          if (tgrp + 1 < ng) rotate_row(gpat1, (tgrp + 1) & 1);
+        } else {
+          rotate_row(pattern, 0);
+        }
       }
+#ifdef LCX_TC_WAITPROF
+      wacc[2] += clock64() - t_first;  // item start: hand-over wait, O restore, Q rotations
+#endif
       const int b = T % NS;
       const uint32_t ph = (T / NS) & 1;
-      const uint32_t sb = tmem + lane_base + COL_S + b * DTN;  // this row's S / P of the DT
-      float sv[64];
+      float sv[kSReread ? 32 : 64];
       WAITP(1, tc::mbar_wait(s_full + b, ph));
       tc::tc_fence_after();
-      // the DT's QKs (and every earlier one) are complete: Q takes the next pattern
-      if (flags & F_EPOCH_AFTER) rotate_row(next_pattern);
-      // masked logits -> -inf (ex2(-inf) = 0), already in log2 units
-      auto load_half = [&](int j, uint64_t mk) {
-        tc::tmem_ld32(sb + j * BN, sv);
-        tc::tmem_ld32_wait(sb + j * BN + 32, sv + 32);
+      if constexpr (!kSReread) {
+        tc::tmem_ld32(tmem + lane_base + b * BN, sv);
+        tc::tmem_ld32_wait(tmem + lane_base + b * BN + 32, sv + 32);
         tc::tmem_wait_ld_dep32(sv);
-        if (!__all_sync(0xffffffffu, mk == ~0ull)) {
-          const uint32_t lo = uint32_t(mk), hi = uint32_t(mk >> 32);
+      }
+#ifdef LCX_TC_TRACE_SM  // owner group's quadrant-0 warp: 5 S got, 0 m handed over, 6 P put
+      if (wq == 0 && lane == 0) trace_mark(p, T, 5);
+#else
+      if (threadIdx.x == 0) trace_mark(p, T, 5);
+#endif
+#ifdef LCX_TC_WAITPROF
+      const long long t_sg = clock64();
+#endif
+      // the group's QKs are complete: its Q buffer takes the group after next
+      if constexpr (kQBufs == 2) {
+        if ((flags & F_EPOCH_AFTER) && tgrp + 2 < ng) rotate_row(gpat2, tgrp & 1);
+      } else {
+        if (flags & F_EPOCH_AFTER) rotate_row(next_pattern, 0);  // old pattern's QKs done
+      }
+#ifdef LCX_TC_FAKE_SOFTMAX  // timing experiment only: no softmax math
+      for (int cc = 0; cc < int(sizeof(sv) / sizeof(float)); ++cc) sv[cc] = -INFINITY;
+      mask = 0ull;
+#endif
+      // masked logits -> -inf (ex2(-inf) = 0), already in log2 units
+      const bool all_in = __all_sync(0xffffffffu, mask == ~0ull);  // no select needed
+      if constexpr (!kSReread) {
+        if (!all_in) {
+          const uint32_t lo = uint32_t(mask), hi = uint32_t(mask >> 32);
 #pragma unroll
           for (int cc = 0; cc < 32; ++cc) {
             sv[cc] = ((lo >> cc) & 1u) ? sv[cc] : -INFINITY;
             sv[32 + cc] = ((hi >> cc) & 1u) ? sv[32 + cc] : -INFINITY;
           }
         }
-      };
-      auto half_max = [&]() -> float {
-        float t4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-        for (int cc = 0; cc < 64; cc += 8)
-#pragma unroll
-          for (int u = 0; u < 4; ++u) t4[u] = fmaxf(t4[u], fmaxf(sv[cc + u], sv[cc + 4 + u]));
-        return fmaxf(fmaxf(t4[0], t4[1]), fmaxf(t4[2], t4[3]));
-      };
-      // ---- P = exp2(x - m) in fp16, written over half j's S columns in TMEM: key c ->
-      // column c / 2 (two fp16 per 32-bit column).  Packed f32x2 subtract / accumulate
-      // (FADD2): half the FP32 instructions per key.  Returns the half's row sum.
-      auto exps_store = [&](int j, float m) -> float {
+      }
+      // ---- P = exp2(x - m) in fp16, written over the tile's S columns in TMEM:
+      // key c -> column c / 2 (two fp16 per 32-bit column).  Packed f32x2 subtract /
+      // accumulate (FADD2): half the FP32 instructions per key.  Returns the row sum.
+      auto exps_store = [&](float m) -> float {
         const float mm = m == -INFINITY ? 0.f : m;
         const float2 nm2 = make_float2(-mm, -mm);
         float2 rs2 = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
+        for (int hf = 0; hf < 2; ++hf) {  // two 32-key halves: fewer live registers
+          if constexpr (kSReread) {  // second read of this half (its P not yet written)
+            tc::tmem_ld32_wait(tmem + lane_base + b * BN + hf * 32, sv);
+            const uint32_t mb = uint32_t(mask >> (32 * hf));
+#pragma unroll
+            for (int cc = 0; cc < 32; ++cc) sv[cc] = ((mb >> cc) & 1u) ? sv[cc] : -INFINITY;
+          }
           uint32_t pw[16];
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const int c = hf * 32 + 2 * q;
+          for (int k = 0; k < 16; ++k) {
+            const int c = (kSReread ? 0 : hf * 32) + 2 * k;
             const float2 x = __fadd2_rn(make_float2(sv[c], sv[c + 1]), nm2);
             const float2 pp = make_float2(ex2(x.x), ex2(x.y));
             rs2 = __fadd2_rn(rs2, pp);
             const __half2 h2 = __floats2half2_rn(pp.x, pp.y);
-            pw[q] = *reinterpret_cast<const uint32_t*>(&h2);
+            pw[k] = *reinterpret_cast<const uint32_t*>(&h2);
           }
-          tc::tmem_st16(sb + j * BN + hf * 16, pw);
+          tc::tmem_st16(tmem + lane_base + b * BN + hf * 16, pw);
         }
         return rs2.x + rs2.y;
+      };
+      auto tile_max = [&]() -> float {
+        float t4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        if constexpr (!kSReread) {
+#pragma unroll
+          for (int cc = 0; cc < 64; cc += 8)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) t4[u] = fmaxf(t4[u], fmaxf(sv[cc + u], sv[cc + 4 + u]));
+        } else {
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            tc::tmem_ld32_wait(tmem + lane_base + b * BN + hf * 32, sv);
+            const uint32_t mb = uint32_t(mask >> (32 * hf));
+#pragma unroll
+            for (int cc = 0; cc < 32; ++cc) sv[cc] = ((mb >> cc) & 1u) ? sv[cc] : -INFINITY;
+#pragma unroll
+            for (int cc = 0; cc < 32; cc += 8)
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                t4[u] = fmaxf(t4[u], fmaxf(sv[cc + u], sv[cc + 4 + u]));
+          }
+        }
+        return fmaxf(fmaxf(t4[0], t4[1]), fmaxf(t4[2], t4[3]));
       };
       auto rescale_o = [&](float f) {
 #pragma unroll 1
         for (int q8 = 0; q8 < 8; ++q8) {  // 16 columns at a time: S is still live here
           float ov[16];
-          const uint32_t ta = tmem + lane_base + COL_O + q8 * 16;
+          const uint32_t ta = tmem + lane_base + col_o + q8 * 16;
           tc::tmem_ld16_wait(ta, ov);
 #pragma unroll
           for (int x = 0; x < 16; ++x) ov[x] *= f;
@@ -888,45 +1077,73 @@ attn_tc_kernel(const TcParams p) {
         }
         tc::tmem_wait_st();
       };
-      // ---- DT max: half 1 (if any) stays in registers for its exponentials
-      load_half(0, mask0);
-      float tmax = half_max();
-      if (nsub > 1) {
-        load_half(1, mask1);
-        tmax = fmaxf(tmax, half_max());
-      }
-      // ---- running max: the previous DT's (other group) unless the item starts here
-      if (!(flags & F_FIRST)) WAITP(3, tc::mbar_wait(h_in, k & 1));
-      const float m_prev =
-          (flags & F_FIRST) ? m_init : mbuf[((T + kGroups - 1) % kGroups) * 128 + r];
+      float rs;
+      if (kSplitO && kSpecExp && __all_sync(0xffffffffu, m_used != -INFINITY)) {
+        // split O: the group's own running max is known before the tile -- exponentiate
+        // at it straight away, independent of the tile max; only when some row's max
+        // moved past the threshold (rare after an item's first tiles) rescale and redo.
+        // The P written is the same as max-first would write.
+        rs = exps_store(m_used);
+        const float tmax = tile_max();
+        const bool need = tmax > m_used + kRescaleThresh;
+        if (__any_sync(0xffffffffu, need)) {
+          const float m = need ? tmax : m_used;
+          rescale_o(need ? ex2(m_used - m) : 1.f);  // own last PV done (S(T) is full)
+          if (need) l *= ex2(m_used - m);
+          m_used = m;
+          tc::tmem_wait_st();  // the speculative P stores land before their rewrite
+          rs = exps_store(m);
+        }
+#ifdef LCX_TC_WAITPROF
+        wacc[5] += clock64() - t_sg;
+#endif
+      } else {
+      const float tmax = tile_max();
+#ifdef LCX_TC_WAITPROF
+      wacc[5] += clock64() - t_sg;
+#endif
+      // ---- running max: previous tile's (other group) unless the item starts here
+      if (!kSplitO && !(flags & F_FIRST)) tc::mbar_wait(h_in, k & 1);
+      const float m_prev = kSplitO ? m_used
+                           : (flags & F_FIRST) ? m_init
+                                               : mbuf[((T + kGroups - 1) % kGroups) * 128 + r];
       // lazy rescale: the max moves only past a threshold (P <= 2^8 in fp16)
       const bool need = tmax > m_prev + kRescaleThresh;
       const float m = need ? tmax : m_prev;
-      mbuf[grp * 128 + r] = m;
-      // an item's last DT hands over only after its epilogue (next item's O / Q)
-      if (!(flags & F_LAST)) {
+      if constexpr (!kSplitO) mbuf[grp * 128 + r] = m;
+#ifdef LCX_TC_TRACE_SM  // column 1: flags | kind << 8 | rescale << 12 (a value, not a time)
+      if (wq == 0 && lane == 0) {
+        trace_mark(p, T, 0);
+        const bool any_need = __any_sync(0x1u, need && m_prev != -INFINITY);
+        if (p.trace && blockIdx.x == 0 && T < kTraceTiles)
+          p.trace[T * 8 + 1] = flags | (kind << 8) | (int(any_need) << 12);
+      }
+#endif
+      // an item's last tile hands over only after its epilogue (next item's O / Q)
+      if (!kSplitO && !(flags & F_LAST)) {
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(h_out);
       }
       if (__any_sync(0xffffffffu, need && m_prev != -INFINITY)) {
-        // O holds PV up to DT T - 1 at max m_prev: complete it, then rescale
-        const uint32_t Tp = T - 1;
-        WAITP(4, tc::mbar_wait(s_free + (Tp % NS), (Tp / NS) & 1));
-        tc::tc_fence_after();
+        // O holds PV up to tile T - 1 at max m_prev: complete it, then rescale
+        // (split O: this group's last PV, T - kGroups, completed before QK(T) took its S
+        // buffer)
+        if constexpr (!kSplitO) {
+          const uint32_t Tp = T - 1;
+          tc::mbar_wait(s_free + (Tp % NS), (Tp / NS) & 1);
+          tc::tc_fence_after();
+        }
         rescale_o((need && m_prev != -INFINITY) ? ex2(m_prev - m) : 1.f);
       }
       if (m != m_used) {  // this group's partial sum follows the row max
         if (m_used != -INFINITY) l *= ex2(m_used - m);
         m_used = m;
       }
-      float rs;
-      if (nsub > 1) {
-        rs = exps_store(1, m);
-        load_half(0, mask0);  // half 0 again (its S columns are untouched so far)
-        rs += exps_store(0, m);
-      } else {
-        rs = exps_store(0, m);
+      rs = exps_store(m);
       }
+#ifdef LCX_TC_WAITPROF
+      const long long t_ex = clock64();
+#endif
       tc::tmem_wait_st();
       l += rs;
       // partial (l, m) for the item's epilogue (ordered before the P release below)
@@ -937,22 +1154,79 @@ attn_tc_kernel(const TcParams p) {
         tc::mbar_arrive(p_full + b);
         tc::mbar_arrive(lpub + grp);
       }
-      // every phase of the other group's partial-sum barrier is waited on: DT T - 1's here,
-      // once this DT's P is out (it was published long before); the CTA's last DT at T_END
-      if (T > 0) {
-        const uint32_t To = T - 1;
-        WAITP(5, tc::mbar_wait(lpub + int(To % kGroups), (To / kGroups) & 1));
-      }
-      if (flags & F_LAST) {
+#ifdef LCX_TC_WAITPROF
+      wacc[6] += clock64() - t_ex;
+#endif
+#ifdef LCX_TC_TRACE_SM
+      if (wq == 0 && lane == 0) trace_mark(p, T, 6);
+#else
+      if (threadIdx.x == 0) trace_mark(p, T, 6);
+#endif
+      if (kSplitO && (flags & F_LAST)) {
+        // ---- epilogue (split O): merge the other group's O (its last tile T - 1) into
+        // this group's, normalize, store; then release both O for the next item ----
+        float sx = l > 0.f ? 1.f : 0.f, sy = 0.f, ly = 0.f, mt = m_used;
+        const bool other = T > T_first;
+        if (other) {
+          const uint32_t To = T - 1, go = To % kGroups, ko = To / kGroups;
+          tc::mbar_wait(lpub + int(go), ko & 1);
+          const float2 lo = lbuf[((ko & 1) * kGroups + go) * 128 + r];
+          ly = lo.x;
+          if (lo.x > 0.f) {
+            if (l > 0.f) {
+              mt = fmaxf(m_used, lo.y);
+              sx = ex2(m_used - mt);
+              sy = ex2(lo.y - mt);
+            } else {
+              mt = lo.y;
+              sy = 1.f;
+            }
+          }
+        }
+        const float lt = l * sx + ly * sy;
+        tc::mbar_wait(s_free + b, ph);  // PV(T) complete, and every PV before it
+        tc::tc_fence_after();
+        const float inv = lt > 0.f ? 1.f / lt : 0.f;
+        const float ax = sx * inv, ay = sy * inv;
+        const uint32_t col_y = COL_O + uint32_t((grp + 1) % kGroups) * HD;
+        float4* o = reinterpret_cast<float4*>(p.out + (i * p.hq + h) * int64_t(HD));
+#pragma unroll 1
+        for (int q8 = 0; q8 < 8; ++q8) {
+          float ov[16], oy[16];
+          tc::tmem_ld16_wait(tmem + lane_base + col_o + q8 * 16, ov);
+          if (other) tc::tmem_ld16_wait(tmem + lane_base + col_y + q8 * 16, oy);
+          if (!other) {
+#pragma unroll
+            for (int x = 0; x < 16; ++x) oy[x] = 0.f;
+          }
+          if (row_ok) {
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+              o[q8 * 4 + x] = make_float4(ov[4 * x] * ax + oy[4 * x] * ay,
+                                          ov[4 * x + 1] * ax + oy[4 * x + 1] * ay,
+                                          ov[4 * x + 2] * ax + oy[4 * x + 2] * ay,
+                                          ov[4 * x + 3] * ax + oy[4 * x + 3] * ay);
+          }
+        }
+        if (row_ok)
+          p.lse[int64_t(h) * p.lse_stride + i] =
+              lt > 0.f ? (mt + log2f(lt)) * 0.69314718055994530942f : -INFINITY;
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(edone);
+      } else if (flags & F_LAST) {
         // ---- epilogue: add the other group's partial sum, wait for the last PV,
         // normalize, store ----
         float lt = l;
-        if (T > T_first) {  // the other group's last DT of this item (T - 1)
-          const uint32_t To = T - 1, go = To % kGroups, ko = To / kGroups;
+#pragma unroll
+        for (uint32_t d = 1; d < uint32_t(kGroups); ++d) {  // the other groups' last tiles
+          if (T < T_first + d) break;
+          const uint32_t To = T - d, go = To % kGroups, ko = To / kGroups;
+          tc::mbar_wait(lpub + int(go), ko & 1);
           const float2 lo = lbuf[((ko & 1) * kGroups + go) * 128 + r];
           if (lo.x > 0.f) lt += lo.x * ex2(lo.y - m_used);
         }
-        WAITP(6, tc::mbar_wait(s_free + b, ph));  // this item's last PV is complete
+        tc::mbar_wait(s_free + b, ph);  // this item's last PV is complete
         tc::tc_fence_after();
         const float inv = lt > 0.f ? 1.f / lt : 0.f;
         float4* o = reinterpret_cast<float4*>(p.out + (i * p.hq + h) * int64_t(HD));
@@ -973,13 +1247,17 @@ attn_tc_kernel(const TcParams p) {
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(h_out);
+
       }
+#ifdef LCX_TC_WAITPROF
+      wacc[4] += clock64() - t_own;  // whole own tile, item start to P release / epilogue
+#endif
       ++T;
     }
 #ifdef LCX_TC_WAITPROF
     wacc[7] = clock64() - t_start;
 #endif
-    if (wq == 0) WAITP_FLUSH(4 + grp);
+    if (wq == 0) WAITP_FLUSH(4);
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -1432,7 +1710,6 @@ int tc_attention(const TcParams& p, const TcBuffers& B, int sm_count, cudaStream
     attr = true;
   }
   if (p.nitems <= 0) return LCX_OK;
-  if (!p.item_counter) return fail(LCX_ERR_INTERNAL, "tcgen05 attention needs an item counter");
   const int grid = std::min(p.nitems, sm_count);
   plan_items_kernel<<<(p.nitems + 127) / 128, 128, 0, st>>>(p, reinterpret_cast<Item*>(p.plans));
   LCX_CHECK_LAUNCH();
@@ -1443,7 +1720,8 @@ int tc_attention(const TcParams& p, const TcBuffers& B, int sm_count, cudaStream
   q.kclo = B.kclo;
   q.vt = B.vt;
   q.vct = B.vct;
-  attn_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(q);
+  attn_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(q, B.m_khi, B.m_klo, B.m_vt, B.m_kchi,
+                                                     B.m_kclo, B.m_vct);
   LCX_CHECK_LAUNCH();
   return LCX_OK;
 }

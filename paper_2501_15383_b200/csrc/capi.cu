@@ -1151,6 +1151,10 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
       LCX_TRY(estimate_simt(ctx, es, a2, st));
       if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[1], st));
       const int neh = eh1 - eh0;
+      if (!do_attend) {  // select phase: this call's head slots are written whole, padding 0
+        LCX_CHECK_CUDA(cudaMemsetAsync(vlist + eh0 * cap_v, 0, sizeof(int32_t) * neh * cap_v, st));
+        LCX_CHECK_CUDA(cudaMemsetAsync(slist + eh0 * cap_s, 0, sizeof(int32_t) * neh * cap_s, st));
+      }
       LCX_TRY(select_lines(col + int64_t(eh0) * t1, neh, t1, cfg->budget_vertical,
                            cfg->opts.force_sink_column, 1, vlist + eh0 * cap_v, vcnt + eh0,
                            cap_v, st));

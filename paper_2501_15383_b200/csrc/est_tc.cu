@@ -9,13 +9,16 @@
 //
 // The two matmul passes (pass 1: per-row max / sum-exp; pass 2: probabilities reduced
 // into column and diagonal partials) run on the tensor cores with fp32-level accuracy:
-// the fp32-rotated operands are split into three bf16 terms (x = h + m + l, 24
-// significant bits) and the six products of order <= 2^-16 are accumulated in fp32
-// TMEM (hh, hm, mh, hl, lh, mm; the far region's raw keys are exact in bf16, so it
-// needs three).  A CTA owns one pair of query heads of one KV head (M = 128 = 2 x 64
-// estimator rows, its Q terms resident in shared memory) and a range of 64-key tiles
-// streamed by TMA (N = 64); tiles whose rows straddle the near / far boundary go to the
-// CUDA-core kernel (at most two per chunk).
+// the fp32-rotated operands are scaled by a power of two (one exponent per query row and
+// per 64-key tile, so the largest magnitude sits in [2^14, 2^15): exact, and far from the
+// fp16 overflow and subnormal ranges) and split into two fp16 terms (x = h + l, 22
+// significant bits); the three products of order >= 2^-11 (hh, hl, lh) are accumulated
+// in fp32 TMEM and the power-of-two factors come off in the epilogue with the logit
+// scale.  The far region's raw keys are exact in fp16 after the scaling (bf16 has 8
+// significant bits) and need two products (h., l.).  A CTA owns one pair of query heads
+// of one KV head (M = 128 = 2 x 64 estimator rows, its Q terms resident in TMEM) and a
+// range of 64-key tiles streamed by TMA (N = 64); tiles whose rows straddle the near /
+// far boundary go to the CUDA-core kernel (at most two per chunk).
 //
 // Warp roles (384 threads): warp 0 TMA producer, warp 1 MMA issuer + TMEM owner,
 // warps 4-11 epilogue (TMEM lane quadrant = warp % 4, column half = (warp - 4) / 4).
@@ -39,20 +42,27 @@ constexpr int BN = 64;             // keys per tile
 constexpr int kEstPieces = LCX_EST_PIECES;  // tensor-core pieces per head pair (see est_tc_plan)
 constexpr int kQBox = 128 * 64 * 2;   // one [128 rows][64 dims] bf16 box = 16 KB
 constexpr int kKBox = 64 * 64 * 2;    // one [64 keys][64 dims] box = 8 KB
-constexpr int kQBytes = 6 * kQBox;    // 3 terms x 2 halves = 96 KB
-constexpr int kKStage = 6 * kKBox;    // near: 3 terms x 2 halves = 48 KB
-constexpr int NKS = 2;          // K stages in the K region
-constexpr int NKS_MAX = 4;      // pass 1 adds two stages in the Q staging area once Q is in TMEM
-constexpr int OFF_Q = 0;     // Q terms (TMA), then reused: pass-2 transposes [2][128][65]
-constexpr int OFF_K = OFF_Q + kQBytes;
-constexpr int OFF_BAR = OFF_K + NKS * kKStage;
+constexpr int kQTerms = 2;
+constexpr int kQBytes = 2 * kQTerms * kQBox;  // 2 terms x 2 halves = 64 KB
+// K tile parts in the key buffer: rotated hi, rotated lo, raw (far region), 2 halves each
+constexpr int kKParts = 3;
+constexpr int kKStage = 4 * kKBox;    // near: 2 terms x 2 halves = 32 KB (far: raw, 16 KB)
 constexpr int kTBuf = 128 * 65;                   // floats per transpose buffer
-static_assert(2 * kTBuf * 4 <= kQBytes, "transpose buffers must fit the Q staging area");
+// Q staging area: Q terms (TMA), then reused: pass-2 transposes [2][128][65] (pass 1:
+// two more K stages)
+constexpr int kQArea = ((2 * kTBuf * 4 > kQBytes ? 2 * kTBuf * 4 : kQBytes) + 1023) / 1024 * 1024;
+constexpr int NKS = 4;          // K stages in the K region
+constexpr int NKS_MAX = 6;      // pass 1 adds two stages in the Q staging area once Q is in TMEM
+static_assert(2 * kKStage <= kQArea, "pass-1 extra stages must fit the Q staging area");
+constexpr int OFF_Q = 0;
+constexpr int OFF_K = OFF_Q + kQArea;
+constexpr int OFF_BAR = OFF_K + NKS * kKStage;
 constexpr int NSB = 4;                            // S buffers in TMEM
-constexpr uint32_t QCOL = NSB * BN;               // TMEM: S [0, 256), Q terms [256, 448)
+constexpr uint32_t QCOL = NSB * BN;               // TMEM: S [0, 256), Q terms [256, 384)
 constexpr int kSmem = OFF_BAR + 256 + 1024;
+static_assert(kSmem <= 227 * 1024, "shared memory");
 constexpr int kThreads = 384;
-constexpr uint32_t IDESC = tc::idesc_f16(128, BN, 1, 1);
+constexpr uint32_t IDESC = tc::idesc_f16(128, BN, 0, 0);  // fp16 x fp16
 
 struct Item {
   int pair;      // head pair index
@@ -91,8 +101,8 @@ __device__ __forceinline__ float ex2(float x) {
 
 template <int PASS>
 __global__ void __launch_bounds__(kThreads, 1)
-est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_k3,
-              const __grid_constant__ CUtensorMap map_kraw) {
+est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q,
+              const __grid_constant__ CUtensorMap map_k3) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
@@ -140,7 +150,7 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
       // resident Q terms of the pair (near: rope(q, gi); far: rope(q, c - 1))
       tc::mbar_expect_tx(q_full, kQBytes);
       const int qbox0 = ((it.far * p.npairs + it.pair) * 6);
-      for (int b = 0; b < 6; ++b)
+      for (int b = 0; b < 2 * kQTerms; ++b)
         tc::tma_load_3d(smem + OFF_Q + b * kQBox, &map_q, q_full, 0, 0, qbox0 + b);
       for (int t = 0; t < ntl; ++t) {
         const int st = t % kStages;
@@ -148,14 +158,15 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
         if (st >= NKS && t < kStages) tc::mbar_wait(q_tmem, 0);  // Q staging area now free
         const int kt = it.t0 + t;
         uint8_t* dst = stage_ptr(st);
+        // key tile parts: [hi h0, hi h1, lo h0, lo h1, raw h0, raw h1]
+        const int b0 = int((int64_t(g) * p.ntiles_k + kt) * (2 * kKParts));
         if (it.far) {
           tc::mbar_expect_tx(k_full + st, 2 * kKBox);
-          tc::tma_load_3d(dst, &map_kraw, k_full + st, 0, g, kt * 64);
-          tc::tma_load_3d(dst + kKBox, &map_kraw, k_full + st, 64, g, kt * 64);
+          for (int b = 0; b < 2; ++b)
+            tc::tma_load_3d(dst + b * kKBox, &map_k3, k_full + st, 0, 0, b0 + 4 + b);
         } else {
-          tc::mbar_expect_tx(k_full + st, 6 * kKBox);
-          const int b0 = int((int64_t(g) * p.ntiles_k + kt) * 6);
-          for (int b = 0; b < 6; ++b)
+          tc::mbar_expect_tx(k_full + st, 4 * kKBox);
+          for (int b = 0; b < 4; ++b)
             tc::tma_load_3d(dst + b * kKBox, &map_k3, k_full + st, 0, 0, b0 + b);
         }
       }
@@ -164,8 +175,9 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
     // Q is the A operand from TMEM: with N = 64 an A operand in shared memory makes each
     // M128 N64 K16 MMA shared-memory-bound (48 vs 32 cycles, tools/micro/mma_rate.cu)
     tc::mbar_wait(q_tmem, 0);
-    // (q term, k term) products of order <= 2^-16: hh hm mh hl lh mm (near), h. m. l. (far)
-    const int qt_near[6] = {0, 0, 1, 0, 2, 1}, kt_near[6] = {0, 1, 0, 2, 0, 1};
+    // (q term, k term) products of order >= 2^-11: hh hl lh (near), h. l. (far, raw keys
+    // in stage part 0)
+    const int qt_near[3] = {0, 0, 1}, kt_near[3] = {0, 1, 0};
     for (int t = 0; t < ntl; ++t) {
       const int st = t % kStages, sb = t % NSB;
       tc::mbar_wait(k_full + st, (t / kStages) & 1);
@@ -173,7 +185,7 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
       tc::tc_fence_after();
       const uint64_t dk = tc::sdesc_sw128(tc::smem_u32(stage_ptr(st)));
       const uint32_t dS = tmem + sb * BN;
-      const int nprod = it.far ? 3 : 6;
+      const int nprod = it.far ? 2 : 3;
       for (int x = 0; x < nprod; ++x) {
         const int qt = it.far ? x : qt_near[x];
         const int kt = it.far ? 0 : kt_near[x];
@@ -203,11 +215,14 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
       rm = ms.x * 1.4426950408889634f;  // natural -> log2 domain
       rinv = ms.y > 0.f ? 1.f / ms.y : 0.f;
     }
-    const float sc = p.scale_log2;
+    // logit scale with this row's power-of-two Q factor; each tile adds its key factor
+    const float sc =
+        p.scale_log2 * p.qinv[(int64_t(it.far) * p.npairs + it.pair) * 128 + r];
+    const float* kinv = p.kinv + int64_t(g) * p.ntiles_k;
     {  // Q terms: shared memory (TMA, SW128) -> TMEM, this thread's row and dim half
       tc::mbar_wait(q_full, 0);
 #pragma unroll
-      for (int tm = 0; tm < 3; ++tm) {
+      for (int tm = 0; tm < kQTerms; ++tm) {
         const uint8_t* box = smem + OFF_Q + (tm * 2 + part) * kQBox;
         uint32_t w[32];
 #pragma unroll
@@ -241,11 +256,12 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
       // valid columns of this row: c < nvalid (causal j <= gi, j < nk); int32 compares
       const int64_t lim = (gi < p.nk - 1 ? gi : p.nk - 1) - jb + 1;
       const int nvalid = !row_ok ? 0 : (lim >= 32 ? 32 : (lim < 0 ? 0 : int(lim)));
+      const float sct = sc * __ldg(kinv + it.t0 + t);
       if (PASS == 1) {
         float tmax = -INFINITY;
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
-          v[c] = c < nvalid ? v[c] * sc : -INFINITY;
+          v[c] = c < nvalid ? v[c] * sct : -INFINITY;
           tmax = fmaxf(tmax, v[c]);
         }
         if (tmax != -INFINITY) {
@@ -262,7 +278,7 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
         float* Tb = T + (t & 1) * kTBuf;
         float* Tr = Tb + r * 65 + part * 32;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) Tr[c] = c < nvalid ? ex2(fmaf(v[c], sc, -rm)) * rinv : 0.f;
+        for (int c = 0; c < 32; ++c) Tr[c] = c < nvalid ? ex2(fmaf(v[c], sct, -rm)) * rinv : 0.f;
         asm volatile("bar.sync 1, 256;" ::: "memory");
         const int et = threadIdx.x - 128;    // 0..255
         // column sums: thread et < 128 -> (head et / 64, key et % 64)
@@ -338,39 +354,84 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q, co
 }
 
 // ------------------------------------------------------------- prep --
-// K3 [hkv][ntiles][3 terms][2 halves][64 keys][64 dims] = split(rope(k_j, j)), rows [r0, r1)
-__global__ void est_k3_kernel(const __nv_bfloat16* __restrict__ k, int64_t r0, int64_t r1,
-                              int hkv, int64_t ntiles, const float2* __restrict__ rope,
-                              __nv_bfloat16* __restrict__ k3) {
-  const int64_t idx = r0 * hkv * 64 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // pair
-  if (idx >= r1 * hkv * 64) return;
-  const int pr = int(idx & 63);
-  const int64_t rowhead = idx >> 6;
-  const int64_t j = rowhead / hkv;
-  const int gg = int(rowhead % hkv);
-  const float2 xy = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(k)[idx]);
-  const float2 cs = rope[j * 64 + pr];
-  const float rx = xy.x * cs.x - xy.y * cs.y, ry = xy.x * cs.y + xy.y * cs.x;
-  const int d = 2 * pr, half = d >> 6;
-  const __nv_bfloat162 h2 = __floats2bfloat162_rn(rx, ry);
-  const float2 hf = __bfloat1622float2(h2);
-  const __nv_bfloat162 m2 = __floats2bfloat162_rn(rx - hf.x, ry - hf.y);
-  const float2 mf = __bfloat1622float2(m2);
-  const __nv_bfloat162 l2 = __floats2bfloat162_rn(rx - hf.x - mf.x, ry - hf.y - mf.y);
-  const __nv_bfloat162 terms[3] = {h2, m2, l2};
+// Power-of-two scale putting the largest magnitude m of a block in [2^14, 2^15): fp16
+// terms then stay far from overflow (65504) and from the subnormal range.
+__device__ __forceinline__ int pow2_exp(float m) {
+  if (!(m > 0.f)) return 0;
+  int e = 14 - ilogbf(m);
+  return e < -120 ? -120 : (e > 120 ? 120 : e);
+}
+
+__device__ __forceinline__ float block_max256(float v, float* red) {
 #pragma unroll
-  for (int tm = 0; tm < 3; ++tm) {
-    const int64_t o = (((((int64_t(gg) * ntiles + (j >> 6)) * 3 + tm) * 2 + half) * 64 + (j & 63)) *
-                           64 + (d & 63)) >> 1;
-    reinterpret_cast<__nv_bfloat162*>(k3)[o] = terms[tm];
+  for (int o = 16; o >= 1; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float m = red[0];
+  for (int w = 1; w < int(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
+  return m;
+}
+
+// Key tiles [tile0, tile1) of KV head blockIdx.y, keys < r1 (the rest of the last tile
+// zero; a later call extending the keys rewrites that tile whole):
+//   K3 [hkv][ntiles][hi h0, hi h1, lo h0, lo h1, raw h0, raw h1][64 keys][64 dims] fp16
+//   hi + lo = rope(k_j, j) * 2^e, raw = k_j * 2^e (exact), kinv [hkv][ntiles] = 2^-e
+// with one exponent per tile (pow2_exp of the tile's largest rotated / raw magnitude).
+__global__ void __launch_bounds__(256) est_k3_kernel(const __nv_bfloat16* __restrict__ k,
+                                                     int64_t tile0, int64_t r1, int hkv,
+                                                     int64_t ntiles,
+                                                     const float2* __restrict__ rope,
+                                                     __half* __restrict__ k3,
+                                                     float* __restrict__ kinv) {
+  __shared__ float red[8];
+  const int64_t tile = tile0 + blockIdx.x;
+  const int gg = blockIdx.y;
+  constexpr int kPer = 64 * 64 / 256;  // (key, pair) elements per thread
+  float2 rot[kPer], raw[kPer];
+  float mx = 0.f;
+#pragma unroll
+  for (int x = 0; x < kPer; ++x) {
+    const int e = x * 256 + threadIdx.x;
+    const int jj = e >> 6, pr = e & 63;
+    const int64_t j = tile * 64 + jj;
+    float2 xy = make_float2(0.f, 0.f), rr = xy;
+    if (j < r1) {
+      xy = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(k)[(j * hkv + gg) * 64 + pr]);
+      const float2 cs = rope[j * 64 + pr];
+      rr = make_float2(xy.x * cs.x - xy.y * cs.y, xy.x * cs.y + xy.y * cs.x);
+    }
+    rot[x] = rr;
+    raw[x] = xy;
+    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(rr.x), fabsf(rr.y)), fmaxf(fabsf(xy.x), fabsf(xy.y))));
+  }
+  const int ex = pow2_exp(block_max256(mx, red));
+  if (threadIdx.x == 0) kinv[int64_t(gg) * ntiles + tile] = exp2f(float(-ex));
+  __half2* base = reinterpret_cast<__half2*>(k3 + (int64_t(gg) * ntiles + tile) * 6 * 64 * 64);
+#pragma unroll
+  for (int x = 0; x < kPer; ++x) {
+    const int e = x * 256 + threadIdx.x;
+    const int jj = e >> 6, pr = e & 63;
+    const int d = 2 * pr, half = d >> 6;
+    const float2 rs = make_float2(ldexpf(rot[x].x, ex), ldexpf(rot[x].y, ex));
+    const __half2 h2 = __floats2half2_rn(rs.x, rs.y);
+    const float2 hf = __half22float2(h2);
+    const __half2 l2 = __floats2half2_rn(rs.x - hf.x, rs.y - hf.y);
+    const __half2 w2 = __floats2half2_rn(ldexpf(raw[x].x, ex), ldexpf(raw[x].y, ex));
+    const int64_t o = (int64_t(jj) * 64 + (d & 63)) >> 1;  // within one [64][64] box
+    base[(0 + half) * 2048 + o] = h2;
+    base[(2 + half) * 2048 + o] = l2;
+    base[(4 + half) * 2048 + o] = w2;
   }
 }
 
-// Q3 [far 0/1][npairs][3 terms][2 halves][128 rows][64 dims]: row = 64 * (head in pair) + r
-__global__ void est_q3_kernel(const __nv_bfloat16* __restrict__ q, int hq, int group,
-                              int pairs_per_group, int npairs, int pair0, int64_t nk,
-                              int64_t block, int far_too, int64_t c,
-                              const float2* __restrict__ rope, __nv_bfloat16* __restrict__ q3) {
+// Q3 [far 0/1][npairs][2 terms][2 halves][128 rows][64 dims] fp16 (box stride: 6 boxes per
+// (far, pair)): row = 64 * (head in pair) + r, hi + lo = rope(q, pos) * 2^e with one
+// exponent per row; qinv [far][npairs][128] = 2^-e.
+__global__ void __launch_bounds__(64) est_q3_kernel(
+    const __nv_bfloat16* __restrict__ q, int hq, int group, int pairs_per_group, int npairs,
+    int pair0, int64_t nk, int64_t block, int far_too, int64_t c,
+    const float2* __restrict__ rope, __half* __restrict__ q3, float* __restrict__ qinv) {
+  __shared__ float red[2];
   const int row = blockIdx.x;        // 0..127
   const int pair = pair0 + int(blockIdx.y);
   const int far = blockIdx.z;
@@ -388,34 +449,53 @@ __global__ void est_q3_kernel(const __nv_bfloat16* __restrict__ q, int hq, int g
     rx = xy.x * cs.x - xy.y * cs.y;
     ry = xy.x * cs.y + xy.y * cs.x;
   }
-  const __nv_bfloat162 h2 = __floats2bfloat162_rn(rx, ry);
-  const float2 hf = __bfloat1622float2(h2);
-  const __nv_bfloat162 m2 = __floats2bfloat162_rn(rx - hf.x, ry - hf.y);
-  const float2 mf = __bfloat1622float2(m2);
-  const __nv_bfloat162 l2 = __floats2bfloat162_rn(rx - hf.x - mf.x, ry - hf.y - mf.y);
-  const __nv_bfloat162 terms[3] = {h2, m2, l2};
+  float m = fmaxf(fabsf(rx), fabsf(ry));
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((pr & 31) == 0) red[pr >> 5] = m;
+  __syncthreads();
+  const int ex = pow2_exp(fmaxf(red[0], red[1]));
+  if (pr == 0) qinv[(int64_t(far) * npairs + pair) * 128 + row] = exp2f(float(-ex));
+  rx = ldexpf(rx, ex);
+  ry = ldexpf(ry, ex);
+  const __half2 h2 = __floats2half2_rn(rx, ry);
+  const float2 hf = __half22float2(h2);
+  const __half2 l2 = __floats2half2_rn(rx - hf.x, ry - hf.y);
+  const __half2 terms[2] = {h2, l2};
   const int d = 2 * pr, half = d >> 6;
 #pragma unroll
-  for (int tm = 0; tm < 3; ++tm) {
-    const int64_t o = (((((int64_t(far) * npairs + pair) * 3 + tm) * 2 + half) * 128 + row) * 64 +
-                       (d & 63)) >> 1;
-    reinterpret_cast<__nv_bfloat162*>(q3)[o] = terms[tm];
+  for (int tm = 0; tm < 2; ++tm) {
+    const int64_t o = (((((int64_t(far) * npairs + pair) * 6 + tm * 2 + half) * 128 + row) * 64 +
+                        (d & 63))) >> 1;
+    reinterpret_cast<__half2*>(q3)[o] = terms[tm];
   }
 }
 
 }  // namespace
 
+// key tile parts (ntiles x hkv x 6 boxes), then the per-tile factors kinv [hkv][ntiles]
+static size_t k3_parts_bytes(int64_t ntiles, int hkv) {
+  return size_t(ntiles) * hkv * 2 * kKParts * kKBox;
+}
+
 size_t est_tc_k3_bytes(int64_t n, int hkv) {
-  return size_t((n + 63) / 64) * hkv * 6 * kKBox;
+  const int64_t nt = (n + 63) / 64;
+  return k3_parts_bytes(nt, hkv) + ((size_t(nt) * hkv * 4 + 255) & ~size_t(255));
+}
+
+static float* k3_kinv(const void* k3, int64_t ntiles, int hkv) {
+  return reinterpret_cast<float*>(const_cast<uint8_t*>(reinterpret_cast<const uint8_t*>(k3)) +
+                                  k3_parts_bytes(ntiles, hkv));
 }
 
 int est_tc_prepare_keys(const void* k, int64_t r0, int64_t r1, int hkv, int64_t ntiles,
                         const float2* rope, void* k3, cudaStream_t st) {
   if (r1 <= r0) return LCX_OK;
-  const int64_t pairs = (r1 - r0) * hkv * 64;
-  est_k3_kernel<<<unsigned((pairs + 255) / 256), 256, 0, st>>>(
-      reinterpret_cast<const __nv_bfloat16*>(k), r0, r1, hkv, ntiles, rope,
-      reinterpret_cast<__nv_bfloat16*>(k3));
+  // whole tiles: a tile that an earlier call left partial is rebuilt with all its keys
+  const int64_t tile0 = r0 / 64, tile1 = (r1 + 63) / 64;
+  est_k3_kernel<<<dim3(unsigned(tile1 - tile0), unsigned(hkv)), 256, 0, st>>>(
+      reinterpret_cast<const __nv_bfloat16*>(k), tile0, r1, hkv, ntiles, rope,
+      reinterpret_cast<__half*>(k3), k3_kinv(k3, ntiles, hkv));
   LCX_CHECK_LAUNCH();
   return LCX_OK;
 }
@@ -427,6 +507,7 @@ bool est_tc_eligible(int dtype, int dim, int64_t block) {
 void est_tc_size(int hq, int hkv, Sizer& sz) {
   const int group = hq / hkv, ppg = (group + 1) / 2, npairs = hkv * ppg;
   sz.take<uint8_t>(size_t(2) * npairs * 6 * kQBox);  // q3
+  sz.take<float>(size_t(2) * npairs * 128);          // qinv
 }
 
 int est_tc_max_splits() { return 2 * (kEstPieces + 2); }
@@ -479,22 +560,21 @@ int est_tc_run(const EstTcArgs& a, const EstTcPlan& pl, Arena& ar, cudaStream_t 
   }
   const int group = a.hq / a.hkv, ppg = (group + 1) / 2, npairs = pl.npairs;
   uint8_t* q3 = ar.take<uint8_t>(size_t(2) * npairs * 6 * kQBox);
+  float* qinv = ar.take<float>(size_t(2) * npairs * 128);
   if (pl.items == 0) return LCX_OK;
   const bool dca = a.pos_mode == 1;
   if (a.pass == 1) {  // operands: rotated, 3-term split query rows (near and far)
     dim3 grid(128, unsigned(pl.pair1 - pl.pair0), 2);
     est_q3_kernel<<<grid, 64, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(a.q), a.hq, group,
                                        ppg, npairs, pl.pair0, a.nk, a.block, dca ? 1 : 0, a.c,
-                                       a.rope, reinterpret_cast<__nv_bfloat16*>(q3));
+                                       a.rope, reinterpret_cast<__half*>(q3), qinv);
     LCX_CHECK_LAUNCH();
   }
-  CUtensorMap mq, mk3, mkr;
-  const auto BF = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
-  LCX_TRY(make_tmap3(&mq, BF, q3, 64, 128, uint64_t(2) * npairs * 6, 128, kQBox, 64, 128, 1));
-  LCX_TRY(make_tmap3(&mk3, BF, const_cast<void*>(a.k3), 64, 64, uint64_t(a.hkv) * a.k3_tiles * 6, 128, kKBox, 64,
-                     64, 1));
-  LCX_TRY(make_tmap3(&mkr, BF, const_cast<void*>(a.k), 128, uint64_t(a.hkv), uint64_t(a.nk), 256,
-                     uint64_t(a.hkv) * 256, 64, 1, 64));
+  CUtensorMap mq, mk3;
+  const auto F16 = CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  LCX_TRY(make_tmap3(&mq, F16, q3, 64, 128, uint64_t(2) * npairs * 6, 128, kQBox, 64, 128, 1));
+  LCX_TRY(make_tmap3(&mk3, F16, const_cast<void*>(a.k3), 64, 64,
+                     uint64_t(a.hkv) * a.k3_tiles * 2 * kKParts, 128, kKBox, 64, 64, 1));
   EstTcParams p{};
   p.group = group;
   p.pairs_per_group = ppg;
@@ -513,10 +593,12 @@ int est_tc_run(const EstTcArgs& a, const EstTcPlan& pl, Arena& ar, cudaStream_t 
   p.rowstat = a.rowstat;
   p.col_part = a.col_part;
   p.diag_part = a.diag_part;
+  p.qinv = qinv;
+  p.kinv = k3_kinv(a.k3, a.k3_tiles, a.hkv);
   if (a.pass == 1)
-    est_tc_kernel<1><<<unsigned(pl.items), kThreads, kSmem, st>>>(p, mq, mk3, mkr);
+    est_tc_kernel<1><<<unsigned(pl.items), kThreads, kSmem, st>>>(p, mq, mk3);
   else
-    est_tc_kernel<2><<<unsigned(pl.items), kThreads, kSmem, st>>>(p, mq, mk3, mkr);
+    est_tc_kernel<2><<<unsigned(pl.items), kThreads, kSmem, st>>>(p, mq, mk3);
   LCX_CHECK_LAUNCH();
   return LCX_OK;
 }

@@ -20,6 +20,8 @@ struct EstTcParams {
   const float2* rowstat;     // [hq][block]
   float* col_part;           // [hq][nk]
   float* diag_part;          // [hq][ntiles][128]
+  const float* qinv;         // [far][npairs][128] power-of-two factor of each Q row
+  const float* kinv;         // [hkv][ntiles_k] power-of-two factor of each key tile
 };
 
 struct EstTcArgs {
@@ -29,7 +31,7 @@ struct EstTcArgs {
   int pos_mode;
   int64_t c;
   const float2* rope;
-  const void* k3; int64_t k3_tiles;  // rotated 3-term keys (est_tc_prepare_keys)
+  const void* k3; int64_t k3_tiles;  // scaled fp16 key tiles (est_tc_prepare_keys)
   int sm_count;
   int h0, h1;                    // query heads of the call: pairs meeting [h0, h1)
   int pass;                      // 1 or 2

@@ -35,13 +35,19 @@ def check_selection(port, got_v, got_s, col32, sl32, col64, sl64, t1, block, bud
     assert list(got_v) == crit.verticals, "verticals differ from the ranking of own scores"
     assert list(got_s) == crit.slashes, "slashes differ from the ranking of own scores"
     ref = port.select_from_scores(col64, sl64, t1, block, budget, sink, band)
-    for got, want, score, k in ((got_v, ref.verticals, col64, budget[0]),
-                                (got_s, ref.slashes, sl64, budget[1])):
+    ties = []
+    for kind, got, want, score, k in (("vertical", got_v, ref.verticals, col64, budget[0]),
+                                      ("slash", got_s, ref.slashes, sl64, budget[1])):
         diff = set(got) ^ set(want)
         if not diff:
             continue
         finite = np.where(np.isfinite(score), score, -np.inf)
         thresh = np.sort(finite)[::-1][min(k, len(finite)) - 1]
         scale = np.abs(finite[np.isfinite(finite)]).max()
-        for x in diff:
+        for x in sorted(diff):
+            margin = abs(score[x] - thresh) / scale
+            ties.append({"line": kind, "index": int(x), "in_device": x in set(got),
+                         "score64": float(score[x]), "threshold64": float(thresh),
+                         "margin_rel_max": float(margin)})
             assert abs(score[x] - thresh) <= rel * scale, (x, score[x], thresh)
+    return ties

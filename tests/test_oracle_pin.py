@@ -173,3 +173,19 @@ def test_row_list_oracle_equals_whole_sequence_oracle(port, dca):
                   port.full_attention(q, k, v, dca=dca, temperature=0.8))
         ro, rl = port.attention_rows(q, k, v, rows, c, dca=dca, temperature=0.8)
         assert np.array_equal(ro, fo[rows]) and np.array_equal(rl, fl[rows])
+
+
+@pytest.mark.parametrize("pm,cfg", [(0, None), (1, (32, 96, 32)), (1, (6, 10, 4))])
+def test_fast_estimator_restatement_pinned(port, pm, cfg):
+    """oracle.estimate_probs_fast / line_scores_fast (the large-scale parity checker) equal
+    the per-entry C restatement of estimate_block + select_critical's line sums."""
+    from oracle import estimate_probs_fast, line_scores_fast
+    rng = np.random.default_rng(7)
+    n, dim, B = 300, 128, 64
+    q, k = rng.standard_normal((n, dim)), rng.standard_normal((n, dim))
+    ref = port.estimate_block(q[n - 100:], k, B, pm, cfg, 1e4)
+    got = estimate_probs_fast(q[n - B:], k, pm, cfg[1] if cfg else 0, 1e4)
+    assert np.abs(got - ref).max() <= 1e-13
+    c1, s1 = port.line_scores(ref, n)
+    c2, s2 = line_scores_fast(got)
+    assert np.abs(c1 - c2).max() <= 1e-12 and np.abs(s1 - s2).max() <= 1e-12
