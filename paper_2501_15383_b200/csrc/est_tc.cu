@@ -47,7 +47,8 @@ constexpr int kQBytes = 2 * kQTerms * kQBox;  // 2 terms x 2 halves = 64 KB
 // K tile parts in the key buffer: rotated hi, rotated lo, raw (far region), 2 halves each
 constexpr int kKParts = 3;
 constexpr int kKStage = 4 * kKBox;    // near: 2 terms x 2 halves = 32 KB (far: raw, 16 KB)
-constexpr int kTBuf = 128 * 65;                   // floats per transpose buffer
+constexpr int kTRow = 66;                         // floats per transpose row (bank skew)
+constexpr int kTBuf = 128 * kTRow;                // floats per transpose buffer
 // Q staging area: Q terms (TMA), then reused: pass-2 transposes [2][128][65] (pass 1:
 // two more K stages)
 constexpr int kQArea = ((2 * kTBuf * 4 > kQBytes ? 2 * kTBuf * 4 : kQBytes) + 1023) / 1024 * 1024;
@@ -72,14 +73,16 @@ struct Item {
 };
 
 // CTA -> (pair, phase, tile range): far tiles [0, far_end) then near tiles
-// [near_begin, ntiles), each cut into `per`-tile pieces; split = piece index of the pair
+// [near_begin, ntiles), each cut into `per`-tile pieces; split = piece index of the pair.
+// Piece-major order (the call's pairs fastest): the CTAs running together cover every
+// pair of a few pieces, so each key tile is fetched from DRAM once and served from L2 to
+// the other head pairs of its KV head.
 __device__ __forceinline__ Item decode_item(const EstTcParams& p, int idx) {
   const int nf = int((p.far_end + p.per - 1) / p.per);
   const int nn = int((p.ntiles - p.near_begin + p.per - 1) / p.per);
   Item it;
-  const int pl = idx / (nf + nn);
-  it.pair = p.pair0 + pl;
-  const int k = idx - pl * (nf + nn);
+  const int k = idx / p.ncall_pairs;
+  it.pair = p.pair0 + (idx - k * p.ncall_pairs);
   it.split = k;
   if (k < nf) {
     it.far = 1;
@@ -273,60 +276,55 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q,
           m = nm;
         }
       } else {
-        // double-buffered transpose: one barrier per tile (tile t + 2 rewrites this buffer
-        // only after every thread passed tile t + 1's barrier, i.e. finished reading it)
+        // double-buffered skewed transpose, one barrier per tile (tile t + 2 rewrites this
+        // buffer only after every thread passed tile t + 1's barrier, i.e. finished reading
+        // it): row rr of a head stores key c at column (c - rr) mod 64, so a column of the
+        // buffer holds the two diagonals -s and 64 - s (rows below / from 64 - s) and a key's
+        // column walks the rows at a fixed skew -- both conflict-free with a row stride of 66
+        // floats, every element read once per reduction.  Rows past the estimator block and
+        // masked keys are stored as 0, so every sum has a fixed trip count.
         float* Tb = T + (t & 1) * kTBuf;
-        float* Tr = Tb + r * 65 + part * 32;
+        {
+          float* Trow = Tb + r * kTRow;
+          const int rr64 = r & 63;
 #pragma unroll
-        for (int c = 0; c < 32; ++c) Tr[c] = c < nvalid ? ex2(fmaf(v[c], sct, -rm)) * rinv : 0.f;
+          for (int c = 0; c < 32; ++c)
+            Trow[(part * 32 + c - rr64) & 63] =
+                c < nvalid ? ex2(fmaf(v[c], sct, -rm)) * rinv : 0.f;
+        }
         asm volatile("bar.sync 1, 256;" ::: "memory");
         const int et = threadIdx.x - 128;    // 0..255
-        // column sums: thread et < 128 -> (head et / 64, key et % 64)
-        if (et < 128) {
-          const int ch = et >> 6, c = et & 63;
-          const int hc = g * p.group + (it.pair % p.pairs_per_group) * 2 + ch;
-          const int64_t j = j0 + c;
-          if ((it.pair % p.pairs_per_group) * 2 + ch < p.group && j < p.nk) {
-            float acc = 0.f;
-            const float* col = Tb + ch * 64 * 65 + c;
-            if (p.block == 64) {
-              float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 chains, all loads up front
-#pragma unroll
-              for (int q = 0; q < 64; q += 8)
-#pragma unroll
-                for (int u = 0; u < 8; ++u) a[u] += col[(q + u) * 65];
-              acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-            } else {
-              for (int q = 0; q < p.block; ++q) acc += col[q * 65];
-            }
-            p.col_part[int64_t(hc) * p.nk + j] = acc;
-          }
-        }
-        // diagonal sums: thread et -> (head et / 128, e = et % 128), e = r - c + 63
-        {
-          const int dh = et >> 7, e = et & 127;
-          const int hd = g * p.group + (it.pair % p.pairs_per_group) * 2 + dh;
-          if ((it.pair % p.pairs_per_group) * 2 + dh < p.group && e < 127) {
-            const int q0 = e > 63 ? e - 63 : 0;
-            const int q1 = min(p.block - 1, e);
-            // diagonal e walks T with stride 66 (= row 65 + column 1); zeros past the
-            // estimator rows make the fixed-count form exact.  Fixed trip count with
-            // predicated loads and adds (8 independent chains, every load in flight at
-            // once); nothing past the diagonal is read (it may be the other buffer, which
-            // the next tile's threads are writing).
-            const float* dg = Tb + (dh * 64 + q0) * 65 + (q0 - e + 63);
-            const int cnt = q1 - q0 + 1;
-            float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const int hh2 = (et >> 6) & 1;       // head of the pair
+        const int x = et & 63;               // key (et < 128) / buffer column (et >= 128)
+        const int hx = g * p.group + (it.pair % p.pairs_per_group) * 2 + hh2;
+        const bool hx_ok = (it.pair % p.pairs_per_group) * 2 + hh2 < p.group;
+        const float* hb = Tb + hh2 * 64 * kTRow;
+        if (et < 128) {  // column sums: key x of head hh2
+          const int64_t j = j0 + x;
+          if (hx_ok && j < p.nk) {
+            float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // 8 chains, loads up front
 #pragma unroll
             for (int q = 0; q < 64; q += 8)
 #pragma unroll
-              for (int u = 0; u < 8; ++u) {
-                const float x = (q + u < cnt) ? dg[(q + u) * 66] : 0.f;
-                a[u] += x;
-              }
-            const float acc = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-            p.diag_part[(int64_t(hd) * p.ntiles + it.t0 + t) * 128 + e] = acc;
+              for (int u = 0; u < 8; ++u) a[u] += hb[(q + u) * kTRow + ((x - q - u) & 63)];
+            p.col_part[int64_t(hx) * p.nk + j] =
+                ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
           }
+        } else if (hx_ok) {  // diagonal sums: buffer column x = diagonals e = 63 - x, 127 - x
+          float a[4] = {0.f, 0.f, 0.f, 0.f}, b2[4] = {0.f, 0.f, 0.f, 0.f};
+          const int lim = 64 - x;  // rows below lim: diagonal 63 - x (e = r - c + 63)
+#pragma unroll
+          for (int q = 0; q < 64; q += 4)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float y = hb[(q + u) * kTRow + x];
+              const bool lo = q + u < lim;
+              a[u] += lo ? y : 0.f;
+              b2[u] += lo ? 0.f : y;
+            }
+          float* dp = p.diag_part + (int64_t(hx) * p.ntiles + it.t0 + t) * 128;
+          dp[63 - x] = (a[0] + a[1]) + (a[2] + a[3]);
+          if (x > 0) dp[127 - x] = (b2[0] + b2[1]) + (b2[2] + b2[3]);
         }
       }
     }
@@ -580,6 +578,7 @@ int est_tc_run(const EstTcArgs& a, const EstTcPlan& pl, Arena& ar, cudaStream_t 
   p.pairs_per_group = ppg;
   p.npairs = npairs;
   p.pair0 = pl.pair0;
+  p.ncall_pairs = pl.pair1 - pl.pair0;
   p.nk = a.nk;
   p.block = int(a.block);
   p.ntiles_k = a.k3_tiles;

@@ -8,6 +8,7 @@ namespace lcx {
 struct EstTcParams {
   int group, pairs_per_group, npairs;
   int pair0;                 // first head pair of this call (items cover pairs [pair0, ...))
+  int ncall_pairs;           // head pairs of this call
   int64_t nk;
   int block;
   int64_t ntiles_k;          // 64-key tiles of the K3 buffer (its row stride)
