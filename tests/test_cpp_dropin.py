@@ -29,9 +29,11 @@ def build_binary():
     if os.path.exists(BIN) and os.path.getmtime(BIN) >= max(os.path.getmtime(SRC),
                                                             os.path.getmtime(_lib.LIB_PATH)):
         return BIN
+    tmp = f"{BIN}.{os.getpid()}.tmp"
     subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), SRC,
-                    "-L", lib_dir, "-llongctx_b200", f"-Wl,-rpath,{lib_dir}", "-o", BIN],
+                    "-L", lib_dir, "-llongctx_b200", f"-Wl,-rpath,{lib_dir}", "-o", tmp],
                    check=True)
+    os.replace(tmp, BIN)  # atomic: parallel workers never exec a half-written binary
     return BIN
 
 

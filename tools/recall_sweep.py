@@ -15,7 +15,7 @@ from paper_2501_15383_b200 import device as D  # noqa: E402
 from paper_2501_15383_b200.synth import make_qkv, yarn_temperature  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 262144
-kind = sys.argv[2] if len(sys.argv) > 2 else "structured"
+kind = sys.argv[2] if len(sys.argv) > 2 else "planted"
 q, k, v = make_qkv(n, 28, 4, kind=kind, seed=1)
 s, c = 131072, 262144
 kw = dict(chunk_len=32768, last_q=64, position_mode="dca_continuous", dca=(s, c, s),

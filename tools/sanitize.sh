@@ -15,7 +15,7 @@ for tool in memcheck racecheck synccheck initcheck; do
     [ $tool = racecheck ] && extra="--racecheck-report all"
     [ $tool = initcheck ] && extra=""
     echo "== $tool $what" | tee -a gpurun_out/sanitize_summary.txt
-    timeout 900 bash -c "$CS --tool $tool $extra --target-processes all --print-limit 50 \
+    timeout 420 bash -c "$CS --tool $tool $extra --target-processes all --print-limit 50 \
         --error-exitcode 99 $cmd" > gpurun_out/sanitize_${tool}_${what}.log 2>&1
     rc=$?
     echo "rc=$rc $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|hazard' gpurun_out/sanitize_${tool}_${what}.log | tail -3 | tr '\n' ' ')" \
