@@ -372,8 +372,15 @@ static_assert(sizeof(TileMeta) <= 448, "tile metadata slot overflow");
         atomicAdd(reinterpret_cast<unsigned long long*>(p.trace + 4096 + (role) * 8 + _j),  \
                   (unsigned long long)wacc[_j]);                                            \
   } while (0)
+#define WAITP2(site, ...)                     \
+  do {                                        \
+    const long long _w0 = clock64();          \
+    __VA_ARGS__;                              \
+    wacc2[site] += clock64() - _w0;           \
+  } while (0)
 #else
 #define WAITP(site, ...) __VA_ARGS__
+#define WAITP2(site, ...) __VA_ARGS__
 #define WAITP_FLUSH(role) \
   do {                    \
   } while (0)
@@ -429,6 +436,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #ifdef LCX_TC_WAITPROF
   long long wacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long wacc2[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // softmax detail (role 5)
   const long long t_start = clock64();
 #endif
   if (threadIdx.x == 0) {
@@ -451,7 +459,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     for (int b = 0; b < kGroups; ++b) tc::mbar_init(lpub + b, 4);
     tc::mbar_init(edone, 4);
     for (int b = 0; b < kMetaSlots; ++b) {
-      tc::mbar_init(m_full + b, 1);
+      tc::mbar_init(m_full + b, 32);  // every producer lane releases its own writes
       tc::mbar_init(m_empty + b, kSoftmaxWarps + 3);  // softmax + QK + PV + V warps
     }
     tc::fence_barrier_init();
@@ -514,7 +522,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           mt.rend = it.rend;
         }
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(m_full + int(M % kMetaSlots));
+        tc::mbar_arrive(m_full + int(M % kMetaSlots));
         ++M;
         continue;
       }
@@ -601,9 +609,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           if (lane == 0) mt.nfar = __popc(f0) + __popc(f1);
         }
         // D: publish (lane j: slot of tile j), then lane j issues tile j's K loads
+        // every lane wrote into the batch's slots (records, vertical key lists): each
+        // lane releases its own writes on every slot of the batch (count 32)
         __syncwarp();
+        for (int j = 0; j < nb; ++j) tc::mbar_arrive(m_full + int((M + j) % kMetaSlots));
         if (lane < nb) {
-          tc::mbar_arrive(m_full + int((M + lane) % kMetaSlots));
           const uint32_t Tj = T + lane;
 #if !defined(LCX_TC_TRACE_PV) && !defined(LCX_TC_TRACE_SM)
           trace_mark(p, Tj, 0);
@@ -648,7 +658,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     slot_wait(M);
     if (lane == 0) metas[M % kMetaSlots].kind = T_END;
     __syncwarp();
-    if (lane == 0) tc::mbar_arrive(m_full + int(M % kMetaSlots));
+    tc::mbar_arrive(m_full + int(M % kMetaSlots));
     ++M;
     if (lane == 0 && p.tile_count)
       atomicAdd(reinterpret_cast<unsigned long long*>(p.tile_count), (unsigned long long)T);
@@ -1103,7 +1113,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       wacc[5] += clock64() - t_sg;
 #endif
       // ---- running max: previous tile's (other group) unless the item starts here
-      if (!kSplitO && !(flags & F_FIRST)) tc::mbar_wait(h_in, k & 1);
+      if (!kSplitO && !(flags & F_FIRST)) WAITP2(0, tc::mbar_wait(h_in, k & 1));
       const float m_prev = kSplitO ? m_used
                            : (flags & F_FIRST) ? m_init
                                                : mbuf[((T + kGroups - 1) % kGroups) * 128 + r];
@@ -1124,6 +1134,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(h_out);
       }
+#ifdef LCX_TC_WAITPROF
+      const long long t_rs = clock64();
+#endif
       if (__any_sync(0xffffffffu, need && m_prev != -INFINITY)) {
         // O holds PV up to tile T - 1 at max m_prev: complete it, then rescale
         // (split O: this group's last PV, T - kGroups, completed before QK(T) took its S
@@ -1139,13 +1152,28 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         if (m_used != -INFINITY) l *= ex2(m_used - m);
         m_used = m;
       }
+#ifdef LCX_TC_WAITPROF
+      wacc2[1] += clock64() - t_rs;
+      const long long t_e0 = clock64();
+#endif
       rs = exps_store(m);
+#ifdef LCX_TC_WAITPROF
+      wacc2[2] += clock64() - t_e0;
+      ++wacc2[3];  // own tiles
+#endif
       }
 #ifdef LCX_TC_WAITPROF
       const long long t_ex = clock64();
 #endif
       tc::tmem_wait_st();
       l += rs;
+      // every phase of the predecessor group's partial-sum barrier is consumed (tile T - 1
+      // released its P before this one is released, so this rarely waits); the epilogue's
+      // wait on the same phase then returns at once
+      if (T >= 1) {
+        const uint32_t Tp = T - 1;
+        tc::mbar_wait(lpub + int(Tp % kGroups), (Tp / kGroups) & 1);
+      }
       // partial (l, m) for the item's epilogue (ordered before the P release below)
       lbuf[((k & 1) * kGroups + grp) * 128 + r] = make_float2(l, m_used);
       tc::tc_fence_before();
@@ -1258,6 +1286,13 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     wacc[7] = clock64() - t_start;
 #endif
     if (wq == 0) WAITP_FLUSH(4);
+#ifdef LCX_TC_WAITPROF
+    if (wq == 0) {
+      for (int _j = 0; _j < 8; ++_j) wacc[_j] = wacc2[_j];
+      wacc[7] = clock64() - t_start;
+      WAITP_FLUSH(5);
+    }
+#endif
   }
   tc::tc_fence_before();
   __syncthreads();

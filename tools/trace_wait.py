@@ -25,10 +25,18 @@ names = {0: ("producer", ["m_empty", "k_empty"]),
          2: ("V", ["m_full", "v_empty"]),
          3: ("PV", ["m_full", "p_full", "v_full"]),
          4: ("softmax", ["m_full", "s_full", "item start", "meta+mask", "own tile (all)", "max phase",
-                         "exp phase"])}
+                         "exp phase"]),
+         5: ("softmax+", ["h_in wait", "rescale", "exps+P store", "own tiles (count)"])}
 for role, (nm, sites) in names.items():
     tot = w[role, 7]
     if tot == 0:
         continue
-    parts = ", ".join(f"{s_}={w[role, j] / tot * 100:.1f}%" for j, s_ in enumerate(sites))
+    parts = ", ".join((f"{s_}={w[role, j]}" if "count" in s_ else
+                       f"{s_}={w[role, j] / tot * 100:.1f}%") for j, s_ in enumerate(sites))
     print(f"{nm:8s} {parts}")
+tiles = w[5, 3]
+if tiles:
+    print("softmax clk per own tile (per warp group, quadrant-0 warps summed):",
+          {nm: round(float(w[r, j]) / tiles, 1) for r, nm, j in
+           [(4, "own tile", 4), (4, "s_full", 1), (4, "max", 5), (5, "h_in", 0), (5, "rescale", 1),
+            (5, "exps", 2), (4, "tail", 6), (4, "meta", 3), (4, "m_full", 0)]})
