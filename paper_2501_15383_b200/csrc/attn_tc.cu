@@ -55,9 +55,18 @@ constexpr int BM = 128, BN = 64, HD = 128;
 #endif
 constexpr int kGroups = LCX_TC_GROUPS;          // softmax warp groups (tile T: T % kGroups)
 constexpr int kSoftmaxWarps = 4 * kGroups;
-constexpr int kThreads = 32 * (kSoftmaxWarps + 4);
+// One warp issues both the QK and the PV MMAs (QK(T), then PV(T - 1); PV first at an item
+// start) and the producer warp issues the V loads after the K loads of each tile: two fewer
+// warps polling barriers (the kernel is issue-bound: ~20 % of its instructions were
+// barrier polls), and the sub-partitions they free run only softmax warps.
+#ifndef LCX_TC_MERGE
+#define LCX_TC_MERGE 1
+#endif
+constexpr bool kMerge = LCX_TC_MERGE;
+constexpr int kThreads = 32 * (kSoftmaxWarps + (kMerge ? 2 : 4));
 constexpr int kWarpProducer = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1,
-              kWarpPv = kSoftmaxWarps + 2, kWarpV = kSoftmaxWarps + 3;
+              kWarpPv = kMerge ? -1 : kSoftmaxWarps + 2, kWarpV = kMerge ? -1 : kSoftmaxWarps + 3;
+constexpr int kRingConsumers = kSoftmaxWarps + (kMerge ? 1 : 3);  // warps reading each slot
 // The softmax code is written for any number of groups, but a third group needs more
 // registers than 65536 / 512 per thread: compiled at 128 it spills ~2.6 KB and ran 3.4x
 // slower (setmaxnreg does not help: ptxas still allocates for the launch-time limit).
@@ -144,6 +153,19 @@ constexpr float kRescaleThresh = 8.f;
 #define LCX_TC_SLEEPY_PV 0
 #endif
 
+// Barrier arrivals on the metadata ring, the running-max hand-off and the partial-sum
+// publication: by every lane that touched the shared data (1), or by lane 0 after a
+// __syncwarp (0; the warp barrier orders the other lanes' accesses, but racecheck does
+// not credit it and reports those accesses as hazards).
+#ifndef LCX_TC_LANE_ARRIVE
+#define LCX_TC_LANE_ARRIVE 1
+#endif
+constexpr uint32_t kArriveLanes = LCX_TC_LANE_ARRIVE ? 32 : 1;
+#define LANE_ARRIVE(bar) \
+  do {                   \
+    if (LCX_TC_LANE_ARRIVE || lane == 0) tc::mbar_arrive(bar); \
+  } while (0)
+
 constexpr uint32_t IDESC_QK = tc::idesc_f16(BM, BN, 1, 1);   // bf16 x bf16
 constexpr uint32_t IDESC_PV = tc::idesc_f16(BM, HD, 0, 0);   // f16 x f16
 
@@ -184,8 +206,19 @@ __device__ __forceinline__ int lower_bound32(const int32_t* a, int n, int64_t x)
 __device__ __forceinline__ int64_t ceil_div64(int64_t a) { return (a + 63) >> 6; }
 
 __device__ void setup_item(const TcParams& p, int item, Item& it) {
+  // KV-group-major order: the query heads of one KV head are adjacent for each row block,
+  // so CTAs drawing neighbouring items read the same K / V tiles (band, dense) from L2
+  // instead of each head re-streaming them from DRAM.
+#ifndef LCX_TC_HEAD_MAJOR
+  const int per_g = p.nblocks * p.group;
+  const int gg = item / per_g;
+  const int rem = item - gg * per_g;
+  const int b = rem / p.group;
+  it.h = gg * p.group + (rem - b * p.group);
+#else
   it.h = item / p.nblocks;
   const int b = item - it.h * p.nblocks;
+#endif
   it.g = it.h / p.group;
   it.i0 = (p.block0 + b) * BM;
   it.rend = lcx_min64(it.i0 + BM, p.t1);
@@ -400,6 +433,8 @@ __device__ __forceinline__ uint64_t window64(const uint32_t* sw, int off) {
   return sh ? ((a >> sh) | (b << (64 - sh))) : a;
 }
 
+// registers: the register file is split over the four sub-partitions and warps go to them
+// round-robin, so 10 or 12 warps both put 3 warps on a sub-partition: 168 per thread
 __global__ void __launch_bounds__(kThreads, 1)
 attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
                const __grid_constant__ CUtensorMap map_k_lo,
@@ -455,12 +490,12 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     }
     tc::mbar_init(q_ready, 4);
     tc::mbar_init(q_ready + 1, 4);
-    for (int b = 0; b < 4 * kGroups; ++b) tc::mbar_init(hand + b, 1);
-    for (int b = 0; b < kGroups; ++b) tc::mbar_init(lpub + b, 4);
+    for (int b = 0; b < 4 * kGroups; ++b) tc::mbar_init(hand + b, kArriveLanes);
+    for (int b = 0; b < kGroups; ++b) tc::mbar_init(lpub + b, 4 * kArriveLanes);
     tc::mbar_init(edone, 4);
     for (int b = 0; b < kMetaSlots; ++b) {
       tc::mbar_init(m_full + b, 32);  // every producer lane releases its own writes
-      tc::mbar_init(m_empty + b, kSoftmaxWarps + 3);  // softmax + QK + PV + V warps
+      tc::mbar_init(m_empty + b, kRingConsumers * kArriveLanes);  // softmax + QK + PV + V warps
     }
     tc::fence_barrier_init();
     tc::fence_proxy_async();
@@ -649,6 +684,21 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #if !defined(LCX_TC_TRACE_PV) && !defined(LCX_TC_TRACE_SM)
           trace_mark(p, Tj, 1);
 #endif
+          if constexpr (kMerge) {  // this tile's V^T
+            const int bv = Tj % NV;
+#if LCX_TC_SLEEPY
+            WAITP(1, tc::mbar_wait_sleepy(v_empty + bv, ((Tj / NV) & 1) ^ 1, LCX_TC_SLEEPY));
+#else
+            WAITP(1, tc::mbar_wait(v_empty + bv, ((Tj / NV) & 1) ^ 1));
+#endif
+            tc::mbar_expect_tx(v_full + bv, kVStage);
+            const int64_t vtile = my.kind == T_VERT
+                                      ? int64_t(it.h) * (p.capp / 64) + my.key0 / 64
+                                      : int64_t(it.g) * p.ntiles_k + my.key0 / 64;
+            tc::bulk_load(smem_base + OFF_V + bv * kVStage,
+                          (my.kind == T_VERT ? p.vct : p.vt) + vtile * (kVStage / 2), kVStage,
+                          v_full + bv);
+          }
         }
         __syncwarp();
         M += nb;
@@ -667,10 +717,32 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #endif
     WAITP_FLUSH(0);
   } else if (warp == kWarpMma) {
-    // ==================================================== QK issuer ====
+    // ========================================= QK issuer (+ PV issuer, kMerge) ====
     uint32_t T = 0, E = 0, M = 0;
-    // QK issuer: all 32 lanes run this loop (warp-uniform); one elected lane issues
+    // all 32 lanes run this loop (warp-uniform); one elected lane issues
     const uint64_t dk0 = tc::sdesc_sw128(tc::smem_u32(smem + OFF_K));
+    // merged PV issue: O += P(Tp) V(Tp), P aliasing S buffer Tp % NS (TS-form MMA)
+    const uint64_t dv0 = tc::sdesc_sw128(tc::smem_u32(smem + OFF_V));
+    uint32_t T_first = 0;
+    bool pend = false;  // PV(T - 1) not issued yet
+    int pflags = 0;
+    auto issue_pv = [&](uint32_t Tp, int fl) {
+      const int bs = Tp % NS, bv = Tp % NV;
+      WAITP(5, tc::mbar_wait(p_full + bs, (Tp / NS) & 1));
+      WAITP(6, tc::mbar_wait(v_full + bv, (Tp / NV) & 1));
+      tc::tc_fence_after();
+      const uint64_t dv = dv0 + ((bv * kVStage) >> 4);
+      if (fl & F_FIRST) T_first = Tp;
+      const bool first = kSplitO ? (Tp - T_first < uint32_t(kGroups) && !(p.init && Tp == T_first))
+                                 : ((fl & F_FIRST) && !p.init);
+      const uint32_t dO = tmem + COL_O + (kSplitO ? (Tp % kGroups) * HD : 0);
+#pragma unroll
+      for (int kk = 0; kk < BN / 16; ++kk)
+        tc::mma_f16_ts_warp(dO, tmem + bs * BN + kk * 8, dv + ((kk * 32) >> 4), IDESC_PV,
+                            (first && kk == 0) ? 0u : 1u);
+      tc::mma_commit_warp(v_empty + bv);
+      tc::mma_commit_warp(s_free + bs);
+    };
     for (;;) {
       const int slot = M % kMetaSlots;
       WAITP(0, tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1));
@@ -678,8 +750,17 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       const int flags = metas[slot].flags;
       const int qb = kQBufs == 2 ? (metas[slot].grp & 1) : 0;  // Q buffer of the tile's group
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(m_empty + slot);
+      LANE_ARRIVE(m_empty + slot);
       ++M;
+      if constexpr (kMerge) {
+        // the previous item's last PV goes first when this tile cannot be issued before it
+        // completes (item start: the new item's Q rotation waits for that item's epilogue,
+        // which waits for its last PV) or when nothing follows
+        if (pend && (kind == T_END || kind == T_EMPTY || (flags & F_FIRST))) {
+          issue_pv(T - 1, pflags);
+          pend = false;
+        }
+      }
       if (kind == T_END) break;
       if (kind == T_EMPTY) continue;
       if (flags & F_EPOCH) {  // first tile of a group: its Q buffer is (or will be) filled
@@ -726,6 +807,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #ifndef LCX_TC_TRACE_PV
       if (lane == 0) trace_mark(p, T, 3);
 #endif
+      if constexpr (kMerge) {
+        if (pend) issue_pv(T - 1, pflags);  // QK(T) runs while the softmax finishes P(T - 1)
+        pend = true;
+        pflags = flags;
+      }
       ++T;
     }
 #ifdef LCX_TC_WAITPROF
@@ -742,7 +828,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       const int h = metas[slot].h;
       const int key0 = int(metas[slot].key0);
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(m_empty + slot);
+      LANE_ARRIVE(m_empty + slot);
       ++M;
       if (kind == T_END) break;
       if (kind == T_EMPTY) continue;
@@ -790,7 +876,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       const int kind = metas[slot].kind;
       const int flags = metas[slot].flags;
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(m_empty + slot);
+      LANE_ARRIVE(m_empty + slot);
       ++M;
       if (kind == T_END) break;
       if (kind == T_EMPTY) continue;
@@ -857,7 +943,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     float l = 0.f, m_used = -INFINITY;  // this group's partial sum, at max m_used
     float m_init = -INFINITY;           // running max at the item start (key-window passes)
     Item qi{};  // only i0 / rend / h used by rotate_q
-    if (!kSplitO && grp == kGroups - 1 && lane == 0) tc::mbar_arrive(h_out);  // tile 0
+    if (!kSplitO && grp == kGroups - 1) LANE_ARRIVE(h_out);  // tile 0
     auto rotate_row = [&](int pattern, int qbuf) {
       rotate_q(p, qi, pattern, r, 0, tmem + lane_base, qbuf);
       rotate_q(p, qi, pattern, r, 1, tmem + lane_base, qbuf);
@@ -903,7 +989,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       const int pattern = mt.pattern, tgrp = mt.grp, ng = mt.ng, next_pattern = mt.next_pattern;
       const int gpat1 = mt.gpat[1], gpat2 = mt.gpat[2];
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(m_empty + slot);
+      LANE_ARRIVE(m_empty + slot);
 #ifdef LCX_TC_WAITPROF
       wacc[3] += clock64() - t_meta;
 #endif
@@ -988,11 +1074,17 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       float sv[kSReread ? 32 : 64];
       WAITP(1, tc::mbar_wait(s_full + b, ph));
       tc::tc_fence_after();
+#ifdef LCX_TC_WAITPROF
+      const long long t_ld = clock64();
+#endif
       if constexpr (!kSReread) {
         tc::tmem_ld32(tmem + lane_base + b * BN, sv);
         tc::tmem_ld32_wait(tmem + lane_base + b * BN + 32, sv + 32);
         tc::tmem_wait_ld_dep32(sv);
       }
+#ifdef LCX_TC_WAITPROF
+      wacc2[4] += clock64() - t_ld;
+#endif
 #ifdef LCX_TC_TRACE_SM  // owner group's quadrant-0 warp: 5 S got, 0 m handed over, 6 P put
       if (wq == 0 && lane == 0) trace_mark(p, T, 5);
 #else
@@ -1132,7 +1224,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       // an item's last tile hands over only after its epilogue (next item's O / Q)
       if (!kSplitO && !(flags & F_LAST)) {
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(h_out);
+        LANE_ARRIVE(h_out);
       }
 #ifdef LCX_TC_WAITPROF
       const long long t_rs = clock64();
@@ -1180,8 +1272,8 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       __syncwarp();
       if (lane == 0) {
         tc::mbar_arrive(p_full + b);
-        tc::mbar_arrive(lpub + grp);
       }
+      LANE_ARRIVE(lpub + grp);
 #ifdef LCX_TC_WAITPROF
       wacc[6] += clock64() - t_ex;
 #endif
@@ -1189,6 +1281,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       if (wq == 0 && lane == 0) trace_mark(p, T, 6);
 #else
       if (threadIdx.x == 0) trace_mark(p, T, 6);
+#endif
+#ifdef LCX_TC_WAITPROF
+      const long long t_epi = clock64();
 #endif
       if (kSplitO && (flags & F_LAST)) {
         // ---- epilogue (split O): merge the other group's O (its last tile T - 1) into
@@ -1274,10 +1369,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
               lt > 0.f ? (m_used + log2f(lt)) * 0.69314718055994530942f : -INFINITY;
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(h_out);
+        LANE_ARRIVE(h_out);
 
       }
 #ifdef LCX_TC_WAITPROF
+      wacc2[5] += clock64() - t_epi;
       wacc[4] += clock64() - t_own;  // whole own tile, item start to P release / epilogue
 #endif
       ++T;

@@ -21,12 +21,12 @@ buf = np.zeros(512 * 8 + 64, np.int64)
 L.lcx_debug_trace(ctx.ptr, 1, buf.ctypes.data)
 w = buf[4096:].reshape(8, 8)
 names = {0: ("producer", ["m_empty", "k_empty"]),
-         1: ("QK", ["m_full", "q_ready", "k_full", "s_free", "issue"]),
+         1: ("QK(+PV)", ["m_full", "q_ready", "k_full", "s_free", "issue", "p_full", "v_full"]),
          2: ("V", ["m_full", "v_empty"]),
          3: ("PV", ["m_full", "p_full", "v_full"]),
          4: ("softmax", ["m_full", "s_full", "item start", "meta+mask", "own tile (all)", "max phase",
                          "exp phase"]),
-         5: ("softmax+", ["h_in wait", "rescale", "exps+P store", "own tiles (count)"])}
+         5: ("softmax+", ["h_in wait", "rescale", "exps+P store", "own tiles (count)", "S tmem ld", "epilogue"])}
 for role, (nm, sites) in names.items():
     tot = w[role, 7]
     if tot == 0:
@@ -39,4 +39,4 @@ if tiles:
     print("softmax clk per own tile (per warp group, quadrant-0 warps summed):",
           {nm: round(float(w[r, j]) / tiles, 1) for r, nm, j in
            [(4, "own tile", 4), (4, "s_full", 1), (4, "max", 5), (5, "h_in", 0), (5, "rescale", 1),
-            (5, "exps", 2), (4, "tail", 6), (4, "meta", 3), (4, "m_full", 0)]})
+            (5, "exps", 2), (4, "tail", 6), (5, "S ld", 4), (5, "epilogue", 5), (4, "item start", 2), (4, "meta", 3), (4, "m_full", 0)]})
