@@ -53,7 +53,10 @@ constexpr int kMinBlocks = LCX_GATHER_MINB;  // resident CTAs per SM
 #ifndef LCX_GATHER_INFLIGHT
 #define LCX_GATHER_INFLIGHT 2
 #endif
-constexpr int kInflight = LCX_GATHER_INFLIGHT;  // entries of a row loaded at once
+constexpr int kInflight = LCX_GATHER_INFLIGHT;
+#ifndef LCX_GATHER_DIAG
+#define LCX_GATHER_DIAG 1  // diagonal-major kernel (below); 0: row-major list scan
+#endif  // entries of a row loaded at once
 static_assert(kLanes == 8 || kLanes == 16 || kLanes == 32, "8, 16 or 32 lanes per row");
 constexpr int kVVec = kDims >= 8 ? kDims / 8 : 1;  // 16-byte (or one 8-byte) V loads per lane
 
@@ -64,6 +67,12 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
     f[2 * t] = __uint_as_float(w[t] << 16);
     f[2 * t + 1] = __uint_as_float(w[t] & 0xffff0000u);
   }
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 struct KVRow {
@@ -325,14 +334,216 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) attn_gather_kernel(const
   }
 }
 
+
+// ---------------------------------------------------------------------------------------
+// Diagonal-major variant (default): the rows of a warp walk the half-block's segment list
+// together, one diagonal d per step, so a step is the entries (i, i - d) of eight
+// consecutive rows -- eight consecutive keys -- with no per-entry list scan, ballot or
+// index shuffle.  Four lanes per row: lane ls holds the k-dims {16 t + 4 ls + c} (eight
+// float4 loads of the fp32 rotated key, 64 contiguous bytes per row per load, partial dot
+// reduced by two shuffles) and the v-dims {32 t + 8 ls + c} (four 16-byte bf16 loads, its
+// own 32 output accumulators).  Online softmax per row in fp32 with a lazy max (rescale
+// only when a logit passes the running max by 8 in log2 units).  Same entries, state and
+// fallback semantics as attn_gather_kernel above.
+namespace diag {
+constexpr int kLanes = 4;                  // lanes per row
+constexpr int kRowsW = 32 / kLanes;        // rows per warp
+constexpr int kWarps = 4;                  // warps per CTA
+constexpr int kRowsC = kRowsW * kWarps;    // rows per CTA (within one 64-row half)
+static_assert(64 % kRowsC == 0, "a CTA's rows lie in one half-block");
+
+__device__ __forceinline__ int64_t qpos(const GatherArgs& a, int pattern, int64_t i, int64_t imod) {
+  if (a.rel_mode == 0) return a.pos_q ? a.pos_q[i] : i;
+  if (pattern == 0) return imod;
+  if (pattern == 1) return lcx_min64(imod + a.s, a.c - 1);
+  return a.c - 1;
+}
+
+__global__ void __launch_bounds__(kWarps * 32, 3) attn_gather_diag_kernel(const GatherArgs a) {
+  if (a.win_flags && !a.win_flags[a.win] && a.key_hi <= a.row_begin) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int ls = lane & (kLanes - 1);
+  const int h = blockIdx.y, g = h / a.group;
+  const int64_t cta_row0 = a.row_begin + int64_t(blockIdx.x) * kRowsC;
+  const int64_t w_row0 = cta_row0 + warp * kRowsW;
+  const int64_t i = w_row0 + (lane / kLanes);
+  const bool row_ok = i < a.row_end;
+  const int r = int((i - a.row_begin) & 127);  // row within its 128-row block
+  const int half = int(((cta_row0 - a.row_begin) & 127) >> 6);
+  const int4* sg = a.segs + (int64_t(h) * 2 + half) * a.cap_seg;
+  const int nseg = a.nseg[h * 2 + half];
+  const int nvh = a.nv[h], nsh = a.ns[h];
+  const bool any = (nvh > 0 && int64_t(a.verts[int64_t(h) * a.cap_v]) <= i) ||
+                   (nsh > 0 && int64_t(a.slashes[int64_t(h) * a.cap_s]) <= i);
+  const bool fallback = row_ok && !any && a.do_fallback && i >= a.key_lo && i < a.key_hi;
+  // the warp's diagonals: d in [w_row0 - key_hi + 1, last row - key_lo], d <= last row
+  const int64_t w_last = lcx_min64(w_row0 + kRowsW, a.row_end) - 1;
+  const int64_t dmin = w_row0 - a.key_hi + 1;
+  const int64_t dmax = lcx_min64(w_last, w_last - a.key_lo);
+  int xs;
+  {
+    int lo = 0, hi = nseg;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (int64_t(__ldg(&sg[mid].x)) < dmin) lo = mid + 1;
+      else hi = mid;
+    }
+    xs = lo;
+  }
+  const bool have = xs < nseg && int64_t(__ldg(&sg[xs].x)) <= dmax;
+  if (!have && !__any_sync(0xffffffffu, fallback)) return;
+
+  // this lane's query dims {16 t + 4 ls + c}: raw bf16 kept packed, rotated per DCA pattern
+  uint2 qraw[8];
+  {
+    const uint2* qp = reinterpret_cast<const uint2*>(a.q + ((row_ok ? i : 0) * a.hq + h) * 128);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) qraw[t] = row_ok ? __ldg(qp + 4 * t + ls) : make_uint2(0u, 0u);
+  }
+  const int64_t qc = a.rel_mode == 1 ? i / a.s : 0;
+  const int64_t imod = i - qc * a.s;
+  const int64_t c_intra = qc * a.s, c_succ = c_intra - a.s;
+  float qr[32];
+  int cur_pat = -1;
+  auto rotate = [&](int pat) {
+    cur_pat = pat;
+    const float4* cs = reinterpret_cast<const float4*>(a.rope + qpos(a, pat, i, imod) * 64);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const float4 c = __ldg(cs + 4 * t + ls);  // pairs 8 t + 2 ls, + 1
+      const float x0 = __uint_as_float(qraw[t].x << 16), y0 = __uint_as_float(qraw[t].x & 0xffff0000u);
+      const float x1 = __uint_as_float(qraw[t].y << 16), y1 = __uint_as_float(qraw[t].y & 0xffff0000u);
+      qr[4 * t] = (x0 * c.x - y0 * c.y) * a.scale_log2;
+      qr[4 * t + 1] = (x0 * c.y + y0 * c.x) * a.scale_log2;
+      qr[4 * t + 2] = (x1 * c.z - y1 * c.w) * a.scale_log2;
+      qr[4 * t + 3] = (x1 * c.w + y1 * c.z) * a.scale_log2;
+    }
+  };
+  auto pattern_of = [&](int64_t j) -> int {
+    return a.rel_mode != 1 ? 0 : (j >= c_intra ? 0 : (j >= c_succ ? 1 : 2));
+  };
+
+  // running state: the partial so far (tensor-core tiles, earlier passes), log2 domain
+  float o[32], m = -INFINITY, l = 0.f;
+  float* orow = a.out + ((row_ok ? i : 0) * a.hq + h) * 128;
+  const float lp = row_ok ? a.lse[int64_t(h) * a.lse_stride + i] : -INFINITY;
+  const bool from_partial = lp != -INFINITY && !fallback;
+#pragma unroll
+  for (int x = 0; x < 32; ++x) o[x] = 0.f;
+  if (from_partial) {
+    m = lp * 1.4426950408889634f;
+    l = 1.f;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const float4 u0 = reinterpret_cast<const float4*>(orow)[8 * t + 2 * ls];
+      const float4 u1 = reinterpret_cast<const float4*>(orow)[8 * t + 2 * ls + 1];
+      o[8 * t] = u0.x; o[8 * t + 1] = u0.y; o[8 * t + 2] = u0.z; o[8 * t + 3] = u0.w;
+      o[8 * t + 4] = u1.x; o[8 * t + 5] = u1.y; o[8 * t + 6] = u1.z; o[8 * t + 7] = u1.w;
+    }
+  }
+  const float* kbase = a.kf + int64_t(g) * 128;
+  const __nv_bfloat16* vbase = a.v + int64_t(g) * 128;
+  const int64_t stride = int64_t(a.hkv) * 128;
+  const uint32_t* vb = a.vbits + int64_t(h) * a.words;
+  int entries = 0;
+
+
+  // entries of diagonal x for this lane's row: key j = i - d, admitted iff the row is in
+  // the segment's row range, j in the pass window (j >= 0) and j not a vertical column
+  auto valid_key = [&](const int4 e, int64_t& j) -> bool {
+    j = i - e.x;
+    return row_ok && r >= e.y && r < e.z && j >= a.key_lo && j < a.key_hi && j >= 0 &&
+           !((__ldg(vb + (j >> 5)) >> (j & 31)) & 1u);
+  };
+  auto process = [&](int64_t j) {  // one admitted entry of this lane's row
+    const int pat = pattern_of(j);
+    if (pat != cur_pat) rotate(pat);
+    const float4* kp = reinterpret_cast<const float4*>(kbase + j * stride);
+    const uint4* vp = reinterpret_cast<const uint4*>(vbase + j * stride);
+    float4 kk[8];
+    uint4 vv[4];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) kk[t] = __ldg(kp + 4 * t + ls);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) vv[t] = __ldg(vp + 4 * t + ls);
+    float d0 = 0.f, d1 = 0.f;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      d0 = fmaf(qr[4 * t], kk[t].x, d0);
+      d1 = fmaf(qr[4 * t + 1], kk[t].y, d1);
+      d0 = fmaf(qr[4 * t + 2], kk[t].z, d0);
+      d1 = fmaf(qr[4 * t + 3], kk[t].w, d1);
+    }
+    float sc = d0 + d1;
+    // the four lanes of a row agree on every branch that leads here (same i): reduce
+    // among the lanes present
+    const unsigned am = __activemask();
+    sc += __shfl_xor_sync(am, sc, 1);
+    sc += __shfl_xor_sync(am, sc, 2);
+    if (sc > m + 8.f) {  // lazy max: p stays <= 2^8 (fp32 accumulators)
+      const float corr = ex2(m - sc);  // 0 on the first entry (m = -inf)
+      l *= corr;
+#pragma unroll
+      for (int x = 0; x < 32; ++x) o[x] *= corr;
+      m = sc;
+    }
+    const float pf = ex2(sc - m);
+    l += pf;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint32_t w4[4] = {vv[t].x, vv[t].y, vv[t].z, vv[t].w};
+#pragma unroll
+      for (int c2 = 0; c2 < 4; ++c2) {
+        o[8 * t + 2 * c2] = fmaf(pf, __uint_as_float(w4[c2] << 16), o[8 * t + 2 * c2]);
+        o[8 * t + 2 * c2 + 1] = fmaf(pf, __uint_as_float(w4[c2] & 0xffff0000u), o[8 * t + 2 * c2 + 1]);
+      }
+    }
+    ++entries;
+  };
+  if (have) {
+    for (int x = xs; x < nseg; ++x) {
+      const int4 e = __ldg(&sg[x]);
+      if (int64_t(e.x) > dmax) break;
+      int64_t j;
+      const bool ok = valid_key(e, j);
+      // the lanes of a row agree on ok (same i); whole rows skip together
+      if (ok) process(j);
+    }
+  }
+  if (fallback) {  // self entry (sparse.cpp:111): the row admits nothing else
+    process(i);
+  }
+  if (!row_ok || entries == 0) return;  // no entry: the running state stands
+  const float inv_l = 1.f / l;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    reinterpret_cast<float4*>(orow)[8 * t + 2 * ls] =
+        make_float4(o[8 * t] * inv_l, o[8 * t + 1] * inv_l, o[8 * t + 2] * inv_l, o[8 * t + 3] * inv_l);
+    reinterpret_cast<float4*>(orow)[8 * t + 2 * ls + 1] =
+        make_float4(o[8 * t + 4] * inv_l, o[8 * t + 5] * inv_l, o[8 * t + 6] * inv_l,
+                    o[8 * t + 7] * inv_l);
+  }
+  if (ls == 0) {
+    a.lse[int64_t(h) * a.lse_stride + i] = (m + log2f(l)) * 0.6931471805599453f;
+    if (a.simt_count)
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.simt_count), (unsigned long long)entries);
+  }
+}
+}  // namespace diag
+
 }  // namespace
 
 int attention_gather(const GatherArgs& a, cudaStream_t st) {
   const int64_t rows = a.row_end - a.row_begin;
   if (rows <= 0) return LCX_OK;
   if (a.row_begin % 128 != 0) return fail(LCX_ERR_INTERNAL, "gather rows must start a block");
+#if LCX_GATHER_DIAG
+  dim3 grid(unsigned((rows + diag::kRowsC - 1) / diag::kRowsC), unsigned(a.hq));
+  diag::attn_gather_diag_kernel<<<grid, diag::kWarps * 32, 0, st>>>(a);
+#else
   dim3 grid(unsigned((rows + kRows - 1) / kRows), unsigned(a.hq));
   attn_gather_kernel<<<grid, kThreads, 0, st>>>(a);
+#endif
   LCX_CHECK_LAUNCH();
   return LCX_OK;
 }
