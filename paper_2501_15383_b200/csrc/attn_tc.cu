@@ -63,10 +63,14 @@ constexpr int kSoftmaxWarps = 4 * kGroups;
 #define LCX_TC_MERGE 1
 #endif
 constexpr bool kMerge = LCX_TC_MERGE;
-constexpr int kThreads = 32 * (kSoftmaxWarps + (kMerge ? 2 : 4));
+// With kMerge the producer warp only builds the tile metadata (running up to the ring's
+// depth ahead) and a loader warp issues each tile's K and V^T loads as stages free up: the
+// metadata of the next tiles no longer waits behind a stage-empty wait.
+constexpr int kThreads = 32 * (kSoftmaxWarps + (kMerge ? 3 : 4));
 constexpr int kWarpProducer = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1,
-              kWarpPv = kMerge ? -1 : kSoftmaxWarps + 2, kWarpV = kMerge ? -1 : kSoftmaxWarps + 3;
-constexpr int kRingConsumers = kSoftmaxWarps + (kMerge ? 1 : 3);  // warps reading each slot
+              kWarpPv = kMerge ? -1 : kSoftmaxWarps + 2, kWarpV = kMerge ? -1 : kSoftmaxWarps + 3,
+              kWarpLoad = kMerge ? kSoftmaxWarps + 2 : -1;
+constexpr int kRingConsumers = kSoftmaxWarps + (kMerge ? 2 : 3);  // warps reading each slot
 // The softmax code is written for any number of groups, but a third group needs more
 // registers than 65536 / 512 per thread: compiled at 128 it spills ~2.6 KB and ran 3.4x
 // slower (setmaxnreg does not help: ptxas still allocates for the launch-time limit).
@@ -85,7 +89,10 @@ static_assert(kGroups == 2, "two softmax groups");
 // two S buffers suffice (NS = 2, 3, 4 measure the same); the TMEM they free holds a
 // second rotated Q, so the Q of the next DCA pattern is in place before its first QK
 #ifndef LCX_TC_QBUFS
-#define LCX_TC_QBUFS 2
+// one Q buffer and four S buffers: with the merged MMA warp issuing PV(T - 2) after QK(T),
+// the QK of the next tiles runs ahead of the softmax (two Q buffers leave room for two S
+// buffers only, and QK(T + 2) then waits for PV(T)): 342-344 vs 351-354 ms per 1M layer
+#define LCX_TC_QBUFS 1
 #endif
 // two rotated-Q buffers with two S buffers, or one Q buffer with four S buffers
 // Split O (LCX_TC_SPLIT_O): each softmax group accumulates its own tiles into its own O
@@ -110,6 +117,7 @@ constexpr int kOBufs = kSplitO ? kGroups : 1;
 constexpr int NK = 4, NV = 4;  // K / V smem stages
 constexpr int NS = kGroups == 3 ? 3 : ((kSplitO || kQBufs == 2) ? 2 : 4);  // S (+P) TMEM
 static_assert(NS % kGroups == 0, "each group must see every phase of its S buffers");
+static_assert(NS / kGroups <= 2, "PV lag");
 static_assert(!kSplitO || NS == kGroups, "split O: S(T) full implies PV(T - kGroups) done");
 constexpr uint32_t kKHalf = BN * 64 * 2;             // 8 KB
 constexpr uint32_t kKStage = 4 * kKHalf;             // hi0 hi1 lo0 lo1 = 32 KB
@@ -434,8 +442,10 @@ __device__ __forceinline__ uint64_t window64(const uint32_t* sw, int off) {
 }
 
 // registers: the register file is split over the four sub-partitions and warps go to them
-// round-robin, so 10 or 12 warps both put 3 warps on a sub-partition: 168 per thread
-__global__ void __launch_bounds__(kThreads, 1)
+// round-robin: up to 12 warps put at most 3 on a sub-partition (168 per thread), 13-16 put 4
+// (128 per thread)
+constexpr int kMaxRegs = (kThreads / 32 + 3) / 4 >= 4 ? 128 : 168;
+__global__ void __maxnreg__(kMaxRegs)
 attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
                const __grid_constant__ CUtensorMap map_k_lo,
                const __grid_constant__ CUtensorMap map_vt,
@@ -653,6 +663,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #if !defined(LCX_TC_TRACE_PV) && !defined(LCX_TC_TRACE_SM)
           trace_mark(p, Tj, 0);
 #endif
+        }
+        if (!kMerge && lane < nb) {
+          const uint32_t Tj = T + lane;
           const int bk = Tj % NK;
 #if LCX_TC_SLEEPY
           WAITP(1, tc::mbar_wait_sleepy(k_empty + bk, ((Tj / NK) & 1) ^ 1, LCX_TC_SLEEPY));
@@ -684,21 +697,6 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #if !defined(LCX_TC_TRACE_PV) && !defined(LCX_TC_TRACE_SM)
           trace_mark(p, Tj, 1);
 #endif
-          if constexpr (kMerge) {  // this tile's V^T
-            const int bv = Tj % NV;
-#if LCX_TC_SLEEPY
-            WAITP(1, tc::mbar_wait_sleepy(v_empty + bv, ((Tj / NV) & 1) ^ 1, LCX_TC_SLEEPY));
-#else
-            WAITP(1, tc::mbar_wait(v_empty + bv, ((Tj / NV) & 1) ^ 1));
-#endif
-            tc::mbar_expect_tx(v_full + bv, kVStage);
-            const int64_t vtile = my.kind == T_VERT
-                                      ? int64_t(it.h) * (p.capp / 64) + my.key0 / 64
-                                      : int64_t(it.g) * p.ntiles_k + my.key0 / 64;
-            tc::bulk_load(smem_base + OFF_V + bv * kVStage,
-                          (my.kind == T_VERT ? p.vct : p.vt) + vtile * (kVStage / 2), kVStage,
-                          v_full + bv);
-          }
         }
         __syncwarp();
         M += nb;
@@ -724,8 +722,13 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     // merged PV issue: O += P(Tp) V(Tp), P aliasing S buffer Tp % NS (TS-form MMA)
     const uint64_t dv0 = tc::sdesc_sw128(tc::smem_u32(smem + OFF_V));
     uint32_t T_first = 0;
-    bool pend = false;  // PV(T - 1) not issued yet
-    int pflags = 0;
+    // PVs not issued yet: tiles T - npend .. T - 1 (flags in pfl, oldest first); the PV of
+    // tile T - kPvLag is issued after QK(T), so the QK of the next tiles never waits for a
+    // P that the softmax has not produced yet (with NS = 2 S buffers QK(T + 1) needs PV(T - 1)
+    // anyway: lag 1; with 4, lag 2)
+    constexpr int kPvLag = NS / kGroups;
+    int npend = 0;
+    int pfl[2] = {0, 0};
     auto issue_pv = [&](uint32_t Tp, int fl) {
       const int bs = Tp % NS, bv = Tp % NV;
       WAITP(5, tc::mbar_wait(p_full + bs, (Tp / NS) & 1));
@@ -742,6 +745,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
                             (first && kk == 0) ? 0u : 1u);
       tc::mma_commit_warp(v_empty + bv);
       tc::mma_commit_warp(s_free + bs);
+      if (lane == 0) trace_mark(p, Tp, 4);
     };
     for (;;) {
       const int slot = M % kMetaSlots;
@@ -756,9 +760,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         // the previous item's last PV goes first when this tile cannot be issued before it
         // completes (item start: the new item's Q rotation waits for that item's epilogue,
         // which waits for its last PV) or when nothing follows
-        if (pend && (kind == T_END || kind == T_EMPTY || (flags & F_FIRST))) {
-          issue_pv(T - 1, pflags);
-          pend = false;
+        if (npend && (kind == T_END || kind == T_EMPTY || (flags & F_FIRST))) {
+          for (int x = 0; x < npend; ++x) issue_pv(T - npend + x, pfl[x]);
+          npend = 0;
         }
       }
       if (kind == T_END) break;
@@ -808,9 +812,12 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       if (lane == 0) trace_mark(p, T, 3);
 #endif
       if constexpr (kMerge) {
-        if (pend) issue_pv(T - 1, pflags);  // QK(T) runs while the softmax finishes P(T - 1)
-        pend = true;
-        pflags = flags;
+        if (npend == kPvLag) {  // QK(T) runs while the softmax finishes P(T - kPvLag)
+          issue_pv(T - kPvLag, pfl[0]);
+          pfl[0] = pfl[1];
+          --npend;
+        }
+        pfl[npend++] = flags;
       }
       ++T;
     }
@@ -818,6 +825,47 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     wacc[7] = clock64() - t_start;
 #endif
     WAITP_FLUSH(1);
+  } else if (warp == kWarpLoad) {
+    // ===================================== K (hi + lo) and V^T loads (kMerge) ====
+    uint32_t T = 0, M = 0;
+    for (;;) {
+      const int slot = M % kMetaSlots;
+      WAITP(0, tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1));
+      const int kind = metas[slot].kind;
+      const int h = metas[slot].h;
+      const int64_t key0 = metas[slot].key0;
+      __syncwarp();
+      LANE_ARRIVE(m_empty + slot);
+      ++M;
+      if (kind == T_END) break;
+      if (kind == T_EMPTY) continue;
+      if (lane == 0) {
+        const int64_t kt = kind == T_VERT ? int64_t(h) * (p.capp / 64) + key0 / 64
+                                          : int64_t(h / p.group) * p.ntiles_k + key0 / 64;
+        const int bk = T % NK;
+        WAITP(1, tc::mbar_wait(k_empty + bk, ((T / NK) & 1) ^ 1));
+        tc::mbar_expect_tx(k_full + bk, kKStage);
+        const uint32_t kdst = smem_base + OFF_K + bk * kKStage;
+        // pre-swizzled tiles: hi (2 halves) and lo are one contiguous 16 KB run each
+        tc::bulk_load(kdst, (kind == T_VERT ? p.kchi : p.khi) + kt * kKHalf, 2 * kKHalf,
+                      k_full + bk);
+        tc::bulk_load(kdst + 2 * kKHalf, (kind == T_VERT ? p.kclo : p.klo) + kt * kKHalf,
+                      2 * kKHalf, k_full + bk);
+        trace_mark(p, T, 1);
+        const int bv = T % NV;
+        WAITP(2, tc::mbar_wait(v_empty + bv, ((T / NV) & 1) ^ 1));
+        tc::mbar_expect_tx(v_full + bv, kVStage);
+        tc::bulk_load(smem_base + OFF_V + bv * kVStage, (kind == T_VERT ? p.vct : p.vt) + kt * (kVStage / 2),
+                      kVStage, v_full + bv);
+        trace_mark(p, T, 2);
+      }
+      __syncwarp();
+      ++T;
+    }
+#ifdef LCX_TC_WAITPROF
+    wacc[7] = clock64() - t_start;
+#endif
+    WAITP_FLUSH(2);
   } else if (warp == kWarpV) {
     // ===================================================== V TMA loads ====
     uint32_t T = 0, M = 0;

@@ -16,8 +16,9 @@ s, c = 131072, 262144
 D.chunked_prefill(q, k, v, chunk_len=32768, last_q=64, budget=(1000, 6096),
                   position_mode="dca_continuous", dca=(s, c, min(s, c - s)),
                   temperature=yarn_temperature(n / c), rope_base=1e7)
-buf = np.zeros((512, 8), np.int64)
+buf = np.zeros((512 * 8 + 64,), np.int64)
 L.lcx_debug_trace(ctx.ptr, 1, buf.ctypes.data)
+buf = buf[:4096].reshape(512, 8)
 t0 = buf[0, 7]
 print("tile grp flg kind resc   QKst  QKend  S_got  m_out  P_put  PV_is   d(S-QKend) d(P-S)")
 for t in range(1, 400):

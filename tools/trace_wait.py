@@ -22,7 +22,7 @@ L.lcx_debug_trace(ctx.ptr, 1, buf.ctypes.data)
 w = buf[4096:].reshape(8, 8)
 names = {0: ("producer", ["m_empty", "k_empty"]),
          1: ("QK(+PV)", ["m_full", "q_ready", "k_full", "s_free", "issue", "p_full", "v_full"]),
-         2: ("V", ["m_full", "v_empty"]),
+         2: ("V|load", ["m_full", "k_empty", "v_empty"]),
          3: ("PV", ["m_full", "p_full", "v_full"]),
          4: ("softmax", ["m_full", "s_full", "item start", "meta+mask", "own tile (all)", "max phase",
                          "exp phase"]),
