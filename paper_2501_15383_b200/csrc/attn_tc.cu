@@ -66,8 +66,12 @@ constexpr bool kMerge = LCX_TC_MERGE;
 // With kMerge the producer warp only builds the tile metadata (running up to the ring's
 // depth ahead) and a loader warp issues each tile's K and V^T loads as stages free up: the
 // metadata of the next tiles no longer waits behind a stage-empty wait.
-constexpr int kThreads = 32 * (kSoftmaxWarps + (kMerge ? 3 : 4));
-constexpr int kWarpProducer = kSoftmaxWarps, kWarpMma = kSoftmaxWarps + 1,
+#ifndef LCX_TC_MMA_WARP3  // experiment: MMA warp on sub-partition 3 (warp 11), warp 9 idle
+#define LCX_TC_MMA_WARP3 0
+#endif
+constexpr int kThreads = 32 * (kSoftmaxWarps + (kMerge && !LCX_TC_MMA_WARP3 ? 3 : 4));
+constexpr int kWarpProducer = kSoftmaxWarps,
+              kWarpMma = LCX_TC_MMA_WARP3 ? kSoftmaxWarps + 3 : kSoftmaxWarps + 1,
               kWarpPv = kMerge ? -1 : kSoftmaxWarps + 2, kWarpV = kMerge ? -1 : kSoftmaxWarps + 3,
               kWarpLoad = kMerge ? kSoftmaxWarps + 2 : -1;
 constexpr int kRingConsumers = kSoftmaxWarps + (kMerge ? 2 : 3);  // warps reading each slot
@@ -156,6 +160,17 @@ constexpr float kRescaleThresh = 8.f;
 // QK / PV MMAs issued eight / four per asm block (one elect, offsets added in PTX)
 #ifndef LCX_TC_MMA_X8
 #define LCX_TC_MMA_X8 0
+#endif
+#ifndef LCX_TC_MMA_DEPTH  // MMA products in flight before the issuer waits (0: no throttle)
+#define LCX_TC_MMA_DEPTH 0
+#endif
+constexpr int kMmaDepth = LCX_TC_MMA_DEPTH;
+static_assert(kMmaDepth >= 0 && kMmaDepth <= 4, "throttle ring of 4");
+#ifndef LCX_TC_SLEEPY_MMA  // merged MMA warp's wait for P: ns between polls (0 = try_wait)
+#define LCX_TC_SLEEPY_MMA 0
+#endif
+#ifndef LCX_TC_SLEEPY_LOAD  // loader warp's stage-empty waits
+#define LCX_TC_SLEEPY_LOAD 0
 #endif
 #ifndef LCX_TC_SLEEPY_PV  // the PV issuer's wait for P (on the critical path)
 #define LCX_TC_SLEEPY_PV 0
@@ -427,9 +442,9 @@ static_assert(sizeof(TileMeta) <= 448, "tile metadata slot overflow");
   } while (0)
 #endif
 
-__device__ __forceinline__ float ex2(float x) {
+__device__ __forceinline__ float ex2(float x) {  // pure: the compiler may schedule it
   float y;
-  asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 
@@ -472,9 +487,10 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
   const tc::SBar hand = m_empty + kMetaSlots;    // [kGroups][4] running max of a tile ready
   const tc::SBar lpub = hand + 4 * kGroups;      // [kGroups] partial sums of a tile written
   const tc::SBar edone = lpub + kGroups;         // split O: an item's epilogue read both O
+  const tc::SBar prog = edone + 1;               // [4] MMA product completions (throttle)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + OFF_BAR) +
-                        2 * (2 * NK + 2 * NV + 3 * NS + 2 + 2 * kMetaSlots + 5 * kGroups + 1);
-  static_assert((2 * NK + 2 * NV + 3 * NS + 2 + 2 * kMetaSlots + 5 * kGroups + 2) * 8 <= 1024,
+                        2 * (2 * NK + 2 * NV + 3 * NS + 2 + 2 * kMetaSlots + 5 * kGroups + 5);
+  static_assert((2 * NK + 2 * NV + 3 * NS + 2 + 2 * kMetaSlots + 5 * kGroups + 6) * 8 <= 1024,
                 "barrier area overflow");
   TileMeta* metas = reinterpret_cast<TileMeta*>(smem + OFF_META);
 
@@ -503,6 +519,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     for (int b = 0; b < 4 * kGroups; ++b) tc::mbar_init(hand + b, kArriveLanes);
     for (int b = 0; b < kGroups; ++b) tc::mbar_init(lpub + b, 4 * kArriveLanes);
     tc::mbar_init(edone, 4);
+    for (int b = 0; b < 4; ++b) tc::mbar_init(prog + b, 1);
     for (int b = 0; b < kMetaSlots; ++b) {
       tc::mbar_init(m_full + b, 32);  // every producer lane releases its own writes
       tc::mbar_init(m_empty + b, kRingConsumers * kArriveLanes);  // softmax + QK + PV + V warps
@@ -717,6 +734,12 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
   } else if (warp == kWarpMma) {
     // ========================================= QK issuer (+ PV issuer, kMerge) ====
     uint32_t T = 0, E = 0, M = 0;
+    // this warp's barrier waits: suspended try_wait, or test_wait polls with a sleep
+    // (LCX_TC_SLEEPY_MMA ns) that keep it out of the barrier unit between polls
+    auto mma_wait = [&](tc::SBar bar, uint32_t par) {
+      if constexpr (LCX_TC_SLEEPY_MMA > 0) tc::mbar_wait_sleepy(bar, par, LCX_TC_SLEEPY_MMA);
+      else tc::mbar_wait(bar, par);
+    };
     // all 32 lanes run this loop (warp-uniform); one elected lane issues
     const uint64_t dk0 = tc::sdesc_sw128(tc::smem_u32(smem + OFF_K));
     // merged PV issue: O += P(Tp) V(Tp), P aliasing S buffer Tp % NS (TS-form MMA)
@@ -727,29 +750,49 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     // P that the softmax has not produced yet (with NS = 2 S buffers QK(T + 1) needs PV(T - 1)
     // anyway: lag 1; with 4, lag 2)
     constexpr int kPvLag = NS / kGroups;
+    // Issue throttle (LCX_TC_MMA_DEPTH products in flight): a tcgen05.mma that finds the
+    // tensor pipe's queue full holds its sub-partition's dispatch, starving the softmax warp
+    // that shares it; waiting on a completion barrier instead parks this warp.
+    uint32_t nprod = 0;
+    auto throttle = [&]() {
+      if constexpr (kMmaDepth > 0) {
+        if (nprod >= uint32_t(kMmaDepth)) {
+          const uint32_t kk = nprod - kMmaDepth;
+          mma_wait(prog + int(kk % 4), (kk / 4) & 1);
+        }
+      }
+    };
+    auto product_done = [&]() {
+      if constexpr (kMmaDepth > 0) tc::mma_commit_warp(prog + int(nprod % 4));
+      ++nprod;
+    };
     int npend = 0;
     int pfl[2] = {0, 0};
     auto issue_pv = [&](uint32_t Tp, int fl) {
       const int bs = Tp % NS, bv = Tp % NV;
-      WAITP(5, tc::mbar_wait(p_full + bs, (Tp / NS) & 1));
-      WAITP(6, tc::mbar_wait(v_full + bv, (Tp / NV) & 1));
+      WAITP(5, mma_wait(p_full + bs, (Tp / NS) & 1));
+      WAITP(6, mma_wait(v_full + bv, (Tp / NV) & 1));
       tc::tc_fence_after();
       const uint64_t dv = dv0 + ((bv * kVStage) >> 4);
       if (fl & F_FIRST) T_first = Tp;
       const bool first = kSplitO ? (Tp - T_first < uint32_t(kGroups) && !(p.init && Tp == T_first))
                                  : ((fl & F_FIRST) && !p.init);
       const uint32_t dO = tmem + COL_O + (kSplitO ? (Tp % kGroups) * HD : 0);
+      throttle();
 #pragma unroll
       for (int kk = 0; kk < BN / 16; ++kk)
         tc::mma_f16_ts_warp(dO, tmem + bs * BN + kk * 8, dv + ((kk * 32) >> 4), IDESC_PV,
                             (first && kk == 0) ? 0u : 1u);
+      product_done();
       tc::mma_commit_warp(v_empty + bv);
       tc::mma_commit_warp(s_free + bs);
+#ifndef LCX_TC_TRACE_Q
       if (lane == 0) trace_mark(p, Tp, 4);
+#endif
     };
     for (;;) {
       const int slot = M % kMetaSlots;
-      WAITP(0, tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1));
+      WAITP(0, mma_wait(m_full + slot, (M / kMetaSlots) & 1));
       const int kind = metas[slot].kind;
       const int flags = metas[slot].flags;
       const int qb = kQBufs == 2 ? (metas[slot].grp & 1) : 0;  // Q buffer of the tile's group
@@ -768,15 +811,17 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       if (kind == T_END) break;
       if (kind == T_EMPTY) continue;
       if (flags & F_EPOCH) {  // first tile of a group: its Q buffer is (or will be) filled
-        WAITP(1, tc::mbar_wait(q_ready + qb, (E >> (qb * 16)) & 1));
+        WAITP(1, mma_wait(q_ready + qb, (E >> (qb * 16)) & 1));
         E += 1u << (qb * 16);  // per-buffer use counts (low / high half)
       }
       const int bk = T % NK, bs = T % NS;
-      WAITP(2, tc::mbar_wait(k_full + bk, (T / NK) & 1));
-      WAITP(3, tc::mbar_wait(s_free + bs, ((T / NS) & 1) ^ 1));  // PV(T - NS) released S/P
+      WAITP(2, mma_wait(k_full + bk, (T / NK) & 1));
+      WAITP(3, mma_wait(s_free + bs, ((T / NS) & 1) ^ 1));  // PV(T - NS) released S/P
       tc::tc_fence_after();
 #ifndef LCX_TC_TRACE_PV
+#ifndef LCX_TC_TRACE_Q
       if (lane == 0) trace_mark(p, T, 7);
+#endif
 #endif
       const uint64_t dk = dk0 + ((bk * kKStage) >> 4);
       const uint32_t dS = tmem + bs * BN;
@@ -791,6 +836,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #endif
         const uint32_t qa = tmem + COL_Q + qb * QBUF + (combo == 2 ? HD / 2 : 0);  // hh, hl, lh
         const uint64_t ka = dk + (combo == 1 ? ((2 * kKHalf) >> 4) : 0);
+        if constexpr (kMerge) throttle();
 #if LCX_TC_MMA_X8
         tc::mma_f16_ts_x8_warp(dS, qa, ka, kKHalf >> 4, IDESC_QK, combo ? 1u : 0u);
 #else
@@ -802,6 +848,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
                                 ka + ((half * kKHalf + kk * 32) >> 4), IDESC_QK,
                                 (combo | half | kk) ? 1u : 0u);
 #endif
+        if constexpr (kMerge) product_done();
       }
       tc::mma_commit_warp(k_empty + bk);
       tc::mma_commit_warp(s_full + bs);
@@ -809,7 +856,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       wacc[4] += clock64() - t_iss;
 #endif
 #ifndef LCX_TC_TRACE_PV
+#ifndef LCX_TC_TRACE_Q
       if (lane == 0) trace_mark(p, T, 3);
+#endif
 #endif
       if constexpr (kMerge) {
         if (npend == kPvLag) {  // QK(T) runs while the softmax finishes P(T - kPvLag)
@@ -830,7 +879,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     uint32_t T = 0, M = 0;
     for (;;) {
       const int slot = M % kMetaSlots;
+      #if LCX_TC_SLEEPY_LOAD
+      WAITP(0, tc::mbar_wait_sleepy(m_full + slot, (M / kMetaSlots) & 1, LCX_TC_SLEEPY_LOAD));
+#else
       WAITP(0, tc::mbar_wait(m_full + slot, (M / kMetaSlots) & 1));
+#endif
       const int kind = metas[slot].kind;
       const int h = metas[slot].h;
       const int64_t key0 = metas[slot].key0;
@@ -843,7 +896,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         const int64_t kt = kind == T_VERT ? int64_t(h) * (p.capp / 64) + key0 / 64
                                           : int64_t(h / p.group) * p.ntiles_k + key0 / 64;
         const int bk = T % NK;
+#if LCX_TC_SLEEPY_LOAD
+        WAITP(1, tc::mbar_wait_sleepy(k_empty + bk, ((T / NK) & 1) ^ 1, LCX_TC_SLEEPY_LOAD));
+#else
         WAITP(1, tc::mbar_wait(k_empty + bk, ((T / NK) & 1) ^ 1));
+#endif
         tc::mbar_expect_tx(k_full + bk, kKStage);
         const uint32_t kdst = smem_base + OFF_K + bk * kKStage;
         // pre-swizzled tiles: hi (2 halves) and lo are one contiguous 16 KB run each
@@ -851,13 +908,21 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
                       k_full + bk);
         tc::bulk_load(kdst + 2 * kKHalf, (kind == T_VERT ? p.kclo : p.klo) + kt * kKHalf,
                       2 * kKHalf, k_full + bk);
+#ifndef LCX_TC_TRACE_SM
         trace_mark(p, T, 1);
+#endif
         const int bv = T % NV;
+#if LCX_TC_SLEEPY_LOAD
+        WAITP(2, tc::mbar_wait_sleepy(v_empty + bv, ((T / NV) & 1) ^ 1, LCX_TC_SLEEPY_LOAD));
+#else
         WAITP(2, tc::mbar_wait(v_empty + bv, ((T / NV) & 1) ^ 1));
+#endif
         tc::mbar_expect_tx(v_full + bv, kVStage);
         tc::bulk_load(smem_base + OFF_V + bv * kVStage, (kind == T_VERT ? p.vct : p.vt) + kt * (kVStage / 2),
                       kVStage, v_full + bv);
+#ifndef LCX_TC_TRACE_SM
         trace_mark(p, T, 2);
+#endif
       }
       __syncwarp();
       ++T;
@@ -967,7 +1032,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     wacc[7] = clock64() - t_start;
 #endif
     WAITP_FLUSH(3);
-  } else {
+  } else if (warp < kSoftmaxWarps) {
     // ============================= softmax / correction / epilogue ====
     // kGroups warp groups take the tiles of the stream in turn (group g: tiles T with
     // T % kGroups == g); within a group, warp = TMEM lane quadrant and thread = query
@@ -1134,7 +1199,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       wacc2[4] += clock64() - t_ld;
 #endif
 #ifdef LCX_TC_TRACE_SM  // owner group's quadrant-0 warp: 5 S got, 0 m handed over, 6 P put
+#ifdef LCX_TC_TRACE_Q  // per quadrant warp: S got in column 4 + wq
+      if (lane == 0) trace_mark(p, T, 4 + wq);
+#else
       if (wq == 0 && lane == 0) trace_mark(p, T, 5);
+#endif
 #else
       if (threadIdx.x == 0) trace_mark(p, T, 5);
 #endif
@@ -1169,7 +1238,8 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       auto exps_store = [&](float m) -> float {
         const float mm = m == -INFINITY ? 0.f : m;
         const float2 nm2 = make_float2(-mm, -mm);
-        float2 rs2 = make_float2(0.f, 0.f);
+        float2 rs2[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                         make_float2(0.f, 0.f)};  // four independent sum chains
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {  // two 32-key halves: fewer live registers
           if constexpr (kSReread) {  // second read of this half (its P not yet written)
@@ -1184,13 +1254,14 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
             const int c = (kSReread ? 0 : hf * 32) + 2 * k;
             const float2 x = __fadd2_rn(make_float2(sv[c], sv[c + 1]), nm2);
             const float2 pp = make_float2(ex2(x.x), ex2(x.y));
-            rs2 = __fadd2_rn(rs2, pp);
+            rs2[k & 3] = __fadd2_rn(rs2[k & 3], pp);
             const __half2 h2 = __floats2half2_rn(pp.x, pp.y);
             pw[k] = *reinterpret_cast<const uint32_t*>(&h2);
           }
           tc::tmem_st16(tmem + lane_base + b * BN + hf * 16, pw);
         }
-        return rs2.x + rs2.y;
+        const float2 ra = __fadd2_rn(rs2[0], rs2[1]), rb = __fadd2_rn(rs2[2], rs2[3]);
+        return (ra.x + rb.x) + (ra.y + rb.y);
       };
       auto tile_max = [&]() -> float {
         float t4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
@@ -1252,6 +1323,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #ifdef LCX_TC_WAITPROF
       wacc[5] += clock64() - t_sg;
 #endif
+#ifdef LCX_TC_TRACE_SM  // column 1: tile max known (before the hand-off wait)
+      if (wq == 0 && lane == 0) trace_mark(p, T, 1);
+#endif
       // ---- running max: previous tile's (other group) unless the item starts here
       if (!kSplitO && !(flags & F_FIRST)) WAITP2(0, tc::mbar_wait(h_in, k & 1));
       const float m_prev = kSplitO ? m_used
@@ -1261,13 +1335,8 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       const bool need = tmax > m_prev + kRescaleThresh;
       const float m = need ? tmax : m_prev;
       if constexpr (!kSplitO) mbuf[grp * 128 + r] = m;
-#ifdef LCX_TC_TRACE_SM  // column 1: flags | kind << 8 | rescale << 12 (a value, not a time)
-      if (wq == 0 && lane == 0) {
-        trace_mark(p, T, 0);
-        const bool any_need = __any_sync(0x1u, need && m_prev != -INFINITY);
-        if (p.trace && blockIdx.x == 0 && T < kTraceTiles)
-          p.trace[T * 8 + 1] = flags | (kind << 8) | (int(any_need) << 12);
-      }
+#ifdef LCX_TC_TRACE_SM
+      if (wq == 0 && lane == 0) trace_mark(p, T, 0);
 #endif
       // an item's last tile hands over only after its epilogue (next item's O / Q)
       if (!kSplitO && !(flags & F_LAST)) {
@@ -1305,6 +1374,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #ifdef LCX_TC_WAITPROF
       const long long t_ex = clock64();
 #endif
+#ifdef LCX_TC_TRACE_SM  // column 2: exponentials and P stores issued (before the tail)
+      if (wq == 0 && lane == 0) trace_mark(p, T, 2);
+#endif
       tc::tmem_wait_st();
       l += rs;
       // every phase of the predecessor group's partial-sum barrier is consumed (tile T - 1
@@ -1326,7 +1398,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       wacc[6] += clock64() - t_ex;
 #endif
 #ifdef LCX_TC_TRACE_SM
+#ifdef LCX_TC_TRACE_Q  // per quadrant warp: P put in column wq
+      if (lane == 0) trace_mark(p, T, wq);
+#else
       if (wq == 0 && lane == 0) trace_mark(p, T, 6);
+#endif
 #else
       if (threadIdx.x == 0) trace_mark(p, T, 6);
 #endif

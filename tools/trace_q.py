@@ -1,4 +1,6 @@
-"""Per-tile softmax timeline of CTA 0 (build with LCX_NVCC_EXTRA='-DLCX_TC_TRACE -DLCX_TC_TRACE_SM')."""
+"""Per-quadrant-warp softmax timeline of CTA 0 (build with
+LCX_NVCC_EXTRA='-DLCX_TC_TRACE -DLCX_TC_TRACE_SM -DLCX_TC_TRACE_Q'): for each tile, when each of
+the owner group's four quadrant warps got S and put P."""
 import ctypes as C
 import sys
 import numpy as np
@@ -19,11 +21,11 @@ D.chunked_prefill(q, k, v, chunk_len=32768, last_q=64, budget=(1000, 6096),
 buf = np.zeros((512 * 8 + 64,), np.int64)
 L.lcx_debug_trace(ctx.ptr, 1, buf.ctypes.data)
 buf = buf[:4096].reshape(512, 8)
-t0 = buf[0, 7]
-print("tile grp  QKst  QKend  S_got   tmax  m_out   exps  P_put  PV_is | S-QKend max hin exp tail")
+t0 = buf[1, 4]
+print("tile grp   S_got(wq0..3)                  P_put(wq0..3)")
 for t in range(1, 400):
     b = buf[t]
-    if b[7] == 0:
+    if b[4] == 0:
         break
-    print(f"{t:4d} {t & 1:3d} " + " ".join(f"{(x - t0):6d}" for x in (b[7], b[3], b[5], b[1], b[0], b[2], b[6], b[4]))
-          + f" | {b[5] - b[3]:5d} {b[1] - b[5]:4d} {b[0] - b[1]:4d} {b[2] - b[0]:4d} {b[6] - b[2]:4d}")
+    print(f"{t:4d} {t & 1:3d} " + " ".join(f"{(x - t0):7d}" for x in b[4:8]) + "  |"
+          + " ".join(f"{(x - t0):7d}" for x in b[0:4]))
