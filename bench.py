@@ -471,7 +471,7 @@ def main():
     e2e = None
     if not a.no_e2e:
         e2e = SH.e2e(plan, qs, ks, vs, a.steps, barrier, world, dev, **kw)
-        if e2e is not None:
+        if e2e is not None and "ms_per_step" in e2e:
             e2e["value"] = a.n / (e2e.pop("ms_per_step") / 1e3)
 
     # ---- roofline of the dominant kernel (this rank's stage times) ----

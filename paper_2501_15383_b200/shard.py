@@ -321,6 +321,19 @@ def e2e(p: Plan, q, k, v, steps, barrier, world, dev, **kw):
 
 def e2e_seq(p: Plan, q, k, v, steps, barrier, world, dev, **kw):
     import torch.distributed as dist
+    # every rank pins a full copy of Q / K / V plus its output rows: skip (all ranks alike)
+    # rather than drive the host out of memory
+    need = (q.numel() + k.numel() + v.numel()) * q.element_size() + q.numel() * 4 // world
+    ok = torch.ones(1, device=dev)
+    try:
+        import psutil
+        if psutil.virtual_memory().available < 1.3 * need * world:
+            ok.zero_()
+    except ImportError:
+        pass
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if ok.item() == 0:
+        return {"value": None, "skipped": "not enough host RAM for every rank's pinned buffers"}
     qh = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
     kh = torch.empty(k.shape, dtype=k.dtype, pin_memory=True)
     vh = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
