@@ -21,11 +21,17 @@ D.chunked_prefill(q, k, v, chunk_len=32768, last_q=64, budget=(1000, 6096),
 buf = np.zeros((512 * 8 + 64,), np.int64)
 L.lcx_debug_trace(ctx.ptr, 1, buf.ctypes.data)
 buf = buf[:4096].reshape(512, 8)
-t0 = buf[1, 4]
-print("tile grp   S_got(wq0..3)                  P_put(wq0..3)")
+t0 = buf[1, 0] if (len(sys.argv) > 2 and sys.argv[2] == 'meta') else buf[1, 4]
+mode2 = len(sys.argv) > 2 and sys.argv[2] == "meta"
+print("tile grp   " + ("meta start (wq0..3) | meta phase clk (wq0..3)" if mode2 else
+                      "S_got(wq0..3)                  P_put(wq0..3)"))
 for t in range(1, 400):
     b = buf[t]
     if b[4] == 0:
         break
+    if mode2:
+        print(f"{t:4d} {t & 1:3d} " + " ".join(f"{(x - t0):7d}" for x in b[0:4]) + "  |"
+              + " ".join(f"{(y - x):6d}" for x, y in zip(b[0:4], b[4:8])))
+        continue
     print(f"{t:4d} {t & 1:3d} " + " ".join(f"{(x - t0):7d}" for x in b[4:8]) + "  |"
           + " ".join(f"{(x - t0):7d}" for x in b[0:4]))
