@@ -64,7 +64,10 @@ int ensure_rope(lcx_context* ctx, double base, int dim, int64_t P, cudaStream_t 
 
 namespace {
 
-constexpr int kDefaultTcMin = 96;  // slash entries per 64-key tile to use tcgen05
+// slash entries a 64-key relative tile needs to go to tcgen05 rather than the gather:
+// profiles/r02/sweep_tcmin_r02.jsonl (1M, 7B): planted flat over 32-160 (482-494 ms),
+// structured 5990 -> 5897 ms and iid 8262 -> 7860 ms from 96 to 160, worse again at 192
+constexpr int kDefaultTcMin = 160;
 constexpr int64_t kGatherSegment = 32768;  // keys per gather pass (L2-resident K / V)
 constexpr int64_t kTcSegment = 32768;      // keys per tcgen05 slash pass (K hi/lo + V^T)
 constexpr int64_t kWindowMinSlashes = 512;  // slash capacity from which windows are used
