@@ -102,6 +102,16 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// Pass 2 epilogue split over specialised warps (LCX_EST_SPLIT_EPI): warps 4-7 turn each
+// tile's S into probabilities (all 64 columns of a row per thread) and store them into the
+// skewed transpose buffer, warps 8-11 reduce the previous buffer into column and diagonal
+// sums, handing the two buffers back and forth on mbarriers -- the two phases of
+// consecutive tiles overlap instead of all eight warps alternating between them behind a
+// CTA barrier.
+#ifndef LCX_EST_SPLIT_EPI
+#define LCX_EST_SPLIT_EPI 1
+#endif
+
 template <int PASS>
 __global__ void __launch_bounds__(kThreads, 1)
 est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q,
@@ -115,7 +125,9 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q,
   uint64_t* s_full = k_empty + NKS_MAX; // [2]
   uint64_t* s_empty = s_full + NSB;     // [NSB]
   uint64_t* q_tmem = s_empty + NSB;     // epilogue warps copied Q into TMEM
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_tmem + 1);
+  uint64_t* t_full = q_tmem + 1;        // [2] pass 2: transpose buffer written
+  uint64_t* t_free = t_full + 2;        // [2] pass 2: transpose buffer reduced
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t_free + 2);
   float* T = reinterpret_cast<float*>(smem + OFF_Q);
 
   const Item it = decode_item(p, blockIdx.x);
@@ -127,6 +139,7 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q,
   };
   const int ntl = it.t1 - it.t0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr bool kSplitEpi = PASS == 2 && LCX_EST_SPLIT_EPI;
   if (threadIdx.x == 0) {
     tc::mbar_init(q_full, 1);
     for (int b = 0; b < NKS_MAX; ++b) {
@@ -135,9 +148,13 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q,
     }
     for (int b = 0; b < NSB; ++b) {
       tc::mbar_init(s_full + b, 1);
-      tc::mbar_init(s_empty + b, 8);
+      tc::mbar_init(s_empty + b, kSplitEpi ? 4 : 8);
     }
     tc::mbar_init(q_tmem, 8);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(t_full + b, 4 * 32);  // every lane of the 4 exp warps
+      tc::mbar_init(t_free + b, 4 * 32);  // every lane of the 4 reduction warps
+    }
     tc::fence_barrier_init();
     tc::fence_proxy_async();
   }
@@ -245,6 +262,81 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q,
       if (lane == 0) tc::mbar_arrive(q_tmem);
       asm volatile("bar.sync 1, 256;" ::: "memory");  // Q staging area free for reuse
     }
+    if constexpr (kSplitEpi) {
+      if (part == 0) {
+        // ---- exp warps: row r, all 64 columns -> probabilities -> skewed transpose ----
+        const int rr64 = r & 63;
+        for (int t = 0; t < ntl; ++t) {
+          const int sb = t % NSB;
+          const int64_t j0 = int64_t(it.t0 + t) * BN;
+          tc::mbar_wait(s_full + sb, (t / NSB) & 1);
+          tc::tc_fence_after();
+          float v[64];
+          tc::tmem_ld32(tmem + lane_base + sb * BN, v);
+          tc::tmem_ld32_wait(tmem + lane_base + sb * BN + 32, v + 32);
+          tc::tmem_wait_ld_dep32(v);
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(s_empty + sb);
+          const int64_t lim = (gi < p.nk - 1 ? gi : p.nk - 1) - j0 + 1;
+          const int nvalid = !row_ok ? 0 : (lim >= 64 ? 64 : (lim < 0 ? 0 : int(lim)));
+          const float sct = sc * __ldg(kinv + it.t0 + t);
+          // buffer t & 1 is free once the reduction warps finished tile t - 2
+          tc::mbar_wait(t_free + (t & 1), ((t >> 1) & 1) ^ 1);
+          float* Trow = T + (t & 1) * kTBuf + r * kTRow;
+          if (__all_sync(0xffffffffu, nvalid == 64)) {
+#pragma unroll
+            for (int c = 0; c < 64; ++c) Trow[(c - rr64) & 63] = ex2(fmaf(v[c], sct, -rm)) * rinv;
+          } else {
+#pragma unroll
+            for (int c = 0; c < 64; ++c)
+              Trow[(c - rr64) & 63] = c < nvalid ? ex2(fmaf(v[c], sct, -rm)) * rinv : 0.f;
+          }
+          __syncwarp();
+          tc::mbar_arrive(t_full + (t & 1));  // every lane releases its own stores
+        }
+      } else {
+        // ---- reduction warps: et = (head of the pair) x 64 + key / buffer column ----
+        const int et = threadIdx.x - 256;  // 0..127
+        const int hh2 = et >> 6, x = et & 63;
+        const int hx = g * p.group + (it.pair % p.pairs_per_group) * 2 + hh2;
+        const bool hx_ok = (it.pair % p.pairs_per_group) * 2 + hh2 < p.group;
+        for (int t = 0; t < ntl; ++t) {
+          const int64_t j0 = int64_t(it.t0 + t) * BN;
+          tc::mbar_wait(t_full + (t & 1), (t >> 1) & 1);
+          const float* hb = T + (t & 1) * kTBuf + hh2 * 64 * kTRow;
+          if (hx_ok) {
+            // column sum of key x (its row-q element sits at buffer column (x - q) & 63)
+            float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int q = 0; q < 64; q += 8)
+#pragma unroll
+              for (int u = 0; u < 8; ++u) a[u] += hb[(q + u) * kTRow + ((x - q - u) & 63)];
+            const int64_t j = j0 + x;
+            if (j < p.nk)
+              p.col_part[int64_t(hx) * p.nk + j] =
+                  ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+            // buffer column x: diagonals e = 63 - x (rows below 64 - x) and 127 - x
+            float d1[4] = {0.f, 0.f, 0.f, 0.f}, d2[4] = {0.f, 0.f, 0.f, 0.f};
+            const int lim = 64 - x;
+#pragma unroll
+            for (int q = 0; q < 64; q += 4)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const float y = hb[(q + u) * kTRow + x];
+                const bool lo = q + u < lim;
+                d1[u] += lo ? y : 0.f;
+                d2[u] += lo ? 0.f : y;
+              }
+            float* dp = p.diag_part + (int64_t(hx) * p.ntiles + it.t0 + t) * 128;
+            dp[63 - x] = (d1[0] + d1[1]) + (d1[2] + d1[3]);
+            if (x > 0) dp[127 - x] = (d2[0] + d2[1]) + (d2[2] + d2[3]);
+          }
+          __syncwarp();
+          tc::mbar_arrive(t_free + (t & 1));
+        }
+      }
+    } else
     for (int t = 0; t < ntl; ++t) {
       const int sb = t % NSB;
       const int64_t j0 = int64_t(it.t0 + t) * BN;
