@@ -353,16 +353,32 @@ est_tc_kernel(const EstTcParams p, const __grid_constant__ CUtensorMap map_q,
       const int nvalid = !row_ok ? 0 : (lim >= 32 ? 32 : (lim < 0 ? 0 : int(lim)));
       const float sct = sc * __ldg(kinv + it.t0 + t);
       if (PASS == 1) {
-        float tmax = -INFINITY;
+        float tmax = -INFINITY, ts = 0.f;
+        if (__all_sync(0xffffffffu, nvalid == 32)) {
+          // every column valid (all but the causal edge tiles): the scale is positive, so the
+          // scaled max is the max's scaled value and the scaling folds into the exponent's FMA
+          float mx[4] = {v[0], v[1], v[2], v[3]};
 #pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          v[c] = c < nvalid ? v[c] * sct : -INFINITY;
-          tmax = fmaxf(tmax, v[c]);
+          for (int c = 4; c < 32; c += 4)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) mx[u] = fmaxf(mx[u], v[c + u]);
+          tmax = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * sct;
+          float t4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int c = 0; c < 32; ++c) t4[c & 3] += ex2(fmaf(v[c], sct, -tmax));
+          ts = (t4[0] + t4[1]) + (t4[2] + t4[3]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            v[c] = c < nvalid ? v[c] * sct : -INFINITY;
+            tmax = fmaxf(tmax, v[c]);
+          }
+          if (tmax != -INFINITY) {
+#pragma unroll
+            for (int c = 0; c < 32; ++c) ts += ex2(v[c] - tmax);
+          }
         }
         if (tmax != -INFINITY) {
-          float ts = 0.f;
-#pragma unroll
-          for (int c = 0; c < 32; ++c) ts += ex2(v[c] - tmax);
           const float nm = fmaxf(m, tmax);
           s = s * ex2(m - nm) + ts * ex2(tmax - nm);
           m = nm;
