@@ -8,8 +8,8 @@ Strategies (``plan``):
           Hkv % G == 0 rank r owns whole KV heads and their query heads.  Selection and
           attention are per query head (D10), so every rank's result is exactly the
           single-GPU result for its heads.
-  seq     KV sharding with a log-sum-exp merge (the "auto" choice when Hkv % G != 0, e.g.
-          Qwen2.5-7B's 4 KV heads on 8 GPUs):
+  seq     KV sharding with a log-sum-exp merge (mode "seq", or "auto" when the query heads
+          do not split over the ranks by KV group):
             1. sharded estimator: rank r runs the Vertical-Slash estimator + selection of
                every chunk for its head pairs only (lcx phase SELECT, est_head_begin/end);
                a head's lists depend only on its own rows and the keys, so they are
@@ -116,7 +116,11 @@ def est_head_ranges(hq: int, hkv: int, world: int):
 def plan(n: int, hq: int, hkv: int, world: int, rank: int, mode: str = "auto") -> Plan:
     if world == 1:
         return Plan("single", 1, 0, n, hq, hkv, 0, 0, 0, n)
-    parts = head_partition(hq, hkv, world, split_groups=mode == "head") \
+    # auto: head sharding whenever the query heads split over the ranks by KV group (north
+    # star (e): "KV-head sharding where heads are at least the GPU count") -- no collective
+    # on the data path; KV-line sharding with the LSE merge only when asked (mode "seq") or
+    # when the heads do not split
+    parts = head_partition(hq, hkv, world, split_groups=True) \
         if mode in ("auto", "head") else None
     if parts is not None:
         h0, h1, g0, g1 = parts[rank]

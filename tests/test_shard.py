@@ -35,12 +35,14 @@ def test_head_partition_covers_every_head_once(hq, hkv, world):
 
 
 def test_plans():
-    # 7B (4 KV heads) on 8 GPUs: KV sharding with the sharded estimator (auto)
-    p = SH.plan(1 << 20, 28, 4, 8, 3)
+    # 7B (4 KV heads, 28 query heads) on 8 GPUs: each KV head's 7 query heads split 4 + 3
+    # over two ranks (auto and head), no collective on the data path
+    for mode in ("auto", "head"):
+        p = SH.plan(1 << 20, 28, 4, 8, 3, mode=mode)
+        assert p.kind == "head" and p.hkv == 1 and p.hq in (3, 4)
+    # ... or KV sharding with the sharded estimator and the LSE merge when asked for
+    p = SH.plan(1 << 20, 28, 4, 8, 3, mode="seq")
     assert p.kind == "seq" and p.notes["est_heads"] == (11, 14)
-    # ... or the unbalanced 4 + 3 query-head split when asked for explicitly
-    p = SH.plan(1 << 20, 28, 4, 8, 3, mode="head")
-    assert p.kind == "head" and p.hkv == 1 and p.hq in (3, 4)
     # 14B (8 KV heads) on 8 GPUs: whole KV heads, no collective
     p = SH.plan(1 << 20, 40, 8, 8, 3)
     assert p.kind == "head" and p.hkv == 1 and p.hq == 5
