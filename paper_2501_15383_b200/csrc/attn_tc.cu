@@ -27,13 +27,15 @@
 // accumulate); P is fp16 (<= 2^8 under a lazy-rescale threshold of 8 in log2
 // units); V is fp16.  Executed MMA work per tile = 4 units vs 2 algorithmic.
 //
-// Warp roles (384 threads): warps 0-7 softmax / correction / epilogue in two groups
-// of four that take alternate tiles (thread = query row, TMEM lane quadrant =
-// warp % 4), warp 8 producer (tile metadata ring + K loads), warp 9 QK issuer + TMEM
-// owner, warp 10 PV issuer, warp 11 V loads.  Pipelines: K (hi+lo) and V^T in four
-// shared-memory stages, S double-buffered in TMEM (2 x 64 columns) with P (fp16)
-// written over it, O in TMEM (128 columns), rotated Q hi/lo in TMEM (two buffers, one
-// per DCA pattern group parity) as the A operand of every QK MMA.
+// Warp roles (352 threads, merged configuration, control warps at the lowest ids):
+// warp 0 metadata producer (tile records into a 16-slot shared ring), warp 1 MMA issuer
+// (QK(T) on three bf16 products with Q hi/lo resident in TMEM, then PV(T - 2)) + TMEM owner,
+// warp 2 K / V^T loader (1-D bulk copies of pre-swizzled tiles), warps 3-10 softmax /
+// correction / epilogue in two groups of four that take alternate tiles and read only their
+// own ring slots (thread = query row, TMEM lane quadrant = warp % 4).  Pipelines: K (hi+lo)
+// and V^T in four shared-memory stages, S in four TMEM buffers of 64 columns with P (fp16)
+// written over it, O in TMEM (128 columns), one rotated-Q buffer (hi/lo) re-rotated at DCA
+// pattern changes.  Design notes and measurements: DESIGN.md §4.
 #include <cuda.h>
 
 #include "lcx_internal.cuh"
