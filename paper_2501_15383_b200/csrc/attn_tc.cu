@@ -1438,22 +1438,22 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #ifdef LCX_TC_TRACE_SM  // column 2: exponentials and P stores issued (before the tail)
       if (wq == 0 && lane == 0) trace_mark(p, T, 2);
 #endif
+      // P released to the PV first (its stores complete and fenced)
       tc::tmem_wait_st();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(p_full + b);
       l += rs;
       // every phase of the predecessor group's partial-sum barrier is consumed (tile T - 1
-      // released its P before this one is released, so this rarely waits); the epilogue's
-      // wait on the same phase then returns at once
+      // published before this one, so this rarely waits); the epilogue's wait on the same
+      // phase then returns at once
       if (T >= 1) {
         const uint32_t Tp = T - 1;
         tc::mbar_wait(lpub + int(Tp % kGroups), (Tp / kGroups) & 1);
       }
-      // partial (l, m) for the item's epilogue (ordered before the P release below)
+      // partial (l, m) for the item's epilogue
       lbuf[((k & 1) * kGroups + grp) * 128 + r] = make_float2(l, m_used);
-      tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        tc::mbar_arrive(p_full + b);
-      }
       LANE_ARRIVE(lpub + grp);
 #ifdef LCX_TC_WAITPROF
       wacc[6] += clock64() - t_ex;
