@@ -78,7 +78,21 @@ constexpr bool kMerge = LCX_TC_MERGE;
 #define LCX_TC_QK2 0  // measured: 330 vs 322 ms per 1M layer with the own-slot softmax
 #endif
 constexpr bool kQk2 = LCX_TC_QK2 && kMerge;
-constexpr int kThreads = 32 * (kSoftmaxWarps + (kMerge && !LCX_TC_MMA_WARP3 && !kQk2 ? 3 : 4));
+// LCX_TC_PRODUCER_LOADS (experiment): the producer issues each batch's K and V loads itself
+// (no loader warp), so only the MMA issuer shares a sub-partition with softmax warps
+#ifndef LCX_TC_PRODUCER_LOADS
+#define LCX_TC_PRODUCER_LOADS 0
+#endif
+constexpr bool kProdLoads = LCX_TC_PRODUCER_LOADS && kMerge;
+// LCX_TC_KV_LOADERS: K and V^T loads from two warps, so a K load never waits behind a V
+// stage release (which follows the PV two tiles behind)
+#ifndef LCX_TC_KV_LOADERS
+#define LCX_TC_KV_LOADERS 0
+#endif
+constexpr bool kKvLoaders = LCX_TC_KV_LOADERS && kMerge && !kProdLoads && !LCX_TC_QK2;
+constexpr int kThreads =
+    32 * (kSoftmaxWarps + (kMerge && !LCX_TC_MMA_WARP3 && !kQk2 && !kKvLoaders ? 3 : 4));
+constexpr bool kLoaderWarp = kMerge && !kProdLoads;
 // Warp ids: each sub-partition's scheduler issues from its highest-id eligible warp first,
 // so a softmax warp with a lower id than a control warp of its sub-partition is starved
 // whenever that warp is eligible -- and the group that owns it runs at its pace (the
@@ -93,11 +107,13 @@ constexpr int kCtrlBase = (LCX_TC_CTRL_FIRST && kMerge) ? 0 : kSoftmaxWarps;
 constexpr int kWarpProducer = kCtrlBase,
               kWarpMma = LCX_TC_MMA_WARP3 ? kCtrlBase + 3 : kCtrlBase + 1,
               kWarpPv = kMerge ? -1 : kCtrlBase + 2, kWarpV = kMerge ? -1 : kCtrlBase + 3,
-              kWarpLoad = kMerge ? kCtrlBase + 2 : -1,
-              kWarpMma2 = kQk2 ? kCtrlBase + 3 : -2;
+              kWarpLoad = kLoaderWarp ? kCtrlBase + 2 : -1,
+              kWarpMma2 = kQk2 ? kCtrlBase + 3 : -2,
+              kWarpLoadV = kKvLoaders ? kCtrlBase + 3 : -3;
 // warps reading each ring slot: one softmax group (slots alternate between the groups) and
 // every control warp but the producer
-constexpr int kRingConsumers = 4 + (kMerge ? (kQk2 ? 3 : 2) : 3);
+constexpr int kRingConsumers =
+    4 + (kMerge ? (kQk2 || kKvLoaders ? 3 : 2) - (kProdLoads ? 1 : 0) : 3);
 // The softmax code is written for any number of groups, but a third group needs more
 // registers than 65536 / 512 per thread: compiled at 128 it spills ~2.6 KB and ran 3.4x
 // slower (setmaxnreg does not help: ptxas still allocates for the launch-time limit).
@@ -258,7 +274,10 @@ __device__ void setup_item(const TcParams& p, int item, Item& it) {
   // KV-group-major order: the query heads of one KV head are adjacent for each row block,
   // so CTAs drawing neighbouring items read the same K / V tiles (band, dense) from L2
   // instead of each head re-streaming them from DRAM.
-#ifndef LCX_TC_HEAD_MAJOR
+#if defined(LCX_TC_BLOCK_MAJOR)  // experiment: every head of a row block adjacent
+  const int b = item / p.hq;
+  it.h = item - b * p.hq;
+#elif !defined(LCX_TC_HEAD_MAJOR)
   const int per_g = p.nblocks * p.group;
   const int gg = item / per_g;
   const int rem = item - gg * per_g;
@@ -713,7 +732,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           trace_mark(p, Tj, 0);
 #endif
         }
-        if (!kMerge && lane < nb) {
+        if ((!kMerge || kProdLoads) && lane < nb) {
           const uint32_t Tj = T + lane;
           const int bk = Tj % NK;
 #if LCX_TC_SLEEPY
@@ -746,6 +765,16 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #if !defined(LCX_TC_TRACE_PV) && !defined(LCX_TC_TRACE_SM)
           trace_mark(p, Tj, 1);
 #endif
+          if constexpr (kProdLoads) {
+            const int bv = Tj % NV;
+            tc::mbar_wait_sleepy(v_empty + bv, ((Tj / NV) & 1) ^ 1, LCX_TC_SLEEPY);
+            tc::mbar_expect_tx(v_full + bv, kVStage);
+            const int64_t vtile = my.kind == T_VERT ? int64_t(it.h) * (p.capp / 64) + my.key0 / 64
+                                                    : int64_t(it.g) * p.ntiles_k + my.key0 / 64;
+            tc::bulk_load(smem_base + OFF_V + bv * kVStage,
+                          (my.kind == T_VERT ? p.vct : p.vt) + vtile * (kVStage / 2), kVStage,
+                          v_full + bv);
+          }
         }
         __syncwarp();
         M += nb;
@@ -915,8 +944,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     wacc[7] = clock64() - t_start;
 #endif
     WAITP_FLUSH(1);
-  } else if (warp == kWarpLoad) {
+  } else if (warp == kWarpLoad || warp == kWarpLoadV) {
     // ===================================== K (hi + lo) and V^T loads (kMerge) ====
+    const bool do_k = warp == kWarpLoad, do_v = !kKvLoaders || warp == kWarpLoadV;
     uint32_t T = 0, M = 0;
     for (;;) {
       const int slot = M % kMetaSlots;
@@ -937,6 +967,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         const int64_t kt = kind == T_VERT ? int64_t(h) * (p.capp / 64) + key0 / 64
                                           : int64_t(h / p.group) * p.ntiles_k + key0 / 64;
         const int bk = T % NK;
+        if (do_k) {
 #if LCX_TC_SLEEPY_LOAD
         WAITP(1, tc::mbar_wait_sleepy(k_empty + bk, ((T / NK) & 1) ^ 1, LCX_TC_SLEEPY_LOAD));
 #else
@@ -952,7 +983,9 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #ifndef LCX_TC_TRACE_SM
         trace_mark(p, T, 1);
 #endif
+        }
         const int bv = T % NV;
+        if (do_v) {
 #if LCX_TC_SLEEPY_LOAD
         WAITP(2, tc::mbar_wait_sleepy(v_empty + bv, ((T / NV) & 1) ^ 1, LCX_TC_SLEEPY_LOAD));
 #else
@@ -964,6 +997,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
 #ifndef LCX_TC_TRACE_SM
         trace_mark(p, T, 2);
 #endif
+        }
       }
       __syncwarp();
       ++T;
