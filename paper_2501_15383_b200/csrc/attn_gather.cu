@@ -363,8 +363,12 @@ __global__ void __launch_bounds__(kWarps * 32, 3) attn_gather_diag_kernel(const 
   if (a.win_flags && !a.win_flags[a.win] && a.key_hi <= a.row_begin) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ls = lane & (kLanes - 1);
-  const int h = blockIdx.y, g = h / a.group;
-  const int64_t cta_row0 = a.row_begin + int64_t(blockIdx.x) * kRowsC;
+  // heads fastest (a.head_fast, one pass over all keys): the query heads of a KV head work
+  // on the same rows together, so a line several of them selected is read from DRAM once;
+  // rows fastest for key-window passes (the window's K / V stay in L2 across the rows)
+  const int h = a.head_fast ? blockIdx.x : blockIdx.y, g = h / a.group;
+  const int64_t cta_row0 =
+      a.row_begin + int64_t(a.head_fast ? blockIdx.y : blockIdx.x) * kRowsC;
   const int64_t w_row0 = cta_row0 + warp * kRowsW;
   const int64_t i = w_row0 + (lane / kLanes);
   const bool row_ok = i < a.row_end;
@@ -538,7 +542,8 @@ int attention_gather(const GatherArgs& a, cudaStream_t st) {
   if (rows <= 0) return LCX_OK;
   if (a.row_begin % 128 != 0) return fail(LCX_ERR_INTERNAL, "gather rows must start a block");
 #if LCX_GATHER_DIAG
-  dim3 grid(unsigned((rows + diag::kRowsC - 1) / diag::kRowsC), unsigned(a.hq));
+  const unsigned nrb = unsigned((rows + diag::kRowsC - 1) / diag::kRowsC);
+  dim3 grid = a.head_fast ? dim3(unsigned(a.hq), nrb) : dim3(nrb, unsigned(a.hq));
   diag::attn_gather_diag_kernel<<<grid, diag::kWarps * 32, 0, st>>>(a);
 #else
   dim3 grid(unsigned((rows + kRows - 1) / kRows), unsigned(a.hq));

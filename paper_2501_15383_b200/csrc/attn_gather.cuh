@@ -26,6 +26,7 @@ struct GatherArgs {
   const int4* segs; const int32_t* nseg; int64_t cap_seg;  // [hq][2 halves][cap_seg]
   float* out; float* lse; int64_t lse_stride;      // tensor-core partial in, merged out
   int64_t* simt_count;
+  int head_fast;                                   // grid: heads fastest (single pass)
 };
 
 int attention_gather(const GatherArgs& a, cudaStream_t st);
