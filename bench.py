@@ -614,6 +614,7 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "budget_1000_64": extra,
             "recall_check": recall, "scattered_inputs": scattered or None,
             "gpu_launches": int(stage["launches"]),
+            "kernel_path": "tcgen05" if ctx.stats().get("tc_path") else "cuda-core",
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -177,6 +177,10 @@ typedef struct {
   double ms_attention;     /* K3 index build + K4 attention (tcgen05 + CUDA-core) */
   double ms_tc_kernel;     /* the tcgen05 attention kernel alone */
   double ms_total;
+  int64_t tc_path;         /* 1: the call ran the tcgen05 kernels, 0: the CUDA-core kernels
+                              (fp32 storage, or bf16 with LCX_PATH_AUTO on a chunk length or
+                              DCA chunk size that is not a multiple of 128 -- the AUTO
+                              fallback also prints a one-time warning on stderr) */
 } lcx_prefill_stats;
 
 typedef struct lcx_context lcx_context;

@@ -69,7 +69,8 @@ class PrefillStatsC(C.Structure):
     _fields_ = [("chunks", C.c_int64), ("launches", C.c_int64), ("tc_tiles", C.c_int64),
                 ("simt_entries", C.c_int64), ("ms_estimate", C.c_double),
                 ("ms_select", C.c_double), ("ms_attention", C.c_double),
-                ("ms_tc_kernel", C.c_double), ("ms_total", C.c_double)]
+                ("ms_tc_kernel", C.c_double), ("ms_total", C.c_double),
+                ("tc_path", C.c_int64)]
 
 
 EXPORTS = [

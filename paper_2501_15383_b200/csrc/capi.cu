@@ -7,6 +7,7 @@
 // head), and the attention computes rows [t0, t1) over their admitted entries.
 // With Q/K/V given, a chunk depends only on K/V[0:t1]; chunks are issued
 // back-to-back on one stream, each launch covering every head.
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <cstdlib>
@@ -309,6 +310,16 @@ int resolve_path(int32_t kernel_path, const lcx_attention_input* in, int64_t chu
                 "tcgen05 path needs bf16 q/k/v, head dim 128, 128-aligned chunks and DCA "
                 "chunk size");
   *tc = (kernel_path == LCX_PATH_AUTO || kernel_path == LCX_PATH_TC) && ok;
+  if (kernel_path == LCX_PATH_AUTO && !ok && in->dtype == LCX_BF16 && in->dim == 128) {
+    static bool warned = false;  // the bf16 tensor-core path needs 128-aligned chunks
+    if (!warned) {
+      warned = true;
+      std::fprintf(stderr,
+                   "longctx_b200: bf16 prefill on the CUDA-core kernels (chunk length %lld%s"
+                   " not a multiple of 128): the tcgen05 path is several times faster\n",
+                   (long long)chunk_len, dca ? " or DCA chunk size" : "");
+    }
+  }
   return LCX_OK;
 }
 
@@ -1242,6 +1253,7 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
   }
   ctx->stats = lcx_prefill_stats{};
   ctx->stats.chunks = nchunks;
+  ctx->stats.tc_path = tc ? 1 : 0;
   ctx->stats.launches = g_launches - launches0;
   if (prof) {
     LCX_CHECK_CUDA(cudaEventSynchronize(ev[6 * (nchunks - 1) + 3]));

@@ -737,3 +737,22 @@ def test_prefill_recall_check(D, port, precision, dca, n, lq):
             assert abs(rec[ci, h] - agg) <= tol, (ci, h, rec[ci, h], agg)
     full = D.chunked_prefill(T(q), T(k), T(v), budget=(n, n), return_recall=True, **kw)
     assert float(full["recall"].min()) >= 1.0 - tol
+
+
+@pytest.mark.gpu
+def test_kernel_path_stat_reports_auto_fallback():
+    """LCX_PATH_AUTO on bf16 runs the tcgen05 kernels on 128-aligned chunks and reports the
+    CUDA-core fallback otherwise (lcx_prefill_stats.tc_path), never silently."""
+    import torch
+    from paper_2501_15383_b200 import device as D
+    from paper_2501_15383_b200._lib import context
+    ctx = context(0)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q, k, v = (torch.randn((512, h, 128), generator=g, device="cuda").to(torch.bfloat16)
+               for h in (2, 1, 1))
+    D.chunked_prefill(q, k, v, chunk_len=256, last_q=64, budget=(16, 32), ctx=ctx)
+    torch.cuda.synchronize()
+    assert ctx.stats()["tc_path"] == 1
+    D.chunked_prefill(q, k, v, chunk_len=200, last_q=64, budget=(16, 32), ctx=ctx)
+    torch.cuda.synchronize()
+    assert ctx.stats()["tc_path"] == 0
