@@ -162,9 +162,6 @@ constexpr int NS = kGroups == 3 ? 3 : ((kSplitO || kQBufs == 2) ? 2 : 4);  // S 
 static_assert(NS % kGroups == 0, "each group must see every phase of its S buffers");
 static_assert(NS / kGroups <= 2, "PV lag");
 static_assert(!kSplitO || NS == kGroups, "split O: S(T) full implies PV(T - kGroups) done");
-// the softmax groups read only their own ring slots and count items per group; split O's
-// epilogue barrier counts items CTA-wide (LCX_TC_SPLIT_O is a closed round-1 experiment)
-static_assert(!kSplitO, "split O needs every group to see every item start");
 constexpr uint32_t kKHalf = BN * 64 * 2;             // 8 KB
 constexpr uint32_t kKStage = 4 * kKHalf;             // hi0 hi1 lo0 lo1 = 32 KB
 constexpr uint32_t kVStage = HD * BN * 2;            // 16 KB
@@ -435,6 +432,7 @@ struct TileMeta {
   int32_t h, count, nfar, grp;  // grp: the tile's pattern group within its item
   int32_t gpat[3], ng;          // the item's group patterns and group count
   int32_t item_t0;              // stream index T of the item's first tile
+  int32_t item_seq;             // non-empty items this CTA started before this one
   int64_t i0, rend, key0, sbase;
   uint64_t vmask;
   uint32_t sw[8];
@@ -594,6 +592,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     // metadata ring, publishes it and issues its K loads -- the batch's global loads and
     // its four ring slots are all in flight at once.
     uint32_t T = 0, M = 0;
+    int32_t item_seq = 0;  // non-empty items started
     const Item* plans = reinterpret_cast<const Item*>(p.plans);
     auto slot_wait = [&](uint32_t mm) {
 #if LCX_TC_SLEEPY
@@ -639,6 +638,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         continue;
       }
       int carry_grp = -1;
+      ++item_seq;
       for (int tb = 0; tb < it.ntiles; tb += 4) {
         const int nb = min(4, it.ntiles - tb);
         // A: lane j <= nb resolves tile tb + j (lane nb: the next tile's group)
@@ -695,6 +695,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
           mt.gpat[2] = it.grp[2].pattern;
           mt.ng = it.ng;
           mt.item_t0 = int32_t(T - tb);  // T counts this batch's first tile
+          mt.item_seq = item_seq - 1;
           mt.h = it.h;
           mt.count = my.count;
           mt.i0 = it.i0;
@@ -1122,7 +1123,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     const int r = wq * 32 + lane;
     const uint32_t lane_base = uint32_t(wq * 32) << 16;
     const uint32_t col_o = COL_O + (kSplitO ? uint32_t(grp) * HD : 0u);  // this group's O
-    uint32_t J = 0, J_cur = 0;  // split O: items started, index of the current one
+    uint32_t J_cur = 0;  // split O: the CTA's index of the current item (record item_seq)
     float* mbuf = reinterpret_cast<float*>(smem + OFF_RED);  // [kGroups][128] m after tile
     float2* lbuf = reinterpret_cast<float2*>(smem + OFF_RED + kGroups * 128 * 4);
     const tc::SBar h_in = hand + (((grp + kGroups - 1) % kGroups) * 4 + wq);  // predecessor
@@ -1185,6 +1186,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       const int pattern = mt.pattern, tgrp = mt.grp, ng = mt.ng, next_pattern = mt.next_pattern;
       const int gpat1 = mt.gpat[1], gpat2 = mt.gpat[2];
       const int32_t item_t0 = mt.item_t0;
+      const int32_t item_seq = mt.item_seq;
       __syncwarp();
       LANE_ARRIVE(m_empty + slot);
 #ifdef LCX_TC_WAITPROF
@@ -1211,7 +1213,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         l = 0.f;
         m_used = -INFINITY;
         T_first = uint32_t(item_t0);
-        J_cur = J++;
+        J_cur = uint32_t(item_seq);
         qi.i0 = i0;
         qi.rend = rend;
         qi.h = h;
