@@ -160,7 +160,7 @@ constexpr int kOBufs = kSplitO ? kGroups : 1;
 constexpr int NK = 4, NV = 4;  // K / V smem stages
 constexpr int NS = kGroups == 3 ? 3 : ((kSplitO || kQBufs == 2) ? 2 : 4);  // S (+P) TMEM
 static_assert(NS % kGroups == 0, "each group must see every phase of its S buffers");
-static_assert(NS / kGroups <= 2, "PV lag");
+
 static_assert(!kSplitO || NS == kGroups, "split O: S(T) full implies PV(T - kGroups) done");
 constexpr uint32_t kKHalf = BN * 64 * 2;             // 8 KB
 constexpr uint32_t kKStage = 4 * kKHalf;             // hi0 hi1 lo0 lo1 = 32 KB
@@ -818,7 +818,11 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
     // tile T - kPvLag is issued after QK(T), so the QK of the next tiles never waits for a
     // P that the softmax has not produced yet (with NS = 2 S buffers QK(T + 1) needs PV(T - 1)
     // anyway: lag 1; with 4, lag 2)
-    constexpr int kPvLag = NS / kGroups;
+#ifndef LCX_TC_PV_LAG
+#define LCX_TC_PV_LAG 0  // 0: NS / kGroups
+#endif
+    constexpr int kPvLag = LCX_TC_PV_LAG > 0 ? LCX_TC_PV_LAG : NS / kGroups;
+    static_assert(kPvLag >= 1 && kPvLag <= 3 && kPvLag < NS, "PV lag");
     // Issue throttle (LCX_TC_MMA_DEPTH products in flight): a tcgen05.mma that finds the
     // tensor pipe's queue full holds its sub-partition's dispatch, starving the softmax warp
     // that shares it; waiting on a completion barrier instead parks this warp.
@@ -836,7 +840,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       ++nprod;
     };
     int npend = 0;
-    int pfl[2] = {0, 0};
+    int pfl[3] = {0, 0, 0};
     auto issue_pv = [&](uint32_t Tp, int fl) {
       const int bs = Tp % NS, bv = Tp % NV;
       WAITP(5, mma_wait(p_full + bs, (Tp / NS) & 1));
@@ -935,6 +939,7 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
         if (npend == kPvLag) {  // QK(T) runs while the softmax finishes P(T - kPvLag)
           issue_pv(T - kPvLag, pfl[0]);
           pfl[0] = pfl[1];
+          pfl[1] = pfl[2];
           --npend;
         }
         pfl[npend++] = flags;
