@@ -1488,10 +1488,12 @@ attn_tc_kernel(const TcParams p, const __grid_constant__ CUtensorMap map_k_hi,
       // every phase of the predecessor group's partial-sum barrier is consumed (tile T - 1
       // published before this one, so this rarely waits); the epilogue's wait on the same
       // phase then returns at once
+#ifndef LCX_TC_NO_LPUB_WAIT  // experiment: skip the per-tile phase consumption
       if (T >= 1) {
         const uint32_t Tp = T - 1;
         tc::mbar_wait(lpub + int(Tp % kGroups), (Tp / kGroups) & 1);
       }
+#endif
       // partial (l, m) for the item's epilogue
       lbuf[((k & 1) * kGroups + grp) * 128 + r] = make_float2(l, m_used);
       __syncwarp();
