@@ -350,6 +350,9 @@ constexpr int kLanes = 4;                  // lanes per row
 constexpr int kRowsW = 32 / kLanes;        // rows per warp
 constexpr int kWarps = 4;                  // warps per CTA
 constexpr int kRowsC = kRowsW * kWarps;    // rows per CTA (within one 64-row half)
+#ifndef LCX_GATHER_DIAG_MINB
+#define LCX_GATHER_DIAG_MINB 3  // resident CTAs per SM (register budget)
+#endif
 static_assert(64 % kRowsC == 0, "a CTA's rows lie in one half-block");
 
 __device__ __forceinline__ int64_t qpos(const GatherArgs& a, int pattern, int64_t i, int64_t imod) {
@@ -359,7 +362,7 @@ __device__ __forceinline__ int64_t qpos(const GatherArgs& a, int pattern, int64_
   return a.c - 1;
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 3) attn_gather_diag_kernel(const GatherArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, LCX_GATHER_DIAG_MINB) attn_gather_diag_kernel(const GatherArgs a) {
   if (a.win_flags && !a.win_flags[a.win] && a.key_hi <= a.row_begin) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ls = lane & (kLanes - 1);
