@@ -66,7 +66,11 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the (V, 64) budget line")
     ap.add_argument("--cpu-reps", type=int, default=3)
-    ap.add_argument("--shard", default="auto", choices=["auto", "head", "seq"])
+    ap.add_argument("--shard", default="auto", choices=["auto", "head", "head-split", "seq"],
+                    help="auto / head: query heads by KV group, or (when a KV head's query heads "
+                         "do not divide over its GPUs) all of them over a cost-balanced chunk "
+                         "range; head-split: the uneven query-head split instead; seq: KV-line "
+                         "sharding with the LSE merge")
     return ap.parse_args()
 
 
@@ -402,7 +406,7 @@ def main():
     # every rank generates the same seeded full inputs, then keeps its shard
     q, k, v = make_qkv(a.n, a.hq, a.hkv, kind=a.kind, seed=a.seed, rope_base=a.rope_base,
                        device=dev)
-    plan = SH.plan(a.n, a.hq, a.hkv, world, rank, a.shard)
+    plan = SH.plan(a.n, a.hq, a.hkv, world, rank, a.shard, chunk_len=a.chunk)
     qs, ks, vs = SH.take(plan, q, k, v)
     del q, k, v
     torch.cuda.empty_cache()
@@ -431,6 +435,8 @@ def main():
     recall = None
     if "recall" in r:
         rc = r["recall"].float()
+        if plan.chunks is not None:  # this rank computes its chunk range only
+            rc = rc[plan.chunks[0]:plan.chunks[1]]
         recall = {"mean": float(rc.mean()), "min": float(rc.min()),
                   "rows": f"last {a.last_q} rows of each chunk, all heads on this rank",
                   "definition": "mean min(1, exp(lse_sparse - lse_dense)) (refine.cpp:51-72)"}

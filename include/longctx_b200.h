@@ -139,6 +139,11 @@ typedef struct {
   /* != 0: record a context-owned CUDA event once chunk c's out / lse rows are final
    * (see lcx_stream_wait_chunk) */
   int32_t record_chunk_events;
+  /* chunks [chunk_begin, chunk_end) only (0 / 0 = every chunk): the keys of the earlier
+   * chunks are still prepared, their rows (and those of later chunks) are left untouched --
+   * a query head's chunks split over GPUs with no exchange (multi-GPU head sharding when a
+   * KV head's query heads do not divide evenly over its GPUs) */
+  int32_t chunk_begin, chunk_end;
 } lcx_prefill_config;
 
 enum { LCX_PHASE_ALL = 0, LCX_PHASE_SELECT = 1, LCX_PHASE_ATTEND = 2 };

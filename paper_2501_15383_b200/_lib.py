@@ -55,7 +55,8 @@ class PrefillConfigC(C.Structure):
                 ("tc_min_entries", C.c_int32), ("shard_rank", C.c_int32),
                 ("shard_count", C.c_int32), ("phase", C.c_int32),
                 ("est_head_begin", C.c_int32), ("est_head_end", C.c_int32),
-                ("record_chunk_events", C.c_int32)]
+                ("record_chunk_events", C.c_int32), ("chunk_begin", C.c_int32),
+                ("chunk_end", C.c_int32)]
 
 
 class PrefillOutputC(C.Structure):

@@ -924,9 +924,14 @@ int lcx_chunked_prefill_host(lcx_context* ctx, const lcx_attention_input* hin,
                              static_cast<const char*>(h) + t0 * row_bytes,
                              (t1 - t0) * row_bytes, cudaMemcpyHostToDevice, ctx->h2d);
     };
-    if (cp(dq, hin->q, size_t(hq) * dim * es) != cudaSuccess ||
-        cp(dk, hin->k, size_t(hkv) * dim * es) != cudaSuccess ||
-        cp(dv, hin->v, size_t(hkv) * dim * es) != cudaSuccess ||
+    // a chunk range (cfg->chunk_begin / chunk_end) reads the query rows of its chunks only and
+    // the keys / values up to its last chunk
+    const bool ranged = cfg->chunk_end > cfg->chunk_begin;
+    const bool need_q = !ranged || (c >= cfg->chunk_begin && c < cfg->chunk_end);
+    const bool need_kv = !ranged || c < cfg->chunk_end;
+    if ((need_q && cp(dq, hin->q, size_t(hq) * dim * es) != cudaSuccess) ||
+        (need_kv && cp(dk, hin->k, size_t(hkv) * dim * es) != cudaSuccess) ||
+        (need_kv && cp(dv, hin->v, size_t(hkv) * dim * es) != cudaSuccess) ||
         cudaEventRecord(ready[c], ctx->h2d) != cudaSuccess)
       rc = fail(LCX_ERR_CUDA, "host-to-device copy failed");
   }
@@ -1139,9 +1144,32 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
     LCX_CHECK_CUDA(cudaEventRecord(ev[6 * nchunks], st));
   }
 
+  // chunk range of this call (multi-GPU: a head's chunks split over GPUs)
+  const int64_t cb = cfg->chunk_end > cfg->chunk_begin ? std::max<int64_t>(0, cfg->chunk_begin) : 0;
+  const int64_t ce = cfg->chunk_end > cfg->chunk_begin ? std::min<int64_t>(nchunks, cfg->chunk_end)
+                                                        : nchunks;
   for (int64_t ci = 0; ci < nchunks; ++ci) {
     const int64_t t0 = ci * L, t1 = std::min(n, t0 + L);
     const int64_t block = std::min(cfg->last_q, t1 - t0);
+    if (ci < cb || ci >= ce) {
+      // outside the range: only the keys this chunk appends are prepared (a later chunk of
+      // the range reads them), nothing is computed or written
+      cudaEvent_t* e = prof ? &ev[6 * ci] : nullptr;
+      if (ready) LCX_CHECK_CUDA(cudaStreamWaitEvent(st, ready[ci], 0));
+      if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[0], st));
+      if (ci < cb) {
+        if (tc && do_attend)
+          LCX_TRY(tc_prepare_rows(in->k, in->v, n, t0, t1, in->hkv, in->positions_k, dca ? 1 : 0,
+                                  s, ctx->rope, w.B, st));
+        if (sparse && do_select && est_tc)
+          LCX_TRY(est_tc_prepare_keys(in->k, t0, t1, in->hkv, k3_tiles, ctx->rope, k3, st));
+      }
+      if (prof)
+        for (int x = 1; x < 6; ++x) LCX_CHECK_CUDA(cudaEventRecord(e[x], st));
+      if (done) LCX_CHECK_CUDA(cudaEventRecord(done[ci], st));
+      if (cfg->record_chunk_events) LCX_CHECK_CUDA(cudaEventRecord(ctx->chunk_done[size_t(ci)], st));
+      continue;
+    }
     int32_t* vlist = out->sel_verticals ? out->sel_verticals + ci * hq * cap_v : iv;
     int32_t* vcnt = out->sel_nv ? out->sel_nv + ci * hq : inv;
     int32_t* slist = out->sel_slashes ? out->sel_slashes + ci * hq * cap_s : is;
@@ -1211,7 +1239,7 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
     // floating-point accumulation order -- deterministic.
     if (sparse && tc) {
       w.windows = false;
-      if (ci > 0 && cap_s > kWindowMinSlashes) {
+      if (ci > cb && cap_s > kWindowMinSlashes) {
         LCX_CHECK_CUDA(cudaEventSynchronize(ctx->far_ev[(ci - 1) & 1]));
         const int* fh = ctx->far_host + 2 * ((ci - 1) & 1);
         w.windows = fh[1] > 0 && 2 * int64_t(fh[0]) > int64_t(fh[1]);

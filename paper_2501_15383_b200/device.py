@@ -92,7 +92,7 @@ def chunked_prefill(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
                     kernel_path="auto", return_selections=True, return_admitted=False,
                     tc_min_entries=0, out=None, lse=None, stream=None, ctx=None, shard=None,
                     return_recall=False, phase="all", est_heads=None, selections=None,
-                    record_chunk_events=False):
+                    record_chunk_events=False, chunks=None):
     """longctx::chunked_prefill (sparse.hpp:125-129) over all heads of one layer.
 
     shard=(rank, count): KV-line sharding -- out / lse are this shard's partials
@@ -102,7 +102,8 @@ def chunked_prefill(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
     phase "select" / "attend" (sharded layers, shard.py): estimator + selection only (for
     query heads est_heads = (h0, h1)), or attention only over the given ``selections``
     (dict verticals / nv / slashes / ns, as returned).  record_chunk_events: per-chunk
-    completion events (see stream_wait_chunk)."""
+    completion events (see stream_wait_chunk).  chunks=(c0, c1): compute chunks [c0, c1)
+    only -- the earlier chunks' keys are still prepared, other rows are left untouched."""
     inp = make_input(q, k, v, positions_q, positions_k, rope_base, temperature)
     opts = opts or Options()
     n, hq, dim = q.shape
@@ -143,7 +144,8 @@ def chunked_prefill(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
     cfg = PrefillConfigC(int(chunk_len), int(last_q), bv, bs, PREFILL_MODES[mode], pm,
                          _chunk(dca) or ChunkConfigC(0, 0, 0), opts.c(),
                          KERNEL_PATHS[kernel_path], int(tc_min_entries), int(sr), int(sc),
-                         phases[phase], int(eh0), int(eh1), int(bool(record_chunk_events)))
+                         phases[phase], int(eh0), int(eh1), int(bool(record_chunk_events)),
+                         *(chunks if chunks is not None else (0, 0)))
     o = PrefillOutputC(out.data_ptr(), lse.data_ptr(),
                        sel["verticals"].data_ptr() if sel else None,
                        sel["nv"].data_ptr() if sel else None,
@@ -318,7 +320,7 @@ def lse_merge(o_parts, lse_parts, *, stream=None, ctx=None):
 def chunked_prefill_host(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
                          position_mode="standard", dca=None, opts: Options | None = None,
                          rope_base=1e4, temperature=1.0, kernel_path="auto", out=None, lse=None,
-                         return_selections=False, stream=None, ctx=None, device=0):
+                         return_selections=False, stream=None, ctx=None, device=0, chunks=None):
     """chunked_prefill on HOST tensors (CPU, ideally pinned) through
     lcx_chunked_prefill_host: chunk-pipelined H2D / compute / D2H inside the library.
     Returns host tensors (out [n, hq, dim] fp32, lse [hq, n] fp32, selections)."""
@@ -351,6 +353,8 @@ def chunked_prefill_host(q, k, v, *, chunk_len, last_q, budget, mode="sparse",
     cfg = PrefillConfigC(int(chunk_len), int(last_q), bv, bs, PREFILL_MODES[mode], pm,
                          _chunk(dca) or ChunkConfigC(0, 0, 0), opts.c(),
                          KERNEL_PATHS[kernel_path], 0, 0, 1)
+    if chunks is not None:
+        cfg.chunk_begin, cfg.chunk_end = int(chunks[0]), int(chunks[1])
     o = PrefillOutputC(out.data_ptr(), lse.data_ptr(),
                        sel["verticals"].data_ptr() if sel else None,
                        sel["nv"].data_ptr() if sel else None,

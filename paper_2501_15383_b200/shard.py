@@ -54,12 +54,14 @@ class Plan:
     row0: int = 0      # first output row owned after the merge ("seq")
     rows: int = 0      # output rows owned after the merge
     notes: dict = field(default_factory=dict)
+    chunks: tuple | None = None  # head plans: this rank's chunk range [c0, c1) (None = all)
 
     def describe(self) -> str:
         if self.kind == "single":
             return "1 GPU"
         if self.kind == "head":
-            return (f"head-sharded x{self.world} ({self.hq} Q / {self.hkv} KV heads on rank "
+            rng = f", chunks [{self.chunks[0]}, {self.chunks[1]})" if self.chunks else ""
+            return (f"head-sharded x{self.world} ({self.hq} Q / {self.hkv} KV heads{rng} on rank "
                     f"{self.rank}; no collective)")
         return (f"KV-sharded x{self.world}: estimator split by head pairs (selections "
                 f"all_reduced), each row's KV entries split by line, per-chunk LSE merge "
@@ -113,19 +115,50 @@ def est_head_ranges(hq: int, hkv: int, world: int):
     return out
 
 
-def plan(n: int, hq: int, hkv: int, world: int, rank: int, mode: str = "auto") -> Plan:
+def chunk_split(nchunks: int, parts: int, depth_weight: float = 0.063):
+    """Contiguous chunk ranges of about equal cost for `parts` ranks sharing a query head.
+    Chunk c costs 1 + depth_weight * (c + 1): a constant part (every row admits ~V + S
+    entries) plus a part growing with the keys before it (the estimator scores all of them,
+    and the far vertical / slash tiles grow with depth); depth_weight fitted to the per-rank
+    times of tools/shard_emulate.py at 1M tokens (chunks [0, 17) vs [17, 32): 55 vs 80 ms)."""
+    cost = [1.0 + depth_weight * (c + 1) for c in range(nchunks)]
+    total = sum(cost)
+    bounds, acc, c = [0], 0.0, 0
+    for p in range(1, parts):
+        target = total * p / parts
+        while c < nchunks and acc + cost[c] / 2 <= target:
+            acc += cost[c]
+            c += 1
+        bounds.append(c)
+    bounds.append(nchunks)
+    return [(bounds[i], bounds[i + 1]) for i in range(parts)]
+
+
+def plan(n: int, hq: int, hkv: int, world: int, rank: int, mode: str = "auto",
+         chunk_len: int = 32768) -> Plan:
     if world == 1:
         return Plan("single", 1, 0, n, hq, hkv, 0, 0, 0, n)
+    group = hq // hkv
+    if mode in ("auto", "head") and hkv % world != 0 and world % hkv == 0 \
+            and group % (world // hkv) != 0:
+        # the query heads of a KV head do not divide over its ranks (7B: 7 heads, 2 ranks):
+        # every rank takes all of its KV head's query heads and a cost-balanced contiguous
+        # range of the chunks -- balanced work, still no collective
+        split = world // hkv
+        g = rank // split
+        nch = -(-n // chunk_len)
+        rng = chunk_split(nch, split)[rank % split]
+        return Plan("head", world, rank, n, group, 1, g * group, g, 0, n, chunks=rng)
     # auto: head sharding whenever the query heads split over the ranks by KV group (north
     # star (e): "KV-head sharding where heads are at least the GPU count") -- no collective
     # on the data path; KV-line sharding with the LSE merge only when asked (mode "seq") or
     # when the heads do not split
     parts = head_partition(hq, hkv, world, split_groups=True) \
-        if mode in ("auto", "head") else None
+        if mode in ("auto", "head", "head-split") else None
     if parts is not None:
         h0, h1, g0, g1 = parts[rank]
         return Plan("head", world, rank, n, h1 - h0, g1 - g0, h0, g0, 0, n)
-    if mode == "head":
+    if mode in ("head", "head-split"):
         raise ValueError(f"cannot head-shard {hq}Q/{hkv}KV over {world} ranks")
     rows = n // world
     eh = est_head_ranges(hq, hkv, world)[rank]
@@ -225,6 +258,8 @@ def seq_row_ranges(n: int, chunk_len: int, world: int, rank: int):
 
 def prefill(p: Plan, q, k, v, **kw):
     if p.kind != "seq":
+        if p.chunks is not None:
+            kw = dict(kw, chunks=p.chunks)
         return D.chunked_prefill(q, k, v, **kw)
     kw = dict(kw)
     kw.pop("return_selections", None)
@@ -295,6 +330,8 @@ def e2e(p: Plan, q, k, v, steps, barrier, world, dev, **kw):
     oh = torch.empty((n, hq, dim), dtype=torch.float32, pin_memory=True)
     lh = torch.empty((hq, n), dtype=torch.float32, pin_memory=True)
     kw = dict(kw)
+    if p.chunks is not None:
+        kw["chunks"] = p.chunks
     # one untimed call sizes the staging buffers
     D.chunked_prefill_host(qh, kh, vh, out=oh, lse=lh, return_selections=True,
                            device=dev.index, **kw)

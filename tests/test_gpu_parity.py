@@ -756,3 +756,44 @@ def test_kernel_path_stat_reports_auto_fallback():
     D.chunked_prefill(q, k, v, chunk_len=200, last_q=64, budget=(16, 32), ctx=ctx)
     torch.cuda.synchronize()
     assert ctx.stats()["tc_path"] == 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["device", "host"])
+def test_chunk_range_matches_full_prefill(kind):
+    """chunks=(c0, c1) computes exactly the full run's rows of chunks [c0, c1) (bitwise),
+    selections and admitted counts included, and leaves the other rows untouched -- the
+    multi-GPU plan that splits a query head's chunks over two ranks relies on it."""
+    import torch
+    from paper_2501_15383_b200 import device as D
+    g = torch.Generator(device="cuda").manual_seed(11)
+    n, L = 2048, 512
+    q, k, v = (torch.randn((n, h, 128), generator=g, device="cuda").to(torch.bfloat16)
+               for h in (4, 2, 2))
+    kw = dict(chunk_len=L, last_q=64, budget=(32, 96), position_mode="dca_continuous",
+              dca=(1024, 2048, 1024), rope_base=1e4)
+    full = D.chunked_prefill(q, k, v, return_admitted=True, **kw)
+    torch.cuda.synchronize()
+    c0, c1 = 1, 3
+    if kind == "device":
+        out = torch.full((n, 4, 128), 7.0, device="cuda")
+        lse = torch.full((4, n), 7.0, device="cuda")
+        part = D.chunked_prefill(q, k, v, out=out, lse=lse, return_admitted=True,
+                                 chunks=(c0, c1), **kw)
+        torch.cuda.synchronize()
+        assert torch.equal(part["admitted"][c0:c1], full["admitted"][c0:c1])
+        assert int(part["admitted"][:c0].sum()) == 0 and int(part["admitted"][c1:].sum()) == 0
+        o, l_ = out.cpu(), lse.cpu()
+    else:
+        hq_, hk_, hv_ = (x.cpu().pin_memory() for x in (q, k, v))
+        out = torch.full((n, 4, 128), 7.0).pin_memory()
+        lse = torch.full((4, n), 7.0).pin_memory()
+        part = D.chunked_prefill_host(hq_, hk_, hv_, out=out, lse=lse, return_selections=True,
+                                      chunks=(c0, c1), **kw)
+        o, l_ = out, lse
+    r0, r1 = c0 * L, c1 * L
+    assert torch.equal(o[r0:r1], full["out"][r0:r1].cpu())
+    assert torch.equal(l_[:, r0:r1], full["lse"][:, r0:r1].cpu())
+    assert torch.all(o[:r0] == 7.0) and torch.all(o[r1:] == 7.0)
+    for key in ("verticals", "nv", "slashes", "ns"):
+        assert torch.equal(part[key][c0:c1].cpu(), full[key][c0:c1].cpu()), key

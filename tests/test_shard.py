@@ -35,11 +35,19 @@ def test_head_partition_covers_every_head_once(hq, hkv, world):
 
 
 def test_plans():
-    # 7B (4 KV heads, 28 query heads) on 8 GPUs: each KV head's 7 query heads split 4 + 3
-    # over two ranks (auto and head), no collective on the data path
+    # 7B (4 KV heads, 28 query heads) on 8 GPUs: each KV head's two ranks take all 7 query
+    # heads and complementary cost-balanced chunk ranges (auto and head), no collective
     for mode in ("auto", "head"):
-        p = SH.plan(1 << 20, 28, 4, 8, 3, mode=mode)
-        assert p.kind == "head" and p.hkv == 1 and p.hq in (3, 4)
+        ps = [SH.plan(1 << 20, 28, 4, 8, r, mode=mode) for r in range(8)]
+        assert all(p.kind == "head" and p.hkv == 1 and p.hq == 7 for p in ps)
+        for g in range(4):
+            a, b = ps[2 * g], ps[2 * g + 1]
+            assert a.g0 == b.g0 == g and a.h0 == b.h0 == 7 * g
+            assert a.chunks[0] == 0 and a.chunks[1] == b.chunks[0] and b.chunks[1] == 32
+            assert 16 <= a.chunks[1] <= 22
+    # the uneven 4 + 3 query-head split when asked for
+    p = SH.plan(1 << 20, 28, 4, 8, 3, mode="head-split")
+    assert p.kind == "head" and p.hkv == 1 and p.hq in (3, 4) and p.chunks is None
     # ... or KV sharding with the sharded estimator and the LSE merge when asked for
     p = SH.plan(1 << 20, 28, 4, 8, 3, mode="seq")
     assert p.kind == "seq" and p.notes["est_heads"] == (11, 14)
@@ -51,6 +59,11 @@ def test_plans():
     assert SH.plan(1 << 20, 28, 4, 1, 0).kind == "single"
     with pytest.raises(ValueError):
         SH.plan(1 << 20, 28, 4, 3, 0, mode="head")
+    # chunk ranges cover every chunk once, contiguously
+    for parts in (2, 3, 4):
+        rs = SH.chunk_split(32, parts)
+        assert rs[0][0] == 0 and rs[-1][1] == 32
+        assert all(rs[i][1] == rs[i + 1][0] for i in range(parts - 1))
 
 
 @pytest.mark.parametrize("hq,hkv", [(28, 4), (40, 8), (14, 2), (4, 2)])
