@@ -66,11 +66,15 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the (V, 64) budget line")
     ap.add_argument("--cpu-reps", type=int, default=3)
-    ap.add_argument("--shard", default="auto", choices=["auto", "head", "head-split", "seq"],
-                    help="auto / head: query heads by KV group, or (when a KV head's query heads "
-                         "do not divide over its GPUs) all of them over a cost-balanced chunk "
-                         "range; head-split: the uneven query-head split instead; seq: KV-line "
-                         "sharding with the LSE merge")
+    ap.add_argument("--shard", default="auto",
+                    choices=["auto", "balanced", "head", "head-split", "seq"],
+                    help="balanced (auto when GPUs >= KV heads): (KV head, chunk) units cut "
+                         "into min-max parts by costs measured in an untimed calibration run; "
+                         "head (auto below that): query heads by "
+                         "KV group, or (when a KV head's query heads do not divide over its "
+                         "GPUs) all of them over a modelled chunk range; head-split: the "
+                         "uneven query-head split instead; seq: KV-line sharding with the LSE "
+                         "merge")
     return ap.parse_args()
 
 
@@ -355,6 +359,12 @@ def run_reference(a, rank):
 
 
 # ------------------------------------------------------------------- ours --
+# LCX_BENCH_ONE_DEVICE=1: every rank on cuda:0 over gloo -- a functional dry run of the
+# multi-rank path (calibration broadcast, balanced parts, max-over-ranks timing) on a box
+# with one GPU; the ranks share the GPU, so its numbers are not measurements
+ONE_DEVICE = os.environ.get("LCX_BENCH_ONE_DEVICE") == "1"
+
+
 def relaunch(a):
     """`bench.py --gpus N` (N > 1) outside torchrun: start N NCCL ranks on this node
     (one process per GPU), the same launch the driver uses.  Fails loudly when the node
@@ -362,7 +372,7 @@ def relaunch(a):
     import socket
     import torch
     have = torch.cuda.device_count()
-    if have < a.gpus:
+    if have < a.gpus and not ONE_DEVICE:
         sys.stderr.write(f"bench.py: --gpus {a.gpus} but this node has {have} CUDA device(s)\n")
         sys.exit(2)
     s = socket.socket()
@@ -396,9 +406,14 @@ def main():
     from paper_2501_15383_b200._lib import context
     from paper_2501_15383_b200.synth import make_qkv
 
+    if ONE_DEVICE:  # dry run of the multi-rank path on a one-GPU box (numbers invalid)
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if ONE_DEVICE:  # NCCL refuses two ranks on one device
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     s, c = a.dca
     dca = (s, c, min(s, c - s))
@@ -406,19 +421,37 @@ def main():
     # every rank generates the same seeded full inputs, then keeps its shard
     q, k, v = make_qkv(a.n, a.hq, a.hkv, kind=a.kind, seed=a.seed, rope_base=a.rope_base,
                        device=dev)
-    plan = SH.plan(a.n, a.hq, a.hkv, world, rank, a.shard, chunk_len=a.chunk)
-    qs, ks, vs = SH.take(plan, q, k, v)
-    del q, k, v
-    torch.cuda.empty_cache()
     ctx = context(local)
     ctx.set_profiling(True)
     kw = dict(chunk_len=a.chunk, last_q=a.last_q, budget=tuple(a.budget),
               position_mode="dca_continuous", dca=dca, temperature=temp, rope_base=a.rope_base)
+    plan = SH.plan(a.n, a.hq, a.hkv, world, rank, "head" if a.shard == "balanced" else a.shard,
+                   chunk_len=a.chunk)
+    if world > 1 and (a.shard == "balanced" or (a.shard == "auto" and world >= a.hkv)):
+        # cost-balanced head sharding: rank 0 measures every (KV head, chunk) unit of this
+        # layer in an untimed calibration run and broadcasts the table (setup, not the data
+        # path); every rank then cuts the same min-max partition (shard.balanced_plan).
+        # auto uses it from one KV head per GPU on: with several KV heads per GPU the static
+        # plan's single call over whole KV heads is already within ~5 % and cheaper per head
+        # than the per-KV-head calibration predicts (tools/shard_emulate.py)
+        nch = -(-a.n // a.chunk)
+        costs = torch.zeros((a.hkv, nch), dtype=torch.float64, device=dev)
+        if rank == 0:
+            costs.copy_(torch.tensor(SH.calibrate(q, k, v, ctx, **kw), dtype=torch.float64))
+        dist.broadcast(costs, 0)
+        plan = SH.balanced_plan(costs.tolist(), a.n, a.hq, a.hkv, world, rank)
+        torch.cuda.empty_cache()
+    qs, ks, vs = SH.take(plan, q, k, v)
+    del q, k, v
+    torch.cuda.empty_cache()
     stream = torch.cuda.current_stream()
 
     def step(return_admitted=False, return_recall=False):
         return SH.prefill(plan, qs, ks, vs, return_admitted=return_admitted,
                           return_recall=return_recall, **kw)
+
+    def stats():  # the last step's stage times (a balanced plan's parts summed)
+        return plan.notes["stats"] if plan.segments is not None else ctx.stats()
 
     def barrier():
         torch.cuda.synchronize()
@@ -453,7 +486,7 @@ def main():
     e0.record(stream)
     for _ in range(a.steps):
         step()
-        st = ctx.stats()
+        st = stats()
         for key in stage:
             stage[key] += st[key]
     e1.record(stream)
@@ -574,7 +607,7 @@ def main():
             f0.record(stream)
             for _ in range(k3):
                 step()
-                st = ctx.stats()
+                st = stats()
                 for key in st3:
                     st3[key] += st[key]
             f1.record(stream)
@@ -622,6 +655,8 @@ def main():
             "gpu_launches": int(stage["launches"]),
             "kernel_path": "tcgen05" if ctx.stats().get("tc_path") else "cuda-core",
         }
+        if ONE_DEVICE and world > 1:
+            line["dry_run"] = "LCX_BENCH_ONE_DEVICE: all ranks shared one GPU; not a measurement"
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -80,7 +80,7 @@ EXPORTS = [
     "lcx_line_scores", "lcx_select_from_scores", "lcx_select_critical", "lcx_sparse_attention",
     "lcx_full_attention", "lcx_chunked_prefill", "lcx_chunked_prefill_host",
     "lcx_attention_recall", "lcx_lse_merge", "lcx_lse_scale_partial", "lcx_attention_rel",
-    "lcx_stream_wait_chunk",
+    "lcx_stream_wait_chunk", "lcx_get_chunk_ms",
 ]
 
 _lib = None
@@ -124,6 +124,7 @@ def lib() -> C.CDLL:
             L.lcx_attention_recall.argtypes = [vp, vp, vp, i64, dbl, vp, P(dbl), vp]
             L.lcx_lse_merge.argtypes = [vp, vp, vp, i32, i64, i32, vp, vp, vp]
             L.lcx_stream_wait_chunk.argtypes = [vp, i64, vp]
+            L.lcx_get_chunk_ms.argtypes = [vp, vp, i64, P(i64)]
             L.lcx_lse_scale_partial.argtypes = [vp, vp, vp, vp, i32, i64, i32, i32, vp, vp]
             L.lcx_attention_rel.argtypes = [vp, P(AttentionInputC), vp, vp, i64, vp, vp, i64, vp,
                                             vp, vp, vp]
@@ -160,6 +161,14 @@ class Context:
         s = PrefillStatsC()
         check(lib().lcx_get_stats(self.ptr, C.byref(s)))
         return {f: getattr(s, f) for f, _ in PrefillStatsC._fields_}
+
+    def chunk_ms(self) -> list:
+        """Per-chunk device ms of the last chunked prefill (profiling on)."""
+        cnt = C.c_int64(0)
+        check(lib().lcx_get_chunk_ms(self.ptr, None, 0, C.byref(cnt)))
+        buf = (C.c_float * max(1, cnt.value))()
+        check(lib().lcx_get_chunk_ms(self.ptr, buf, cnt.value, C.byref(cnt)))
+        return [float(buf[i]) for i in range(cnt.value)]
 
     def set_profiling(self, on: bool):
         check(lib().lcx_set_profiling(self.ptr, int(on)))

@@ -8,6 +8,14 @@ Strategies (``plan``):
           Hkv % G == 0 rank r owns whole KV heads and their query heads.  Selection and
           attention are per query head (D10), so every rank's result is exactly the
           single-GPU result for its heads.
+  balanced  (``auto`` at G > 1) the same per-KV-head independence, cut by measured cost:
+          the (KV head, chunk) units in KV-head-major order, each costed by one untimed
+          calibration run per KV head (per-chunk device times, lcx_get_chunk_ms -- the
+          measured chunk costs a DCPP schedule is fitted to, engine_sim.cpp:117-166), are
+          split into G contiguous parts of minimal maximum cost; a rank runs each of its
+          parts as one chunked prefill over that KV head's query heads and a chunk range
+          (whole KV heads in one call).  Rank 0 calibrates and broadcasts the cost table
+          (setup only), so every rank derives the same cut; the data path has no collective.
   seq     KV sharding with a log-sum-exp merge (mode "seq", or "auto" when the query heads
           do not split over the ranks by KV group):
             1. sharded estimator: rank r runs the Vertical-Slash estimator + selection of
@@ -55,10 +63,20 @@ class Plan:
     rows: int = 0      # output rows owned after the merge
     notes: dict = field(default_factory=dict)
     chunks: tuple | None = None  # head plans: this rank's chunk range [c0, c1) (None = all)
+    # balanced plans: this rank's parts [(g0, g1, c0, c1)] -- KV heads [g0, g1) with their
+    # query heads over chunks [c0, c1) (None, None = all chunks)
+    segments: list | None = None
 
     def describe(self) -> str:
         if self.kind == "single":
             return "1 GPU"
+        if self.segments is not None:
+            parts = "; ".join(
+                f"KV {a}" + (f"-{b - 1}" if b - a > 1 else "")
+                + (f" chunks [{c0}, {c1})" if c0 is not None else "")
+                for a, b, c0, c1 in self.segments)
+            return (f"cost-balanced head sharding x{self.world} (rank {self.rank}: {parts}; "
+                    f"no collective on the data path)")
         if self.kind == "head":
             rng = f", chunks [{self.chunks[0]}, {self.chunks[1]})" if self.chunks else ""
             return (f"head-sharded x{self.world} ({self.hq} Q / {self.hkv} KV heads{rng} on rank "
@@ -166,9 +184,101 @@ def plan(n: int, hq: int, hkv: int, world: int, rank: int, mode: str = "auto",
                 notes={"est_heads": eh})
 
 
+def balance_units(costs, world: int):
+    """Cut the (KV head, chunk) units, KV-head-major, into `world` contiguous non-empty parts
+    minimising the largest part's cost (exact: min-max linear partition by dynamic
+    programming).  costs [hkv][nchunks].  Returns [(u0, u1)] per rank."""
+    import numpy as np
+    flat = np.asarray(costs, dtype=np.float64).reshape(-1)
+    U = flat.size
+    if U < world:
+        raise ValueError(f"{U} units cannot feed {world} ranks")
+    pre = np.concatenate([[0.0], np.cumsum(flat)])
+    # best[i] = min over cuts of the max part cost of units [0, i) in p parts; arg = last cut
+    best = pre.copy()
+    best[0] = 0.0
+    args = []
+    for _ in range(1, world):
+        nb = np.full(U + 1, np.inf)
+        arg = np.zeros(U + 1, dtype=np.int64)
+        for i in range(1, U + 1):
+            j = np.arange(0, i)
+            cand = np.maximum(best[:i], pre[i] - pre[:i])
+            cand[0] = np.inf  # every part non-empty
+            m = int(np.argmin(cand))
+            nb[i], arg[i] = cand[m], j[m]
+        best = nb
+        args.append(arg)
+    cuts = [U]
+    i = U
+    for arg in reversed(args):
+        i = int(arg[i])
+        cuts.append(i)
+    cuts.append(0)
+    cuts = cuts[::-1]
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
+
+
+def units_to_segments(u0: int, u1: int, nchunks: int):
+    """Unit range [u0, u1) (KV-head-major) -> [(g0, g1, c0, c1)], whole KV heads merged into
+    one part with (c0, c1) = (None, None)."""
+    segs = []
+    g = u0 // nchunks
+    while g * nchunks < u1:
+        c0 = max(0, u0 - g * nchunks)
+        c1 = min(nchunks, u1 - g * nchunks)
+        if c0 == 0 and c1 == nchunks:
+            if segs and segs[-1][2] is None and segs[-1][1] == g:
+                segs[-1] = (segs[-1][0], g + 1, None, None)
+            else:
+                segs.append((g, g + 1, None, None))
+        else:
+            segs.append((g, g + 1, c0, c1))
+        g += 1
+    return segs
+
+
+def balanced_plan(costs, n: int, hq: int, hkv: int, world: int, rank: int) -> Plan:
+    """The cost-balanced head plan of `rank` from the per-(KV head, chunk) cost table."""
+    nch = len(costs[0])
+    u0, u1 = balance_units(costs, world)[rank]
+    segs = units_to_segments(u0, u1, nch)
+    group = hq // hkv
+    g_first, g_last = segs[0][0], segs[-1][1]
+    heads = sum((b - a) * group for a, b, _, _ in segs)
+    load = float(sum(sum(costs[g][c0 or 0:c1 or nch]) for a, b, c0, c1 in segs
+                     for g in range(a, b)))
+    return Plan("head", world, rank, n, heads, g_last - g_first, g_first * group, g_first,
+                0, n, notes={"group": group, "balanced_cost_ms": load}, segments=segs)
+
+
+def calibrate(q, k, v, ctx, **kw):
+    """Per-(KV head, chunk) device ms of this layer: one untimed chunked prefill per KV head
+    over its query heads, with per-chunk events (the second of two runs)."""
+    n, hq, _ = q.shape
+    hkv = k.shape[1]
+    group = hq // hkv
+    ctx.set_profiling(True)
+    costs = []
+    for g in range(hkv):
+        qg = q[:, g * group:(g + 1) * group].contiguous()
+        kg, vg = k[:, g:g + 1].contiguous(), v[:, g:g + 1].contiguous()
+        for _ in range(2):
+            D.chunked_prefill(qg, kg, vg, return_selections=False, **kw)
+        torch.cuda.synchronize()
+        costs.append(ctx.chunk_ms())
+        del qg, kg, vg
+    return costs
+
+
 def take(p: Plan, q, k, v):
     if p.kind != "head":
         return q, k, v
+    if p.segments is not None:
+        grp = p.notes["group"]
+        return ([q[:, a * grp:b * grp].contiguous() for a, b, _, _ in p.segments],
+                [k[:, a:b].contiguous() for a, b, _, _ in p.segments],
+                [v[:, a:b].contiguous() for a, b, _, _ in p.segments])
     return (q[:, p.h0:p.h0 + p.hq].contiguous(), k[:, p.g0:p.g0 + p.hkv].contiguous(),
             v[:, p.g0:p.g0 + p.hkv].contiguous())
 
@@ -256,7 +366,30 @@ def seq_row_ranges(n: int, chunk_len: int, world: int, rank: int):
     return out
 
 
+def prefill_segments(p: Plan, qs, ks, vs, **kw):
+    """A balanced plan's parts, one chunked prefill each (see take()).  Returns
+    {"segments": [per-part result]} plus "admitted" / "recall" flattened over the parts'
+    own chunks when asked for."""
+    from ._lib import context
+    res, agg = [], None
+    for (a, b, c0, c1), q, k, v in zip(p.segments, qs, ks, vs):
+        kw2 = dict(kw, chunks=(c0, c1)) if c0 is not None else kw
+        res.append(D.chunked_prefill(q, k, v, **kw2))
+        st = context(q.device.index).stats()  # per call: summed over the parts
+        agg = st if agg is None else {x: (max if x == "tc_path" else sum)((agg[x], st[x]))
+                                      for x in st}
+    p.notes["stats"] = agg
+    out = {"segments": res}
+    for key in ("admitted", "recall"):
+        if key in res[0]:
+            out[key] = torch.cat([r[key][slice(s[2], s[3])].reshape(-1)
+                                  for r, s in zip(res, p.segments)])
+    return out
+
+
 def prefill(p: Plan, q, k, v, **kw):
+    if p.segments is not None:
+        return prefill_segments(p, q, k, v, **kw)
     if p.kind != "seq":
         if p.chunks is not None:
             kw = dict(kw, chunks=p.chunks)
@@ -312,6 +445,8 @@ def e2e(p: Plan, q, k, v, steps, barrier, world, dev, **kw):
     selection log copied out)."""
     if p.kind == "seq":
         return e2e_seq(p, q, k, v, steps, barrier, world, dev, **kw)
+    if p.segments is not None:
+        return e2e_segments(p, q, k, v, steps, barrier, world, dev, **kw)
     try:
         import psutil
         need = (q.numel() + k.numel() + v.numel()) * q.element_size() \
@@ -358,6 +493,76 @@ def e2e(p: Plan, q, k, v, steps, barrier, world, dev, **kw):
             "d2h_bytes_per_step": oh.numel() * 4 + lh.numel() * 4 + sel_bytes,
             "host_wall_ms_per_step": wall / steps,
             "api": "lcx_chunked_prefill_host (pinned host buffers, chunk-pipelined copies)"}
+
+
+def e2e_segments(p: Plan, qs, ks, vs, steps, barrier, world, dev, **kw):
+    """e2e of a balanced plan: each part through lcx_chunked_prefill_host from its own
+    pinned buffers (the host entry copies only the part's Q rows and the K / V rows up to its
+    last chunk), the parts one after another, all inside the timed region."""
+    import torch.distributed as dist
+    need = sum((q.numel() + k.numel() + v.numel()) * q.element_size() + q.numel() * 4
+               + q.shape[1] * q.shape[0] * 4 for q, k, v in zip(qs, ks, vs))
+    ok = torch.ones(1, device=dev)
+    try:
+        import psutil
+        if psutil.virtual_memory().available < 1.3 * need * max(1, world):
+            ok.zero_()
+    except ImportError:
+        pass
+    if world > 1:
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if ok.item() == 0:
+        return {"value": None, "skipped": "not enough host RAM for every rank's pinned buffers"}
+    bufs = []
+    for (a, b, c0, c1), q, k, v in zip(p.segments, qs, ks, vs):
+        hs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in (q, k, v)]
+        for h, t in zip(hs, (q, k, v)):
+            h.copy_(t)
+        n, hq, dim = q.shape
+        oh = torch.empty((n, hq, dim), dtype=torch.float32, pin_memory=True)
+        lh = torch.empty((hq, n), dtype=torch.float32, pin_memory=True)
+        kw2 = dict(kw, chunks=(c0, c1)) if c0 is not None else dict(kw)
+        bufs.append((hs, oh, lh, kw2, (c0, c1)))
+
+    def one():
+        rs = []
+        for hs, oh, lh, kw2, _ in bufs:
+            rs.append(D.chunked_prefill_host(*hs, out=oh, lse=lh, return_selections=True,
+                                             device=dev.index, **kw2))
+        return rs
+
+    one()  # sizes the staging buffers
+    barrier()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        rs = one()
+    e1.record(stream)
+    barrier()
+    wall = (time.perf_counter() - t0) * 1e3
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    h2d = d2h = 0
+    for (hs, oh, lh, kw2, (c0, c1)), r in zip(bufs, rs):
+        n, hq, dim = hs[0].shape
+        L = int(kw["chunk_len"])
+        a0 = 0 if c0 is None else c0 * L
+        a1 = n if c1 is None else min(n, c1 * L)
+        h2d += (a1 - a0) * hq * dim * hs[0].element_size() \
+            + 2 * a1 * hs[1].shape[1] * dim * hs[1].element_size()
+        d2h += (a1 - a0) * hq * (dim + 1) * 4 \
+            + sum(r[x][slice(c0, c1)].numel() * 4 for x in ("verticals", "slashes") if x in r) \
+            + sum(r[x].numel() * 4 for x in ("nv", "ns") if x in r)
+    return {"ms_per_step": ms / steps, "unit": "tokens/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "host_wall_ms_per_step": wall / steps,
+            "api": "lcx_chunked_prefill_host per part of the balanced plan (pinned host "
+                   "buffers, chunk-pipelined copies of the part's rows)"}
 
 
 def e2e_seq(p: Plan, q, k, v, steps, barrier, world, dev, **kw):

@@ -797,3 +797,44 @@ def test_chunk_range_matches_full_prefill(kind):
     assert torch.all(o[:r0] == 7.0) and torch.all(o[r1:] == 7.0)
     for key in ("verticals", "nv", "slashes", "ns"):
         assert torch.equal(part[key][c0:c1].cpu(), full[key][c0:c1].cpu()), key
+
+
+@pytest.mark.gpu
+def test_balanced_plan_parts_match_full_prefill():
+    """The cost-balanced multi-GPU plan (shard.balanced_plan, auto at G > 1): calibrated
+    per-(KV head, chunk) costs, every rank's parts run as chunk-ranged prefills over their
+    KV heads -- together they reproduce the single-GPU layer bitwise, every (head, row) once."""
+    import torch
+    from paper_2501_15383_b200 import device as D, shard as SH
+    from paper_2501_15383_b200._lib import context
+    g = torch.Generator(device="cuda").manual_seed(12)
+    n, L, hq, hkv = 2048, 512, 6, 3
+    q = torch.randn((n, hq, 128), generator=g, device="cuda").to(torch.bfloat16)
+    k, v = (torch.randn((n, hkv, 128), generator=g, device="cuda").to(torch.bfloat16)
+            for _ in range(2))
+    kw = dict(chunk_len=L, last_q=64, budget=(32, 96), position_mode="dca_continuous",
+              dca=(1024, 2048, 1024), rope_base=1e4)
+    full = D.chunked_prefill(q, k, v, return_admitted=True, **kw)
+    torch.cuda.synchronize()
+    costs = SH.calibrate(q, k, v, context(0), **kw)
+    assert len(costs) == hkv and all(len(r) == n // L and min(r) > 0 for r in costs)
+    covered = torch.zeros((n, hq), dtype=torch.int32)
+    adm_total = 0
+    for world in (2, 4):
+        covered.zero_()
+        adm_total = 0
+        for rank in range(world):
+            p = SH.balanced_plan(costs, n, hq, hkv, world, rank)
+            qs, ks, vs = SH.take(p, q, k, v)
+            r = SH.prefill(p, qs, ks, vs, return_admitted=True, **kw)
+            torch.cuda.synchronize()
+            adm_total += int(r["admitted"].sum())
+            for (a, b, c0, c1), part in zip(p.segments, r["segments"]):
+                r0, r1 = (c0 or 0) * L, n if c1 is None else c1 * L
+                h0, h1 = a * 2, b * 2
+                assert torch.equal(part["out"][r0:r1], full["out"][r0:r1, h0:h1])
+                assert torch.equal(part["lse"][:, r0:r1], full["lse"][h0:h1, r0:r1])
+                covered[r0:r1, h0:h1] += 1
+            assert p.notes["stats"]["chunks"] > 0
+        assert torch.all(covered == 1)
+        assert adm_total == int(full["admitted"].sum())

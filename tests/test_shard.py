@@ -220,3 +220,96 @@ def test_seq_prefill_orchestration_gloo_world2():
         assert err_o < 1e-5 and err_l < 1e-5, (rank, err_o, err_l)
         assert nrows == 96 // 2
         assert seen == [SH.est_head_ranges(6, 2, 2)[rank]]
+
+
+def _brute_minmax(flat, world):
+    import itertools
+    best = float("inf")
+    for cuts in itertools.combinations(range(1, len(flat)), world - 1):
+        b = (0,) + cuts + (len(flat),)
+        best = min(best, max(sum(flat[b[i]:b[i + 1]]) for i in range(world)))
+    return best
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_balance_units_is_minmax_optimal(seed, world):
+    rng = np.random.default_rng(seed)
+    costs = rng.uniform(0.5, 3.0, (3, 4)).tolist()
+    parts = SH.balance_units(costs, world)
+    flat = [x for r in costs for x in r]
+    assert parts[0][0] == 0 and parts[-1][1] == len(flat)
+    assert all(parts[i][1] == parts[i + 1][0] and parts[i][1] > parts[i][0]
+               for i in range(world - 1))
+    got = max(sum(flat[a:b]) for a, b in parts)
+    assert got == pytest.approx(_brute_minmax(flat, world))
+
+
+@pytest.mark.parametrize("hq,hkv,nch", [(28, 4, 32), (40, 8, 32), (14, 2, 5)])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_balanced_plan_covers_every_unit_once(hq, hkv, nch, world):
+    rng = np.random.default_rng(world)
+    # per-KV-head density differences and costs growing with depth, as measured
+    costs = [[(1 + 0.06 * c) * rng.uniform(0.7, 1.3) for c in range(nch)] for _ in range(hkv)]
+    seen, loads = [], []
+    group = hq // hkv
+    for r in range(world):
+        p = SH.balanced_plan(costs, nch * 1024, hq, hkv, world, r)
+        assert p.kind == "head" and p.segments and p.chunks is None
+        assert p.hq == sum((b - a) * group for a, b, _, _ in p.segments)
+        for a, b, c0, c1 in p.segments:
+            for g in range(a, b):
+                seen += [(g, c) for c in range(c0 or 0, nch if c1 is None else c1)]
+        loads.append(p.notes["balanced_cost_ms"])
+        assert "cost-balanced" in p.describe()
+    assert sorted(seen) == [(g, c) for g in range(hkv) for c in range(nch)]
+    assert len(set(seen)) == len(seen)
+    total = sum(map(sum, costs))
+    # min-max: no part exceeds the mean by more than one unit's cost
+    assert max(loads) <= total / world + max(max(r) for r in costs) + 1e-9
+
+
+def test_units_to_segments_merges_whole_kv_heads():
+    assert SH.units_to_segments(0, 64, 32) == [(0, 2, None, None)]
+    assert SH.units_to_segments(10, 70, 32) == [(0, 1, 10, 32), (1, 2, None, None),
+                                                (2, 3, 0, 6)]
+    assert SH.units_to_segments(40, 50, 32) == [(1, 2, 8, 18)]
+
+
+def _balanced_worker(rank, world, port, q):
+    """Rank 0 'calibrates' (a seeded cost table), broadcasts it; every rank cuts its part."""
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        costs = torch.zeros((4, 8), dtype=torch.float64)
+        if rank == 0:
+            costs.copy_(torch.tensor(np.random.default_rng(5).uniform(1, 4, (4, 8))))
+        dist.broadcast(costs, 0)
+        p = SH.balanced_plan(costs.tolist(), 8 * 4096, 28, 4, world, rank)
+        q.put((rank, p.segments))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_balanced_plan_agrees_across_ranks_gloo_world2():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_balanced_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    res = dict(q.get(timeout=10) for _ in procs)
+    costs = np.random.default_rng(5).uniform(1, 4, (4, 8)).tolist()
+    for r in range(2):
+        assert res[r] == SH.balanced_plan(costs, 8 * 4096, 28, 4, 2, r).segments
+    units = []
+    for r in range(2):
+        for a, b, c0, c1 in res[r]:
+            units += [(g, c) for g in range(a, b) for c in range(c0 or 0, 8 if c1 is None else c1)]
+    assert sorted(units) == [(g, c) for g in range(4) for c in range(8)]

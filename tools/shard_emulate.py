@@ -1,4 +1,5 @@
-"""Multi-GPU scaling of the default head-sharded plan, emulated rank by rank on one GPU:
+"""Multi-GPU scaling of the head-sharded plans (static, and cost-balanced -- bench.py's auto),
+emulated rank by rank on one GPU:
 each rank of a G-GPU run is a separate single-GPU prefill over its query heads / KV heads
 (no collective on the data path), so the G-GPU step time is the max over the ranks' device
 times.  Prints one JSON line per (geometry, G).   python tools/shard_emulate.py [n]
@@ -31,15 +32,22 @@ def timed(fn):
     return ev[0].elapsed_time(ev[1])
 
 
+from paper_2501_15383_b200._lib import context  # noqa: E402
+
 for hq, hkv, name in ((28, 4, "Qwen2.5-7B"), (40, 8, "Qwen2.5-14B")):
     q, k, v = make_qkv(n, hq, hkv, kind="planted", seed=1)
     base = timed(lambda: D.chunked_prefill(q, k, v, **kw))
-    for G in (1, 2, 4, 8):
+    costs = SH.calibrate(q, k, v, context(0), **kw)  # bench.py: rank 0, broadcast
+    for G, mode in ((1, "head"), (2, "head"), (4, "head"), (8, "head"), (2, "balanced"),
+                    (4, "balanced"), (8, "balanced")):
         ranks = []
         for r in range(G):
-            p = SH.plan(n, hq, hkv, G, r)
+            p = SH.balanced_plan(costs, n, hq, hkv, G, r) if mode == "balanced" \
+                else SH.plan(n, hq, hkv, G, r)
             qs, ks, vs = SH.take(p, q, k, v)
-            ranks.append(dict(rank=r, kind=p.kind, heads=p.hq, kv_heads=p.hkv,
+            ranks.append(dict(rank=r, kind=mode if G > 1 else "single", heads=p.hq,
+                              kv_heads=p.hkv, parts=p.segments, chunks=p.chunks,
+                              predicted_ms=p.notes.get("balanced_cost_ms"),
                               ms=timed(lambda: SH.prefill(p, qs, ks, vs, **kw))))
             del qs, ks, vs
         ms = max(x["ms"] for x in ranks)
