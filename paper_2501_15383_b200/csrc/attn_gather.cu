@@ -354,6 +354,13 @@ constexpr int kRowsC = kRowsW * kWarps;    // rows per CTA (within one 64-row ha
 #define LCX_GATHER_DIAG_MINB 3  // resident CTAs per SM (register budget)
 #endif
 static_assert(64 % kRowsC == 0, "a CTA's rows lie in one half-block");
+// LCX_GATHER_BATCH (default 1): batched per-warp segment control (see the kernel); 0: the
+// per-diagonal dependent-load loop.  Measured at 1M (per layer): planted gather 81.8 ->
+// 67.7 ms, iid 5.39 -> 4.52 s.  Staging the K / V rows of the next 1-3 live diagonals with
+// cp.async on top of it measured 65.9-66.6 ms planted but 4.99-5.17 s iid: not kept.
+#ifndef LCX_GATHER_BATCH
+#define LCX_GATHER_BATCH 1
+#endif
 
 __device__ __forceinline__ int64_t qpos(const GatherArgs& a, int pattern, int64_t i, int64_t imod) {
   if (a.rel_mode == 0) return a.pos_q ? a.pos_q[i] : i;
@@ -507,6 +514,55 @@ __global__ void __launch_bounds__(kWarps * 32, LCX_GATHER_DIAG_MINB) attn_gather
     }
     ++entries;
   };
+#if LCX_GATHER_BATCH
+  // batched control: lane k of the warp loads segment x0 + k and works out, for the warp's 8
+  // rows, which of them admit its entry (row range, key window, not a vertical column) --
+  // one coalesced segment load and two bitmap words per lane per 32 diagonals, instead of
+  // a dependent segment -> bitmap load chain per diagonal; the warp then walks the
+  // diagonals some row admits
+  if (have) {
+    int xe;
+    {
+      int lo = xs, hi = nseg;  // first diagonal > dmax
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (int64_t(__ldg(&sg[mid].x)) <= dmax) lo = mid + 1;
+        else hi = mid;
+      }
+      xe = lo;
+    }
+    const int rr = lane / kLanes;
+    const int rb = int((w_row0 - a.row_begin) & 127);
+    for (int x0 = xs; x0 < xe; x0 += 32) {
+      const int cnt = min(32, xe - x0);
+      int dk = 0;
+      uint32_t rm = 0;
+      if (lane < cnt) {
+        const int4 e = __ldg(&sg[x0 + lane]);
+        dk = e.x;
+        const int64_t jb = w_row0 - e.x;  // key of the warp's first row on this diagonal
+        const int64_t w0 = jb >= 0 ? (jb >> 5) : 0;
+        const uint64_t bits = uint64_t(__ldg(vb + w0)) | (uint64_t(__ldg(vb + w0 + 1)) << 32);
+#pragma unroll
+        for (int q = 0; q < kRowsW; ++q) {
+          const int64_t j = jb + q;
+          const int rq = rb + q;
+          const bool ok = w_row0 + q < a.row_end && rq >= e.y && rq < e.z && j >= a.key_lo &&
+                          j < a.key_hi && j >= 0 && !((bits >> ((j - (w0 << 5)) & 63)) & 1u);
+          rm |= uint32_t(ok) << q;
+        }
+      }
+      uint32_t live = __ballot_sync(0xffffffffu, rm != 0);
+      while (live) {
+        const int k = __ffs(live) - 1;
+        live &= live - 1;
+        const uint32_t mk = __shfl_sync(0xffffffffu, rm, k);
+        const int d = __shfl_sync(0xffffffffu, dk, k);
+        if ((mk >> rr) & 1u) process(i - d);
+      }
+    }
+  }
+#else
   if (have) {
     for (int x = xs; x < nseg; ++x) {
       const int4 e = __ldg(&sg[x]);
@@ -517,6 +573,7 @@ __global__ void __launch_bounds__(kWarps * 32, LCX_GATHER_DIAG_MINB) attn_gather
       if (ok) process(j);
     }
   }
+#endif
   if (fallback) {  // self entry (sparse.cpp:111): the row admits nothing else
     process(i);
   }
