@@ -67,7 +67,9 @@ namespace {
 
 // slash entries a 64-key relative tile needs to go to tcgen05 rather than the gather:
 // profiles/r02/sweep_tcmin_r02.jsonl (1M, 7B): planted flat over 32-160 (482-494 ms),
-// structured 5990 -> 5897 ms and iid 8262 -> 7860 ms from 96 to 160, worse again at 192
+// structured 5990 -> 5897 ms and iid 8262 -> 7860 ms from 96 to 160, worse again at 192;
+// re-swept with the batched gather (sweep_tcmin_r02_gather_batch.jsonl): still the optimum
+// for iid / structured (7041 / 5438 ms), planted flat over 160-192 (470 / 469 ms)
 constexpr int kDefaultTcMin = 160;
 constexpr int64_t kGatherSegment = 32768;  // keys per gather pass (L2-resident K / V)
 constexpr int64_t kTcSegment = 32768;      // keys per tcgen05 slash pass (K hi/lo + V^T)
