@@ -357,7 +357,9 @@ static_assert(64 % kRowsC == 0, "a CTA's rows lie in one half-block");
 // LCX_GATHER_BATCH (default 1): batched per-warp segment control (see the kernel); 0: the
 // per-diagonal dependent-load loop.  Measured at 1M (per layer): planted gather 81.8 ->
 // 67.7 ms, iid 5.39 -> 4.52 s.  Staging the K / V rows of the next 1-3 live diagonals with
-// cp.async on top of it measured 65.9-66.6 ms planted but 4.99-5.17 s iid: not kept.
+// cp.async on top of it measured 65.9-66.6 ms planted but 4.99-5.17 s iid, and a second
+// entry per row in registers (255 registers, 2 CTAs per SM) 91 ms planted, 5.92 s iid:
+// neither kept.
 #ifndef LCX_GATHER_BATCH
 #define LCX_GATHER_BATCH 1
 #endif
