@@ -3,6 +3,9 @@
 # reference arm, ncu launch list + full captures of the top kernels, sanitizers.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
+# build from the sources in this snapshot (an in-tree .so built before a later edit would
+# otherwise be what runs)
+python -m paper_2501_15383_b200.build > gpurun_out/build.log 2>&1 || { echo build failed; exit 1; }
 timeout 90 python -c 'import __graft_entry__ as g; g.smoke()' > gpurun_out/smoke.log 2>&1; rc=$?; echo smoke rc=$rc
 [ $rc -ne 0 ] && exit 1
 timeout 600 python -m pytest tests -m gpu -q -x -n 4 --timeout 300 -p no:cacheprovider > gpurun_out/gputest.log 2>&1
