@@ -427,14 +427,15 @@ def main():
               position_mode="dca_continuous", dca=dca, temperature=temp, rope_base=a.rope_base)
     plan = SH.plan(a.n, a.hq, a.hkv, world, rank, "head" if a.shard == "balanced" else a.shard,
                    chunk_len=a.chunk)
-    if world > 1 and (a.shard == "balanced" or (a.shard == "auto" and world >= a.hkv)):
+    nch = -(-a.n // a.chunk)
+    if world > 1 and a.hkv * nch >= world and \
+            (a.shard == "balanced" or (a.shard == "auto" and world >= a.hkv)):
         # cost-balanced head sharding: rank 0 measures every (KV head, chunk) unit of this
         # layer in an untimed calibration run and broadcasts the table (setup, not the data
         # path); every rank then cuts the same min-max partition (shard.balanced_plan).
         # auto uses it from one KV head per GPU on: with several KV heads per GPU the static
         # plan's single call over whole KV heads is already within ~5 % and cheaper per head
         # than the per-KV-head calibration predicts (tools/shard_emulate.py)
-        nch = -(-a.n // a.chunk)
         costs = torch.zeros((a.hkv, nch), dtype=torch.float64, device=dev)
         if rank == 0:
             costs.copy_(torch.tensor(SH.calibrate(q, k, v, ctx, **kw), dtype=torch.float64))
