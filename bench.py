@@ -440,7 +440,25 @@ def main():
         if rank == 0:
             costs.copy_(torch.tensor(SH.calibrate(q, k, v, ctx, **kw), dtype=torch.float64))
         dist.broadcast(costs, 0)
-        plan = SH.balanced_plan(costs.tolist(), a.n, a.hq, a.hkv, world, rank)
+        costs = costs.tolist()
+        plan = SH.balanced_plan(costs, a.n, a.hq, a.hkv, world, rank)
+        # one refinement (setup, untimed): every rank times its parts once, the times are
+        # gathered, each rank's units are rescaled by measured / predicted and the cut redone
+        # (shard.refine_costs) -- the same table and times on every rank give the same cut
+        qs, ks, vs = SH.take(plan, q, k, v)
+        SH.prefill(plan, qs, ks, vs, **kw)
+        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        r0.record()
+        SH.prefill(plan, qs, ks, vs, **kw)
+        r1.record()
+        torch.cuda.synchronize()
+        mine = torch.tensor([r0.elapsed_time(r1)], dtype=torch.float64, device=dev)
+        times = [torch.zeros_like(mine) for _ in range(world)]
+        dist.all_gather(times, mine)
+        del qs, ks, vs
+        refined = SH.refine_costs(costs, world, [float(t[0]) for t in times])
+        plan = SH.balanced_plan(refined, a.n, a.hq, a.hkv, world, rank)
+        plan.notes["first_cut_ms"] = [round(float(t[0]), 2) for t in times]
         torch.cuda.empty_cache()
     qs, ks, vs = SH.take(plan, q, k, v)
     del q, k, v

@@ -252,6 +252,21 @@ def balanced_plan(costs, n: int, hq: int, hkv: int, world: int, rank: int) -> Pl
                 0, n, notes={"group": group, "balanced_cost_ms": load}, segments=segs)
 
 
+def refine_costs(costs, world: int, measured_ms):
+    """One refinement of the balanced cut: every rank's units scaled by that rank's measured
+    / predicted time (the per-call overheads a per-KV-head calibration does not see: cold
+    chunk ranges, a second call per rank).  Pure and deterministic, so every rank that holds
+    the same table and the same gathered times derives the same new cut."""
+    nch = len(costs[0])
+    out = [list(map(float, r)) for r in costs]
+    for r, (u0, u1) in enumerate(balance_units(costs, world)):
+        pred = sum(costs[u // nch][u % nch] for u in range(u0, u1))
+        f = float(measured_ms[r]) / pred if pred > 0 else 1.0
+        for u in range(u0, u1):
+            out[u // nch][u % nch] *= f
+    return out
+
+
 def calibrate(q, k, v, ctx, **kw):
     """Per-(KV head, chunk) device ms of this layer: one untimed chunked prefill per KV head
     over its query heads, with per-chunk events (the second of two runs)."""

@@ -313,3 +313,21 @@ def test_balanced_plan_agrees_across_ranks_gloo_world2():
         for a, b, c0, c1 in res[r]:
             units += [(g, c) for g in range(a, b) for c in range(c0 or 0, 8 if c1 is None else c1)]
     assert sorted(units) == [(g, c) for g in range(4) for c in range(8)]
+
+
+def test_refine_costs_rescales_each_ranks_units():
+    rng = np.random.default_rng(3)
+    costs = rng.uniform(1, 3, (4, 16)).tolist()
+    parts = SH.balance_units(costs, 4)
+    flat = [x for r in costs for x in r]
+    pred = [sum(flat[a:b]) for a, b in parts]
+    meas = [p * f for p, f in zip(pred, (1.0, 1.2, 0.9, 1.05))]
+    new = SH.refine_costs(costs, 4, meas)
+    nf = [x for r in new for x in r]
+    for (a, b), m in zip(parts, meas):  # each rank's units now sum to its measured time
+        assert sum(nf[a:b]) == pytest.approx(m)
+    # the re-cut moves work off the slow rank
+    parts2 = SH.balance_units(new, 4)
+    assert max(sum(nf[a:b]) for a, b in parts2) <= max(meas) + 1e-9
+    # identical inputs, identical cut (every rank derives the same plan)
+    assert SH.balance_units(SH.refine_costs(costs, 4, meas), 4) == parts2

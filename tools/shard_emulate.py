@@ -38,12 +38,18 @@ for hq, hkv, name in ((28, 4, "Qwen2.5-7B"), (40, 8, "Qwen2.5-14B")):
     q, k, v = make_qkv(n, hq, hkv, kind="planted", seed=1)
     base = timed(lambda: D.chunked_prefill(q, k, v, **kw))
     costs = SH.calibrate(q, k, v, context(0), **kw)  # bench.py: rank 0, broadcast
+    refined = {}
     for G, mode in ((1, "head"), (2, "head"), (4, "head"), (8, "head"), (2, "balanced"),
-                    (4, "balanced"), (8, "balanced")):
+                    (4, "balanced"), (8, "balanced"), (4, "balanced+refine"),
+                    (8, "balanced+refine")):
         ranks = []
         for r in range(G):
-            p = SH.balanced_plan(costs, n, hq, hkv, G, r) if mode == "balanced" \
-                else SH.plan(n, hq, hkv, G, r)
+            if mode == "balanced":
+                p = SH.balanced_plan(costs, n, hq, hkv, G, r)
+            elif mode == "balanced+refine":  # bench.py: one measured re-cut
+                p = SH.balanced_plan(refined[G], n, hq, hkv, G, r)
+            else:
+                p = SH.plan(n, hq, hkv, G, r)
             qs, ks, vs = SH.take(p, q, k, v)
             ranks.append(dict(rank=r, kind=mode if G > 1 else "single", heads=p.hq,
                               kv_heads=p.hkv, parts=p.segments, chunks=p.chunks,
@@ -51,6 +57,8 @@ for hq, hkv, name in ((28, 4, "Qwen2.5-7B"), (40, 8, "Qwen2.5-14B")):
                               ms=timed(lambda: SH.prefill(p, qs, ks, vs, **kw))))
             del qs, ks, vs
         ms = max(x["ms"] for x in ranks)
+        if mode == "balanced":
+            refined[G] = SH.refine_costs(costs, G, [x["ms"] for x in ranks])
         print(json.dumps(dict(geometry=name, n=n, gpus=G, plan=ranks[0]["kind"],
                               step_ms_max_over_ranks=ms, tokens_per_s=n / (ms / 1e3),
                               speedup_vs_1=base / ms, efficiency=base / ms / G,
