@@ -68,9 +68,10 @@ def parse():
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--shard", default="auto",
                     choices=["auto", "balanced", "head", "head-split", "seq"],
-                    help="balanced (auto when GPUs >= KV heads): (KV head, chunk) units cut "
-                         "into min-max parts by costs measured in an untimed calibration run; "
-                         "head (auto below that): query heads by "
+                    help="auto: the fastest (measured in setup) of the static head plan and "
+                         "the balanced cuts; balanced: (KV head, chunk) units cut into min-max "
+                         "parts by costs measured in an untimed calibration run, refined once "
+                         "by the ranks' measured times; head: query heads by "
                          "KV group, or (when a KV head's query heads do not divide over its "
                          "GPUs) all of them over a modelled chunk range; head-split: the "
                          "uneven query-head split instead; seq: KV-line sharding with the LSE "
@@ -425,41 +426,49 @@ def main():
     ctx.set_profiling(True)
     kw = dict(chunk_len=a.chunk, last_q=a.last_q, budget=tuple(a.budget),
               position_mode="dca_continuous", dca=dca, temperature=temp, rope_base=a.rope_base)
-    plan = SH.plan(a.n, a.hq, a.hkv, world, rank, "head" if a.shard == "balanced" else a.shard,
+    plan = SH.plan(a.n, a.hq, a.hkv, world, rank, "auto" if a.shard == "balanced" else a.shard,
                    chunk_len=a.chunk)
     nch = -(-a.n // a.chunk)
-    if world > 1 and a.hkv * nch >= world and \
-            (a.shard == "balanced" or (a.shard == "auto" and world >= a.hkv)):
-        # cost-balanced head sharding: rank 0 measures every (KV head, chunk) unit of this
-        # layer in an untimed calibration run and broadcasts the table (setup, not the data
-        # path); every rank then cuts the same min-max partition (shard.balanced_plan).
-        # auto uses it from one KV head per GPU on: with several KV heads per GPU the static
-        # plan's single call over whole KV heads is already within ~5 % and cheaper per head
-        # than the per-KV-head calibration predicts (tools/shard_emulate.py)
+    plan_selection = None
+    if world > 1 and a.hkv * nch >= world and a.shard in ("auto", "balanced"):
+        # cost-balanced head sharding (shard.balanced_plan): rank 0 measures every (KV head,
+        # chunk) unit of this layer in an untimed calibration run and broadcasts the table;
+        # every rank cuts the same min-max partition, times its parts once, and the gathered
+        # times refine the cut (shard.refine_costs).  auto then keeps whichever of the static
+        # head plan, the first cut and the refined cut ran fastest (max over ranks) -- all of
+        # it setup, untimed, and the same choice on every rank (same gathered times); the
+        # data path has no collective either way
         costs = torch.zeros((a.hkv, nch), dtype=torch.float64, device=dev)
         if rank == 0:
             costs.copy_(torch.tensor(SH.calibrate(q, k, v, ctx, **kw), dtype=torch.float64))
         dist.broadcast(costs, 0)
         costs = costs.tolist()
-        plan = SH.balanced_plan(costs, a.n, a.hq, a.hkv, world, rank)
-        # one refinement (setup, untimed): every rank times its parts once, the times are
-        # gathered, each rank's units are rescaled by measured / predicted and the cut redone
-        # (shard.refine_costs) -- the same table and times on every rank give the same cut
-        qs, ks, vs = SH.take(plan, q, k, v)
-        SH.prefill(plan, qs, ks, vs, **kw)
-        r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        r0.record()
-        SH.prefill(plan, qs, ks, vs, **kw)
-        r1.record()
-        torch.cuda.synchronize()
-        mine = torch.tensor([r0.elapsed_time(r1)], dtype=torch.float64, device=dev)
-        times = [torch.zeros_like(mine) for _ in range(world)]
-        dist.all_gather(times, mine)
-        del qs, ks, vs
-        refined = SH.refine_costs(costs, world, [float(t[0]) for t in times])
-        plan = SH.balanced_plan(refined, a.n, a.hq, a.hkv, world, rank)
-        plan.notes["first_cut_ms"] = [round(float(t[0]), 2) for t in times]
-        torch.cuda.empty_cache()
+
+        def measure(p):  # this rank's parts: one warm and one timed run; all ranks' times
+            qs_, ks_, vs_ = SH.take(p, q, k, v)
+            SH.prefill(p, qs_, ks_, vs_, **kw)
+            r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            r0.record()
+            SH.prefill(p, qs_, ks_, vs_, **kw)
+            r1.record()
+            torch.cuda.synchronize()
+            del qs_, ks_, vs_
+            torch.cuda.empty_cache()
+            mine = torch.tensor([r0.elapsed_time(r1)], dtype=torch.float64, device=dev)
+            times = [torch.zeros_like(mine) for _ in range(world)]
+            dist.all_gather(times, mine)
+            return [float(t[0]) for t in times]
+
+        cut = SH.balanced_plan(costs, a.n, a.hq, a.hkv, world, rank)
+        t_cut = measure(cut)
+        refined = SH.balanced_plan(SH.refine_costs(costs, world, t_cut), a.n, a.hq, a.hkv,
+                                   world, rank)
+        cands = [("refined cut", refined, measure(refined)), ("first cut", cut, t_cut)]
+        if a.shard == "auto":
+            cands.append(("static head plan", plan, measure(plan)))
+        name, plan, _ = min(cands, key=lambda c: max(c[2]))
+        plan_selection = {"chosen": name, "setup_ms_max_over_ranks":
+                          {c[0]: round(max(c[2]), 2) for c in cands}}
     qs, ks, vs = SH.take(plan, q, k, v)
     del q, k, v
     torch.cuda.empty_cache()
@@ -663,7 +672,8 @@ def main():
             "data": f"synthetic, seeded, generated on device ({a.kind}: "
                     + ("vertical + local-band slash structure, synth.make_planted" if
                        a.kind == "planted" else "synth.make_qkv") + ")",
-            "config": {**workload(a), "parallelism": plan.describe()},
+            "config": {**workload(a), "parallelism": plan.describe(),
+                       **({"plan_selection": plan_selection} if plan_selection else {})},
             "roofline": roofline, "kernels": kernels,
             "algorithmic_tflops_whole_step": alg_tflops,
             "pct_tc_roofline_whole_step": alg_tflops / tflops_peak,
