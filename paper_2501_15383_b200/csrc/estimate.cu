@@ -267,21 +267,30 @@ est_tile_kernel(EstDev a, float2* __restrict__ stats, const float2* __restrict__
   }
 }
 
+// One warp per (head, row): lane l folds splits l, l + 32, ... in ascending order, then a
+// fixed xor tree -- deterministic, and ~600 splits (the tensor-core plan) no longer walked
+// by one thread (a latency-bound 65 us per chunk before)
 __global__ void est_combine_stats(const float2* __restrict__ stats, int h0, int nh, int nsplit,
                                   int64_t block, float2* __restrict__ rowstat) {
-  const int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (x >= int64_t(nh) * block) return;
+  const int64_t x = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (x >= int64_t(nh) * block) return;  // whole warps
   const int h = h0 + int(x / block);
   const int64_t r = x % block;
   const int64_t idx = int64_t(h) * block + r;
+  const float2* sp = stats + int64_t(h) * nsplit * block + r;
   float m = -INFINITY;
-  for (int s = 0; s < nsplit; ++s) m = fmaxf(m, stats[(int64_t(h) * nsplit + s) * block + r].x);
+  for (int s = lane; s < nsplit; s += 32) m = fmaxf(m, sp[int64_t(s) * block].x);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   float sum = 0.f;
-  for (int s = 0; s < nsplit; ++s) {
-    const float2 v = stats[(int64_t(h) * nsplit + s) * block + r];
+  for (int s = lane; s < nsplit; s += 32) {
+    const float2 v = sp[int64_t(s) * block];
     if (v.x != -INFINITY) sum += v.y * expf(v.x - m);
   }
-  rowstat[idx] = make_float2(m, sum);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  if (lane == 0) rowstat[idx] = make_float2(m, sum);
 }
 
 // col_score[h][j] = sum over row tiles ascending; slash_score[h][d] = sum over the
@@ -510,8 +519,8 @@ int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream
   }
   {
     const int64_t rows = int64_t(nh) * a.block;
-    est_combine_stats<<<unsigned((rows + 255) / 256), 256, 0, st>>>(stats, h0, nh, nst, a.block,
-                                                                    rowstat);
+    est_combine_stats<<<unsigned((rows * 32 + 255) / 256), 256, 0, st>>>(stats, h0, nh, nst,
+                                                                         a.block, rowstat);
     LCX_CHECK_LAUNCH();
   }
   // ---- pass 2: probabilities -> column / diagonal partials ----
