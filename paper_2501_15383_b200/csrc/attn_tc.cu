@@ -1636,34 +1636,36 @@ __global__ void plan_items_kernel(const TcParams p, Item* __restrict__ plans) {
 // ---------------------------------------------------------------- prep --
 // K_hi / K_lo [n][hkv][128] bf16 = split(rope(k_j, kpos(j))), kpos = pos_k[j]
 // (standard) or j mod s (DCA).
+// One block per key row j (blockIdx.x over [r0, r1)), threadIdx.x = dim pair, threadIdx.y
+// striding the KV heads: the row's position is worked out once per block, and no thread
+// divides by a runtime 64-bit value.
 __global__ void k_prep_kernel(const __nv_bfloat16* __restrict__ k, int64_t n, int64_t r0,
-                              int64_t r1, int hkv, const int64_t* __restrict__ pos_k,
-                              int rel_mode, int64_t s, const float2* __restrict__ rope,
+                              int hkv, const int64_t* __restrict__ pos_k, int rel_mode,
+                              int64_t s, const float2* __restrict__ rope,
                               __nv_bfloat16* __restrict__ khi, __nv_bfloat16* __restrict__ klo,
                               float2* __restrict__ kf) {
-  // pair index over rows [r0, r1)
-  const int64_t idx = r0 * hkv * (HD / 2) + int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t total = r1 * hkv * (HD / 2);
-  if (idx >= total) return;
-  const int pr = int(idx % (HD / 2));
-  const int64_t rowhead = idx / (HD / 2);
-  const int64_t j = rowhead / hkv;
-  const int64_t kp = rel_mode ? (j % s) : (pos_k ? pos_k[j] : j);
-  const float2 xy = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(k)[idx]);
-  const float2 c = rope[kp * (HD / 2) + pr];
-  const float rx = xy.x * c.x - xy.y * c.y, ry = xy.x * c.y + xy.y * c.x;
-  kf[idx] = make_float2(rx, ry);
-  const __nv_bfloat162 h2 = __floats2bfloat162_rn(rx, ry);
-  const float2 hf = __bfloat1622float2(h2);
+  __shared__ int64_t kp_s;
+  const int64_t j = r0 + blockIdx.x;
+  const int pr = threadIdx.x;
+  if (pr == 0 && threadIdx.y == 0) kp_s = rel_mode ? (j % s) : (pos_k ? pos_k[j] : j);
+  __syncthreads();
+  const float2 c = rope[kp_s * (HD / 2) + pr];
   // tiled [hkv][n/64][half][64 keys][64 dims]: each TMA box is one contiguous 8 KB block
-  const int g = int(rowhead % hkv);
-  const int64_t nt = (n + 63) / 64;
+  const int64_t nt = (n + 63) >> 6;
   const int d = 2 * pr;
-  const int jr = int(j % 64), dd = d % 64;
-  const int64_t o = ((((int64_t(g) * nt + j / 64) * 2 + d / 64) * 64 + jr) * 64 +
-                     sw128_chunk(jr, dd / 8) * 8 + dd % 8) / 2;
-  reinterpret_cast<__nv_bfloat162*>(khi)[o] = h2;
-  reinterpret_cast<__nv_bfloat162*>(klo)[o] = __floats2bfloat162_rn(rx - hf.x, ry - hf.y);
+  const int jr = int(j & 63), dd = d & 63;
+  for (int g = threadIdx.y; g < hkv; g += blockDim.y) {
+    const int64_t idx = (j * hkv + g) * (HD / 2) + pr;
+    const float2 xy = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(k)[idx]);
+    const float rx = xy.x * c.x - xy.y * c.y, ry = xy.x * c.y + xy.y * c.x;
+    kf[idx] = make_float2(rx, ry);
+    const __nv_bfloat162 h2 = __floats2bfloat162_rn(rx, ry);
+    const float2 hf = __bfloat1622float2(h2);
+    const int64_t o = ((((int64_t(g) * nt + (j >> 6)) * 2 + (d >> 6)) * 64 + jr) * 64 +
+                       sw128_chunk(jr, dd >> 3) * 8 + (dd & 7)) >> 1;
+    reinterpret_cast<__nv_bfloat162*>(khi)[o] = h2;
+    reinterpret_cast<__nv_bfloat162*>(klo)[o] = __floats2bfloat162_rn(rx - hf.x, ry - hf.y);
+  }
 }
 
 // V^T [hkv][128][npad] fp16 from V [n][hkv][128] bf16 (smem-tiled transpose)
@@ -1991,9 +1993,8 @@ int tc_prepare_rows(const void* k, const void* v, int64_t n, int64_t r0, int64_t
                     const TcBuffers& B, cudaStream_t st) {
   r1 = lcx_min64(r1, n);
   if (r1 <= r0) return LCX_OK;
-  const int64_t pairs = (r1 - r0) * hkv * (HD / 2);
-  k_prep_kernel<<<unsigned((pairs + 255) / 256), 256, 0, st>>>(
-      reinterpret_cast<const __nv_bfloat16*>(k), n, r0, r1, hkv, pos_k, rel_mode, s, rope, B.khi,
+  k_prep_kernel<<<unsigned(r1 - r0), dim3(HD / 2, unsigned(std::min(hkv, 8))), 0, st>>>(
+      reinterpret_cast<const __nv_bfloat16*>(k), n, r0, hkv, pos_k, rel_mode, s, rope, B.khi,
       B.klo, reinterpret_cast<float2*>(B.kf));
   LCX_CHECK_LAUNCH();
   // V^T tiles covering [r0, r1); a partial trailing tile is rewritten (zero-padded) by the

@@ -300,10 +300,10 @@ __global__ void est_combine_lines(const float* __restrict__ col_part,
                                   int nrt, int64_t nk, int64_t block, int64_t gbase,
                                   int64_t ntiles, int slash_mean, float* __restrict__ col,
                                   float* __restrict__ slash) {
-  const int64_t y = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (y >= int64_t(nh) * nk) return;
-  const int h = h0 + int(y / nk);
-  const int64_t x = y % nk;
+  // grid (key blocks, heads): no 64-bit division per thread
+  const int64_t x = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= nk) return;
+  const int h = h0 + int(blockIdx.y);
   const int64_t idx = int64_t(h) * nk + x;
   if (col) {
     float s = 0.f;
@@ -539,8 +539,7 @@ int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream
     LCX_CHECK_LAUNCH();
   }
   if (a.col || a.slash) {
-    const int64_t total = int64_t(nh) * a.nk;
-    est_combine_lines<<<unsigned((total + 255) / 256), 256, 0, st>>>(
+    est_combine_lines<<<dim3(unsigned((a.nk + 255) / 256), unsigned(nh)), 256, 0, st>>>(
         col_part, diag_part, a.hq, h0, nh, nrt, a.nk, a.block, a.nk - a.block, ntiles,
         a.slash_mean, a.col, a.slash);
     LCX_CHECK_LAUNCH();
