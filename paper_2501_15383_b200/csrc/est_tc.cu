@@ -468,6 +468,10 @@ __device__ __forceinline__ int pow2_exp(float m) {
   return e < -120 ? -120 : (e > 120 ? 120 : e);
 }
 
+// 2^e as a float, e in [-120, 120] (pow2_exp's range): x * pow2f(e) == ldexpf(x, e) bitwise
+// (scaling by a normal power of two rounds like ldexpf), without ldexpf's special-case code
+__device__ __forceinline__ float pow2f(int e) { return __int_as_float((127 + e) << 23); }
+
 __device__ __forceinline__ float block_max256(float v, float* red) {
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -512,17 +516,18 @@ __global__ void __launch_bounds__(256) est_k3_kernel(const __nv_bfloat16* __rest
   }
   const int ex = pow2_exp(block_max256(mx, red));
   if (threadIdx.x == 0) kinv[int64_t(gg) * ntiles + tile] = exp2f(float(-ex));
+  const float sc = pow2f(ex);
   __half2* base = reinterpret_cast<__half2*>(k3 + (int64_t(gg) * ntiles + tile) * 6 * 64 * 64);
 #pragma unroll
   for (int x = 0; x < kPer; ++x) {
     const int e = x * 256 + threadIdx.x;
     const int jj = e >> 6, pr = e & 63;
     const int d = 2 * pr, half = d >> 6;
-    const float2 rs = make_float2(ldexpf(rot[x].x, ex), ldexpf(rot[x].y, ex));
+    const float2 rs = make_float2(rot[x].x * sc, rot[x].y * sc);
     const __half2 h2 = __floats2half2_rn(rs.x, rs.y);
     const float2 hf = __half22float2(h2);
     const __half2 l2 = __floats2half2_rn(rs.x - hf.x, rs.y - hf.y);
-    const __half2 w2 = __floats2half2_rn(ldexpf(raw[x].x, ex), ldexpf(raw[x].y, ex));
+    const __half2 w2 = __floats2half2_rn(raw[x].x * sc, raw[x].y * sc);
     const int64_t o = (int64_t(jj) * 64 + (d & 63)) >> 1;  // within one [64][64] box
     base[(0 + half) * 2048 + o] = h2;
     base[(2 + half) * 2048 + o] = l2;
@@ -562,8 +567,8 @@ __global__ void __launch_bounds__(64) est_q3_kernel(
   __syncthreads();
   const int ex = pow2_exp(fmaxf(red[0], red[1]));
   if (pr == 0) qinv[(int64_t(far) * npairs + pair) * 128 + row] = exp2f(float(-ex));
-  rx = ldexpf(rx, ex);
-  ry = ldexpf(ry, ex);
+  rx *= pow2f(ex);
+  ry *= pow2f(ex);
   const __half2 h2 = __floats2half2_rn(rx, ry);
   const float2 hf = __half22float2(h2);
   const __half2 l2 = __floats2half2_rn(rx - hf.x, ry - hf.y);
