@@ -584,6 +584,9 @@ int lcx_context_destroy(lcx_context* ctx) {
   if (ctx->stage) cudaFree(ctx->stage);
   if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
   if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
+  if (ctx->est_side) cudaStreamDestroy(ctx->est_side);
+  if (ctx->est_fork) cudaEventDestroy(ctx->est_fork);
+  if (ctx->est_join) cudaEventDestroy(ctx->est_join);
   delete ctx;
   return LCX_OK;
 }

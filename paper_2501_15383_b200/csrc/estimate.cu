@@ -497,7 +497,35 @@ int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream
     return LCX_OK;
   };
   dim3 grid(unsigned(std::max(nsplit, 1)), unsigned(nh), unsigned(nrt));
+  // With both estimators, the CUDA-core mixed tiles (a few dozen CTAs) run on a side stream
+  // beside the tensor-core pass instead of after it: disjoint stats slots and partial
+  // columns / diagonals, joined before the combines that read them.
+  const bool side = tc && simt;
+  cudaStream_t ss = st;
+  if (side) {
+    if (!ctx->est_side) {
+      LCX_CHECK_CUDA(cudaStreamCreateWithFlags(&ctx->est_side, cudaStreamNonBlocking));
+      LCX_CHECK_CUDA(cudaEventCreateWithFlags(&ctx->est_fork, cudaEventDisableTiming));
+      LCX_CHECK_CUDA(cudaEventCreateWithFlags(&ctx->est_join, cudaEventDisableTiming));
+    }
+    ss = ctx->est_side;
+  }
+  auto fork = [&]() -> int {
+    if (side) {
+      LCX_CHECK_CUDA(cudaEventRecord(ctx->est_fork, st));
+      LCX_CHECK_CUDA(cudaStreamWaitEvent(ss, ctx->est_fork, 0));
+    }
+    return LCX_OK;
+  };
+  auto join = [&]() -> int {
+    if (side) {
+      LCX_CHECK_CUDA(cudaEventRecord(ctx->est_join, ss));
+      LCX_CHECK_CUDA(cudaStreamWaitEvent(st, ctx->est_join, 0));
+    }
+    return LCX_OK;
+  };
   // ---- pass 1: row max / sum-exp ----
+  LCX_TRY(fork());
   if (tc) {
     Arena ta_ar = tc_ar;
     ta.pass = 1;
@@ -507,16 +535,17 @@ int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream
     if (bf) {
       LCX_TRY(set_attr((const void*)est_tile_kernel<__nv_bfloat16, 1>, 0));
       LCX_TRY(set_attr((const void*)est_tile_kernel<__nv_bfloat16, 2>, 1));
-      est_tile_kernel<__nv_bfloat16, 1><<<grid, kThreads, smem, st>>>(d, stats, nullptr, nullptr,
+      est_tile_kernel<__nv_bfloat16, 1><<<grid, kThreads, smem, ss>>>(d, stats, nullptr, nullptr,
                                                                        nullptr, nullptr);
     } else {
       LCX_TRY(set_attr((const void*)est_tile_kernel<float, 1>, 2));
       LCX_TRY(set_attr((const void*)est_tile_kernel<float, 2>, 3));
-      est_tile_kernel<float, 1><<<grid, kThreads, smem, st>>>(d, stats, nullptr, nullptr,
+      est_tile_kernel<float, 1><<<grid, kThreads, smem, ss>>>(d, stats, nullptr, nullptr,
                                                                nullptr, nullptr);
     }
     LCX_CHECK_LAUNCH();
   }
+  LCX_TRY(join());
   {
     const int64_t rows = int64_t(nh) * a.block;
     est_combine_stats<<<unsigned((rows * 32 + 255) / 256), 256, 0, st>>>(stats, h0, nh, nst,
@@ -524,6 +553,7 @@ int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream
     LCX_CHECK_LAUNCH();
   }
   // ---- pass 2: probabilities -> column / diagonal partials ----
+  LCX_TRY(fork());
   if (tc) {
     Arena ta_ar = tc_ar;
     ta.pass = 2;
@@ -531,13 +561,14 @@ int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream
   }
   if (simt) {
     if (bf)
-      est_tile_kernel<__nv_bfloat16, 2><<<grid, kThreads, smem, st>>>(d, nullptr, rowstat,
+      est_tile_kernel<__nv_bfloat16, 2><<<grid, kThreads, smem, ss>>>(d, nullptr, rowstat,
                                                                        a.est, col_part, diag_part);
     else
-      est_tile_kernel<float, 2><<<grid, kThreads, smem, st>>>(d, nullptr, rowstat, a.est,
+      est_tile_kernel<float, 2><<<grid, kThreads, smem, ss>>>(d, nullptr, rowstat, a.est,
                                                                col_part, diag_part);
     LCX_CHECK_LAUNCH();
   }
+  LCX_TRY(join());
   if (a.col || a.slash) {
     est_combine_lines<<<dim3(unsigned((a.nk + 255) / 256), unsigned(nh)), 256, 0, st>>>(
         col_part, diag_part, a.hq, h0, nh, nrt, a.nk, a.block, a.nk - a.block, ntiles,

@@ -148,6 +148,9 @@ struct lcx_context {
   char* stage = nullptr;
   size_t stage_bytes = 0;
   cudaStream_t h2d = nullptr, d2h = nullptr;
+  // estimator: the CUDA-core mixed tiles run on a side stream beside the tensor-core passes
+  cudaStream_t est_side = nullptr;
+  cudaEvent_t est_fork = nullptr, est_join = nullptr;
   // key-window decision of chunked prefill: far-slash counts of the last two chunks
   int* far_dev = nullptr;        // device [2]
   int* far_host = nullptr;       // pinned, mapped [2][2]
