@@ -587,6 +587,9 @@ int lcx_context_destroy(lcx_context* ctx) {
   if (ctx->est_side) cudaStreamDestroy(ctx->est_side);
   if (ctx->est_fork) cudaEventDestroy(ctx->est_fork);
   if (ctx->est_join) cudaEventDestroy(ctx->est_join);
+  if (ctx->prep_side) cudaStreamDestroy(ctx->prep_side);
+  if (ctx->prep_fork) cudaEventDestroy(ctx->prep_fork);
+  if (ctx->prep_join) cudaEventDestroy(ctx->prep_join);
   delete ctx;
   return LCX_OK;
 }
@@ -1182,10 +1185,26 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
     cudaEvent_t* e = prof ? &ev[6 * ci] : nullptr;
     if (ready) LCX_CHECK_CUDA(cudaStreamWaitEvent(st, ready[ci], 0));
     if (prof) LCX_CHECK_CUDA(cudaEventRecord(e[0], st));
-    // rotated K / V^T of this chunk's new key rows (chunks only ever append keys)
-    if (tc && do_attend)
+    // rotated K / V^T of this chunk's new key rows (chunks only ever append keys).  With an
+    // estimator to run first, on a side stream beside it (joined before the attention): it
+    // writes only rows [t0, t1), which no earlier chunk's attention reads when t0 is
+    // 64-aligned (otherwise the shared V^T tile is rewritten: in order, on the main stream)
+    const bool prep_beside = tc && do_attend && sparse && do_select && t0 % 64 == 0;
+    if (prep_beside) {
+      if (!ctx->prep_side) {
+        LCX_CHECK_CUDA(cudaStreamCreateWithFlags(&ctx->prep_side, cudaStreamNonBlocking));
+        LCX_CHECK_CUDA(cudaEventCreateWithFlags(&ctx->prep_fork, cudaEventDisableTiming));
+        LCX_CHECK_CUDA(cudaEventCreateWithFlags(&ctx->prep_join, cudaEventDisableTiming));
+      }
+      LCX_CHECK_CUDA(cudaEventRecord(ctx->prep_fork, st));
+      LCX_CHECK_CUDA(cudaStreamWaitEvent(ctx->prep_side, ctx->prep_fork, 0));
+      LCX_TRY(tc_prepare_rows(in->k, in->v, n, t0, t1, in->hkv, in->positions_k, dca ? 1 : 0, s,
+                              ctx->rope, w.B, ctx->prep_side));
+      LCX_CHECK_CUDA(cudaEventRecord(ctx->prep_join, ctx->prep_side));
+    } else if (tc && do_attend) {
       LCX_TRY(tc_prepare_rows(in->k, in->v, n, t0, t1, in->hkv, in->positions_k, dca ? 1 : 0, s,
                               ctx->rope, w.B, st));
+    }
     if (sparse && do_select) {
       if (est_tc)
         LCX_TRY(est_tc_prepare_keys(in->k, t0, t1, in->hkv, k3_tiles, ctx->rope, k3, st));
@@ -1261,6 +1280,7 @@ int prefill_impl(lcx_context* ctx, const lcx_attention_input* in, const lcx_pref
       asl = os;
       asc = ons;
     }
+    if (prep_beside) LCX_CHECK_CUDA(cudaStreamWaitEvent(st, ctx->prep_join, 0));
     LCX_TRY(attention_chunk(ctx, in, w, t0, t1, sparse, avl, avc, cap_v, asl, asc, cap_s,
                             dca, s, dca ? c : 1, tc_min, out->out, out->lse, n,
                             out->admitted ? out->admitted + ci * hq : nullptr, st,

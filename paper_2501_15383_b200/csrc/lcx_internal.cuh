@@ -151,6 +151,9 @@ struct lcx_context {
   // estimator: the CUDA-core mixed tiles run on a side stream beside the tensor-core passes
   cudaStream_t est_side = nullptr;
   cudaEvent_t est_fork = nullptr, est_join = nullptr;
+  // chunked prefill: a chunk's attention-operand prep beside its estimator
+  cudaStream_t prep_side = nullptr;
+  cudaEvent_t prep_fork = nullptr, prep_join = nullptr;
   // key-window decision of chunked prefill: far-slash counts of the last two chunks
   int* far_dev = nullptr;        // device [2]
   int* far_host = nullptr;       // pinned, mapped [2][2]
