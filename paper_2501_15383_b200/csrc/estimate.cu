@@ -460,7 +460,7 @@ int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream
     ta.nsplit = nst;
     ta.stats = stats;
     ta.rowstat = rowstat;
-    ta.col_part = col_part;
+    ta.col_part = a.col && nrt == 1 ? a.col : col_part;
     ta.diag_part = diag_part;
   }
 
@@ -559,20 +559,23 @@ int estimate_simt(lcx_context* ctx, const EstimateArgs& a, Arena& ar, cudaStream
     ta.pass = 2;
     LCX_TRY(est_tc_run(ta, pl, ta_ar, st));
   }
+  // one row tile: every key's column sum has exactly one writer (its tile), so pass 2
+  // writes the column scores in place and the combine only forms the diagonals
+  float* colp = a.col && nrt == 1 ? a.col : col_part;
   if (simt) {
     if (bf)
       est_tile_kernel<__nv_bfloat16, 2><<<grid, kThreads, smem, ss>>>(d, nullptr, rowstat,
-                                                                       a.est, col_part, diag_part);
+                                                                       a.est, colp, diag_part);
     else
       est_tile_kernel<float, 2><<<grid, kThreads, smem, ss>>>(d, nullptr, rowstat, a.est,
-                                                               col_part, diag_part);
+                                                               colp, diag_part);
     LCX_CHECK_LAUNCH();
   }
   LCX_TRY(join());
-  if (a.col || a.slash) {
+  if ((a.col && colp != a.col) || a.slash) {
     est_combine_lines<<<dim3(unsigned((a.nk + 255) / 256), unsigned(nh)), 256, 0, st>>>(
         col_part, diag_part, a.hq, h0, nh, nrt, a.nk, a.block, a.nk - a.block, ntiles,
-        a.slash_mean, a.col, a.slash);
+        a.slash_mean, colp != a.col ? a.col : nullptr, a.slash);
     LCX_CHECK_LAUNCH();
   }
   return LCX_OK;
